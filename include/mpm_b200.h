@@ -1,0 +1,286 @@
+/*
+ * mpm_b200.h — C-ABI of the B200-native MPM hot path (CRESSim-MPM, arxiv 2502.18437).
+ *
+ * Two layers, both plain C (no torch / C++ types in any signature):
+ *
+ *  1. Solver layer (mpmb_state_*, mpmb_step_*): one SimState resident in HBM.
+ *     Replaces the free functions of the reference's header-only C++ API:
+ *       mpm::step_mls                 proj/include/mpm/solvers.hpp:141-198
+ *       mpm::step_pbmpm               proj/include/mpm/solvers.hpp:207-279
+ *       mpm::apply_boundary_conditions proj/include/mpm/solvers.hpp:30-50
+ *       mpm::apply_contact_pass       proj/include/mpm/contact.hpp:97-136  (as the step's grid hook)
+ *       mpm::particle_pushout         proj/include/mpm/contact.hpp:140-179
+ *       mpm::deactivate_out_of_domain proj/include/mpm/state.hpp:153-164
+ *       mpm::integrate_free_body      proj/include/mpm/rigid_dynamics.hpp:82-103
+ *     plus the NEW binning/sort stage (no reference function; key arithmetic of
+ *     quadratic_bspline_weights math.hpp:219-225 and Grid::index state.hpp:39-43).
+ *
+ *  2. Scene facade (mpmb_create_scene ... mpmb_shape_impulse): the flat handle API
+ *     of proj/include/mpm/facade.hpp:67-219 (itself the FFI boundary of the
+ *     reference), with the same handle rules (never reused, 0 = invalid) and the
+ *     same Status codes, plus batched scene replicas (mpmb_create_scene_batch)
+ *     that advance together in one launch per kernel.
+ *
+ * Arrays are host pointers in the reference's layouts: Vec3 = 3 floats, Mat3 = 9
+ * floats row-major (math.hpp:46-48), particles in ORIGINAL index order
+ * (state.hpp:92-97, scene.hpp:255-257) regardless of the device-side sort.
+ * No function throws; every function returns an mpmb_status (or a handle where
+ * the reference facade returns one).  Without a usable CUDA device every entry
+ * point that needs one returns MPMB_NO_DEVICE — there is no CPU fallback.
+ */
+#ifndef MPM_B200_H
+#define MPM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MPMB_ABI_VERSION 1
+
+/* mpm::facade::Status (facade.hpp:18-24) + device errors. */
+typedef enum {
+    MPMB_OK = 0,
+    MPMB_BAD_HANDLE = 1,
+    MPMB_LIFECYCLE_ERROR = 2,
+    MPMB_INVALID_ARGUMENT = 3,
+    MPMB_BUFFER_TOO_SMALL = 4,
+    MPMB_CUDA_ERROR = 5,
+    MPMB_NO_DEVICE = 6
+} mpmb_status;
+
+/* mpm::SolverKind (scene.hpp:13) */
+enum { MPMB_SOLVER_STANDARD = 0, MPMB_SOLVER_MLS = 1, MPMB_SOLVER_PBMPM = 2 };
+/* mpm::BoundaryKind (solvers.hpp:21) */
+enum { MPMB_BC_SLIP = 0, MPMB_BC_STICKY = 1 };
+/* mpm::MaterialKind (materials.hpp:11) */
+enum { MPMB_MAT_NEO_HOOKEAN = 0, MPMB_MAT_COROTATIONAL_PB = 1 };
+/* alternatives of mpm::Geometry, in variant order (geometry.hpp:84-86) */
+enum {
+    MPMB_GEOM_PLANE = 0,
+    MPMB_GEOM_SPHERE = 1,
+    MPMB_GEOM_BOX = 2,
+    MPMB_GEOM_QUAD_SLICER = 3,
+    MPMB_GEOM_TRI_MESH_SLICER = 4,
+    MPMB_GEOM_ARC = 5,
+    MPMB_GEOM_POLYLINE = 6
+};
+/* mpm::MotionKind (rigid_dynamics.hpp:105) */
+enum { MPMB_MOTION_FIXED = 0, MPMB_MOTION_KINEMATIC = 1, MPMB_MOTION_FREE_BODY = 2 };
+/* mpm::SdfRegion (geometry.hpp:34) */
+enum { MPMB_REGION_BULK = 0, MPMB_REGION_SURFACE = 1, MPMB_REGION_EDGE = 2,
+       MPMB_REGION_SPINE = 3, MPMB_REGION_CURVE = 4 };
+
+/* mpm::ShapePose (geometry.hpp:14-27); quaternion is (x, y, z, w). */
+typedef struct {
+    float position[3];
+    float orientation[4];
+    float linear_velocity[3];
+    float angular_velocity[3];
+} mpmb_pose;
+
+/* mpm::Keyframe (rigid_dynamics.hpp:11-15) */
+typedef struct {
+    float time;
+    float position[3];
+    float orientation[4];
+} mpmb_keyframe;
+
+/* mpm::Material (materials.hpp:13-18) */
+typedef struct {
+    int32_t kind;
+    float mu;
+    float lambda;
+    float beta;
+} mpmb_material;
+
+/*
+ * mpm::Shape (rigid_dynamics.hpp:107-117) with the Geometry variant flattened.
+ * gparam by geometry:
+ *   sphere: [radius]; box: [hx, hy, hz]; quad slicer: [half_length, half_height,
+ *   spine_radius]; tri mesh slicer: [spine_radius]; arc: [radius, angle];
+ *   plane / polyline: unused.
+ * vertices (local frame, 3 floats each) are used by the mesh slicer and polyline;
+ * indices (triangle list) and spine_edges (vertex pairs) by the mesh slicer.
+ * keyframes are read for motion == KINEMATIC (scene layer only), body_mass and
+ * inertia for motion == FREE_BODY.  All pointers are copied at the call.
+ */
+typedef struct {
+    int32_t geometry;
+    float gparam[4];
+    const float* vertices;
+    int32_t n_vertices;
+    const int32_t* indices;
+    int32_t n_indices;
+    const int32_t* spine_edges;
+    int32_t n_spine_edges;
+    mpmb_pose pose;
+    float mu_k;
+    float c_d;
+    float collision_halfwidth;
+    int32_t motion;
+    const mpmb_keyframe* keyframes;
+    int32_t n_keyframes;
+    float body_mass;
+    float inertia[3];
+} mpmb_shape_desc;
+
+/* mpm::StepStats (solvers.hpp:23-26) */
+typedef struct {
+    int32_t inverted_f;
+    int32_t projection_failures;
+} mpmb_step_stats;
+
+/* mpm::SceneConfig (scene.hpp:15-24) */
+typedef struct {
+    int32_t solver;
+    int32_t substeps;
+    int32_t iterations;
+    float gravity[3];
+    int32_t grid_dims[3];
+    float dx;
+    float origin[3];
+    int32_t boundary;
+} mpmb_scene_config;
+
+/* Scalar part of mpm::FrameResult (scene.hpp:28-43); arrays via mpmb_result_copy. */
+typedef struct {
+    float time;
+    int32_t n_particles;
+    int32_t n_shapes;
+    double total_mass;
+    double momentum[3];
+    double kinetic_energy;
+    int32_t pushed_out;
+    int32_t inverted_f;
+    int32_t projection_failures;
+    int32_t deactivated;
+} mpmb_frame_summary;
+
+/* Device-side timing of the last advance()s, accumulated while profiling is on. */
+typedef struct {
+    double ms_sort;
+    double ms_p2g;
+    double ms_grid;
+    double ms_g2p;
+    double ms_other;
+    int64_t launches;            /* kernels launched by the library while profiling */
+    int64_t particle_substeps;   /* active particles x substeps (PB: x iterations) */
+} mpmb_profile;
+
+/* ------------------------------------------------------------------ library */
+int32_t mpmb_abi_version(void);
+/* 1 when a CUDA device is usable by this process, else 0. */
+int32_t mpmb_device_available(void);
+/* Last error text of the calling thread ("" if none). */
+const char* mpmb_last_error(void);
+/* Total kernels this process launched through the library. */
+int64_t mpmb_kernel_launch_count(void);
+
+/* ------------------------------------------------------------ solver layer */
+typedef struct mpmb_state_s* mpmb_state;
+
+/* mpm::Grid(nx, ny, nz, dx, origin) (state.hpp:29-37): dims >= 4, dx > 0. */
+mpmb_status mpmb_state_create(const int32_t dims[3], float dx, const float origin[3],
+                              mpmb_state* out);
+mpmb_status mpmb_state_destroy(mpmb_state st);
+mpmb_status mpmb_state_set_materials(mpmb_state st, const mpmb_material* mats, int32_t n);
+/* Upload a ParticleStore (state.hpp:65-90). stress may be NULL (= cached sigma of F). */
+mpmb_status mpmb_state_set_particles(mpmb_state st, int32_t n, const float* x, const float* v,
+                                     const float* mass, const float* volume0, const float* F,
+                                     const float* C, const float* stress,
+                                     const int32_t* material_id, const uint8_t* active);
+/* Download in original order; any pointer may be NULL. */
+mpmb_status mpmb_state_get_particles(mpmb_state st, int32_t n, float* x, float* v, float* mass,
+                                     float* volume0, float* F, float* C, float* stress,
+                                     int32_t* material_id, uint8_t* active);
+int32_t mpmb_state_particle_count(mpmb_state st);
+/* Shapes used by the contact pass, push-out and free-body integration. */
+mpmb_status mpmb_state_set_shapes(mpmb_state st, const mpmb_shape_desc* shapes, int32_t n);
+mpmb_status mpmb_state_get_shape_poses(mpmb_state st, mpmb_pose* out, int32_t n);
+/* ContactAccumulator per shape (contact.hpp:10-16), summed since the last reset. */
+mpmb_status mpmb_state_get_contact(mpmb_state st, float* impulse, float* torque_impulse,
+                                   int32_t* contact_node_count, int32_t n);
+mpmb_status mpmb_state_reset_contact(mpmb_state st);
+
+/* step_mls; contact != 0 installs apply_contact_pass over the state's shapes as the hook. */
+mpmb_status mpmb_step_mls(mpmb_state st, float dt, const float gravity[3], int32_t contact,
+                          int32_t boundary, mpmb_step_stats* stats);
+/* step_pbmpm with PbmpmConfig{iterations}. */
+mpmb_status mpmb_step_pbmpm(mpmb_state st, float dt, const float gravity[3], int32_t iterations,
+                            int32_t contact, int32_t boundary, mpmb_step_stats* stats);
+
+/* Host GridHook adapter (solvers.hpp:19, 63): called after v = p/m + g dt (and after the
+ * contact pass when contact != 0), before BC, with the dense grid in node-major order
+ * (state.hpp:26); edits are uploaded back.  Debug path: synchronous download/upload. */
+typedef void (*mpmb_grid_hook)(void* user, int32_t n_nodes, float* mass, float* momentum,
+                               float* velocity);
+mpmb_status mpmb_step_mls_hooked(mpmb_state st, float dt, const float gravity[3],
+                                 int32_t contact, int32_t boundary, mpmb_grid_hook hook,
+                                 void* user, mpmb_step_stats* stats);
+
+mpmb_status mpmb_particle_pushout(mpmb_state st, int32_t* count);
+mpmb_status mpmb_deactivate_out_of_domain(mpmb_state st, int32_t* count);
+/* integrate_free_body for every FREE_BODY shape with its accumulated impulse. */
+mpmb_status mpmb_integrate_free_bodies(mpmb_state st, const float gravity[3], float dt);
+
+/* Dense grid after the last step (post-BC); any pointer may be NULL.
+ * Node-major i + nx*(j + ny*k); momentum/velocity are 3 floats per node. */
+mpmb_status mpmb_state_get_grid(mpmb_state st, float* mass, float* momentum, float* velocity);
+
+/* Binning (NEW stage, K1): for every particle in original order, keys[i] = linear stencil-base
+ * cell b_x + nx*(b_y + ny*b_z) (0xFFFFFFFF for inactive); perm = original indices sorted stably
+ * by (key, original index), inactive last.  Any pointer may be NULL. */
+mpmb_status mpmb_bin_particles(mpmb_state st, uint32_t* keys, uint32_t* perm);
+
+/* --------------------------------------------------------- facade layer */
+typedef uint64_t mpmb_handle;
+#define MPMB_INVALID_HANDLE ((mpmb_handle)0)
+
+mpmb_handle mpmb_create_scene(const mpmb_scene_config* config);
+/* Batched replicas: n scenes with one config advancing together.  Returns the batch handle
+ * and writes n scene handles; per-scene calls (materials, objects, shapes, pose targets,
+ * copy_positions, shape_impulse) take the scene handles, advance/fetch take the batch. */
+mpmb_handle mpmb_create_scene_batch(const mpmb_scene_config* config, int32_t n,
+                                    mpmb_handle* scenes_out);
+mpmb_status mpmb_destroy(mpmb_handle h);
+mpmb_handle mpmb_create_material(mpmb_handle scene, const mpmb_material* mat);
+mpmb_handle mpmb_create_particle_object(mpmb_handle scene, mpmb_handle material,
+                                        const float min_corner[3], const float max_corner[3],
+                                        int32_t particles_per_cell, float density,
+                                        uint64_t seed);
+mpmb_handle mpmb_create_shape(mpmb_handle scene, const mpmb_shape_desc* shape);
+mpmb_status mpmb_set_shape_pose_target(mpmb_handle scene, mpmb_handle shape,
+                                       const float position[3], const float orientation[4]);
+/* Enqueues one frame (asynchronous; the paper's advance/fetch split). Scene or batch handle. */
+mpmb_status mpmb_advance(mpmb_handle h, float dt);
+/* Waits for the pending frame and snapshots FrameResult. For a batch, out has n entries. */
+mpmb_status mpmb_fetch_results(mpmb_handle h, mpmb_frame_summary* out);
+/* Arrays of the last fetched FrameResult of one scene (any pointer may be NULL):
+ * positions/velocities 3n floats, active n bytes, shape ids/impulses/torques per shape. */
+mpmb_status mpmb_result_copy(mpmb_handle scene, float* positions, float* velocities,
+                             uint8_t* active, int32_t* shape_ids, float* shape_impulses,
+                             float* shape_torque_impulses);
+int32_t mpmb_particle_count(mpmb_handle scene);
+mpmb_status mpmb_copy_positions(mpmb_handle scene, float* out, size_t capacity_floats,
+                                size_t* written_floats);
+mpmb_status mpmb_shape_impulse(mpmb_handle scene, mpmb_handle shape, float out[3]);
+/* Synchronous ParticleStore read-back of a scene in original order (any pointer NULL). */
+mpmb_status mpmb_scene_get_particles(mpmb_handle scene, float* x, float* v, float* F, float* C,
+                                     uint8_t* active);
+
+/* Execution control: run on the caller's cudaStream_t (NULL = library stream), re-bin every
+ * k substeps (0 = once per frame), profile kernel classes with CUDA events. */
+mpmb_status mpmb_set_stream(mpmb_handle h, void* cuda_stream);
+mpmb_status mpmb_set_resort_interval(mpmb_handle h, int32_t substeps);
+mpmb_status mpmb_set_profiling(mpmb_handle h, int32_t on);
+mpmb_status mpmb_get_profile(mpmb_handle h, mpmb_profile* out);
+/* Blocks until every frame enqueued on h has finished. */
+mpmb_status mpmb_synchronize(mpmb_handle h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPM_B200_H */

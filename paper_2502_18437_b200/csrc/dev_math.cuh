@@ -1,0 +1,482 @@
+// dev_math.cuh — device-side math, SDF, contact and constitutive functions of the
+// B200 MPM hot path.  Each function names the reference definition it reproduces
+// (CRESSim-MPM CPU reference, proj/include/mpm/*.hpp).  Arithmetic is FP32 with
+// FMA contraction allowed (tolerance-checked against the oracle) EXCEPT the
+// stencil-base arithmetic, which uses explicit round-to-nearest intrinsics so the
+// binning keys are bit-identical to the reference (math.hpp:219-223).
+#pragma once
+#include <cstdint>
+#include <cfloat>
+
+#include "dev_types.h"
+
+namespace mpmb {
+
+struct V3 { float x, y, z; };
+struct M3 { float m[9]; };   // row-major, math.hpp:46-48
+struct Q4 { float x, y, z, w; };
+
+__device__ __forceinline__ V3 mk(float x, float y, float z) { return V3{x, y, z}; }
+__device__ __forceinline__ V3 operator+(V3 a, V3 b) { return V3{a.x + b.x, a.y + b.y, a.z + b.z}; }
+__device__ __forceinline__ V3 operator-(V3 a, V3 b) { return V3{a.x - b.x, a.y - b.y, a.z - b.z}; }
+__device__ __forceinline__ V3 operator-(V3 a) { return V3{-a.x, -a.y, -a.z}; }
+__device__ __forceinline__ V3 operator*(V3 a, float s) { return V3{a.x * s, a.y * s, a.z * s}; }
+__device__ __forceinline__ V3 vdiv(V3 a, float s) { return V3{a.x / s, a.y / s, a.z / s}; }
+__device__ __forceinline__ float dot(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ V3 cross(V3 a, V3 b) {
+    return V3{a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+__device__ __forceinline__ float norm2(V3 a) { return dot(a, a); }
+__device__ __forceinline__ float norm(V3 a) { return sqrtf(norm2(a)); }
+// math.hpp:35-38
+__device__ __forceinline__ V3 normalized(V3 a) {
+    float n = norm(a);
+    return n > 0.f ? vdiv(a, n) : V3{1.f, 0.f, 0.f};
+}
+
+// math.hpp:157-162
+__device__ __forceinline__ V3 qrotate(Q4 q, V3 v) {
+    V3 u{q.x, q.y, q.z};
+    V3 t = cross(u, v) * 2.f;
+    return v + t * q.w + cross(u, t);
+}
+__device__ __forceinline__ V3 qrotate_inv(Q4 q, V3 v) { return qrotate(Q4{-q.x, -q.y, -q.z, q.w}, v); }
+// math.hpp:151-156
+__device__ __forceinline__ Q4 qmul(Q4 a, Q4 o) {
+    return Q4{a.w * o.x + a.x * o.w + a.y * o.z - a.z * o.y,
+              a.w * o.y - a.x * o.z + a.y * o.w + a.z * o.x,
+              a.w * o.z + a.x * o.y - a.y * o.x + a.z * o.w,
+              a.w * o.w - a.x * o.x - a.y * o.y - a.z * o.z};
+}
+// math.hpp:144-149
+__device__ __forceinline__ Q4 qnormalized(Q4 q) {
+    float n = sqrtf(q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w);
+    if (n <= 0.f) return Q4{0.f, 0.f, 0.f, 1.f};
+    return Q4{q.x / n, q.y / n, q.z / n, q.w / n};
+}
+
+// ---------------------------------------------------------------- spline (math.hpp)
+// Stencil base and fractional coordinate, exactly the reference's P2G arithmetic
+// (math.hpp:219-224): inv_dx = 1/dx (host-computed), p = (x - o) * inv_dx,
+// base = (int)floor(p - 0.5), fx = p - base.  No contraction: bit-exact keys.
+__device__ __forceinline__ int stencil_base(float x, float o, float inv_dx, float& fx) {
+    float p = __fmul_rn(__fsub_rn(x, o), inv_dx);
+    int base = static_cast<int>(floorf(__fsub_rn(p, 0.5f)));
+    fx = __fsub_rn(p, static_cast<float>(base));
+    return base;
+}
+// Quadratic B-spline weights (math.hpp:226-228).
+__device__ __forceinline__ void bspline_w(float fx, float w[3]) {
+    float a = 1.5f - fx, b = fx - 1.f, c = fx - 0.5f;
+    w[0] = 0.5f * a * a;
+    w[1] = 0.75f - b * b;
+    w[2] = 0.5f * c * c;
+}
+// Interior band test, DIVIDING by dx (math.hpp:203-213) as deactivation does.
+__device__ __forceinline__ bool spline_in_domain(V3 pos, const DevScene& S) {
+    const float p[3] = {__fdiv_rn(__fsub_rn(pos.x, S.origin[0]), S.dx),
+                        __fdiv_rn(__fsub_rn(pos.y, S.origin[1]), S.dx),
+                        __fdiv_rn(__fsub_rn(pos.z, S.origin[2]), S.dx)};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        int base = static_cast<int>(floorf(__fsub_rn(p[a], 0.5f)));
+        if (base < 0 || base + 2 > S.dims[a] - 1) return false;
+    }
+    return true;
+}
+
+// ------------------------------------------------------------- matrices
+__device__ __forceinline__ float det3(const float a[9]) {  // math.hpp:273-277
+    return a[0] * (a[4] * a[8] - a[5] * a[7]) + a[1] * (a[5] * a[6] - a[3] * a[8]) +
+           a[2] * (a[3] * a[7] - a[4] * a[6]);
+}
+
+// Cauchy stress (materials.hpp:35-54), FP64 internally, J clamped >= 1e-6.
+// b = F F^T is symmetric; the 6 unique entries are computed once.
+__device__ __forceinline__ void neo_hookean(const float F[9], float mu, float lambda, float s[9]) {
+    double f[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) f[i] = static_cast<double>(F[i]);
+    double J = f[0] * (f[4] * f[8] - f[5] * f[7]) - f[1] * (f[3] * f[8] - f[5] * f[6]) +
+               f[2] * (f[3] * f[7] - f[4] * f[6]);
+    double Jc = J < 1e-6 ? 1e-6 : J;
+    double d = static_cast<double>(lambda) * log(Jc);
+    double inv = 1.0 / Jc;
+    double mu_d = static_cast<double>(mu);
+    double b00 = f[0] * f[0] + f[1] * f[1] + f[2] * f[2];
+    double b11 = f[3] * f[3] + f[4] * f[4] + f[5] * f[5];
+    double b22 = f[6] * f[6] + f[7] * f[7] + f[8] * f[8];
+    double b01 = f[0] * f[3] + f[1] * f[4] + f[2] * f[5];
+    double b02 = f[0] * f[6] + f[1] * f[7] + f[2] * f[8];
+    double b12 = f[3] * f[6] + f[4] * f[7] + f[5] * f[8];
+    s[0] = static_cast<float>((mu_d * (b00 - 1.0) + d) * inv);
+    s[4] = static_cast<float>((mu_d * (b11 - 1.0) + d) * inv);
+    s[8] = static_cast<float>((mu_d * (b22 - 1.0) + d) * inv);
+    float o01 = static_cast<float>(mu_d * b01 * inv);
+    float o02 = static_cast<float>(mu_d * b02 * inv);
+    float o12 = static_cast<float>(mu_d * b12 * inv);
+    s[1] = o01; s[3] = o01;
+    s[2] = o02; s[6] = o02;
+    s[5] = o12; s[7] = o12;
+}
+
+// Scaled-Newton polar decomposition in FP64 (math.hpp:286-340); returns R only
+// (U is not used by the projection).  false on failure.
+__device__ __forceinline__ bool polar_R(const float m[9], float R[9]) {
+#pragma unroll
+    for (int i = 0; i < 9; ++i)
+        if (!isfinite(m[i])) return false;
+    if (det3(m) <= 0.f) return false;
+    double x[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) x[i] = m[i];
+    for (int iter = 0; iter < 50; ++iter) {
+        double d = x[0] * (x[4] * x[8] - x[5] * x[7]) + x[1] * (x[5] * x[6] - x[3] * x[8]) +
+                   x[2] * (x[3] * x[7] - x[4] * x[6]);
+        if (!(d > 0.0) || !isfinite(d)) return false;
+        double id = 1.0 / d;
+        double it[9];
+        it[0] = (x[4] * x[8] - x[5] * x[7]) * id;
+        it[1] = (x[5] * x[6] - x[3] * x[8]) * id;
+        it[2] = (x[3] * x[7] - x[4] * x[6]) * id;
+        it[3] = (x[2] * x[7] - x[1] * x[8]) * id;
+        it[4] = (x[0] * x[8] - x[2] * x[6]) * id;
+        it[5] = (x[1] * x[6] - x[0] * x[7]) * id;
+        it[6] = (x[1] * x[5] - x[2] * x[4]) * id;
+        it[7] = (x[2] * x[3] - x[0] * x[5]) * id;
+        it[8] = (x[0] * x[4] - x[1] * x[3]) * id;
+        double nx = 0.0, ni = 0.0;
+#pragma unroll
+        for (int i = 0; i < 9; ++i) {
+            nx += x[i] * x[i];
+            ni += it[i] * it[i];
+        }
+        double gamma = sqrt(sqrt(ni / nx));
+        double ig = 1.0 / gamma;
+        double delta = 0.0;
+#pragma unroll
+        for (int i = 0; i < 9; ++i) {
+            double next = 0.5 * (gamma * x[i] + it[i] * ig);
+            double diff = next - x[i];
+            delta += diff * diff;
+            x[i] = next;
+        }
+        if (delta < 1e-16) break;  // sqrt(delta) < 1e-8
+    }
+#pragma unroll
+    for (int i = 0; i < 9; ++i) R[i] = static_cast<float>(x[i]);
+    return true;
+}
+
+// Co-rotational projection (materials.hpp:59-72).
+__device__ __forceinline__ bool corotational_project(const float Fp[9], const float Cc[9], float dt,
+                                                     float beta, float out[9]) {
+    if (dt <= 0.f) return false;
+    float A[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) A[i] = Cc[i] * dt + ((i % 4) == 0 ? 1.f : 0.f);
+    float Ft[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            Ft[3 * i + j] = A[3 * i] * Fp[j] + A[3 * i + 1] * Fp[3 + j] + A[3 * i + 2] * Fp[6 + j];
+    float R[9];
+    if (!polar_R(Ft, R)) return false;
+    float dtr = det3(Ft);
+    if (!(dtr > 0.f)) return false;
+    float s = (1.f - beta) / dtr;
+    float Fq[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) Fq[i] = R[i] * beta + Ft[i] * s;
+    // inverse of F_prev (math.hpp:252-271)
+    const float c00 = Fp[4] * Fp[8] - Fp[5] * Fp[7];
+    const float c01 = Fp[5] * Fp[6] - Fp[3] * Fp[8];
+    const float c02 = Fp[3] * Fp[7] - Fp[4] * Fp[6];
+    float det = Fp[0] * c00 + Fp[1] * c01 + Fp[2] * c02;
+    if (fabsf(det) <= 1e-12f) return false;
+    float idt = 1.f / det;
+    float inv[9];
+    inv[0] = c00 * idt;
+    inv[3] = c01 * idt;
+    inv[6] = c02 * idt;
+    inv[1] = (Fp[2] * Fp[7] - Fp[1] * Fp[8]) * idt;
+    inv[4] = (Fp[0] * Fp[8] - Fp[2] * Fp[6]) * idt;
+    inv[7] = (Fp[1] * Fp[6] - Fp[0] * Fp[7]) * idt;
+    inv[2] = (Fp[1] * Fp[5] - Fp[2] * Fp[4]) * idt;
+    inv[5] = (Fp[2] * Fp[3] - Fp[0] * Fp[5]) * idt;
+    inv[8] = (Fp[0] * Fp[4] - Fp[1] * Fp[3]) * idt;
+    float idtt = 1.f / dt;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            float v = Fq[3 * i] * inv[j] + Fq[3 * i + 1] * inv[3 + j] + Fq[3 * i + 2] * inv[6 + j];
+            out[3 * i + j] = (v - (i == j ? 1.f : 0.f)) * idtt;
+        }
+    return true;
+}
+
+// ------------------------------------------------------------------- SDF (geometry.hpp)
+struct Sdf {
+    float distance;
+    V3 normal;
+    V3 tangent;
+    int region;
+};
+
+__device__ __forceinline__ float clampf(float v, float lo, float hi) {
+    return v < lo ? lo : (hi < v ? hi : v);
+}
+
+// geometry.hpp:204-213
+__device__ __forceinline__ V3 closest_on_segment(V3 a, V3 b, V3 p, float& t) {
+    V3 ab = b - a;
+    float len2 = norm2(ab);
+    t = len2 > 1e-18f ? clampf(dot(p - a, ab) / len2, 0.f, 1.f) : 0.f;
+    return a + ab * t;
+}
+
+// geometry.hpp:217-242
+__device__ __forceinline__ V3 closest_on_triangle(V3 a, V3 b, V3 c, V3 p) {
+    V3 ab = b - a, ac = c - a, ap = p - a;
+    float d1 = dot(ab, ap), d2 = dot(ac, ap);
+    if (d1 <= 0.f && d2 <= 0.f) return a;
+    V3 bp = p - b;
+    float d3 = dot(ab, bp), d4 = dot(ac, bp);
+    if (d3 >= 0.f && d4 <= d3) return b;
+    float vc = d1 * d4 - d3 * d2;
+    if (vc <= 0.f && d1 >= 0.f && d3 <= 0.f) return a + ab * (d1 / (d1 - d3));
+    V3 cp = p - c;
+    float d5 = dot(ab, cp), d6 = dot(ac, cp);
+    if (d6 >= 0.f && d5 <= d6) return c;
+    float vb = d5 * d2 - d1 * d6;
+    if (vb <= 0.f && d2 >= 0.f && d6 <= 0.f) return a + ac * (d2 / (d2 - d6));
+    float va = d3 * d6 - d5 * d4;
+    if (va <= 0.f && (d4 - d3) >= 0.f && (d5 - d6) >= 0.f) {
+        float w = (d4 - d3) / ((d4 - d3) + (d5 - d6));
+        return b + (c - b) * w;
+    }
+    float denom = 1.f / (va + vb + vc);
+    return a + ab * (vb * denom) + ac * (vc * denom);
+}
+
+// World-space SDF query (geometry.hpp:370-395) against one device shape.
+__device__ inline Sdf sdf_query(const DevShape& g, const DevPose& pose, const float* verts,
+                                const int* ints, V3 point) {
+    Q4 q{pose.rot[0], pose.rot[1], pose.rot[2], pose.rot[3]};
+    V3 p = qrotate_inv(q, point - mk(pose.pos[0], pose.pos[1], pose.pos[2]));
+    Sdf s;
+    s.distance = 0.f;
+    s.normal = mk(1.f, 0.f, 0.f);
+    s.tangent = mk(0.f, 1.f, 0.f);
+    s.region = REGION_BULK;
+    switch (g.geom) {
+        case GEOM_PLANE:  // geometry.hpp:136-142
+            s.distance = p.y;
+            s.normal = mk(0.f, 1.f, 0.f);
+            s.region = REGION_SURFACE;
+            break;
+        case GEOM_SPHERE: {  // geometry.hpp:144-151
+            float r = norm(p);
+            s.distance = r - g.gp[0];
+            s.normal = r > 1e-9f ? vdiv(p, r) : mk(1.f, 0.f, 0.f);
+            s.region = REGION_SURFACE;
+            break;
+        }
+        case GEOM_BOX: {  // geometry.hpp:153-176
+            s.region = REGION_SURFACE;
+            V3 h = mk(g.gp[0], g.gp[1], g.gp[2]);
+            V3 qv = mk(fabsf(p.x) - h.x, fabsf(p.y) - h.y, fabsf(p.z) - h.z);
+            float qmax = qv.x;
+            if (qmax < qv.y) qmax = qv.y;
+            if (qmax < qv.z) qmax = qv.z;
+            if (qmax <= 0.f) {
+                s.distance = qmax;
+                if (qv.x >= qv.y && qv.x >= qv.z)
+                    s.normal = mk(p.x >= 0.f ? 1.f : -1.f, 0.f, 0.f);
+                else if (qv.y >= qv.z)
+                    s.normal = mk(0.f, p.y >= 0.f ? 1.f : -1.f, 0.f);
+                else
+                    s.normal = mk(0.f, 0.f, p.z >= 0.f ? 1.f : -1.f);
+            } else {
+                V3 cl = mk(clampf(p.x, -h.x, h.x), clampf(p.y, -h.y, h.y), clampf(p.z, -h.z, h.z));
+                V3 d = p - cl;
+                s.distance = norm(d);
+                s.normal = s.distance > 1e-9f ? vdiv(d, s.distance) : mk(1.f, 0.f, 0.f);
+            }
+            break;
+        }
+        case GEOM_QUAD_SLICER: {  // geometry.hpp:178-202
+            const float hl = g.gp[0], hh = g.gp[1], sr = g.gp[2];
+            if (p.y >= hh) {
+                V3 axis = mk(clampf(p.x, -hl, hl), hh, 0.f);
+                V3 d = p - axis;
+                float r = norm(d);
+                s.distance = r - sr;
+                s.normal = r > 1e-9f ? vdiv(d, r) : mk(0.f, 1.f, 0.f);
+                s.region = REGION_SPINE;
+            } else if (fabsf(p.x) <= hl && p.y >= -hh) {
+                s.distance = p.z;
+                s.normal = mk(0.f, 0.f, p.z >= 0.f ? 1.f : -1.f);
+                s.region = REGION_EDGE;
+            } else {
+                s.region = REGION_BULK;
+                s.distance = FLT_MAX;
+            }
+            break;
+        }
+        case GEOM_TRI_MESH_SLICER: {  // geometry.hpp:244-293
+            const V3* vt = reinterpret_cast<const V3*>(verts) + g.vtx_begin;
+            const int* sp = ints + g.spine_begin;
+            const int* ix = ints + g.idx_begin;
+            float best_spine = FLT_MAX;
+            V3 spine_pt = mk(0.f, 0.f, 0.f);
+            for (int e = 0; e + 1 < g.n_spine; e += 2) {
+                float t;
+                V3 qq = closest_on_segment(vt[sp[e]], vt[sp[e + 1]], p, t);
+                float d = norm(p - qq);
+                if (d < best_spine) { best_spine = d; spine_pt = qq; }
+            }
+            float best_surf = FLT_MAX;
+            V3 surf_pt = mk(0.f, 0.f, 0.f), surf_n = mk(0.f, 0.f, 0.f);
+            for (int t = 0; t + 2 < g.n_idx; t += 3) {
+                V3 a = vt[ix[t]], b = vt[ix[t + 1]], c = vt[ix[t + 2]];
+                V3 qq = closest_on_triangle(a, b, c, p);
+                float d = norm(p - qq);
+                if (d < best_surf) {
+                    best_surf = d;
+                    surf_pt = qq;
+                    surf_n = normalized(cross(b - a, c - a));
+                }
+            }
+            if (best_spine <= best_surf + 1e-9f && best_spine < FLT_MAX) {
+                V3 d = p - spine_pt;
+                float r = norm(d);
+                s.distance = r - g.gp[0];
+                s.normal = r > 1e-9f ? vdiv(d, r) : mk(0.f, 1.f, 0.f);
+                s.region = REGION_SPINE;
+            } else {
+                float side = dot(p - surf_pt, surf_n) >= 0.f ? 1.f : -1.f;
+                s.distance = side * best_surf;
+                s.normal = surf_n * side;
+                s.region = REGION_EDGE;
+            }
+            break;
+        }
+        case GEOM_ARC: {  // geometry.hpp:295-327
+            const float kTwoPi = 6.28318548f;  // float(2*pi), as Real(2*3.14159...)
+            float t;
+            if (sqrtf(p.x * p.x + p.y * p.y) < 1e-9f) {
+                t = 0.f;
+            } else {
+                t = atan2f(p.y, p.x);
+                if (t < 0.f) t += kTwoPi;
+                if (t > g.gp[1]) {
+                    float to_end = t - g.gp[1];
+                    float to_start = kTwoPi - t;
+                    t = to_end <= to_start ? g.gp[1] : 0.f;
+                }
+            }
+            float st, ct;
+            sincosf(t, &st, &ct);
+            V3 qq = mk(g.gp[0] * ct, g.gp[0] * st, 0.f);
+            s.region = REGION_CURVE;
+            s.tangent = mk(-st, ct, 0.f);
+            V3 d = p - qq;
+            float dist = norm(d);
+            s.distance = dist;
+            s.normal = dist < 1e-9f ? mk(-ct, -st, 0.f) : vdiv(d, dist);
+            break;
+        }
+        default: {  // GEOM_POLYLINE, geometry.hpp:329-365
+            const V3* vt = reinterpret_cast<const V3*>(verts) + g.vtx_begin;
+            const int nv = g.n_vtx;
+            float best = FLT_MAX;
+            V3 best_pt = mk(0.f, 0.f, 0.f), best_tan = mk(1.f, 0.f, 0.f);
+            for (int i = 0; i + 1 < nv; ++i) {
+                float t;
+                V3 qq = closest_on_segment(vt[i], vt[i + 1], p, t);
+                float d = norm(p - qq);
+                if (d < best) {
+                    best = d;
+                    best_pt = qq;
+                    V3 dir = normalized(vt[i + 1] - vt[i]);
+                    if (t <= 1e-6f && i > 0) {
+                        V3 prev = normalized(vt[i] - vt[i - 1]);
+                        dir = normalized(dir + prev);
+                    } else if (t >= 1.f - 1e-6f && i + 2 < nv) {
+                        V3 next = normalized(vt[i + 2] - vt[i + 1]);
+                        dir = normalized(dir + next);
+                    }
+                    best_tan = dir;
+                }
+            }
+            s.region = REGION_CURVE;
+            s.tangent = best_tan;
+            s.distance = best;
+            if (best < 1e-9f) {
+                V3 ref = fabsf(best_tan.x) < 0.9f ? mk(1.f, 0.f, 0.f) : mk(0.f, 1.f, 0.f);
+                s.normal = normalized(cross(best_tan, ref));
+            } else {
+                s.normal = vdiv(p - best_pt, best);
+            }
+            break;
+        }
+    }
+    s.normal = qrotate(q, s.normal);
+    s.tangent = qrotate(q, s.tangent);
+    return s;
+}
+
+// geometry.hpp:29-32
+__device__ __forceinline__ V3 rigid_point_velocity(const DevPose& pose, V3 p) {
+    V3 w = mk(pose.ang[0], pose.ang[1], pose.ang[2]);
+    return mk(pose.lin[0], pose.lin[1], pose.lin[2]) +
+           cross(w, p - mk(pose.pos[0], pose.pos[1], pose.pos[2]));
+}
+
+// contact.hpp:82-92
+__device__ __forceinline__ bool node_in_contact(const Sdf& s, float hw) {
+    switch (s.region) {
+        case REGION_SURFACE: return s.distance < 0.f;
+        case REGION_EDGE: return fabsf(s.distance) < hw;
+        case REGION_SPINE: return s.distance < 0.f;
+        case REGION_CURVE: return s.distance < hw;
+        default: return false;
+    }
+}
+
+// contact.hpp:33-38
+__device__ __forceinline__ float friction_drag(float vn, float vtg, float mu_k, float c_d) {
+    if (vtg < 1e-12f) return 0.f;
+    float f = 1.f - mu_k * vn / vtg;
+    return c_d * fmaxf(f, 0.f);
+}
+
+// One shape's grid correction (contact.hpp:106-133): returns the corrected velocity
+// and sets delta (zero when the node is untouched).
+__device__ __forceinline__ V3 contact_correct(const DevShape& g, const Sdf& s, V3 vnode, V3 vrig,
+                                              V3& delta) {
+    if (s.region == REGION_SPINE) {  // contact.hpp:77-80 sticky
+        delta = vrig - vnode;
+        return vrig;
+    }
+    V3 vrel = vnode - vrig;
+    float vn = dot(vrel, s.normal);
+    if (vn >= 0.f) {
+        delta = mk(0.f, 0.f, 0.f);
+        return vnode;
+    }
+    V3 vt;
+    if (s.region == REGION_CURVE)  // contact.hpp:60-74
+        vt = s.tangent * dot(vrel, s.tangent);
+    else  // contact.hpp:43-56
+        vt = vrel - s.normal * vn;
+    float tg = norm(vt);
+    V3 vc = vrig + vt * friction_drag(-vn, tg, g.mu_k, g.c_d);
+    delta = vc - vnode;
+    return vc;
+}
+
+}  // namespace mpmb

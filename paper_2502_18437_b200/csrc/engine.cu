@@ -1,0 +1,745 @@
+// engine.cu — Engine: device buffers and the enqueue order of the hot path.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <utility>
+
+#include "engine.h"
+#include "launch.h"
+
+namespace mpmb {
+
+namespace {
+
+std::atomic<int64_t> g_launches{0};
+
+void check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    void alloc(size_t b) {
+        if (b <= bytes && p) return;
+        release();
+        if (b == 0) b = 16;
+        check(cudaMalloc(&p, b), "cudaMalloc");
+        bytes = b;
+    }
+    template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+struct PinnedBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    ~PinnedBuf() { if (p) cudaFreeHost(p); }
+    void alloc(size_t b) {
+        if (b <= bytes && p) return;
+        if (p) cudaFreeHost(p);
+        check(cudaMallocHost(&p, b ? b : 16), "cudaMallocHost");
+        bytes = b ? b : 16;
+    }
+};
+
+enum Cat { CAT_SORT = 0, CAT_P2G, CAT_GRID, CAT_G2P, CAT_OTHER };
+
+}  // namespace
+
+bool device_available() {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return n > 0;
+}
+
+int64_t global_launch_count() { return g_launches.load(); }
+
+struct Engine::Impl {
+    cudaStream_t own = nullptr;
+    cudaStream_t st = nullptr;
+    std::vector<DevScene> hs;
+    DevBuf d_scenes;
+    uint64_t total_nodes = 0;
+    uint32_t total_bricks = 0;
+    DevBuf grid_acc, grid_vel, brick_flag, brick_stamp, active_bricks, brick_scene, misc;
+    // misc u32 slots: [0] n_active_bricks
+    int64_t n = 0;
+    DevBuf planes[2][kPlanes];
+    int cur = 0;
+    bool binned = false;
+    DevBuf b_count, b_off, b_key, b_rank, b_cell, b_orig, e_orig, e_cell, e_src, b_tmp, g_orig,
+        g_src, g_cell, s_src, s_orig, s_rank, b_flag, c_start, c_len, g_base, b_counts, scan_tmp,
+        key_by_orig;
+    BinBuffers bb{};
+    DevBuf mats;
+    DevBuf shapes, verts, ints, free_pose, pose_table, pose_override;
+    int n_shapes = 0;
+    int table_subs = 1;
+    PinnedBuf pin_table[2];
+    cudaEvent_t pin_done[2] = {nullptr, nullptr};
+    int pin_slot = 0;
+    DevBuf acc_sub, cnt_sub, acc_frame, cnt_frame, counters;
+    DevBuf stress_in;
+    bool use_stress_in = false;
+    uint32_t epoch = 0;
+    DevBuf io_x, io_v, io_a, io_tot;
+    PinnedBuf pin_io;
+    // profiling
+    bool profiling = false;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> events;
+    std::vector<cudaEvent_t> event_pool;
+    KernelTimes times;
+    int64_t* launch_counter = nullptr;
+
+    cudaEvent_t get_event() {
+        if (!event_pool.empty()) {
+            cudaEvent_t e = event_pool.back();
+            event_pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        check(cudaEventCreate(&e), "cudaEventCreate");
+        return e;
+    }
+    std::pair<cudaEvent_t, cudaEvent_t> begin() {
+        if (!profiling) return {nullptr, nullptr};
+        cudaEvent_t a = get_event(), b = get_event();
+        cudaEventRecord(a, st);
+        return {a, b};
+    }
+    void end(int cat, std::pair<cudaEvent_t, cudaEvent_t> ev) {
+        if (!profiling || !ev.first) return;
+        cudaEventRecord(ev.second, st);
+        events.push_back({cat, ev});
+    }
+    void collect() {
+        for (auto& e : events) {
+            cudaEventSynchronize(e.second.second);
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, e.second.first, e.second.second);
+            double* dst = e.first == CAT_SORT ? &times.ms_sort
+                          : e.first == CAT_P2G ? &times.ms_p2g
+                          : e.first == CAT_GRID ? &times.ms_grid
+                          : e.first == CAT_G2P ? &times.ms_g2p
+                                               : &times.ms_other;
+            *dst += ms;
+            event_pool.push_back(e.second.first);
+            event_pool.push_back(e.second.second);
+        }
+        events.clear();
+    }
+    void counted(int64_t k) {
+        g_launches += k;
+        *launch_counter += k;
+        if (profiling) times.launches += k;
+    }
+
+    Params params() {
+        Params P{};
+        for (int q = 0; q < kPlanes; ++q) P.pl[q] = planes[cur][q].as<float4>();
+        P.scenes = d_scenes.as<DevScene>();
+        P.shapes = shapes.as<DevShape>();
+        P.verts = verts.as<float>();
+        P.ints = ints.as<int>();
+        P.pose_table = pose_table.as<DevPose>();
+        P.pose_override = pose_override.as<uint8_t>();
+        P.free_pose = free_pose.as<DevPose>();
+        P.n_shapes = n_shapes;
+        P.mats = mats.as<float4>();
+        P.grid_acc = grid_acc.as<float4>();
+        P.grid_vel = grid_vel.as<float4>();
+        P.brick_flag = brick_flag.as<uint32_t>();
+        P.brick_stamp = brick_stamp.as<uint32_t>();
+        P.active_bricks = active_bricks.as<uint32_t>();
+        P.n_active_bricks = misc.as<uint32_t>();
+        P.brick_scene = brick_scene.as<uint32_t>();
+        P.group_base = g_base.as<uint32_t>();
+        P.chunk_len = c_len.as<uint8_t>();
+        P.n_chunks = b_counts.as<uint32_t>();
+        P.n_groups = b_counts.as<uint32_t>() + 1;
+        P.n_active = b_counts.as<uint32_t>() + 2;
+        P.n_total = n;
+        P.stress_in = stress_in.as<float>();
+        P.use_stress_in = use_stress_in ? 1 : 0;
+        P.acc_sub = acc_sub.as<double>();
+        P.cnt_sub = cnt_sub.as<int>();
+        P.acc_frame = acc_frame.as<double>();
+        P.cnt_frame = cnt_frame.as<int>();
+        P.counters = counters.as<int>();
+        P.epoch = epoch;
+        return P;
+    }
+};
+
+Engine::Engine(const std::vector<SceneGrid>& scenes) : impl_(new Impl), scenes_(scenes) {
+    Impl& I = *impl_;
+    launches_total_ = 0;
+    I.launch_counter = &launches_total_;
+    check(cudaStreamCreateWithFlags(&I.own, cudaStreamNonBlocking), "cudaStreamCreate");
+    I.st = I.own;
+    stream_ = I.own;
+    uint64_t node_base = 0;
+    uint32_t brick_base = 0;
+    for (const SceneGrid& g : scenes) {
+        DevScene d{};
+        for (int a = 0; a < 3; ++a) {
+            d.origin[a] = g.origin[a];
+            d.dims[a] = g.dims[a];
+            d.nb[a] = (g.dims[a] + kBrick - 1) / kBrick;
+        }
+        d.dx = g.dx;
+        d.inv_dx = 1.0f / g.dx;                 // math.hpp:219
+        d.m_inv = 4.0f / (g.dx * g.dx);         // solvers.hpp:149
+        d.node_base = node_base;
+        d.brick_base = brick_base;
+        const uint64_t nb = static_cast<uint64_t>(d.nb[0]) * d.nb[1] * d.nb[2];
+        if (brick_base + nb >= 0xFFFFFFF0ull) throw std::invalid_argument("engine: too many grid bricks");
+        node_base += nb * kBrickNodes;
+        brick_base += static_cast<uint32_t>(nb);
+        I.hs.push_back(d);
+    }
+    I.total_nodes = node_base;
+    I.total_bricks = brick_base;
+    I.d_scenes.alloc(sizeof(DevScene) * std::max<size_t>(1, I.hs.size()));
+    check(cudaMemcpy(I.d_scenes.p, I.hs.data(), sizeof(DevScene) * I.hs.size(), cudaMemcpyHostToDevice), "scenes");
+    I.grid_acc.alloc(sizeof(float4) * I.total_nodes);
+    I.grid_vel.alloc(sizeof(float4) * I.total_nodes);
+    check(cudaMemset(I.grid_acc.p, 0, sizeof(float4) * I.total_nodes), "memset");
+    check(cudaMemset(I.grid_vel.p, 0, sizeof(float4) * I.total_nodes), "memset");
+    I.brick_flag.alloc(sizeof(uint32_t) * I.total_bricks);
+    I.brick_stamp.alloc(sizeof(uint32_t) * I.total_bricks);
+    I.active_bricks.alloc(sizeof(uint32_t) * I.total_bricks);
+    check(cudaMemset(I.brick_flag.p, 0, sizeof(uint32_t) * I.total_bricks), "memset");
+    check(cudaMemset(I.brick_stamp.p, 0xFF, sizeof(uint32_t) * I.total_bricks), "memset");
+    std::vector<uint32_t> bs(I.total_bricks);
+    for (size_t s = 0; s < I.hs.size(); ++s) {
+        const uint32_t nb = static_cast<uint32_t>(I.hs[s].nb[0]) * I.hs[s].nb[1] * I.hs[s].nb[2];
+        std::fill(bs.begin() + I.hs[s].brick_base, bs.begin() + I.hs[s].brick_base + nb,
+                  static_cast<uint32_t>(s));
+    }
+    I.brick_scene.alloc(sizeof(uint32_t) * I.total_bricks);
+    check(cudaMemcpy(I.brick_scene.p, bs.data(), sizeof(uint32_t) * bs.size(), cudaMemcpyHostToDevice), "bs");
+    I.misc.alloc(64);
+    check(cudaMemset(I.misc.p, 0, 64), "memset");
+    I.counters.alloc(sizeof(int) * 4 * std::max<size_t>(1, I.hs.size()));
+    check(cudaMemset(I.counters.p, 0, I.counters.bytes), "memset");
+    I.b_counts.alloc(16);
+    check(cudaMemset(I.b_counts.p, 0, 16), "memset");
+    set_shapes(std::vector<std::vector<EngineShape>>(scenes.size()));
+    mpmb_material dflt{0, 0.f, 0.f, 0.f};
+    set_materials({dflt});
+    for (int i = 0; i < 2; ++i) check(cudaEventCreateWithFlags(&I.pin_done[i], cudaEventDisableTiming), "event");
+}
+
+Engine::~Engine() {
+    Impl& I = *impl_;
+    cudaStreamSynchronize(I.st);
+    for (auto& e : I.events) {
+        cudaEventDestroy(e.second.first);
+        cudaEventDestroy(e.second.second);
+    }
+    for (auto e : I.event_pool) cudaEventDestroy(e);
+    for (int i = 0; i < 2; ++i)
+        if (I.pin_done[i]) cudaEventDestroy(I.pin_done[i]);
+    if (I.own) cudaStreamDestroy(I.own);
+    delete impl_;
+}
+
+void Engine::set_stream(void* s) {
+    impl_->st = s ? static_cast<cudaStream_t>(s) : impl_->own;
+    stream_ = impl_->st;
+}
+
+void Engine::set_profiling(bool on) { impl_->profiling = on; }
+
+KernelTimes Engine::kernel_times() const {
+    impl_->collect();
+    return impl_->times;
+}
+
+void Engine::reset_kernel_times() {
+    impl_->collect();
+    impl_->times = KernelTimes{};
+}
+
+void Engine::set_materials(const std::vector<mpmb_material>& m) {
+    Impl& I = *impl_;
+    std::vector<float4> h(std::max<size_t>(1, m.size()));
+    for (size_t i = 0; i < m.size(); ++i)
+        h[i] = make_float4(static_cast<float>(m[i].kind), m[i].mu, m[i].lambda, m[i].beta);
+    I.mats.alloc(sizeof(float4) * h.size());
+    check(cudaMemcpyAsync(I.mats.p, h.data(), sizeof(float4) * h.size(), cudaMemcpyHostToDevice, I.st), "mats");
+    check(cudaStreamSynchronize(I.st), "sync");
+}
+
+void Engine::upload_particles(int64_t n, const float* x, const float* v, const float* mass,
+                              const float* vol0, const float* F, const float* C, const float* stress,
+                              const int32_t* material, const uint8_t* active, const int32_t* scene) {
+    Impl& I = *impl_;
+    if (n >= 0x7FFFFFFF) throw std::invalid_argument("engine: particle count exceeds 2^31");
+    check(cudaStreamSynchronize(I.st), "sync");
+    I.n = n;
+    n_total_ = n;
+    for (int b = 0; b < 2; ++b)
+        for (int q = 0; q < kPlanes; ++q) I.planes[b][q].alloc(sizeof(float4) * std::max<int64_t>(n, 1));
+    I.cur = 0;
+    // sort scratch
+    const size_t N = static_cast<size_t>(std::max<int64_t>(n, 1));
+    I.b_key.alloc(4 * N); I.b_rank.alloc(4 * N); I.b_cell.alloc(N); I.b_orig.alloc(4 * N);
+    I.e_orig.alloc(4 * N); I.e_cell.alloc(N); I.e_src.alloc(4 * N); I.b_tmp.alloc(4 * N);
+    I.g_orig.alloc(4 * N); I.g_src.alloc(4 * N); I.g_cell.alloc(N); I.s_src.alloc(4 * N);
+    I.s_orig.alloc(4 * N); I.s_rank.alloc(4 * N); I.b_flag.alloc(4 * (N + 1));
+    I.c_start.alloc(4 * N); I.c_len.alloc(N); I.g_base.alloc(4 * (N / 32 + 2));
+    const size_t nbk = static_cast<size_t>(I.total_bricks) + 1;
+    I.b_count.alloc(4 * nbk);
+    I.b_off.alloc(4 * (nbk + 1));
+    const size_t tiles = (std::max(N + 1, nbk + 1) + 4095) / 4096 + 2;
+    I.scan_tmp.alloc(4 * tiles);
+    BinBuffers& B = I.bb;
+    B.n_buckets = static_cast<uint32_t>(nbk);
+    B.bucket_count = I.b_count.as<uint32_t>(); B.bucket_off = I.b_off.as<uint32_t>();
+    B.key = I.b_key.as<uint32_t>(); B.rank = I.b_rank.as<uint32_t>(); B.cell = I.b_cell.as<uint8_t>();
+    B.orig = I.b_orig.as<uint32_t>(); B.e_orig = I.e_orig.as<uint32_t>(); B.e_cell = I.e_cell.as<uint8_t>();
+    B.e_src = I.e_src.as<uint32_t>(); B.tmp = I.b_tmp.as<uint32_t>(); B.g_orig = I.g_orig.as<uint32_t>();
+    B.g_src = I.g_src.as<uint32_t>(); B.g_cell = I.g_cell.as<uint8_t>(); B.sorted_src = I.s_src.as<uint32_t>();
+    B.sorted_orig = I.s_orig.as<uint32_t>(); B.rank_in_cell = I.s_rank.as<uint32_t>();
+    B.flag = I.b_flag.as<uint32_t>(); B.chunk_start = I.c_start.as<uint32_t>(); B.chunk_len = I.c_len.as<uint8_t>();
+    B.group_base = I.g_base.as<uint32_t>(); B.counts = I.b_counts.as<uint32_t>(); B.scan_tmp = I.scan_tmp.as<uint32_t>();
+    B.key_by_orig = nullptr;
+    if (n == 0) {
+        I.binned = false;
+        return;
+    }
+    // stage original-order arrays on the device, then scatter into the planes
+    DevBuf dx, dv, dm, dvol, dF, dC, dmat, dact, dsc;
+    dx.alloc(12 * N); dv.alloc(12 * N); dm.alloc(4 * N); dvol.alloc(4 * N); dF.alloc(36 * N);
+    dC.alloc(36 * N); dmat.alloc(4 * N); dact.alloc(N); dsc.alloc(4 * N);
+    check(cudaMemcpyAsync(dx.p, x, 12 * n, cudaMemcpyHostToDevice, I.st), "h2d");
+    check(cudaMemcpyAsync(dv.p, v, 12 * n, cudaMemcpyHostToDevice, I.st), "h2d");
+    check(cudaMemcpyAsync(dm.p, mass, 4 * n, cudaMemcpyHostToDevice, I.st), "h2d");
+    check(cudaMemcpyAsync(dvol.p, vol0, 4 * n, cudaMemcpyHostToDevice, I.st), "h2d");
+    check(cudaMemcpyAsync(dF.p, F, 36 * n, cudaMemcpyHostToDevice, I.st), "h2d");
+    check(cudaMemcpyAsync(dC.p, C, 36 * n, cudaMemcpyHostToDevice, I.st), "h2d");
+    check(cudaMemcpyAsync(dmat.p, material, 4 * n, cudaMemcpyHostToDevice, I.st), "h2d");
+    check(cudaMemcpyAsync(dact.p, active, n, cudaMemcpyHostToDevice, I.st), "h2d");
+    check(cudaMemcpyAsync(dsc.p, scene, 4 * n, cudaMemcpyHostToDevice, I.st), "h2d");
+    IoArrays io{dx.as<float>(), dv.as<float>(), dm.as<float>(), dvol.as<float>(), dF.as<float>(),
+                dC.as<float>(), dmat.as<int32_t>(), dact.as<uint8_t>(), dsc.as<int32_t>()};
+    Params P = I.params();
+    launch_upload(P, io, n, I.st);
+    I.counted(1);
+    if (stress) {
+        I.stress_in.alloc(36 * N);
+        check(cudaMemcpyAsync(I.stress_in.p, stress, 36 * n, cudaMemcpyHostToDevice, I.st), "h2d");
+        I.use_stress_in = true;
+    } else {
+        I.use_stress_in = false;
+    }
+    check(cudaStreamSynchronize(I.st), "upload");
+    I.binned = false;
+}
+
+void Engine::download_particles(int64_t begin, int64_t count, float* x, float* v, float* mass,
+                                float* vol0, float* F, float* C, float* stress, int32_t* material,
+                                uint8_t* active) {
+    Impl& I = *impl_;
+    if (I.n == 0 || count <= 0) return;
+    const size_t N = static_cast<size_t>(I.n);
+    DevBuf dx, dv, dm, dvol, dF, dC, dmat, dact, dsig;
+    IoArrays io{};
+    if (x) { dx.alloc(12 * N); io.x = dx.as<float>(); }
+    if (v) { dv.alloc(12 * N); io.v = dv.as<float>(); }
+    if (mass) { dm.alloc(4 * N); io.mass = dm.as<float>(); }
+    if (vol0) { dvol.alloc(4 * N); io.vol0 = dvol.as<float>(); }
+    if (F) { dF.alloc(36 * N); io.F = dF.as<float>(); }
+    if (C) { dC.alloc(36 * N); io.C = dC.as<float>(); }
+    if (material) { dmat.alloc(4 * N); io.mat = dmat.as<int32_t>(); }
+    if (active) { dact.alloc(N); io.active = dact.as<uint8_t>(); }
+    Params P = I.params();
+    launch_download(P, io, I.st);
+    I.counted(1);
+    if (stress) {
+        dsig.alloc(36 * N);
+        launch_stress(P, dsig.as<float>(), I.st);
+        I.counted(1);
+    }
+    auto cp = [&](void* dst, const DevBuf& src, size_t elem) {
+        if (dst)
+            check(cudaMemcpyAsync(dst, static_cast<char*>(src.p) + elem * begin, elem * count,
+                                  cudaMemcpyDeviceToHost, I.st), "d2h");
+    };
+    cp(x, dx, 12); cp(v, dv, 12); cp(mass, dm, 4); cp(vol0, dvol, 4); cp(F, dF, 36); cp(C, dC, 36);
+    cp(material, dmat, 4); cp(active, dact, 1); cp(stress, dsig, 36);
+    check(cudaStreamSynchronize(I.st), "download");
+}
+
+void Engine::set_shapes(const std::vector<std::vector<EngineShape>>& per_scene) {
+    Impl& I = *impl_;
+    check(cudaStreamSynchronize(I.st), "sync");
+    std::vector<DevShape> ds;
+    std::vector<DevPose> poses;
+    std::vector<float> verts;
+    std::vector<int> ints;
+    for (size_t s = 0; s < per_scene.size(); ++s) {
+        I.hs[s].shape_begin = static_cast<int>(ds.size());
+        I.hs[s].shape_count = static_cast<int>(per_scene[s].size());
+        for (const EngineShape& e : per_scene[s]) {
+            DevShape d = e.d;
+            d.scene = static_cast<int>(s);
+            d.vtx_begin = static_cast<int>(verts.size() / 3);
+            d.n_vtx = static_cast<int>(e.verts.size() / 3);
+            verts.insert(verts.end(), e.verts.begin(), e.verts.end());
+            d.idx_begin = static_cast<int>(ints.size());
+            d.n_idx = static_cast<int>(e.indices.size());
+            ints.insert(ints.end(), e.indices.begin(), e.indices.end());
+            d.spine_begin = static_cast<int>(ints.size());
+            d.n_spine = static_cast<int>(e.spine.size());
+            ints.insert(ints.end(), e.spine.begin(), e.spine.end());
+            ds.push_back(d);
+            poses.push_back(e.pose);
+        }
+    }
+    I.n_shapes = static_cast<int>(ds.size());
+    n_shapes_ = I.n_shapes;
+    check(cudaMemcpy(I.d_scenes.p, I.hs.data(), sizeof(DevScene) * I.hs.size(), cudaMemcpyHostToDevice), "scenes");
+    const size_t ns = std::max<size_t>(1, ds.size());
+    I.shapes.alloc(sizeof(DevShape) * ns);
+    I.verts.alloc(sizeof(float) * std::max<size_t>(3, verts.size()));
+    I.ints.alloc(sizeof(int) * std::max<size_t>(1, ints.size()));
+    I.free_pose.alloc(sizeof(DevPose) * ns);
+    I.acc_sub.alloc(sizeof(double) * 6 * ns);
+    I.acc_frame.alloc(sizeof(double) * 6 * ns);
+    I.cnt_sub.alloc(sizeof(int) * ns);
+    I.cnt_frame.alloc(sizeof(int) * ns);
+    if (!ds.empty()) {
+        check(cudaMemcpy(I.shapes.p, ds.data(), sizeof(DevShape) * ds.size(), cudaMemcpyHostToDevice), "shapes");
+        check(cudaMemcpy(I.free_pose.p, poses.data(), sizeof(DevPose) * poses.size(), cudaMemcpyHostToDevice), "poses");
+    }
+    if (!verts.empty())
+        check(cudaMemcpy(I.verts.p, verts.data(), sizeof(float) * verts.size(), cudaMemcpyHostToDevice), "verts");
+    if (!ints.empty())
+        check(cudaMemcpy(I.ints.p, ints.data(), sizeof(int) * ints.size(), cudaMemcpyHostToDevice), "ints");
+    check(cudaMemset(I.acc_sub.p, 0, I.acc_sub.bytes), "memset");
+    check(cudaMemset(I.acc_frame.p, 0, I.acc_frame.bytes), "memset");
+    check(cudaMemset(I.cnt_sub.p, 0, I.cnt_sub.bytes), "memset");
+    check(cudaMemset(I.cnt_frame.p, 0, I.cnt_frame.bytes), "memset");
+    // default pose table: one substep holding the current poses, no overrides
+    I.table_subs = 1;
+    I.pose_table.alloc(sizeof(DevPose) * ns);
+    I.pose_override.alloc(ns);
+    if (!poses.empty())
+        check(cudaMemcpy(I.pose_table.p, poses.data(), sizeof(DevPose) * poses.size(), cudaMemcpyHostToDevice), "table");
+    check(cudaMemset(I.pose_override.p, 0, ns), "memset");
+}
+
+void Engine::set_pose_table(int n_sub, const std::vector<DevPose>& poses,
+                            const std::vector<uint8_t>& ovr) {
+    Impl& I = *impl_;
+    if (I.n_shapes == 0) return;
+    const size_t np = static_cast<size_t>(n_sub) * I.n_shapes;
+    if (poses.size() != np || ovr.size() != np) throw std::invalid_argument("pose table size");
+    const size_t bytes = sizeof(DevPose) * np + np;
+    const int slot = I.pin_slot;
+    I.pin_slot ^= 1;
+    check(cudaEventSynchronize(I.pin_done[slot]), "pin wait");
+    I.pin_table[slot].alloc(bytes);
+    char* h = static_cast<char*>(I.pin_table[slot].p);
+    std::memcpy(h, poses.data(), sizeof(DevPose) * np);
+    std::memcpy(h + sizeof(DevPose) * np, ovr.data(), np);
+    if (n_sub > I.table_subs || !I.pose_table.p) {
+        check(cudaStreamSynchronize(I.st), "sync");
+        I.pose_table.alloc(sizeof(DevPose) * np);
+        I.pose_override.alloc(np);
+    }
+    I.table_subs = std::max(I.table_subs, n_sub);
+    check(cudaMemcpyAsync(I.pose_table.p, h, sizeof(DevPose) * np, cudaMemcpyHostToDevice, I.st), "table");
+    check(cudaMemcpyAsync(I.pose_override.p, h + sizeof(DevPose) * np, np, cudaMemcpyHostToDevice, I.st), "ovr");
+    check(cudaEventRecord(I.pin_done[slot], I.st), "record");
+}
+
+void Engine::set_free_pose(int shape, const DevPose& pose) {
+    Impl& I = *impl_;
+    check(cudaStreamSynchronize(I.st), "sync");
+    check(cudaMemcpy(I.free_pose.as<DevPose>() + shape, &pose, sizeof(DevPose), cudaMemcpyHostToDevice), "pose");
+}
+
+std::vector<DevPose> Engine::read_free_poses() {
+    Impl& I = *impl_;
+    std::vector<DevPose> out(I.n_shapes);
+    check(cudaStreamSynchronize(I.st), "sync");
+    if (I.n_shapes)
+        check(cudaMemcpy(out.data(), I.free_pose.p, sizeof(DevPose) * I.n_shapes, cudaMemcpyDeviceToHost), "poses");
+    return out;
+}
+
+// --------------------------------------------------------------- hot path
+void Engine::bin() {
+    Impl& I = *impl_;
+    if (I.n == 0) return;
+    auto ev = I.begin();
+    Params P = I.params();
+    float4* np[kPlanes];
+    for (int q = 0; q < kPlanes; ++q) np[q] = I.planes[1 - I.cur][q].as<float4>();
+    int64_t k = 0;
+    launch_bin(P, I.bb, np, I.n, I.st, &k);
+    I.counted(k);
+    I.cur = 1 - I.cur;
+    I.binned = true;
+    I.end(CAT_SORT, ev);
+}
+
+void Engine::p2g(bool mls, float dt) {
+    Impl& I = *impl_;
+    if (I.n == 0) return;
+    if (!I.binned) bin();
+    auto ev = I.begin();
+    cudaMemsetAsync(I.misc.p, 0, sizeof(uint32_t), I.st);  // active brick count
+    Params P = I.params();
+    P.dt = dt;
+    launch_p2g(P, mls, (I.n + 31) / 32, I.st);
+    I.counted(1);
+    if (mls) I.use_stress_in = false;  // consumed by the first MLS P2G
+    I.end(CAT_P2G, ev);
+}
+
+void Engine::grid_update(int sub, float dt, const float g[3], bool gravity, bool contact, int bc) {
+    Impl& I = *impl_;
+    if (I.n == 0) return;
+    auto ev = I.begin();
+    ++I.epoch;
+    if (I.epoch == 0xFFFFFFFFu) I.epoch = 1;
+    Params P = I.params();
+    P.sub = std::min(sub, I.table_subs - 1);
+    P.dt = dt;
+    P.g[0] = g[0]; P.g[1] = g[1]; P.g[2] = g[2];
+    P.gravity = gravity ? 1 : 0;
+    P.contact = contact ? 1 : 0;
+    P.bc = bc;
+    launch_grid_update(P, I.total_bricks, I.st);
+    I.counted(1);
+    I.end(CAT_GRID, ev);
+}
+
+void Engine::g2p_mls(int sub, float dt, bool pushout, bool deactivate) {
+    Impl& I = *impl_;
+    if (I.n == 0) return;
+    auto ev = I.begin();
+    Params P = I.params();
+    P.sub = std::min(sub, I.table_subs - 1);
+    P.dt = dt;
+    P.pushout = pushout ? 1 : 0;
+    P.deactivate = deactivate ? 1 : 0;
+    P.commit = 1;
+    launch_g2p(P, false, (I.n + 31) / 32, I.st);
+    I.counted(1);
+    I.end(CAT_G2P, ev);
+}
+
+void Engine::g2p_pb(int sub, float dt, bool commit, bool pushout, bool deactivate) {
+    Impl& I = *impl_;
+    if (I.n == 0) return;
+    auto ev = I.begin();
+    Params P = I.params();
+    P.sub = std::min(sub, I.table_subs - 1);
+    P.dt = dt;
+    P.commit = commit ? 1 : 0;
+    P.pushout = pushout ? 1 : 0;
+    P.deactivate = deactivate ? 1 : 0;
+    launch_g2p(P, true, (I.n + 31) / 32, I.st);
+    I.counted(1);
+    I.end(CAT_G2P, ev);
+}
+
+void Engine::free_bodies(int sub, float dt, const float g[3], bool integrate, bool merge) {
+    Impl& I = *impl_;
+    if (I.n_shapes == 0) return;
+    auto ev = I.begin();
+    Params P = I.params();
+    P.sub = std::min(sub, I.table_subs - 1);
+    P.dt = dt;
+    P.g[0] = g[0]; P.g[1] = g[1]; P.g[2] = g[2];
+    launch_free_bodies(P, integrate, merge, I.st);
+    I.counted(1);
+    I.end(CAT_OTHER, ev);
+}
+
+void Engine::bc_pass(int bc) {
+    Impl& I = *impl_;
+    if (I.n == 0) return;
+    Params P = I.params();
+    P.bc = bc;
+    launch_grid_bc(P, I.total_bricks, I.st);
+    I.counted(1);
+}
+
+void Engine::materialize_stress() {
+    Impl& I = *impl_;
+    if (I.n == 0 || I.use_stress_in) return;
+    I.stress_in.alloc(36 * static_cast<size_t>(I.n));
+    Params P = I.params();
+    launch_stress(P, I.stress_in.as<float>(), I.st);
+    I.counted(1);
+    I.use_stress_in = true;
+}
+
+void Engine::pushout(int sub) {
+    Impl& I = *impl_;
+    if (I.n == 0 || I.n_shapes == 0) return;
+    Params P = I.params();
+    P.sub = std::min(sub, I.table_subs - 1);
+    launch_pushout(P, I.st);
+    I.counted(1);
+}
+
+void Engine::deactivate() {
+    Impl& I = *impl_;
+    if (I.n == 0) return;
+    Params P = I.params();
+    launch_deactivate(P, I.st);
+    I.counted(1);
+}
+
+// ---------------------------------------------------------------- results
+void Engine::reset_counters() {
+    Impl& I = *impl_;
+    check(cudaMemsetAsync(I.counters.p, 0, I.counters.bytes, I.st), "memset");
+}
+
+void Engine::reset_contact(bool frame, bool sub) {
+    Impl& I = *impl_;
+    if (sub) {
+        check(cudaMemsetAsync(I.acc_sub.p, 0, I.acc_sub.bytes, I.st), "memset");
+        check(cudaMemsetAsync(I.cnt_sub.p, 0, I.cnt_sub.bytes, I.st), "memset");
+    }
+    if (frame) {
+        check(cudaMemsetAsync(I.acc_frame.p, 0, I.acc_frame.bytes, I.st), "memset");
+        check(cudaMemsetAsync(I.cnt_frame.p, 0, I.cnt_frame.bytes, I.st), "memset");
+    }
+}
+
+std::vector<SceneCounters> Engine::read_counters() {
+    Impl& I = *impl_;
+    std::vector<SceneCounters> out(I.hs.size());
+    check(cudaMemcpyAsync(out.data(), I.counters.p, sizeof(SceneCounters) * out.size(),
+                          cudaMemcpyDeviceToHost, I.st), "d2h");
+    check(cudaStreamSynchronize(I.st), "sync");
+    return out;
+}
+
+void Engine::read_contact(int which, std::vector<double>& imp, std::vector<double>& tq,
+                          std::vector<int32_t>& cnt) {
+    Impl& I = *impl_;
+    const int ns = I.n_shapes;
+    std::vector<double> buf(6 * std::max(ns, 1));
+    cnt.assign(ns, 0);
+    imp.assign(3 * ns, 0.0);
+    tq.assign(3 * ns, 0.0);
+    if (ns == 0) return;
+    check(cudaMemcpyAsync(buf.data(), which ? I.acc_frame.p : I.acc_sub.p, sizeof(double) * 6 * ns,
+                          cudaMemcpyDeviceToHost, I.st), "d2h");
+    check(cudaMemcpyAsync(cnt.data(), which ? I.cnt_frame.p : I.cnt_sub.p, sizeof(int) * ns,
+                          cudaMemcpyDeviceToHost, I.st), "d2h");
+    check(cudaStreamSynchronize(I.st), "sync");
+    for (int i = 0; i < ns; ++i)
+        for (int a = 0; a < 3; ++a) {
+            imp[3 * i + a] = buf[6 * i + a];
+            tq[3 * i + a] = buf[6 * i + 3 + a];
+        }
+}
+
+void Engine::snapshot(float* x, float* v, uint8_t* active, std::vector<double>& totals) {
+    Impl& I = *impl_;
+    const size_t N = static_cast<size_t>(std::max<int64_t>(I.n, 1));
+    const size_t S = I.hs.size();
+    I.io_tot.alloc(sizeof(double) * 5 * std::max<size_t>(S, 1));
+    check(cudaMemsetAsync(I.io_tot.p, 0, I.io_tot.bytes, I.st), "memset");
+    Params P = I.params();
+    if (I.n > 0) {
+        IoArrays io{};
+        if (x) { I.io_x.alloc(12 * N); io.x = I.io_x.as<float>(); }
+        if (v) { I.io_v.alloc(12 * N); io.v = I.io_v.as<float>(); }
+        if (active) { I.io_a.alloc(N); io.active = I.io_a.as<uint8_t>(); }
+        launch_download(P, io, I.st);
+        launch_totals(P, I.io_tot.as<double>(), I.st);
+        I.counted(2);
+        if (x) check(cudaMemcpyAsync(x, I.io_x.p, 12 * I.n, cudaMemcpyDeviceToHost, I.st), "d2h");
+        if (v) check(cudaMemcpyAsync(v, I.io_v.p, 12 * I.n, cudaMemcpyDeviceToHost, I.st), "d2h");
+        if (active) check(cudaMemcpyAsync(active, I.io_a.p, I.n, cudaMemcpyDeviceToHost, I.st), "d2h");
+    }
+    totals.assign(5 * S, 0.0);
+    check(cudaMemcpyAsync(totals.data(), I.io_tot.p, sizeof(double) * 5 * S, cudaMemcpyDeviceToHost, I.st), "d2h");
+    check(cudaStreamSynchronize(I.st), "snapshot");
+}
+
+void Engine::download_grid(int scene, float* mass, float* mom, float* vel) {
+    Impl& I = *impl_;
+    const DevScene& S = I.hs[scene];
+    const size_t nn = static_cast<size_t>(S.dims[0]) * S.dims[1] * S.dims[2];
+    DevBuf dm, dp, dv;
+    dm.alloc(4 * nn); dp.alloc(12 * nn); dv.alloc(12 * nn);
+    Params P = I.params();
+    launch_grid_download(P, scene, S, dm.as<float>(), dp.as<float>(), dv.as<float>(), I.st);
+    I.counted(1);
+    if (mass) check(cudaMemcpyAsync(mass, dm.p, 4 * nn, cudaMemcpyDeviceToHost, I.st), "d2h");
+    if (mom) check(cudaMemcpyAsync(mom, dp.p, 12 * nn, cudaMemcpyDeviceToHost, I.st), "d2h");
+    if (vel) check(cudaMemcpyAsync(vel, dv.p, 12 * nn, cudaMemcpyDeviceToHost, I.st), "d2h");
+    check(cudaStreamSynchronize(I.st), "grid");
+}
+
+void Engine::upload_grid_velocity(int scene, const float* mass, const float* mom, const float* vel) {
+    Impl& I = *impl_;
+    const DevScene& S = I.hs[scene];
+    const size_t nn = static_cast<size_t>(S.dims[0]) * S.dims[1] * S.dims[2];
+    DevBuf dm, dp, dv;
+    dm.alloc(4 * nn); dp.alloc(12 * nn); dv.alloc(12 * nn);
+    check(cudaMemcpyAsync(dm.p, mass, 4 * nn, cudaMemcpyHostToDevice, I.st), "h2d");
+    check(cudaMemcpyAsync(dp.p, mom, 12 * nn, cudaMemcpyHostToDevice, I.st), "h2d");
+    check(cudaMemcpyAsync(dv.p, vel, 12 * nn, cudaMemcpyHostToDevice, I.st), "h2d");
+    Params P = I.params();
+    launch_grid_upload(P, scene, S, dm.as<float>(), dp.as<float>(), dv.as<float>(), I.st);
+    I.counted(1);
+    check(cudaStreamSynchronize(I.st), "grid");
+}
+
+void Engine::read_binning(uint32_t* keys, uint32_t* perm) {
+    Impl& I = *impl_;
+    if (I.n == 0) return;
+    const size_t N = static_cast<size_t>(I.n);
+    DevBuf kbo;
+    kbo.alloc(4 * N);
+    I.bb.key_by_orig = kbo.as<uint32_t>();
+    bin();
+    I.bb.key_by_orig = nullptr;
+    if (keys) check(cudaMemcpyAsync(keys, kbo.p, 4 * N, cudaMemcpyDeviceToHost, I.st), "d2h");
+    if (perm) check(cudaMemcpyAsync(perm, I.s_orig.p, 4 * N, cudaMemcpyDeviceToHost, I.st), "d2h");
+    check(cudaStreamSynchronize(I.st), "binning");
+}
+
+int64_t Engine::n_active_sorted() {
+    Impl& I = *impl_;
+    uint32_t c[3] = {0, 0, 0};
+    check(cudaMemcpyAsync(c, I.b_counts.p, 12, cudaMemcpyDeviceToHost, I.st), "d2h");
+    check(cudaStreamSynchronize(I.st), "sync");
+    return c[2];
+}
+
+void Engine::synchronize() { check(cudaStreamSynchronize(impl_->st), "synchronize"); }
+
+}  // namespace mpmb

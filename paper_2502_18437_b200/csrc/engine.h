@@ -1,0 +1,133 @@
+// engine.h — device engine of the B200 MPM hot path (host-side interface).
+//
+// One Engine holds a BATCH of independent scenes (1 for a plain Scene / SimState)
+// resident in HBM and advances all of them with one launch per kernel:
+//   particles  : 7 float4 planes per particle slot (112 B), cell-sorted, laid out
+//                warp-interleaved by chunk
+//   grid       : per-scene dense virtual grid in 4x4x4-node bricks (float4 nodes),
+//                only bricks touched by P2G are updated/cleared
+//   shapes     : flattened shape table + per-substep pose table + free-body poses
+// Every public method enqueues on the engine's stream; only the explicit download /
+// read_* methods synchronise.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/mpm_b200.h"
+#include "dev_types.h"
+
+namespace mpmb {
+
+struct SceneGrid {
+    int dims[3];
+    float dx;
+    float origin[3];
+};
+
+struct EngineShape {            // host copy of one shape (per scene, in order)
+    DevShape d;
+    DevPose pose;               // current pose (kinematic / fixed / initial free)
+    std::vector<float> verts;   // local-frame vertices (3 floats each)
+    std::vector<int> indices;
+    std::vector<int> spine;
+};
+
+struct SceneCounters {          // per scene, summed since reset_counters()
+    int32_t inverted_f;
+    int32_t projection_failures;
+    int32_t pushed_out;
+    int32_t deactivated;
+};
+
+struct KernelTimes {
+    double ms_sort = 0, ms_p2g = 0, ms_grid = 0, ms_g2p = 0, ms_other = 0;
+    int64_t launches = 0;
+};
+
+class Engine {
+  public:
+    explicit Engine(const std::vector<SceneGrid>& scenes);
+    ~Engine();
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+
+    int n_scenes() const { return static_cast<int>(scenes_.size()); }
+    int64_t n_particles() const { return n_total_; }
+    const SceneGrid& grid(int s) const { return scenes_[s]; }
+
+    void set_stream(void* stream);
+    void* stream() const { return stream_; }
+    void set_profiling(bool on);
+    KernelTimes kernel_times() const;
+    void reset_kernel_times();
+
+    // Global material table (deduplicated across scenes by the caller).
+    void set_materials(const std::vector<mpmb_material>& mats);
+    // Particles in ORIGINAL order (scene ranges concatenated); stress may be null.
+    void upload_particles(int64_t n, const float* x, const float* v, const float* mass,
+                          const float* vol0, const float* F, const float* C, const float* stress,
+                          const int32_t* material, const uint8_t* active, const int32_t* scene);
+    // Synchronous download in original order (null pointers skipped).
+    void download_particles(int64_t begin, int64_t count, float* x, float* v, float* mass,
+                            float* vol0, float* F, float* C, float* stress, int32_t* material,
+                            uint8_t* active);
+    // Shapes of all scenes: shapes[s] in order.  Resets free-body poses and accumulators.
+    void set_shapes(const std::vector<std::vector<EngineShape>>& shapes);
+    int n_shapes() const { return n_shapes_; }
+    // Pose table for the next frame: poses[sub * n_shapes + i], override mask
+    // (1 = use the table pose even for a free body).  Copied asynchronously.
+    void set_pose_table(int n_sub, const std::vector<DevPose>& poses,
+                        const std::vector<uint8_t>& override_mask);
+    // Overwrite the device pose of free-body shape i (pose-target consumption).
+    void set_free_pose(int shape, const DevPose& pose);
+    std::vector<DevPose> read_free_poses();
+
+    // ---- hot path (enqueue only) ----
+    void bin();                                   // K1: keys, sort, chunks, gather
+    void p2g(bool mls, float dt);                 // K2 / K5
+    void grid_update(int sub, float dt, const float g[3], bool gravity, bool contact, int bc);
+    void g2p_mls(int sub, float dt, bool pushout, bool deactivate);   // K4
+    void g2p_pb(int sub, float dt, bool commit, bool pushout, bool deactivate);  // K6
+    void free_bodies(int sub, float dt, const float g[3], bool integrate, bool merge);  // K7
+    void bc_pass(int bc);                         // BC alone (hook adapter)
+    void materialize_stress();                    // sigma(F) -> cached stress array
+    void pushout(int sub);
+    void deactivate();
+
+    // ---- results ----
+    void reset_counters();
+    void reset_contact(bool frame, bool sub);
+    std::vector<SceneCounters> read_counters();
+    // contact accumulators (per shape, double): which = 0 substep, 1 frame
+    void read_contact(int which, std::vector<double>& impulse, std::vector<double>& torque,
+                      std::vector<int32_t>& count);
+    // FrameResult snapshot for all scenes: positions/velocities/active in original order
+    // (device -> pinned host), totals per scene (double).  Enqueue + wait.
+    void snapshot(float* x, float* v, uint8_t* active, std::vector<double>& totals /*5 per scene*/);
+    // dense grid of one scene (node-major i + nx*(j + ny*k)); for tests and the hook adapter
+    void download_grid(int scene, float* mass, float* momentum, float* velocity);
+    void upload_grid_velocity(int scene, const float* mass, const float* momentum,
+                              const float* velocity);
+    // keys/perm of the binning stage (original indices), see mpmb_bin_particles
+    void read_binning(uint32_t* keys, uint32_t* perm);
+    int64_t n_active_sorted();
+
+    void synchronize();
+    int64_t launches() const { return launches_total_; }
+
+  private:
+    struct Impl;
+    Impl* impl_;
+    std::vector<SceneGrid> scenes_;
+    int64_t n_total_ = 0;
+    int n_shapes_ = 0;
+    void* stream_ = nullptr;
+    int64_t launches_total_ = 0;
+};
+
+// Process-wide launch counter (all engines).
+int64_t global_launch_count();
+bool device_available();
+
+}  // namespace mpmb

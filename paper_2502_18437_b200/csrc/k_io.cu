@@ -1,0 +1,194 @@
+// k_io.cu — boundary kernels: original-order upload/download of the ParticleStore
+// (state.hpp:65-90), FrameResult totals (scene.hpp:251-266), dense grid export/import
+// for the GridHook adapter (solvers.hpp:19, 63).
+#include <cuda_runtime.h>
+
+#include "launch.h"
+
+namespace mpmb {
+
+static int blocks_for(int64_t n, int threads, int cap) {
+    int64_t b = (n + threads - 1) / threads;
+    if (b < 1) b = 1;
+    if (b > cap) b = cap;
+    return static_cast<int>(b);
+}
+
+// Slot = original index (the layout before the first binning).
+__global__ void k_upload(const Params P, IoArrays in, int64_t n) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        Part p;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            p.x[a] = in.x[3 * i + a];
+            p.v[a] = in.v[3 * i + a];
+        }
+#pragma unroll
+        for (int a = 0; a < 9; ++a) {
+            p.F[a] = in.F[9 * i + a];
+            p.C[a] = in.C[9 * i + a];
+        }
+        store_part(P, static_cast<uint32_t>(i), p);
+        uint32_t flags = (static_cast<uint32_t>(in.mat[i]) & kMatMask) |
+                         ((static_cast<uint32_t>(in.scene[i]) & kSceneMask) << kSceneShift);
+        if (in.active[i]) flags |= kActiveBit;
+        P.pl[PR][i] = make_float4(in.mass[i], in.vol0[i], __uint_as_float(flags),
+                                  __uint_as_float(static_cast<uint32_t>(i)));
+    }
+}
+
+__global__ void k_download(const Params P, IoArrays out) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < P.n_total; s += stride) {
+        const float4 r = P.pl[PR][s];
+        const uint32_t flags = __float_as_uint(r.z);
+        const uint64_t o = __float_as_uint(r.w);
+        Part p;
+        load_part(P, static_cast<uint32_t>(s), p);
+        if (out.x) for (int a = 0; a < 3; ++a) out.x[3 * o + a] = p.x[a];
+        if (out.v) for (int a = 0; a < 3; ++a) out.v[3 * o + a] = p.v[a];
+        if (out.F) for (int a = 0; a < 9; ++a) out.F[9 * o + a] = p.F[a];
+        if (out.C) for (int a = 0; a < 9; ++a) out.C[9 * o + a] = p.C[a];
+        if (out.mass) out.mass[o] = r.x;
+        if (out.vol0) out.vol0[o] = r.y;
+        if (out.mat) out.mat[o] = static_cast<int32_t>(flags & kMatMask);
+        if (out.active) out.active[o] = (flags & kActiveBit) ? 1 : 0;
+        if (out.scene) out.scene[o] = static_cast<int32_t>((flags >> kSceneShift) & kSceneMask);
+    }
+}
+
+// Per-scene double totals: mass, momentum[3], kinetic energy (scene.hpp:258-266).
+__global__ void k_totals(const Params P, double* totals) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < P.n_total; base += stride) {
+        const int64_t s = base + threadIdx.x;
+        double t[5] = {0, 0, 0, 0, 0};
+        int scene = -1;
+        if (s < P.n_total) {
+            const float4 r = P.pl[PR][s];
+            const uint32_t flags = __float_as_uint(r.z);
+            if (flags & kActiveBit) {
+                scene = static_cast<int>((flags >> kSceneShift) & kSceneMask);
+                const float4 a = P.pl[0][s], b = P.pl[1][s];
+                const double m = r.x;
+                const float vx = a.w, vy = b.x, vz = b.y;
+                t[0] = m;
+                t[1] = m * vx;
+                t[2] = m * vy;
+                t[3] = m * vz;
+                t[4] = 0.5 * m * static_cast<double>(vx * vx + vy * vy + vz * vz);
+            }
+        }
+        const unsigned has = __ballot_sync(full, scene >= 0);
+        if (!has) continue;
+        const int lead = __ffs(has) - 1;
+        const int s0 = __shfl_sync(full, scene, lead);
+        if (__all_sync(full, scene < 0 || scene == s0)) {
+#pragma unroll
+            for (int q = 0; q < 5; ++q)
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) t[q] += __shfl_xor_sync(full, t[q], o);
+            if (lane == lead)
+                for (int q = 0; q < 5; ++q) atomicAdd(&totals[5 * s0 + q], t[q]);
+        } else if (scene >= 0) {
+            for (int q = 0; q < 5; ++q) atomicAdd(&totals[5 * scene + q], t[q]);
+        }
+    }
+}
+
+// sigma(F) into an original-order array (materialises the cached stress, solvers.hpp:69-74).
+__global__ void k_stress(const Params P, float* out) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < P.n_total; s += stride) {
+        const float4 r = P.pl[PR][s];
+        const uint32_t flags = __float_as_uint(r.z);
+        const uint64_t o = __float_as_uint(r.w);
+        if (P.use_stress_in) {
+            for (int a = 0; a < 9; ++a) out[9 * o + a] = P.stress_in[9 * o + a];
+            continue;
+        }
+        Part p;
+        load_part(P, static_cast<uint32_t>(s), p);
+        const float4 mat = P.mats[flags & kMatMask];
+        float sig[9];
+        neo_hookean(p.F, mat.y, mat.z, sig);
+        for (int a = 0; a < 9; ++a) out[9 * o + a] = sig[a];
+    }
+}
+
+// Dense node-major export of one scene's grid after the last update: nodes of bricks
+// updated in the current epoch carry {mass, velocity} (or {mass, momentum} below eps).
+__global__ void k_grid_download(const Params P, DevScene S, int64_t n_nodes, float* mass,
+                                float* mom, float* vel) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < n_nodes; q += stride) {
+        const int i = static_cast<int>(q % S.dims[0]);
+        const int j = static_cast<int>((q / S.dims[0]) % S.dims[1]);
+        const int k = static_cast<int>(q / (static_cast<int64_t>(S.dims[0]) * S.dims[1]));
+        const uint32_t local = ((k >> 2) * S.nb[1] + (j >> 2)) * S.nb[0] + (i >> 2);
+        const uint32_t gb = S.brick_base + local;
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (P.brick_stamp[gb] == P.epoch)
+            a = P.grid_vel[S.node_base + static_cast<uint64_t>(local) * kBrickNodes +
+                           ((k & 3) << 4) + ((j & 3) << 2) + (i & 3)];
+        const bool live = a.x > kMassEps;
+        if (mass) mass[q] = a.x;
+        if (vel) {
+            vel[3 * q + 0] = live ? a.y : 0.f;
+            vel[3 * q + 1] = live ? a.z : 0.f;
+            vel[3 * q + 2] = live ? a.w : 0.f;
+        }
+        if (mom) {  // solvers.hpp:48, 61: momentum = velocity * mass after the update
+            mom[3 * q + 0] = live ? a.y * a.x : a.y;
+            mom[3 * q + 1] = live ? a.z * a.x : a.z;
+            mom[3 * q + 2] = live ? a.w * a.x : a.w;
+        }
+    }
+}
+
+__global__ void k_grid_upload(const Params P, DevScene S, int64_t n_nodes, const float* mass,
+                              const float* mom, const float* vel) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < n_nodes; q += stride) {
+        const int i = static_cast<int>(q % S.dims[0]);
+        const int j = static_cast<int>((q / S.dims[0]) % S.dims[1]);
+        const int k = static_cast<int>(q / (static_cast<int64_t>(S.dims[0]) * S.dims[1]));
+        const uint32_t local = ((k >> 2) * S.nb[1] + (j >> 2)) * S.nb[0] + (i >> 2);
+        const uint32_t gb = S.brick_base + local;
+        if (P.brick_stamp[gb] != P.epoch) continue;
+        const float m = mass[q];
+        const bool live = m > kMassEps;
+        P.grid_vel[S.node_base + static_cast<uint64_t>(local) * kBrickNodes + ((k & 3) << 4) +
+                   ((j & 3) << 2) + (i & 3)] =
+            live ? make_float4(m, vel[3 * q], vel[3 * q + 1], vel[3 * q + 2])
+                 : make_float4(m, mom[3 * q], mom[3 * q + 1], mom[3 * q + 2]);
+    }
+}
+
+void launch_upload(const Params& P, const IoArrays& in, int64_t n, cudaStream_t st) {
+    k_upload<<<blocks_for(n, 256, 148 * 16), 256, 0, st>>>(P, in, n);
+}
+void launch_download(const Params& P, const IoArrays& out, cudaStream_t st) {
+    k_download<<<blocks_for(P.n_total, 256, 148 * 16), 256, 0, st>>>(P, out);
+}
+void launch_totals(const Params& P, double* totals, cudaStream_t st) {
+    k_totals<<<blocks_for(P.n_total, 256, 148 * 16), 256, 0, st>>>(P, totals);
+}
+void launch_stress(const Params& P, float* stress_orig, cudaStream_t st) {
+    k_stress<<<blocks_for(P.n_total, 256, 148 * 16), 256, 0, st>>>(P, stress_orig);
+}
+void launch_grid_download(const Params& P, int, const DevScene& S, float* mass, float* mom,
+                          float* vel, cudaStream_t st) {
+    const int64_t n = static_cast<int64_t>(S.dims[0]) * S.dims[1] * S.dims[2];
+    k_grid_download<<<blocks_for(n, 256, 148 * 16), 256, 0, st>>>(P, S, n, mass, mom, vel);
+}
+void launch_grid_upload(const Params& P, int, const DevScene& S, const float* mass,
+                        const float* mom, const float* vel, cudaStream_t st) {
+    const int64_t n = static_cast<int64_t>(S.dims[0]) * S.dims[1] * S.dims[2];
+    k_grid_upload<<<blocks_for(n, 256, 148 * 16), 256, 0, st>>>(P, S, n, mass, mom, vel);
+}
+
+}  // namespace mpmb

@@ -1,0 +1,321 @@
+// k_sort.cu — K1: particle binning / stable sort by (brick, cell, original index) and the
+// warp-interleaved chunk layout consumed by P2G/G2P.  No reference function exists for
+// this stage (the reference transfers in particle-index order, solvers.hpp:151); the
+// key arithmetic is the reference's stencil base (math.hpp:219-223, bit-exact).
+//
+// Pipeline (all on device, no host round trip):
+//   keys      bucket = brick of the stencil base, warp-aggregated rank in the bucket
+//   scan      bucket offsets (exclusive scan; the inactive bucket is last)
+//   scatter   entries to their bucket
+//   local     per bucket: counting sort by cell (64 bins) + rank by original index in
+//             the cell -> (brick, cell, original index) order, rank-in-cell
+//   chunks    chunk = run of <= KMAX particles of one cell; chunk starts by scan
+//   gather    physical permutation of the 7 planes into the chunk-interleaved layout
+#include <cuda_runtime.h>
+
+#include "launch.h"
+
+namespace mpmb {
+
+// ------------------------------------------------------------------- scan
+constexpr int kScanThreads = 512;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t& total) {
+    constexpr int NW = kScanThreads / 32;
+    __shared__ uint32_t warp_tot[NW + 1];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) warp_tot[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        const uint32_t w = lane < NW ? warp_tot[lane] : 0u;
+        uint32_t wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += t;
+        }
+        if (lane < NW) warp_tot[lane] = wi - w;
+        if (lane == NW - 1) warp_tot[NW] = wi;
+    }
+    __syncthreads();
+    const uint32_t excl = warp_tot[wid] + inc - v;
+    total = warp_tot[NW];
+    __syncthreads();
+    return excl;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const uint32_t* in, int64_t n,
+                                                              uint32_t* sums) {
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile + threadIdx.x * kScanItems;
+    uint32_t s = 0;
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i)
+        if (base + i < n) s += in[base + i];
+    uint32_t total;
+    block_exclusive_scan(s, total);
+    if (threadIdx.x == 0) sums[blockIdx.x] = total;
+}
+
+// single block: exclusive scan of the tile sums in place
+__global__ void __launch_bounds__(kScanThreads) k_scan_sums(uint32_t* sums, int n) {
+    uint32_t carry = 0;
+    for (int base = 0; base < n; base += kScanThreads) {
+        const int i = base + threadIdx.x;
+        const uint32_t v = i < n ? sums[i] : 0u;
+        uint32_t total;
+        const uint32_t e = block_exclusive_scan(v, total);
+        if (i < n) sums[i] = carry + e;
+        carry += total;
+    }
+    if (threadIdx.x == 0) sums[n] = carry;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_down(const uint32_t* in, int64_t n,
+                                                            const uint32_t* sums, uint32_t* out,
+                                                            int n_tiles) {
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile + threadIdx.x * kScanItems;
+    uint32_t vals[kScanItems];
+    uint32_t s = 0;
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+        vals[i] = base + i < n ? in[base + i] : 0u;
+        s += vals[i];
+    }
+    uint32_t total;
+    uint32_t e = block_exclusive_scan(s, total) + sums[blockIdx.x];
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+        if (base + i < n) out[base + i] = e;
+        e += vals[i];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) out[n] = sums[n_tiles];
+}
+
+void launch_exclusive_scan(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* tmp,
+                           cudaStream_t st, int64_t* launches) {
+    const int tiles = static_cast<int>((n + kScanTile - 1) / kScanTile);
+    const int t = tiles > 0 ? tiles : 1;
+    k_scan_reduce<<<t, kScanThreads, 0, st>>>(in, n, tmp);
+    k_scan_sums<<<1, kScanThreads, 0, st>>>(tmp, t);
+    k_scan_down<<<t, kScanThreads, 0, st>>>(in, n, tmp, out, t);
+    *launches += 3;
+}
+
+// ------------------------------------------------------------------- keys
+__global__ void __launch_bounds__(256) k_bin_keys(const Params P, BinBuffers B) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < P.n_total; base += stride) {
+        const int64_t s = base + threadIdx.x;
+        const bool valid = s < P.n_total;
+        uint32_t bucket = 0xFFFFFFFFu, cell = 0, orig = 0;
+        if (valid) {
+            const float4 r = P.pl[PR][s];
+            const uint32_t flags = __float_as_uint(r.z);
+            orig = __float_as_uint(r.w);
+            if (flags & kActiveBit) {
+                const int scene = static_cast<int>((flags >> kSceneShift) & kSceneMask);
+                const DevScene& S = P.scenes[scene];
+                const float4 a = P.pl[0][s];
+                const float x[3] = {a.x, a.y, a.z};
+                int b[3];
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    float fx;
+                    b[q] = stencil_base(x[q], S.origin[q], S.inv_dx, fx);
+                    b[q] = min(max(b[q], 0), S.dims[q] - 3);
+                }
+                const uint32_t local = (static_cast<uint32_t>(b[2] >> 2) * S.nb[1] +
+                                        static_cast<uint32_t>(b[1] >> 2)) * S.nb[0] +
+                                       static_cast<uint32_t>(b[0] >> 2);
+                bucket = S.brick_base + local;
+                cell = static_cast<uint32_t>(((b[2] & 3) << 4) | ((b[1] & 3) << 2) | (b[0] & 3));
+                if (B.key_by_orig) B.key_by_orig[orig] = (local << 6) | cell;
+            } else {
+                bucket = B.n_buckets - 1;
+                if (B.key_by_orig) B.key_by_orig[orig] = 0xFFFFFFFFu;
+            }
+        }
+        // warp-aggregated rank inside the bucket (sorted input: usually one bucket per warp)
+        const unsigned peers = __match_any_sync(full, bucket);
+        const int leader = __ffs(peers) - 1;
+        uint32_t start = 0;
+        if (valid && lane == leader) start = atomicAdd(&B.bucket_count[bucket], __popc(peers));
+        start = __shfl_sync(full, start, leader);
+        if (valid) {
+            B.key[s] = bucket;
+            B.rank[s] = start + __popc(peers & lanemask_lt());
+            B.cell[s] = static_cast<uint8_t>(cell);
+            B.orig[s] = orig;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_bin_scatter(BinBuffers B, int64_t n) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < n; s += stride) {
+        const uint32_t pos = B.bucket_off[B.key[s]] + B.rank[s];
+        B.e_orig[pos] = B.orig[s];
+        B.e_cell[pos] = B.cell[s];
+        B.e_src[pos] = static_cast<uint32_t>(s);
+    }
+}
+
+// One block per bucket (grid-stride): counting sort by cell, then rank by original index.
+__global__ void __launch_bounds__(256) k_bin_local(BinBuffers B) {
+    __shared__ uint32_t hist[64];
+    __shared__ uint32_t cstart[64];
+    const uint32_t inactive = B.n_buckets - 1;
+    for (uint32_t b = blockIdx.x; b < B.n_buckets; b += gridDim.x) {
+        const uint32_t beg = B.bucket_off[b], end = B.bucket_off[b + 1];
+        if (beg == end) continue;
+        if (b == inactive) {
+            for (uint32_t q = beg + threadIdx.x; q < end; q += blockDim.x) {
+                B.sorted_src[q] = B.e_src[q];
+                B.sorted_orig[q] = B.e_orig[q];
+                B.rank_in_cell[q] = 0u;
+            }
+            continue;
+        }
+        if (threadIdx.x < 64) hist[threadIdx.x] = 0u;
+        __syncthreads();
+        for (uint32_t q = beg + threadIdx.x; q < end; q += blockDim.x)
+            B.tmp[q] = atomicAdd(&hist[B.e_cell[q]], 1u);
+        __syncthreads();
+        if (threadIdx.x < 32) {  // exclusive scan of 64 bins by one warp
+            const uint32_t a = hist[2 * threadIdx.x], c = hist[2 * threadIdx.x + 1];
+            uint32_t inc = a + c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+                if (threadIdx.x >= o) inc += t;
+            }
+            const uint32_t ex = inc - a - c;
+            cstart[2 * threadIdx.x] = ex;
+            cstart[2 * threadIdx.x + 1] = ex + a;
+        }
+        __syncthreads();
+        for (uint32_t q = beg + threadIdx.x; q < end; q += blockDim.x) {
+            const uint32_t c = B.e_cell[q];
+            const uint32_t d = beg + cstart[c] + B.tmp[q];
+            B.g_orig[d] = B.e_orig[q];
+            B.g_src[d] = B.e_src[q];
+            B.g_cell[d] = static_cast<uint8_t>(c);
+        }
+        __syncthreads();
+        for (uint32_t q = beg + threadIdx.x; q < end; q += blockDim.x) {
+            const uint32_t c = B.g_cell[q];
+            const uint32_t o = B.g_orig[q];
+            const uint32_t lo = beg + cstart[c], hi = lo + hist[c];
+            uint32_t rk = 0;
+            for (uint32_t f = lo; f < hi; ++f) rk += B.g_orig[f] < o ? 1u : 0u;
+            B.sorted_src[lo + rk] = B.g_src[q];
+            B.sorted_orig[lo + rk] = o;
+            B.rank_in_cell[lo + rk] = rk;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(256) k_chunk_flags(BinBuffers B, int64_t n) {
+    const uint32_t n_active = B.bucket_off[B.n_buckets - 1];
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < n; q += stride)
+        B.tmp[q] = (q < n_active && (B.rank_in_cell[q] % KMAX) == 0u) ? 1u : 0u;
+}
+
+__global__ void __launch_bounds__(256) k_chunk_emit(BinBuffers B, int64_t n) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < n; q += stride)
+        if (B.tmp[q]) B.chunk_start[B.flag[q]] = static_cast<uint32_t>(q);
+}
+
+__global__ void __launch_bounds__(256) k_chunk_finalize(BinBuffers B, int64_t n) {
+    const uint32_t n_chunks = B.flag[n];
+    const uint32_t n_active = B.bucket_off[B.n_buckets - 1];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        B.counts[0] = n_chunks;
+        B.counts[1] = (n_chunks + 31u) / 32u;
+        B.counts[2] = n_active;
+    }
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; c < n_chunks; c += stride) {
+        const uint32_t st = B.chunk_start[c];
+        const uint32_t en = (c + 1 < n_chunks) ? B.chunk_start[c + 1] : n_active;
+        B.chunk_len[c] = static_cast<uint8_t>(en - st);
+        if ((c & 31) == 0) B.group_base[c >> 5] = st;
+    }
+}
+
+// Warp per group of 32 chunks: the k-th particles of the group's chunks become adjacent.
+__global__ void __launch_bounds__(256) k_group_gather(const Params P, BinBuffers B, int64_t n_total,
+                                                      float4* n0, float4* n1, float4* n2, float4* n3,
+                                                      float4* n4, float4* n5, float4* n6) {
+    float4* np[kPlanes] = {n0, n1, n2, n3, n4, n5, n6};
+    const uint32_t n_chunks = B.counts[0], n_groups = B.counts[1], n_active = B.counts[2];
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = lanemask_lt();
+    const uint32_t wpb = blockDim.x >> 5;
+    const uint32_t gw = blockIdx.x * wpb + (threadIdx.x >> 5), nw = gridDim.x * wpb;
+    for (uint32_t g = gw; g < n_groups; g += nw) {
+        const uint32_t c = g * 32u + lane;
+        const int len = c < n_chunks ? B.chunk_len[c] : 0;
+        const uint32_t st = c < n_chunks ? B.chunk_start[c] : 0u;
+        const uint32_t base = B.group_base[g];
+        uint32_t off = 0;
+        for (int k = 0; k < KMAX; ++k) {
+            const unsigned mask = __ballot_sync(0xffffffffu, len > k);
+            if (!mask) break;
+            if (len > k) {
+                const uint32_t src = B.sorted_src[st + k];
+                const uint32_t dst = base + off + __popc(mask & lt);
+#pragma unroll
+                for (int q = 0; q < kPlanes; ++q) np[q][dst] = P.pl[q][src];
+            }
+            off += __popc(mask);
+        }
+    }
+    // inactive tail keeps the bucket order
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t q = n_active + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < n_total; q += stride) {
+        const uint32_t src = B.sorted_src[q];
+#pragma unroll
+        for (int p = 0; p < kPlanes; ++p) np[p][q] = P.pl[p][src];
+    }
+}
+
+static int blocks_for(int64_t n, int threads, int cap) {
+    int64_t b = (n + threads - 1) / threads;
+    if (b < 1) b = 1;
+    if (b > cap) b = cap;
+    return static_cast<int>(b);
+}
+
+void launch_bin(const Params& P, const BinBuffers& B, float4* const new_planes[kPlanes],
+                int64_t n_total, cudaStream_t st, int64_t* launches) {
+    cudaMemsetAsync(B.bucket_count, 0, sizeof(uint32_t) * B.n_buckets, st);
+    const int cap = 148 * 16;
+    k_bin_keys<<<blocks_for(n_total, 256, cap), 256, 0, st>>>(P, B);
+    launch_exclusive_scan(B.bucket_count, B.bucket_off, B.n_buckets, B.scan_tmp, st, launches);
+    k_bin_scatter<<<blocks_for(n_total, 256, cap), 256, 0, st>>>(B, n_total);
+    k_bin_local<<<blocks_for(static_cast<int64_t>(B.n_buckets) * 256, 256, 148 * 8), 256, 0, st>>>(B);
+    k_chunk_flags<<<blocks_for(n_total, 256, cap), 256, 0, st>>>(B, n_total);
+    launch_exclusive_scan(B.tmp, B.flag, n_total, B.scan_tmp, st, launches);
+    k_chunk_emit<<<blocks_for(n_total, 256, cap), 256, 0, st>>>(B, n_total);
+    k_chunk_finalize<<<blocks_for(n_total, 256, cap), 256, 0, st>>>(B, n_total);
+    k_group_gather<<<blocks_for(n_total, 256, cap), 256, 0, st>>>(
+        P, B, n_total, new_planes[0], new_planes[1], new_planes[2], new_planes[3],
+        new_planes[4], new_planes[5], new_planes[6]);
+    *launches += 7;
+}
+
+}  // namespace mpmb

@@ -1,0 +1,144 @@
+// kernels.cuh — sm_100a kernels of the MPM hot path.  See DESIGN.md §3 for the data
+// layout and the roofline of each kernel.
+//
+//   K1 k_bin_*         binning / stable sort by (brick, cell, original index) and the
+//                      warp-interleaved chunk layout (NEW stage; keys from math.hpp:219-223)
+//   K2 k_p2g<true>     MLS P2G with the stress impulse (solvers.hpp:151-169)
+//   K5 k_p2g<false>    PB-MPM P2G (solvers.hpp:218-235)
+//   K3 k_grid_update   v = p/m (+g dt), contact pass over the scene's shapes in order,
+//                      per-shape impulse/torque reduction, BC (solvers.hpp:54-65, 30-50;
+//                      contact.hpp:97-136)
+//   K4 k_g2p_mls       G2P + F update (+ push-out, deactivation) (solvers.hpp:173-196,
+//                      contact.hpp:140-179, state.hpp:153-164)
+//   K6 k_g2p_pb        PB-MPM G2P + co-rotational projection (+ commit) (solvers.hpp:240-277)
+//   K7 k_free_bodies   free-body integration + accumulator merge (rigid_dynamics.hpp:82-103,
+//                      scene.hpp:220-232)
+#pragma once
+#include <climits>
+#include <cstdint>
+
+#include "dev_math.cuh"
+
+namespace mpmb {
+
+constexpr int KMAX = 8;  // max particles per chunk (one chunk = one cell's run)
+
+// Particle slot = 7 float4 planes (112 B):
+//   P0 {x.x, x.y, x.z, v.x}   P1 {v.y, v.z, C0, C1}   P2 {C2, C3, C4, C5}
+//   P3 {C6, C7, C8, F0}       P4 {F1, F2, F3, F4}     P5 {F5, F6, F7, F8}
+//   PR {mass, volume0, flags(u32), original index(u32)}
+constexpr int kPlanes = 7;
+constexpr int PR = 6;
+
+struct Params {
+    float4* pl[kPlanes];
+    const DevScene* scenes;
+    const DevShape* shapes;
+    const float* verts;
+    const int* ints;
+    const DevPose* pose_table;
+    const uint8_t* pose_override;
+    DevPose* free_pose;
+    int n_shapes;
+    const float4* mats;  // {kind, mu, lambda, beta}
+    float4* grid_acc;
+    float4* grid_vel;
+    uint32_t* brick_flag;
+    uint32_t* brick_stamp;
+    uint32_t* active_bricks;
+    uint32_t* n_active_bricks;
+    const uint32_t* brick_scene;
+    const uint32_t* group_base;
+    const uint8_t* chunk_len;
+    const uint32_t* n_chunks;
+    const uint32_t* n_groups;
+    const uint32_t* n_active;
+    int64_t n_total;
+    const float* stress_in;  // original-order uploaded sigma (first MLS P2G only)
+    int use_stress_in;
+    double* acc_sub;   // per shape: impulse[3], torque[3]
+    int* cnt_sub;      // per shape: contact node count
+    double* acc_frame;
+    int* cnt_frame;
+    int* counters;     // per scene: inverted, proj failures, pushed, deactivated
+    uint32_t epoch;
+    float dt;
+    float g[3];
+    int sub;
+    int gravity;
+    int contact;
+    int bc;
+    int pushout;
+    int deactivate;
+    int commit;
+};
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+struct Part {
+    float x[3], v[3], C[9], F[9];
+};
+
+__device__ __forceinline__ void load_part(const Params& P, uint32_t s, Part& p) {
+    float4 a = P.pl[0][s], b = P.pl[1][s], c = P.pl[2][s], d = P.pl[3][s], e = P.pl[4][s],
+           f = P.pl[5][s];
+    p.x[0] = a.x; p.x[1] = a.y; p.x[2] = a.z; p.v[0] = a.w;
+    p.v[1] = b.x; p.v[2] = b.y; p.C[0] = b.z; p.C[1] = b.w;
+    p.C[2] = c.x; p.C[3] = c.y; p.C[4] = c.z; p.C[5] = c.w;
+    p.C[6] = d.x; p.C[7] = d.y; p.C[8] = d.z; p.F[0] = d.w;
+    p.F[1] = e.x; p.F[2] = e.y; p.F[3] = e.z; p.F[4] = e.w;
+    p.F[5] = f.x; p.F[6] = f.y; p.F[7] = f.z; p.F[8] = f.w;
+}
+
+__device__ __forceinline__ void store_part(const Params& P, uint32_t s, const Part& p) {
+    P.pl[0][s] = make_float4(p.x[0], p.x[1], p.x[2], p.v[0]);
+    P.pl[1][s] = make_float4(p.v[1], p.v[2], p.C[0], p.C[1]);
+    P.pl[2][s] = make_float4(p.C[2], p.C[3], p.C[4], p.C[5]);
+    P.pl[3][s] = make_float4(p.C[6], p.C[7], p.C[8], p.F[0]);
+    P.pl[4][s] = make_float4(p.F[1], p.F[2], p.F[3], p.F[4]);
+    P.pl[5][s] = make_float4(p.F[5], p.F[6], p.F[7], p.F[8]);
+}
+
+__device__ __forceinline__ const DevPose& pose_of(const Params& P, int i) {
+    const int t = P.sub * P.n_shapes + i;
+    return (P.shapes[i].motion == MOTION_FREE && !P.pose_override[t]) ? P.free_pose[i]
+                                                                         : P.pose_table[t];
+}
+
+// Offsets of the bricked node layout along each axis for stencil base b:
+// node index = tz[dk] + ty[dj] + tx[di] within the scene's node pool.
+__device__ __forceinline__ void node_offsets(const DevScene& S, const int b[3], uint32_t tx[3],
+                                             uint32_t ty[3], uint32_t tz[3]) {
+    const uint32_t sy = static_cast<uint32_t>(S.nb[0]) * kBrickNodes;
+    const uint32_t sz = sy * static_cast<uint32_t>(S.nb[1]);
+#pragma unroll
+    for (int o = 0; o < 3; ++o) {
+        const uint32_t ix = b[0] + o, iy = b[1] + o, iz = b[2] + o;
+        tx[o] = (ix >> 2) * kBrickNodes + (ix & 3u);
+        ty[o] = (iy >> 2) * sy + (iy & 3u) * 4u;
+        tz[o] = (iz >> 2) * sz + (iz & 3u) * 16u;
+    }
+}
+
+// Warp-aggregated per-scene counter add; must be called by all 32 lanes.  Lanes of a
+// warp almost always share one scene: one atomic per warp, per-lane atomics otherwise.
+__device__ __forceinline__ void add_scene_counter(int* counters, int scene, int slot, int value) {
+    const unsigned full = 0xffffffffu;
+    const unsigned has = __ballot_sync(full, value != 0);
+    if (has == 0) return;
+    const int lead = __ffs(has) - 1;
+    const int s0 = __shfl_sync(full, scene, lead);
+    const bool uniform = __all_sync(full, value == 0 || scene == s0);
+    if (uniform) {
+        const int total = __reduce_add_sync(full, value);
+        if ((threadIdx.x & 31) == lead) atomicAdd(&counters[4 * s0 + slot], total);
+    } else if (value != 0) {
+        atomicAdd(&counters[4 * scene + slot], value);
+    }
+}
+
+}  // namespace mpmb

@@ -1,0 +1,67 @@
+// launch.h — host launchers of the kernels (one translation unit per kernel family).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.cuh"
+
+namespace mpmb {
+
+// ---- K1 binning (k_sort.cu) ----
+struct BinBuffers {
+    uint32_t n_buckets;        // bricks of all scenes + 1 (inactive bucket last)
+    uint32_t* bucket_count;    // [n_buckets]
+    uint32_t* bucket_off;      // [n_buckets + 1]
+    uint32_t* key;             // per slot: bucket
+    uint32_t* rank;            // per slot: rank inside bucket (atomic order)
+    uint8_t* cell;             // per slot: cell inside brick (6 bits)
+    uint32_t* orig;            // per slot: original index
+    uint32_t* e_orig;          // bucketed entries
+    uint8_t* e_cell;
+    uint32_t* e_src;
+    uint32_t* tmp;             // scratch (per slot)
+    uint32_t* g_orig;          // grouped by cell
+    uint32_t* g_src;
+    uint8_t* g_cell;
+    uint32_t* sorted_src;      // final sorted position -> old slot
+    uint32_t* sorted_orig;     // final sorted position -> original index
+    uint32_t* rank_in_cell;
+    uint32_t* flag;            // chunk-start flags, then their exclusive scan (n+1)
+    uint32_t* chunk_start;     // [n_chunks]
+    uint8_t* chunk_len;
+    uint32_t* group_base;
+    uint32_t* counts;          // [0] n_chunks, [1] n_groups, [2] n_active
+    uint32_t* scan_tmp;        // block sums for the scans
+    uint32_t* key_by_orig;     // optional (binning readback), may be null
+};
+
+void launch_bin(const Params& P, const BinBuffers& B, float4* const new_planes[kPlanes],
+                int64_t n_total, cudaStream_t st, int64_t* launches);
+void launch_exclusive_scan(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* tmp,
+                           cudaStream_t st, int64_t* launches);
+
+// ---- K2..K7 (k_step.cu) ----
+void launch_p2g(const Params& P, bool mls, int64_t max_groups, cudaStream_t st);
+void launch_grid_update(const Params& P, int64_t max_bricks, cudaStream_t st);
+void launch_g2p(const Params& P, bool pb, int64_t max_groups, cudaStream_t st);
+void launch_pushout(const Params& P, cudaStream_t st);
+void launch_deactivate(const Params& P, cudaStream_t st);
+void launch_free_bodies(const Params& P, bool integrate, bool merge, cudaStream_t st);
+void launch_grid_bc(const Params& P, int64_t max_bricks, cudaStream_t st);
+
+// ---- I/O (k_io.cu) ----
+struct IoArrays {  // original-order device staging arrays (any may be null)
+    float* x; float* v; float* mass; float* vol0; float* F; float* C; int32_t* mat;
+    uint8_t* active; int32_t* scene;
+};
+void launch_upload(const Params& P, const IoArrays& in, int64_t n, cudaStream_t st);
+void launch_download(const Params& P, const IoArrays& out, cudaStream_t st);
+void launch_totals(const Params& P, double* totals /*5 per scene*/, cudaStream_t st);
+void launch_stress(const Params& P, float* stress_orig, cudaStream_t st);
+void launch_grid_download(const Params& P, int scene, const DevScene& S, float* mass, float* mom,
+                          float* vel, cudaStream_t st);
+void launch_grid_upload(const Params& P, int scene, const DevScene& S, const float* mass,
+                        const float* mom, const float* vel, cudaStream_t st);
+
+}  // namespace mpmb
