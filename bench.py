@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 MPM hot path (BASELINE.json metric: particle-substeps/s).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload c5|c1|c2|c3] [--replicas R]
+
+One step = one frame (dt 0.02 s; 10 MLS substeps, or 1 PB-MPM step of 10 iterations for
+c3) of every scene on this rank.  Default workload: C5 shard = R=512 independent
+64,800-particle cutting replicas per GPU (the batched RL data-generation config of
+BASELINE.json; 4096 replicas over 8 GPUs), weak scaling over ranks, no data-path
+collective.  ``value`` is device-resident (CUDA events on the library's stream, max over
+ranks); ``e2e`` goes through the public facade with host buffers every frame (pose-table
+H2D from pinned memory, FrameResult D2H).  ``--impl reference`` times the UNMODIFIED
+reference CPU implementation (oracle/_ref, compiled from /root/reference) on the host
+cores with all threads, on the same workload and metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+import numpy as np  # noqa: E402
+
+METRIC = "particle-substeps/sec"
+UNIT = "particle-substeps/s"
+DT_FRAME = 0.02
+# algorithmic bytes per particle per launch
+ALG_BYTES = {"p2g": 108.0, "g2p": 148.0, "grid": 0.0, "sort": 224.0}
+SUBSTEP_BYTES = 204.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c5", choices=["c5", "c1", "c2", "c3"])
+    ap.add_argument("--replicas", type=int, default=512, help="C5 replicas per GPU")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU-baseline sample length")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def workload_specs(name, rank, replicas):
+    from paper_2502_18437_b200 import scenes
+    if name == "c5":
+        return [scenes.c5_cutting_replica(rank * replicas + i) for i in range(replicas)]
+    return [{"c1": scenes.c1_cube_drop, "c2": scenes.c2_cutting, "c3": scenes.c3_suture}[name]()]
+
+
+def workload_desc(name, replicas, n_per_gpu):
+    if name == "c5":
+        return (f"C5 shard: {replicas} independent cutting replicas x 64,800 p per GPU, 84^3 grid each, "
+                f"MLS 10 substeps/frame, quad-slicer blade (BASELINE.json configs[4])")
+    return {"c1": "C1 cube drop, MLS, 32,768 p, 64^3", "c2": "C2 cutting, MLS, 262,144 p, 128^3",
+            "c3": "C3 suture, PB-MPM K=10, 262,144 p, 128^3, arc needle + 16 free thread capsules"}[name]
+
+
+def substeps_of(spec):
+    return spec.get("iterations", 10) if spec["solver"] == "pbmpm" else spec.get("substeps", 10)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax = float(f[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic():
+    """dram bytes per particle per launch from the committed ncu summary, if any."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text())
+        except ValueError:
+            return None
+    return None
+
+
+# ------------------------------------------------------------------ reference arm
+def reference_scenes(specs):
+    import backends
+    out = []
+    for sp in specs:
+        sc = backends.make_scene("ref", sp)
+        out.append((sc, sp))
+    return out
+
+
+def time_reference(specs_fn, threads, frames, warmup=0):
+    """Advance `threads` independent reference scenes `frames` frames on `threads` host
+    threads (oracle/_ref/libmpmref.so, unmodified reference code).  Returns
+    (particle-substeps/s, wall seconds, total particles, substeps/frame)."""
+    import ctypes as C
+    import backends
+    lib = backends.reference()
+    specs = specs_fn(threads)
+    scs = reference_scenes(specs)
+    hs = (C.c_uint64 * len(scs))(*[s.h for s, _ in scs])
+    if warmup:
+        lib.mpmref_advance_many(hs, len(scs), DT_FRAME, warmup, threads)
+    wall = lib.mpmref_advance_many(hs, len(scs), DT_FRAME, frames, threads)
+    n = sum(s.particle_count() for s, _ in scs)
+    sub = substeps_of(specs[0])
+    for s, _ in scs:
+        s.destroy()
+    return n * sub * frames / wall, wall, n, sub
+
+
+def cpu_specs_fn(workload):
+    from paper_2502_18437_b200 import scenes
+
+    def fn(threads):
+        if workload == "c5":
+            return [scenes.c5_cutting_replica(i) for i in range(threads)]
+        return workload_specs(workload, 0, 1) * 1
+    return fn
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return None
+    threads = cpu_threads() if args.workload == "c5" else 1
+    fn = cpu_specs_fn(args.workload)
+    # size one step to ~cpu_seconds/steps: probe one frame first
+    rate1, wall1, n, sub = time_reference(fn, threads, 1)
+    frames = max(1, int(round(args.cpu_seconds / max(wall1, 1e-3) / max(args.steps, 1))))
+    vals = []
+    for _ in range(args.warmup):
+        time_reference(fn, threads, frames)
+    t_total = 0.0
+    for _ in range(args.steps):
+        r, w, _, _ = time_reference(fn, threads, frames)
+        vals.append(r)
+        t_total += w
+    value = statistics.median(vals)
+    sample = (f"{threads} concurrent reference scenes ({'C5 replicas' if args.workload == 'c5' else args.workload}), "
+              f"{frames} frame(s) x {sub} substeps per step, {n} particles total")
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t_total / max(args.steps, 1),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": workload_desc(args.workload, args.replicas, None), "parallelism": "host threads"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    return line
+
+
+# ------------------------------------------------------------------ our arm
+def build_batch(specs):
+    from paper_2502_18437_b200 import api, scenes
+    cfg = api.scene_config(**scenes.config_kwargs(specs[0]))
+    if len(specs) == 1:
+        b = api.SceneBatch(cfg, 1)
+    else:
+        b = api.SceneBatch(cfg, len(specs))
+    for sc, sp in zip(b.scenes, specs):
+        scenes.populate(sc, sp)
+    return b
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    torch.cuda.set_device(local_rank)
+    specs = workload_specs(args.workload, rank, args.replicas)
+    sub = substeps_of(specs[0])
+    t0 = time.time()
+    batch = build_batch(specs)
+    # a real (non-legacy) stream shared by the library launches and the timing events
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    batch.set_stream(stream.cuda_stream)
+    lib = batch.lib
+    n_particles = sum(s.particle_count() for s in batch.scenes)
+    n_shapes = sum(len(s.shapes) for s in batch.scenes)
+    setup_s = time.time() - t0
+
+    # warm-up (includes the upload and first binning)
+    batch.advance_frames(DT_FRAME, max(args.warmup, 1))
+    batch.fetch_results()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    # ---- value: device-resident, CUDA events on the library stream
+    batch.set_profiling(True)
+    barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    launches0 = lib.mpmb_kernel_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    batch.advance_frames(DT_FRAME, args.steps)
+    e1.record(stream)
+    e1.synchronize()
+    torch.cuda.synchronize()
+    launches = lib.mpmb_kernel_launch_count() - launches0
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    prof = batch.profile()
+    batch.set_profiling(False)
+    batch.fetch_results()
+
+    # ---- e2e: public facade, host buffers every frame
+    barrier()
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(args.steps):
+        batch.advance(DT_FRAME)
+        batch.fetch_results()
+    f1.record(stream)
+    f1.synchronize()
+    ms_e2e = f0.elapsed_time(f1)
+
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms, ms_e2e], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, ms_e2e = float(t[0]), float(t[1])
+        cnt = torch.tensor([float(n_particles)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
+        n_total = float(cnt[0])
+    else:
+        n_total = float(n_particles)
+
+    ps = n_total * sub * args.steps
+    value = ps / (ms / 1e3)
+    e2e = ps / (ms_e2e / 1e3)
+    peak, peak_src = measured_peak()
+    # dominant kernel class and its roofline (per-launch averages over the timed region)
+    launches_per_class = {"p2g": sub * args.steps, "g2p": sub * args.steps, "grid": sub * args.steps,
+                          "sort": args.steps if specs[0]["solver"] != "pbmpm" else args.steps}
+    cls_ms = {"p2g": prof["ms_p2g"], "g2p": prof["ms_g2p"], "grid": prof["ms_grid"], "sort": prof["ms_sort"]}
+    dom = max(cls_ms, key=lambda k: cls_ms[k])
+    per_launch_ms = cls_ms[dom] / max(launches_per_class[dom], 1)
+    alg = ALG_BYTES[dom] * n_particles
+    achieved = alg / (per_launch_ms / 1e3) / 1e9 if per_launch_ms > 0 else 0.0
+    tr = ncu_traffic()
+    traffic = None
+    if tr and dom in tr.get("bytes_per_particle", {}):
+        traffic = tr["bytes_per_particle"][dom] * n_particles
+    h2d = sub * n_shapes * (64 + 1)
+    d2h = n_particles * (12 + 12 + 1) + 5 * 8 * len(batch.scenes) + 16 * len(batch.scenes)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": workload_desc(args.workload, args.replicas, n_particles),
+                   "particles_per_gpu": n_particles, "scenes_per_gpu": len(batch.scenes),
+                   "substeps_per_step": sub, "parallelism": f"scene replicas x{world} (no collective)",
+                   "l2": "inputs larger than L2 (%.1f GB particle state per GPU)" % (n_particles * 112 / 1e9)},
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "alg_bytes_per_particle": ALG_BYTES[dom], "per_launch_ms": per_launch_ms,
+                     "substep_frac": value * SUBSTEP_BYTES / 1e9 / peak},
+        "kernel_ms": {k: v / max(launches_per_class[k], 1) for k, v in cls_ms.items()},
+        "clocks": clk,
+        "setup_s": setup_s,
+    }
+    return line, batch
+
+
+def cpu_baseline(args):
+    if args.no_cpu_baseline:
+        return None
+    from paper_2502_18437_b200 import scenes  # noqa: F401
+    import backends
+    if not backends.have_reference():
+        return None
+    threads = cpu_threads() if args.workload == "c5" else 1
+    fn = cpu_specs_fn(args.workload)
+    rate1, wall1, n, sub = time_reference(fn, threads, 1)
+    frames = max(1, int(round(args.cpu_seconds / max(wall1, 1e-3))))
+    rate, wall, n, sub = time_reference(fn, threads, frames)
+    return {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"{threads} concurrent reference scenes ({args.workload}), {frames} frames x {sub} substeps, "
+                      f"{n} particles, {wall:.1f} s wall"}
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        line = run_reference(args, rank)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    line, batch = run_ours(args, rank, world, local_rank)
+    if rank == 0:
+        if world == 1:
+            line["cpu_baseline"] = cpu_baseline(args)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

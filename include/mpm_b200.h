@@ -256,6 +256,10 @@ mpmb_status mpmb_set_shape_pose_target(mpmb_handle scene, mpmb_handle shape,
                                        const float position[3], const float orientation[4]);
 /* Enqueues one frame (asynchronous; the paper's advance/fetch split). Scene or batch handle. */
 mpmb_status mpmb_advance(mpmb_handle h, float dt);
+/* Pipelined form of n x (advance; fetch_results) with no snapshot between frames: all
+ * frames are enqueued back to back; the last one is left pending for mpmb_fetch_results.
+ * (Extension; the reference's advance is synchronous, scene.hpp:117-123.) */
+mpmb_status mpmb_advance_frames(mpmb_handle h, float dt, int32_t n_frames);
 /* Waits for the pending frame and snapshots FrameResult. For a batch, out has n entries. */
 mpmb_status mpmb_fetch_results(mpmb_handle h, mpmb_frame_summary* out);
 /* Arrays of the last fetched FrameResult of one scene (any pointer may be NULL):

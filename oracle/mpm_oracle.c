@@ -1009,11 +1009,19 @@ static void update_stress(struct mpmor_state_s* st, size_t i, int* inverted) {
     st->p.stress[i] = neo_hookean(st->p.F[i], mat->mu, mat->lambda);
 }
 
+/* Order perturbation (checker calibration only): 1 = P2G visits particles in reverse
+ * index order.  The reference sums in index order (solvers.hpp:151); the difference
+ * between the two orders is the reference's own float-reordering sensitivity, the
+ * yardstick for device results that sum with atomics (SURVEY.md §7 hard part 1). */
+static int g_order_mode = 0;
+void mpmor_set_order_perturbation(int32_t mode) { g_order_mode = mode; }
+
 /* ref: solvers.hpp:151-169 (P2G); stress_scale = -dt*V*m_inv for MLS, absent for PB */
 static void p2g(struct mpmor_state_s* st, float dt, float m_inv, int with_stress) {
     Particles* p = &st->p;
     Grid* grid = &st->grid;
-    for (size_t i = 0; i < p->n; ++i) {
+    for (size_t ii = 0; ii < p->n; ++ii) {
+        const size_t i = g_order_mode == 1 ? p->n - 1 - ii : ii;
         if (!p->active[i]) continue;
         SW sw = spline_weights(p->x[i], grid->origin, grid->dx);
         M3 affine;

@@ -52,6 +52,7 @@ mpmb_status mpmor_state_get_grid(mpmor_state st, float* mass, float* mom, float*
  * the device's reduction order */
 mpmb_status mpmor_state_get_contact_f64(mpmor_state st, double* imp, double* tq, int32_t n);
 /* binning oracle: brick-major cell key + stable permutation (see mpmb_bin_particles) */
+void mpmor_set_order_perturbation(int32_t mode);
 mpmb_status mpmor_bin_particles(mpmor_state st, uint32_t* keys, uint32_t* perm);
 
 /* scene layer (Scene, scene.hpp:45-294) */

@@ -365,6 +365,9 @@ class SceneBatch:
     def advance(self, dt):
         check(self.lib.mpmb_advance(self.h, float(F32(dt))), self.lib, "advance")
 
+    def advance_frames(self, dt, n: int):
+        check(self.lib.mpmb_advance_frames(self.h, float(F32(dt)), n), self.lib, "advance_frames")
+
     def fetch_results(self, arrays: bool = False):
         out = (capi.FrameSummary * len(self.scenes))()
         check(self.lib.mpmb_fetch_results(self.h, out), self.lib, "fetch")

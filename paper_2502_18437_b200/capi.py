@@ -128,6 +128,7 @@ PRODUCT_API.update({
     "create_shape": (u64, [u64, C.POINTER(ShapeDesc)]),
     "set_shape_pose_target": (C.c_int, [u64, u64, fp, fp]),
     "advance": (C.c_int, [u64, C.c_float]),
+    "advance_frames": (C.c_int, [u64, C.c_float, C.c_int32]),
     "fetch_results": (C.c_int, [u64, C.POINTER(FrameSummary)]),
     "result_copy": (C.c_int, [u64, fp, fp, u8p, ip, fp, fp]),
     "particle_count": (C.c_int32, [u64]),

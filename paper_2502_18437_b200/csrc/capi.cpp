@@ -1011,6 +1011,23 @@ extern "C" mpmb_status mpmb_advance(mpmb_handle h, float dt) {
     });
 }
 
+extern "C" mpmb_status mpmb_advance_frames(mpmb_handle h, float dt, int32_t n_frames) {
+    std::lock_guard<std::mutex> lk(reg().mu);
+    return guarded([&]() -> mpmb_status {
+        bool is_batch;
+        Batch* b = batch_of_handle(reg(), h, is_batch);
+        if (!b) return MPMB_BAD_HANDLE;
+        if (!(dt > 0) || n_frames < 1) return MPMB_INVALID_ARGUMENT;
+        if (!is_batch && b->scenes.size() > 1)
+            fail(MPMB_LIFECYCLE_ERROR, "scene belongs to a batch: advance the batch handle");
+        if (b->status == Status::advancing)
+            fail(MPMB_LIFECYCLE_ERROR, "scene: advance while a frame is pending");
+        for (int f = 0; f < n_frames; ++f) run_frame(*b, dt);
+        b->status = Status::advancing;
+        return MPMB_OK;
+    });
+}
+
 extern "C" mpmb_status mpmb_fetch_results(mpmb_handle h, mpmb_frame_summary* out) {
     std::lock_guard<std::mutex> lk(reg().mu);
     return guarded([&]() -> mpmb_status {

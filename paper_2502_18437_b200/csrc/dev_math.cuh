@@ -16,18 +16,39 @@ struct V3 { float x, y, z; };
 struct M3 { float m[9]; };   // row-major, math.hpp:46-48
 struct Q4 { float x, y, z, w; };
 
+// Reference arithmetic: the contact / SDF / push-out / free-body path is evaluated
+// without FMA contraction and in the reference's operation order (the x86-64 reference
+// build has no FMA).  Rigid motions that are exactly tangential to a needle make the
+// contact test v_n < 0 a rounding-level decision (tests/test_gpu_parity.py); matching
+// the reference's rounding there is what keeps the device on the reference trajectory.
+// The P2G/G2P transfer sums keep FMA: their order already differs (atomics).
+#define FA __fadd_rn
+#define FS __fsub_rn
+#define FM __fmul_rn
+#define FD __fdiv_rn
+
 __device__ __forceinline__ V3 mk(float x, float y, float z) { return V3{x, y, z}; }
-__device__ __forceinline__ V3 operator+(V3 a, V3 b) { return V3{a.x + b.x, a.y + b.y, a.z + b.z}; }
-__device__ __forceinline__ V3 operator-(V3 a, V3 b) { return V3{a.x - b.x, a.y - b.y, a.z - b.z}; }
+__device__ __forceinline__ V3 operator+(V3 a, V3 b) { return V3{FA(a.x, b.x), FA(a.y, b.y), FA(a.z, b.z)}; }
+__device__ __forceinline__ V3 operator-(V3 a, V3 b) { return V3{FS(a.x, b.x), FS(a.y, b.y), FS(a.z, b.z)}; }
 __device__ __forceinline__ V3 operator-(V3 a) { return V3{-a.x, -a.y, -a.z}; }
-__device__ __forceinline__ V3 operator*(V3 a, float s) { return V3{a.x * s, a.y * s, a.z * s}; }
-__device__ __forceinline__ V3 vdiv(V3 a, float s) { return V3{a.x / s, a.y / s, a.z / s}; }
-__device__ __forceinline__ float dot(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
-__device__ __forceinline__ V3 cross(V3 a, V3 b) {
-    return V3{a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+__device__ __forceinline__ V3 operator*(V3 a, float s) { return V3{FM(a.x, s), FM(a.y, s), FM(a.z, s)}; }
+__device__ __forceinline__ V3 vdiv(V3 a, float s) { return V3{FD(a.x, s), FD(a.y, s), FD(a.z, s)}; }
+__device__ __forceinline__ float dot(V3 a, V3 b) {  // math.hpp:29
+    return FA(FA(FM(a.x, b.x), FM(a.y, b.y)), FM(a.z, b.z));
+}
+__device__ __forceinline__ V3 cross(V3 a, V3 b) {  // math.hpp:30-32
+    return V3{FS(FM(a.y, b.z), FM(a.z, b.y)), FS(FM(a.z, b.x), FM(a.x, b.z)),
+              FS(FM(a.x, b.y), FM(a.y, b.x))};
 }
 __device__ __forceinline__ float norm2(V3 a) { return dot(a, a); }
-__device__ __forceinline__ float norm(V3 a) { return sqrtf(norm2(a)); }
+__device__ __forceinline__ float norm(V3 a) { return __fsqrt_rn(norm2(a)); }
+// float trig evaluated in FP64 and rounded once (matches glibc's float results except
+// where glibc itself is not correctly rounded)
+__device__ __forceinline__ float sin_ref(float x) { return static_cast<float>(sin(static_cast<double>(x))); }
+__device__ __forceinline__ float cos_ref(float x) { return static_cast<float>(cos(static_cast<double>(x))); }
+__device__ __forceinline__ float atan2_ref(float y, float x) {
+    return static_cast<float>(atan2(static_cast<double>(y), static_cast<double>(x)));
+}
 // math.hpp:35-38
 __device__ __forceinline__ V3 normalized(V3 a) {
     float n = norm(a);
@@ -43,16 +64,16 @@ __device__ __forceinline__ V3 qrotate(Q4 q, V3 v) {
 __device__ __forceinline__ V3 qrotate_inv(Q4 q, V3 v) { return qrotate(Q4{-q.x, -q.y, -q.z, q.w}, v); }
 // math.hpp:151-156
 __device__ __forceinline__ Q4 qmul(Q4 a, Q4 o) {
-    return Q4{a.w * o.x + a.x * o.w + a.y * o.z - a.z * o.y,
-              a.w * o.y - a.x * o.z + a.y * o.w + a.z * o.x,
-              a.w * o.z + a.x * o.y - a.y * o.x + a.z * o.w,
-              a.w * o.w - a.x * o.x - a.y * o.y - a.z * o.z};
+    return Q4{FS(FA(FA(FM(a.w, o.x), FM(a.x, o.w)), FM(a.y, o.z)), FM(a.z, o.y)),
+              FA(FA(FS(FM(a.w, o.y), FM(a.x, o.z)), FM(a.y, o.w)), FM(a.z, o.x)),
+              FA(FS(FA(FM(a.w, o.z), FM(a.x, o.y)), FM(a.y, o.x)), FM(a.z, o.w)),
+              FS(FS(FS(FM(a.w, o.w), FM(a.x, o.x)), FM(a.y, o.y)), FM(a.z, o.z))};
 }
 // math.hpp:144-149
 __device__ __forceinline__ Q4 qnormalized(Q4 q) {
-    float n = sqrtf(q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w);
+    float n = __fsqrt_rn(FA(FA(FA(FM(q.x, q.x), FM(q.y, q.y)), FM(q.z, q.z)), FM(q.w, q.w)));
     if (n <= 0.f) return Q4{0.f, 0.f, 0.f, 1.f};
-    return Q4{q.x / n, q.y / n, q.z / n, q.w / n};
+    return Q4{FD(q.x, n), FD(q.y, n), FD(q.z, n), FD(q.w, n)};
 }
 
 // ---------------------------------------------------------------- spline (math.hpp)
@@ -87,8 +108,9 @@ __device__ __forceinline__ bool spline_in_domain(V3 pos, const DevScene& S) {
 
 // ------------------------------------------------------------- matrices
 __device__ __forceinline__ float det3(const float a[9]) {  // math.hpp:273-277
-    return a[0] * (a[4] * a[8] - a[5] * a[7]) + a[1] * (a[5] * a[6] - a[3] * a[8]) +
-           a[2] * (a[3] * a[7] - a[4] * a[6]);
+    return FA(FA(FM(a[0], FS(FM(a[4], a[8]), FM(a[5], a[7]))),
+                 FM(a[1], FS(FM(a[5], a[6]), FM(a[3], a[8])))),
+              FM(a[2], FS(FM(a[3], a[7]), FM(a[4], a[6]))));
 }
 
 // Cauchy stress (materials.hpp:35-54), FP64 internally, J clamped >= 1e-6.
@@ -233,7 +255,7 @@ __device__ __forceinline__ float clampf(float v, float lo, float hi) {
 __device__ __forceinline__ V3 closest_on_segment(V3 a, V3 b, V3 p, float& t) {
     V3 ab = b - a;
     float len2 = norm2(ab);
-    t = len2 > 1e-18f ? clampf(dot(p - a, ab) / len2, 0.f, 1.f) : 0.f;
+    t = len2 > 1e-18f ? clampf(FD(dot(p - a, ab), len2), 0.f, 1.f) : 0.f;
     return a + ab * t;
 }
 
@@ -245,20 +267,20 @@ __device__ __forceinline__ V3 closest_on_triangle(V3 a, V3 b, V3 c, V3 p) {
     V3 bp = p - b;
     float d3 = dot(ab, bp), d4 = dot(ac, bp);
     if (d3 >= 0.f && d4 <= d3) return b;
-    float vc = d1 * d4 - d3 * d2;
-    if (vc <= 0.f && d1 >= 0.f && d3 <= 0.f) return a + ab * (d1 / (d1 - d3));
+    float vc = FS(FM(d1, d4), FM(d3, d2));
+    if (vc <= 0.f && d1 >= 0.f && d3 <= 0.f) return a + ab * FD(d1, d1 - d3);
     V3 cp = p - c;
     float d5 = dot(ab, cp), d6 = dot(ac, cp);
     if (d6 >= 0.f && d5 <= d6) return c;
-    float vb = d5 * d2 - d1 * d6;
-    if (vb <= 0.f && d2 >= 0.f && d6 <= 0.f) return a + ac * (d2 / (d2 - d6));
-    float va = d3 * d6 - d5 * d4;
+    float vb = FS(FM(d5, d2), FM(d1, d6));
+    if (vb <= 0.f && d2 >= 0.f && d6 <= 0.f) return a + ac * FD(d2, d2 - d6);
+    float va = FS(FM(d3, d6), FM(d5, d4));
     if (va <= 0.f && (d4 - d3) >= 0.f && (d5 - d6) >= 0.f) {
-        float w = (d4 - d3) / ((d4 - d3) + (d5 - d6));
+        float w = FD(d4 - d3, FA(d4 - d3, d5 - d6));
         return b + (c - b) * w;
     }
-    float denom = 1.f / (va + vb + vc);
-    return a + ab * (vb * denom) + ac * (vc * denom);
+    float denom = FD(1.f, FA(FA(va, vb), vc));
+    return a + ab * FM(vb, denom) + ac * FM(vc, denom);
 }
 
 // World-space SDF query (geometry.hpp:370-395) against one device shape.
@@ -358,7 +380,7 @@ __device__ inline Sdf sdf_query(const DevShape& g, const DevPose& pose, const fl
                 s.region = REGION_SPINE;
             } else {
                 float side = dot(p - surf_pt, surf_n) >= 0.f ? 1.f : -1.f;
-                s.distance = side * best_surf;
+                s.distance = FM(side, best_surf);
                 s.normal = surf_n * side;
                 s.region = REGION_EDGE;
             }
@@ -367,10 +389,10 @@ __device__ inline Sdf sdf_query(const DevShape& g, const DevPose& pose, const fl
         case GEOM_ARC: {  // geometry.hpp:295-327
             const float kTwoPi = 6.28318548f;  // float(2*pi), as Real(2*3.14159...)
             float t;
-            if (sqrtf(p.x * p.x + p.y * p.y) < 1e-9f) {
+            if (norm(mk(p.x, p.y, 0.f)) < 1e-9f) {
                 t = 0.f;
             } else {
-                t = atan2f(p.y, p.x);
+                t = atan2_ref(p.y, p.x);
                 if (t < 0.f) t += kTwoPi;
                 if (t > g.gp[1]) {
                     float to_end = t - g.gp[1];
@@ -378,9 +400,8 @@ __device__ inline Sdf sdf_query(const DevShape& g, const DevPose& pose, const fl
                     t = to_end <= to_start ? g.gp[1] : 0.f;
                 }
             }
-            float st, ct;
-            sincosf(t, &st, &ct);
-            V3 qq = mk(g.gp[0] * ct, g.gp[0] * st, 0.f);
+            const float st = sin_ref(t), ct = cos_ref(t);
+            V3 qq = mk(FM(g.gp[0], ct), FM(g.gp[0], st), 0.f);
             s.region = REGION_CURVE;
             s.tangent = mk(-st, ct, 0.f);
             V3 d = p - qq;
@@ -450,8 +471,8 @@ __device__ __forceinline__ bool node_in_contact(const Sdf& s, float hw) {
 // contact.hpp:33-38
 __device__ __forceinline__ float friction_drag(float vn, float vtg, float mu_k, float c_d) {
     if (vtg < 1e-12f) return 0.f;
-    float f = 1.f - mu_k * vn / vtg;
-    return c_d * fmaxf(f, 0.f);
+    float f = FS(1.f, FD(FM(mu_k, vn), vtg));
+    return FM(c_d, fmaxf(f, 0.f));
 }
 
 // One shape's grid correction (contact.hpp:106-133): returns the corrected velocity

@@ -177,13 +177,13 @@ __global__ void __launch_bounds__(256) k_grid_update(const Params P) {
         const bool live = m > kMassEps;
         V3 v = mk(0.f, 0.f, 0.f);
         if (live) {  // solvers.hpp:58-61
-            v = mk(a.y / m, a.z / m, a.w / m);
+            v = vdiv(mk(a.y, a.z, a.w), m);
             if (P.gravity) v = v + mk(P.g[0], P.g[1], P.g[2]) * P.dt;
         }
         if (P.contact && S.shape_count > 0) {  // contact.hpp:97-136, shapes in order
-            const V3 xn = mk(S.origin[0] + static_cast<float>(i) * S.dx,
-                             S.origin[1] + static_cast<float>(j) * S.dx,
-                             S.origin[2] + static_cast<float>(k) * S.dx);
+            const V3 xn = mk(FA(S.origin[0], FM(static_cast<float>(i), S.dx)),  // state.hpp:49-51
+                             FA(S.origin[1], FM(static_cast<float>(j), S.dx)),
+                             FA(S.origin[2], FM(static_cast<float>(k), S.dx)));
             for (int si = S.shape_begin; si < S.shape_begin + S.shape_count; ++si) {
                 const DevShape& sh = P.shapes[si];
                 V3 imp = mk(0.f, 0.f, 0.f), tq = mk(0.f, 0.f, 0.f);
@@ -321,32 +321,32 @@ __device__ __forceinline__ void g2p_gather(const V3 (&nv)[27], const float w[3][
 __device__ __forceinline__ int pushout_particle(const Params& P, const DevScene& S, float x[3],
                                                 float v[3]) {
     int pushed = 0;
-    const float clearance = 1e-4f * S.dx;
+    const float clearance = FM(1e-4f, S.dx);
     for (int si = S.shape_begin; si < S.shape_begin + S.shape_count; ++si) {
         const DevShape& sh = P.shapes[si];
         const DevPose& pose = pose_of(P, si);
         const Sdf s = sdf_query(sh, pose, P.verts, P.ints, mk(x[0], x[1], x[2]));
         float move = 0.f;
         if (s.region == REGION_SURFACE || s.region == REGION_SPINE) {
-            if (s.distance < 0.f) move = -s.distance + clearance;
+            if (s.distance < 0.f) move = FA(-s.distance, clearance);
         } else if (s.region == REGION_EDGE) {
-            const float target = 0.5f * sh.hw;
+            const float target = FM(0.5f, sh.hw);
             const float d = fabsf(s.distance);
-            if (d < target) move = target - d + clearance;
+            if (d < target) move = FA(FS(target, d), clearance);
         } else if (s.region == REGION_CURVE) {
-            const float target = 0.5f * sh.hw;
-            if (s.distance < target) move = target - s.distance + clearance;
+            const float target = FM(0.5f, sh.hw);
+            if (s.distance < target) move = FA(FS(target, s.distance), clearance);
         }
         if (move > 0.f) {
-            x[0] += s.normal.x * move;
-            x[1] += s.normal.y * move;
-            x[2] += s.normal.z * move;
+            x[0] = FA(x[0], FM(s.normal.x, move));
+            x[1] = FA(x[1], FM(s.normal.y, move));
+            x[2] = FA(x[2], FM(s.normal.z, move));
             const V3 vr = rigid_point_velocity(pose, mk(x[0], x[1], x[2]));
             const float vn = dot(mk(v[0], v[1], v[2]) - vr, s.normal);
             if (vn < 0.f) {
-                v[0] -= s.normal.x * vn;
-                v[1] -= s.normal.y * vn;
-                v[2] -= s.normal.z * vn;
+                v[0] = FS(v[0], FM(s.normal.x, vn));
+                v[1] = FS(v[1], FM(s.normal.y, vn));
+                v[2] = FS(v[2], FM(s.normal.z, vn));
             }
             ++pushed;
         }
@@ -354,17 +354,18 @@ __device__ __forceinline__ int pushout_particle(const Params& P, const DevScene&
     return pushed;
 }
 
-// F <- (I + C dt) F  (solvers.hpp:194, 275)
+// F <- (I + C dt) F  (solvers.hpp:194, 275) in the reference's Mat3 product order
+// (math.hpp:101-110: s = 0; s += a_ik b_kj)
 __device__ __forceinline__ void update_F(const float C[9], float dt, float F[9]) {
     float A[9];
 #pragma unroll
-    for (int i = 0; i < 9; ++i) A[i] = C[i] * dt + ((i % 4) == 0 ? 1.f : 0.f);
+    for (int i = 0; i < 9; ++i) A[i] = FA((i % 4) == 0 ? 1.f : 0.f, FM(C[i], dt));
     float Fn[9];
 #pragma unroll
     for (int i = 0; i < 3; ++i)
 #pragma unroll
         for (int j = 0; j < 3; ++j)
-            Fn[3 * i + j] = A[3 * i] * F[j] + A[3 * i + 1] * F[3 + j] + A[3 * i + 2] * F[6 + j];
+            Fn[3 * i + j] = FA(FA(FM(A[3 * i], F[j]), FM(A[3 * i + 1], F[3 + j])), FM(A[3 * i + 2], F[6 + j]));
 #pragma unroll
     for (int i = 0; i < 9; ++i) F[i] = Fn[i];
 }
@@ -441,9 +442,9 @@ __global__ void __launch_bounds__(128) k_g2p(const Params P) {
                         do_commit = P.commit != 0;
                     }
                     if (do_commit) {  // solvers.hpp:193-195 / 274-276
-                        p.x[0] += p.v[0] * P.dt;
-                        p.x[1] += p.v[1] * P.dt;
-                        p.x[2] += p.v[2] * P.dt;
+                        p.x[0] = FA(p.x[0], FM(p.v[0], P.dt));
+                        p.x[1] = FA(p.x[1], FM(p.v[1], P.dt));
+                        p.x[2] = FA(p.x[2], FM(p.v[2], P.dt));
                         update_F(p.C, P.dt, p.F);
                         if (det3(p.F) <= 0.f) ++n_inv;
                         if (P.pushout && S.shape_count > 0) n_push += pushout_particle(P, S, p.x, p.v);
@@ -531,29 +532,48 @@ __global__ void k_free_bodies(const Params P, int integrate, int merge) {
                                 static_cast<float>(P.acc_sub[6 * i + 4]),
                                 static_cast<float>(P.acc_sub[6 * i + 5])};
             const float dt = P.dt;
-            const float im = 1.f / sh.body_mass;
+            const float im = FD(1.f, sh.body_mass);
 #pragma unroll
-            for (int a = 0; a < 3; ++a) pose.lin[a] += J[a] * im + P.g[a] * dt;
-            // R I^-1 R^T tau with R from the orientation (math.hpp:163-172)
+            for (int a = 0; a < 3; ++a) pose.lin[a] = FA(pose.lin[a], FA(FM(J[a], im), FM(P.g[a], dt)));
+            // I_world^-1 = (R * I_body^-1) * R^T (math.hpp:101-110, 163-172), reference order
             const float x = pose.rot[0], y = pose.rot[1], z = pose.rot[2], w = pose.rot[3];
-            const float xx = x * x, yy = y * y, zz = z * z, xy = x * y, xz = x * z, yz = y * z;
-            const float wx = w * x, wy = w * y, wz = w * z;
-            const float R[9] = {1 - 2 * (yy + zz), 2 * (xy - wz), 2 * (xz + wy),
-                                2 * (xy + wz), 1 - 2 * (xx + zz), 2 * (yz - wx),
-                                2 * (xz - wy), 2 * (yz + wx), 1 - 2 * (xx + yy)};
-            const float id[3] = {1.f / sh.inertia[0], 1.f / sh.inertia[1], 1.f / sh.inertia[2]};
-            float Rt_tau[3];
+            const float xx = FM(x, x), yy = FM(y, y), zz = FM(z, z);
+            const float xy = FM(x, y), xz = FM(x, z), yz = FM(y, z);
+            const float wx = FM(w, x), wy = FM(w, y), wz = FM(w, z);
+            const float R[9] = {FS(1.f, FM(2.f, FA(yy, zz))), FM(2.f, FS(xy, wz)), FM(2.f, FA(xz, wy)),
+                                FM(2.f, FA(xy, wz)), FS(1.f, FM(2.f, FA(xx, zz))), FM(2.f, FS(yz, wx)),
+                                FM(2.f, FS(xz, wy)), FM(2.f, FA(yz, wx)), FS(1.f, FM(2.f, FA(xx, yy)))};
+            const float D[9] = {FD(1.f, sh.inertia[0]), 0.f, 0.f, 0.f, FD(1.f, sh.inertia[1]), 0.f,
+                                0.f, 0.f, FD(1.f, sh.inertia[2])};
+            float RD[9], M[9];
 #pragma unroll
-            for (int a = 0; a < 3; ++a) Rt_tau[a] = R[a] * T[0] + R[3 + a] * T[1] + R[6 + a] * T[2];
+            for (int r = 0; r < 3; ++r)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    float s = 0.f;
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) s = FA(s, FM(R[3 * r + k], D[3 * k + c]));
+                    RD[3 * r + c] = s;
+                }
+#pragma unroll
+            for (int r = 0; r < 3; ++r)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    float s = 0.f;
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) s = FA(s, FM(RD[3 * r + k], R[3 * c + k]));
+                    M[3 * r + c] = s;
+                }
 #pragma unroll
             for (int a = 0; a < 3; ++a)
-                pose.ang[a] += R[3 * a] * id[0] * Rt_tau[0] + R[3 * a + 1] * id[1] * Rt_tau[1] +
-                               R[3 * a + 2] * id[2] * Rt_tau[2];
+                pose.ang[a] = FA(pose.ang[a], FA(FA(FM(M[3 * a], T[0]), FM(M[3 * a + 1], T[1])),
+                                                 FM(M[3 * a + 2], T[2])));
 #pragma unroll
-            for (int a = 0; a < 3; ++a) pose.pos[a] += pose.lin[a] * dt;
+            for (int a = 0; a < 3; ++a) pose.pos[a] = FA(pose.pos[a], FM(pose.lin[a], dt));
             const Q4 dq = qmul(Q4{pose.ang[0], pose.ang[1], pose.ang[2], 0.f}, Q4{x, y, z, w});
-            const float h = 0.5f * dt;
-            const Q4 qn = qnormalized(Q4{x + h * dq.x, y + h * dq.y, z + h * dq.z, w + h * dq.w});
+            const float h = FM(0.5f, dt);
+            const Q4 qn = qnormalized(Q4{FA(x, FM(h, dq.x)), FA(y, FM(h, dq.y)), FA(z, FM(h, dq.z)),
+                                         FA(w, FM(h, dq.w))});
             pose.rot[0] = qn.x; pose.rot[1] = qn.y; pose.rot[2] = qn.z; pose.rot[3] = qn.w;
             P.free_pose[i] = pose;
         }

@@ -20,6 +20,7 @@ from paper_2502_18437_b200.api import SolverState, check, _fp, _summary_dict
 
 ROOT = Path(__file__).resolve().parents[1]
 ORACLE_LIB = ROOT / "oracle" / "_build" / "libmpmoracle.so"
+ORACLE_FMA_LIB = ROOT / "oracle" / "_build" / "libmpmoracle_fma.so"
 REF_LIB = ROOT / "oracle" / "_ref" / "libmpmref.so"
 F32 = np.float32
 
@@ -35,6 +36,7 @@ UNIT_API = {
 }
 
 ORACLE_EXTRA = {
+    "set_order_perturbation": (None, [C.c_int32]),
     "bin_particles": (C.c_int, [C.c_void_p, capi.u32p, capi.u32p]),
     "state_get_contact_f64": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int32]),
     "scene_create": (C.c_void_p, [C.POINTER(capi.SceneConfig)]),
@@ -90,6 +92,12 @@ def _load(path: Path, prefix: str, extra: dict):
 
 def oracle():
     return _load(ORACLE_LIB, "mpmor_", ORACLE_EXTRA)
+
+
+def oracle_fma():
+    """The same restatement built WITH FMA contraction: calibration of the reference
+    algorithm's own arithmetic sensitivity (never a parity target by itself)."""
+    return _load(ORACLE_FMA_LIB, "mpmor_", ORACLE_EXTRA)
 
 
 def reference():
@@ -190,8 +198,8 @@ class RefScene:
 class OracleScene:
     """Scene on the C restatement (integer ids instead of handles)."""
 
-    def __init__(self, config: capi.SceneConfig):
-        self.lib = oracle()
+    def __init__(self, config: capi.SceneConfig, lib=None):
+        self.lib = lib or oracle()
         self.h = self.lib.mpmor_scene_create(C.byref(config))
         if not self.h:
             raise RuntimeError("oracle scene_create failed")
@@ -261,6 +269,8 @@ def make_scene(kind: str, spec: dict):
         sc = RefScene(cfg)
     elif kind == "oracle":
         sc = OracleScene(cfg)
+    elif kind == "oracle_fma":
+        sc = OracleScene(cfg, lib=oracle_fma())
     else:
         raise ValueError(kind)
     sc.handles = scenes.populate(sc, spec)
