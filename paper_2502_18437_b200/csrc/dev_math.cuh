@@ -94,7 +94,8 @@ __device__ __forceinline__ void bspline_w(float fx, float w[3]) {
     w[2] = 0.5f * c * c;
 }
 // Interior band test, DIVIDING by dx (math.hpp:203-213) as deactivation does.
-__device__ __forceinline__ bool spline_in_domain(V3 pos, const DevScene& S) {
+template <class SceneT>
+__device__ __forceinline__ bool spline_in_domain(V3 pos, const SceneT& S) {
     const float p[3] = {__fdiv_rn(__fsub_rn(pos.x, S.origin[0]), S.dx),
                         __fdiv_rn(__fsub_rn(pos.y, S.origin[1]), S.dx),
                         __fdiv_rn(__fsub_rn(pos.z, S.origin[2]), S.dx)};
@@ -140,6 +141,45 @@ __device__ __forceinline__ void neo_hookean(const float F[9], float mu, float la
     s[1] = o01; s[3] = o01;
     s[2] = o02; s[6] = o02;
     s[5] = o12; s[7] = o12;
+}
+
+// The same Cauchy stress in FP32 without cancellation, for the P2G hot loop:
+//   F F^T - I = H + H^T + H H^T   and   J - 1 = tr H + (principal 2x2 minors of H) + det H
+// with H = F - I (exact for F near I), ln J = log1p(J - 1).  The reference evaluates in
+// FP64 because the float difference F F^T - I cancels (materials.hpp:29-34); this form
+// has no such difference, and agrees with the FP64 value to a few float ulps.  J is
+// clamped at 1e-6 exactly as the reference (materials.hpp:42).
+__device__ __forceinline__ float neo_hookean_f32(const float F[9], float mu, float lambda, float s[9]) {
+    const float h0 = F[0] - 1.f, h1 = F[1], h2 = F[2];
+    const float h3 = F[3], h4 = F[4] - 1.f, h5 = F[5];
+    const float h6 = F[6], h7 = F[7], h8 = F[8] - 1.f;
+    const float m2 = fmaf(h0, h4, -h1 * h3) + fmaf(h0, h8, -h2 * h6) + fmaf(h4, h8, -h5 * h7);
+    const float dh = h0 * fmaf(h4, h8, -h5 * h7) + h1 * fmaf(h5, h6, -h3 * h8) + h2 * fmaf(h3, h7, -h4 * h6);
+    const float j1 = (h0 + h4 + h8) + m2 + dh;
+    const float J = 1.f + j1;
+    float lnJ, invJ;
+    if (J < 1e-6f) {
+        lnJ = -13.815510558f;  // log(1e-6)
+        invJ = 1e6f;
+    } else {
+        lnJ = log1pf(j1);
+        invJ = 1.f / J;
+    }
+    const float d = lambda * lnJ;
+    // (b - I)_ij = h_ij + h_ji + sum_k h_ik h_jk
+    const float b00 = 2.f * h0 + fmaf(h0, h0, fmaf(h1, h1, h2 * h2));
+    const float b11 = 2.f * h4 + fmaf(h3, h3, fmaf(h4, h4, h5 * h5));
+    const float b22 = 2.f * h8 + fmaf(h6, h6, fmaf(h7, h7, h8 * h8));
+    const float b01 = (h1 + h3) + fmaf(h0, h3, fmaf(h1, h4, h2 * h5));
+    const float b02 = (h2 + h6) + fmaf(h0, h6, fmaf(h1, h7, h2 * h8));
+    const float b12 = (h5 + h7) + fmaf(h3, h6, fmaf(h4, h7, h5 * h8));
+    s[0] = fmaf(mu, b00, d) * invJ;
+    s[4] = fmaf(mu, b11, d) * invJ;
+    s[8] = fmaf(mu, b22, d) * invJ;
+    s[1] = s[3] = mu * b01 * invJ;
+    s[2] = s[6] = mu * b02 * invJ;
+    s[5] = s[7] = mu * b12 * invJ;
+    return J;
 }
 
 // Scaled-Newton polar decomposition in FP64 (math.hpp:286-340); returns R only

@@ -37,6 +37,22 @@ struct DevScene {
     int pad;
 };
 
+// Grid geometry shared by every scene of an engine (one SceneConfig per batch): kernels
+// read it from the parameter bank (constant cache), never per particle from memory.
+struct Geo {
+    float origin[3];
+    float dx;
+    float inv_dx;
+    float m_inv;
+    int dims[3];
+    int nb[3];
+    uint64_t nodes_per_scene;
+    uint32_t bricks_per_scene;
+    int pad;
+};
+
+constexpr int kMaxConstMats = 16;  // materials carried in the kernel parameter bank
+
 // Flattened mpm::Shape minus pose (rigid_dynamics.hpp:107-117, geometry.hpp:44-86).
 struct DevShape {
     int geom;

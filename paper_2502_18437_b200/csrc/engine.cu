@@ -75,6 +75,8 @@ struct Engine::Impl {
     cudaStream_t own = nullptr;
     cudaStream_t st = nullptr;
     std::vector<DevScene> hs;
+    Geo geo{};
+    std::vector<mpmb_material> hmats;
     DevBuf d_scenes;
     uint64_t total_nodes = 0;
     uint32_t total_bricks = 0;
@@ -154,6 +156,10 @@ struct Engine::Impl {
     Params params() {
         Params P{};
         for (int q = 0; q < kPlanes; ++q) P.pl[q] = planes[cur][q].as<float4>();
+        P.geo = geo;
+        for (size_t i = 0; i < hmats.size() && i < static_cast<size_t>(kMaxConstMats); ++i)
+            P.mats_c[i] = make_float4(static_cast<float>(hmats[i].kind), hmats[i].mu, hmats[i].lambda,
+                                      hmats[i].beta);
         P.scenes = d_scenes.as<DevScene>();
         P.shapes = shapes.as<DevShape>();
         P.verts = verts.as<float>();
@@ -213,7 +219,27 @@ Engine::Engine(const std::vector<SceneGrid>& scenes) : impl_(new Impl), scenes_(
         if (brick_base + nb >= 0xFFFFFFF0ull) throw std::invalid_argument("engine: too many grid bricks");
         node_base += nb * kBrickNodes;
         brick_base += static_cast<uint32_t>(nb);
+        if (!I.hs.empty()) {
+            const DevScene& d0 = I.hs[0];
+            for (int a = 0; a < 3; ++a)
+                if (d.dims[a] != d0.dims[a] || d.origin[a] != d0.origin[a])
+                    throw std::invalid_argument("engine: scenes of a batch must share the grid geometry");
+            if (d.dx != d0.dx) throw std::invalid_argument("engine: scenes of a batch must share dx");
+        }
         I.hs.push_back(d);
+    }
+    if (!I.hs.empty()) {  // uniform geometry for the kernels' parameter bank
+        const DevScene& d0 = I.hs[0];
+        for (int a = 0; a < 3; ++a) {
+            I.geo.origin[a] = d0.origin[a];
+            I.geo.dims[a] = d0.dims[a];
+            I.geo.nb[a] = d0.nb[a];
+        }
+        I.geo.dx = d0.dx;
+        I.geo.inv_dx = d0.inv_dx;
+        I.geo.m_inv = d0.m_inv;
+        I.geo.bricks_per_scene = static_cast<uint32_t>(d0.nb[0]) * d0.nb[1] * d0.nb[2];
+        I.geo.nodes_per_scene = static_cast<uint64_t>(I.geo.bricks_per_scene) * kBrickNodes;
     }
     I.total_nodes = node_base;
     I.total_bricks = brick_base;
@@ -281,6 +307,7 @@ void Engine::reset_kernel_times() {
 
 void Engine::set_materials(const std::vector<mpmb_material>& m) {
     Impl& I = *impl_;
+    I.hmats = m;
     std::vector<float4> h(std::max<size_t>(1, m.size()));
     for (size_t i = 0; i < m.size(); ++i)
         h[i] = make_float4(static_cast<float>(m[i].kind), m[i].mu, m[i].lambda, m[i].beta);
@@ -514,7 +541,8 @@ void Engine::p2g(bool mls, float dt) {
     Params P = I.params();
     P.dt = dt;
     launch_p2g(P, mls, (I.n + 31) / 32, I.st);
-    I.counted(1);
+    launch_collect_bricks(P, I.total_bricks, I.st);
+    I.counted(2);
     if (mls) I.use_stress_in = false;  // consumed by the first MLS P2G
     I.end(CAT_P2G, ev);
 }

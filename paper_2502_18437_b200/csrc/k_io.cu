@@ -112,7 +112,7 @@ __global__ void k_stress(const Params P, float* out) {
         }
         Part p;
         load_part(P, static_cast<uint32_t>(s), p);
-        const float4 mat = P.mats[flags & kMatMask];
+        const float4 mat = material(P, flags & kMatMask);
         float sig[9];
         neo_hookean(p.F, mat.y, mat.z, sig);
         for (int a = 0; a < 9; ++a) out[9 * o + a] = sig[a];
@@ -134,17 +134,17 @@ __global__ void k_grid_download(const Params P, DevScene S, int64_t n_nodes, flo
         if (P.brick_stamp[gb] == P.epoch)
             a = P.grid_vel[S.node_base + static_cast<uint64_t>(local) * kBrickNodes +
                            ((k & 3) << 4) + ((j & 3) << 2) + (i & 3)];
-        const bool live = a.x > kMassEps;
-        if (mass) mass[q] = a.x;
+        const bool live = a.w > kMassEps;  // node = {x, y, z, mass}
+        if (mass) mass[q] = a.w;
         if (vel) {
-            vel[3 * q + 0] = live ? a.y : 0.f;
-            vel[3 * q + 1] = live ? a.z : 0.f;
-            vel[3 * q + 2] = live ? a.w : 0.f;
+            vel[3 * q + 0] = live ? a.x : 0.f;
+            vel[3 * q + 1] = live ? a.y : 0.f;
+            vel[3 * q + 2] = live ? a.z : 0.f;
         }
         if (mom) {  // solvers.hpp:48, 61: momentum = velocity * mass after the update
-            mom[3 * q + 0] = live ? a.y * a.x : a.y;
-            mom[3 * q + 1] = live ? a.z * a.x : a.z;
-            mom[3 * q + 2] = live ? a.w * a.x : a.w;
+            mom[3 * q + 0] = live ? __fmul_rn(a.x, a.w) : a.x;
+            mom[3 * q + 1] = live ? __fmul_rn(a.y, a.w) : a.y;
+            mom[3 * q + 2] = live ? __fmul_rn(a.z, a.w) : a.z;
         }
     }
 }
@@ -163,8 +163,8 @@ __global__ void k_grid_upload(const Params P, DevScene S, int64_t n_nodes, const
         const bool live = m > kMassEps;
         P.grid_vel[S.node_base + static_cast<uint64_t>(local) * kBrickNodes + ((k & 3) << 4) +
                    ((j & 3) << 2) + (i & 3)] =
-            live ? make_float4(m, vel[3 * q], vel[3 * q + 1], vel[3 * q + 2])
-                 : make_float4(m, mom[3 * q], mom[3 * q + 1], mom[3 * q + 2]);
+            live ? make_float4(vel[3 * q], vel[3 * q + 1], vel[3 * q + 2], m)
+                 : make_float4(mom[3 * q], mom[3 * q + 1], mom[3 * q + 2], m);
     }
 }
 

@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(256) k_bin_keys(const Params P, BinBuffers B) 
             orig = __float_as_uint(r.w);
             if (flags & kActiveBit) {
                 const int scene = static_cast<int>((flags >> kSceneShift) & kSceneMask);
-                const DevScene& S = P.scenes[scene];
+                const SceneView S = scene_view(P, scene);
                 const float4 a = P.pl[0][s];
                 const float x[3] = {a.x, a.y, a.z};
                 int b[3];

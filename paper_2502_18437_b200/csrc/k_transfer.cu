@@ -1,0 +1,593 @@
+// k_transfer.cu — particle <-> grid transfers: P2G (K2 MLS / K5 PB-MPM) and G2P (K4 MLS /
+// K6 PB-MPM, with the F update, push-out and deactivation fused), plus standalone push-out
+// and deactivation for the solver-layer API.
+//
+// Work decomposition: one warp per GROUP of 32 chunks, one lane per chunk (a chunk is a
+// run of <= KMAX particles that shared a stencil base cell at binning time).  The k-th
+// particles of the group's chunks are adjacent in memory (chunk-interleaved layout,
+// k_sort.cu), so at every iteration k the warp's loads are one contiguous span.
+//
+// Latency hiding: each lane stages its particles' planes into shared memory with
+// cp.async (LDGSTS) kStages-1 iterations ahead of use (per-lane ring, no cross-lane
+// hazard), so HBM latency overlaps the arithmetic of the previous particles.
+//
+// P2G accumulates the 27 stencil nodes x {momentum, mass} in registers while the base
+// stays the same (packed FP32x2 FMAs, FFMA2), then flushes with 27 red.global.add.v4.f32.
+// G2P loads the 27 stencil velocities into registers once per base and reuses them.
+#include <cuda_runtime.h>
+
+#include "kernels.cuh"
+#include "launch.h"
+
+namespace mpmb {
+
+constexpr int kStages = 3;
+constexpr int kWarpsPerBlock = 4;
+// resident blocks per SM the register allocation targets (A/B-tuned)
+#ifndef MPMB_P2G_MINB
+#define MPMB_P2G_MINB 3
+#endif
+#ifndef MPMB_G2P_MINB
+#define MPMB_G2P_MINB 3
+#endif
+
+__device__ __forceinline__ void cp_async16(float4* smem, const float4* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+
+// Stage plane set: P2G and PB G2P read all 7 planes; MLS G2P reads x, F and flags only.
+template <int NP>
+struct PlaneSet;
+template <>
+struct PlaneSet<7> {
+    __device__ static constexpr int plane(int q) { return q; }
+};
+template <>
+struct PlaneSet<5> {  // P0 {x, vx}, P3 {C6..8, F0}, P4, P5 {F}, PR
+    __device__ static constexpr int plane(int q) { return q == 0 ? 0 : (q == 4 ? PR : q + 2); }
+};
+
+// Per-lane producer of the staging ring: issues iteration k's plane copies (all lanes
+// call it; lanes without a k-th particle commit an empty group).
+template <int NP>
+struct Stager {
+    float4* buf;     // this warp's ring: [kStages][NP][32]
+    uint32_t slot0;  // first slot of the group
+    uint32_t off;    // particles of iterations < k already issued
+    int len;
+    int lane;
+    unsigned lt;
+    __device__ __forceinline__ void issue(const Params& P, int k) {
+        const unsigned m = __ballot_sync(0xffffffffu, len > k);
+        if (len > k) {
+            const uint32_t s = slot0 + off + __popc(m & lt);
+            float4* dst = buf + (k % kStages) * NP * 32 + lane;
+#pragma unroll
+            for (int q = 0; q < NP; ++q) cp_async16(dst + q * 32, P.pl[PlaneSet<NP>::plane(q)] + s);
+        }
+        off += __popc(m);
+        cp_commit();
+    }
+};
+
+// =====================================================================  P2G
+__device__ __forceinline__ void p2g_flush(const Params& P, const SceneView& S, const int cb[3],
+                                          float2 (&pa)[27], float2 (&pb)[27]) {
+    uint32_t tx[3], ty[3], tz[3];
+    node_offsets(S, cb, tx, ty, tz);
+    float4* g = P.grid_acc + S.node_base;
+#pragma unroll
+    for (int dk = 0; dk < 3; ++dk)
+#pragma unroll
+        for (int dj = 0; dj < 3; ++dj)
+#pragma unroll
+            for (int di = 0; di < 3; ++di) {
+                const int n = (dk * 3 + dj) * 3 + di;
+                atomicAdd(g + (tz[dk] + ty[dj] + tx[di]), make_float4(pa[n].x, pa[n].y, pb[n].x, pb[n].y));
+                pa[n] = f2(0.f, 0.f);
+                pb[n] = f2(0.f, 0.f);
+            }
+    // mark the <= 8 bricks this stencil touches: plain stores of 1 (benign races, no
+    // dependent loads); k_collect_bricks compacts the marks into the active list
+    const int bx0 = cb[0] >> 2, bx1 = (cb[0] + 2) >> 2;
+    const int by0 = cb[1] >> 2, by1 = (cb[1] + 2) >> 2;
+    const int bz0 = cb[2] >> 2, bz1 = (cb[2] + 2) >> 2;
+    uint32_t* f = P.brick_flag + S.brick_base;
+    const int sy = S.nb[0], sz = S.nb[0] * S.nb[1];
+    f[bz0 * sz + by0 * sy + bx0] = 1u;
+    f[bz0 * sz + by0 * sy + bx1] = 1u;
+    f[bz0 * sz + by1 * sy + bx0] = 1u;
+    f[bz0 * sz + by1 * sy + bx1] = 1u;
+    f[bz1 * sz + by0 * sy + bx0] = 1u;
+    f[bz1 * sz + by0 * sy + bx1] = 1u;
+    f[bz1 * sz + by1 * sy + bx0] = 1u;
+    f[bz1 * sz + by1 * sy + bx1] = 1u;
+}
+
+// Active-brick list from the P2G marks (warp-aggregated append; order is irrelevant).
+// Marks are reset here, so the next P2G starts from a clean slate.
+__global__ void __launch_bounds__(256) k_collect_bricks(const Params P, uint32_t n_bricks) {
+    const unsigned full = 0xffffffffu;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t base = blockIdx.x * blockDim.x; base < n_bricks; base += stride) {
+        const uint32_t b = base + threadIdx.x;
+        const bool on = b < n_bricks && P.brick_flag[b] != 0u;
+        const unsigned m = __ballot_sync(full, on);
+        if (m == 0u) continue;
+        uint32_t start = 0;
+        if ((threadIdx.x & 31) == 0) start = atomicAdd(P.n_active_bricks, __popc(m));
+        start = __shfl_sync(full, start, 0);
+        if (on) {
+            P.active_bricks[start + __popc(m & lanemask_lt())] = b;
+            P.brick_flag[b] = 0u;
+        }
+    }
+}
+
+void launch_collect_bricks(const Params& P, uint32_t n_bricks, cudaStream_t st) {
+    int64_t blocks = (static_cast<int64_t>(n_bricks) + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks < 1) blocks = 1;
+    k_collect_bricks<<<static_cast<int>(blocks), 256, 0, st>>>(P, n_bricks);
+}
+
+template <bool MLS>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_p2g(const Params P) {
+    extern __shared__ float4 smem[];
+    constexpr int NP = kPlanes;
+    const int lane = threadIdx.x & 31;
+    const uint32_t n_groups = *P.n_groups;
+    const uint32_t n_chunks = *P.n_chunks;
+    const uint32_t wpb = blockDim.x >> 5;
+    Stager<NP> st;
+    st.buf = smem + (threadIdx.x >> 5) * (kStages * NP * 32);
+    st.lane = lane;
+    st.lt = lanemask_lt();
+    for (uint32_t g = blockIdx.x * wpb + (threadIdx.x >> 5); g < n_groups; g += gridDim.x * wpb) {
+        const uint32_t c = g * 32u + lane;
+        st.len = c < n_chunks ? P.chunk_len[c] : 0;
+        st.slot0 = P.group_base[g];
+        st.off = 0;
+        const int kmax = __reduce_max_sync(0xffffffffu, st.len);
+        for (int k = 0; k < kStages - 1; ++k) st.issue(P, k);
+        float2 pa[27], pb[27];  // (mom_x, mom_y), (mom_z, mass) per stencil node
+#pragma unroll
+        for (int n = 0; n < 27; ++n) {
+            pa[n] = f2(0.f, 0.f);
+            pb[n] = f2(0.f, 0.f);
+        }
+        int cb[3] = {INT_MIN, INT_MIN, INT_MIN};
+        int cscene = -1;
+        for (int k = 0; k < kmax; ++k) {
+            st.issue(P, k + kStages - 1);
+            cp_wait<kStages - 1>();
+            if (st.len <= k) continue;
+            const float4* src = st.buf + (k % kStages) * NP * 32 + lane;
+            const float4 r = src[PR * 32];
+            const uint32_t flags = __float_as_uint(r.z);
+            if (!(flags & kActiveBit)) continue;
+            const float4 q0 = src[0], q1 = src[32], q2 = src[64], q3 = src[96], q4 = src[128], q5 = src[160];
+            const float x[3] = {q0.x, q0.y, q0.z};
+            const float v[3] = {q0.w, q1.x, q1.y};
+            const float Cm[9] = {q1.z, q1.w, q2.x, q2.y, q2.z, q2.w, q3.x, q3.y, q3.z};
+            const int scene = static_cast<int>((flags >> kSceneShift) & kSceneMask);
+            const SceneView S = scene_view(P, scene);
+            int b[3];
+            float fx[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                b[a] = stencil_base(x[a], S.origin[a], S.inv_dx, fx[a]);
+                b[a] = min(max(b[a], 0), S.dims[a] - 3);  // memory guard only
+            }
+            if (b[0] != cb[0] || b[1] != cb[1] || b[2] != cb[2] || scene != cscene) {
+                if (cscene >= 0) p2g_flush(P, scene_view(P, cscene), cb, pa, pb);
+                cb[0] = b[0]; cb[1] = b[1]; cb[2] = b[2];
+                cscene = scene;
+            }
+            const float m = r.x;
+            // affine = m C - dt V (4/dx^2) sigma  (solvers.hpp:154-156; PB: m C, :222)
+            float A[9];
+            if (MLS) {
+                const float F[9] = {q3.w, q4.x, q4.y, q4.z, q4.w, q5.x, q5.y, q5.z, q5.w};
+                float sig[9];
+                float J;  // det F (solvers.hpp:154)
+                if (P.use_stress_in) {  // explicitly uploaded stress cache (solvers.hpp:156)
+                    const float* s9 = P.stress_in + 9ull * __float_as_uint(r.w);
+#pragma unroll
+                    for (int i = 0; i < 9; ++i) sig[i] = s9[i];
+                    J = det3(F);
+                } else {  // cached stress == sigma(F) of the last G2P (solvers.hpp:69-74)
+                    const float4 mat = material(P, flags & kMatMask);
+                    J = neo_hookean_f32(F, mat.y, mat.z, sig);
+                }
+                const float sc = -P.dt * (J * r.y) * S.m_inv;
+#pragma unroll
+                for (int i = 0; i < 9; ++i) A[i] = fmaf(Cm[i], m, sig[i] * sc);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 9; ++i) A[i] = Cm[i] * m;
+            }
+            float w[3][3], rel[3][3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                bspline_w(fx[a], w[a]);
+#pragma unroll
+                for (int o = 0; o < 3; ++o)  // node_position - x (state.hpp:49-51)
+                    rel[a][o] = (S.origin[a] + static_cast<float>(b[a] + o) * S.dx) - x[a];
+            }
+            // node (di,dj,dk) receives w (m v + A (x_I - x_p)) and w m, with
+            //   w (m v + A r) = w_x (w_yz u_jk) + (w_x r_x) (w_yz A_col0),  u_jk = m v + A_col1 r_y + A_col2 r_z
+            // so every per-node op is an FFMA2 with a per-particle scalar broadcast (w_x or
+            // w_x r_x) and a per-row pair.  Pairs: (mom_x, mom_y) and (mom_z, mass) -- the .y
+            // lane of the second carries m through u and 0 through A.
+            const float2 A01_0 = f2(A[0], A[3]), A2m_0 = f2(A[6], 0.f);
+            const float2 A01_1 = f2(A[1], A[4]), A2m_1 = f2(A[7], 0.f);
+            const float2 A01_2 = f2(A[2], A[5]), A2m_2 = f2(A[8], 0.f);
+            const float2 mv01 = f2(v[0] * m, v[1] * m), mv2m = f2(v[2] * m, m);
+            float wr0[3];
+#pragma unroll
+            for (int di = 0; di < 3; ++di) wr0[di] = w[0][di] * rel[0][di];
+#pragma unroll
+            for (int dk = 0; dk < 3; ++dk) {
+                const float rz = rel[2][dk];
+                const float2 uz01 = __ffma2_rn(A01_2, f2(rz, rz), mv01);
+                const float2 uz2m = __ffma2_rn(A2m_2, f2(rz, rz), mv2m);
+#pragma unroll
+                for (int dj = 0; dj < 3; ++dj) {
+                    const float ry = rel[1][dj];
+                    const float wyz = w[1][dj] * w[2][dk];
+                    const float2 U01 = __fmul2_rn(__ffma2_rn(A01_1, f2(ry, ry), uz01), f2(wyz, wyz));
+                    const float2 U2m = __fmul2_rn(__ffma2_rn(A2m_1, f2(ry, ry), uz2m), f2(wyz, wyz));
+                    const float2 G01 = __fmul2_rn(A01_0, f2(wyz, wyz));
+                    const float2 G2m = __fmul2_rn(A2m_0, f2(wyz, wyz));
+#pragma unroll
+                    for (int di = 0; di < 3; ++di) {
+                        const int n = (dk * 3 + dj) * 3 + di;
+                        const float wx = w[0][di], wr = wr0[di];
+                        pa[n] = __ffma2_rn(f2(wx, wx), U01, pa[n]);
+                        pa[n] = __ffma2_rn(f2(wr, wr), G01, pa[n]);
+                        pb[n] = __ffma2_rn(f2(wx, wx), U2m, pb[n]);  // .y: mass += w m
+                        pb[n] = __ffma2_rn(f2(wr, wr), G2m, pb[n]);
+                    }
+                }
+            }
+        }
+        if (cscene >= 0) p2g_flush(P, scene_view(P, cscene), cb, pa, pb);
+    }
+    cp_wait<0>();
+}
+
+// ================================================================  G2P
+// grid_vel node = {v.x, v.y, v.z, mass}; nodes at or below kMassEps contribute nothing
+// (solvers.hpp:186).
+__device__ __forceinline__ void g2p_load_nodes(const Params& P, const SceneView& S, const int b[3],
+                                               float2 (&n01)[27], float (&n2)[27]) {
+    uint32_t tx[3], ty[3], tz[3];
+    node_offsets(S, b, tx, ty, tz);
+    const float4* g = P.grid_vel + S.node_base;
+#pragma unroll
+    for (int dk = 0; dk < 3; ++dk)
+#pragma unroll
+        for (int dj = 0; dj < 3; ++dj)
+#pragma unroll
+            for (int di = 0; di < 3; ++di) {
+                const int n = (dk * 3 + dj) * 3 + di;
+                const float4 q = __ldg(g + (tz[dk] + ty[dj] + tx[di]));
+                const bool live = q.w > kMassEps;
+                n01[n] = live ? f2(q.x, q.y) : f2(0.f, 0.f);
+                n2[n] = live ? q.z : 0.f;
+            }
+}
+
+// v = sum w v_I,  B = sum (w v_I)(x_I - x_p)^T  (solvers.hpp:178-190), summed per row
+// (dk, dj) over di with the x-weights, then scaled by w_y w_z.
+__device__ __forceinline__ void g2p_gather(const float2 (&n01)[27], const float (&n2)[27],
+                                           const float w[3][3], const float rel[3][3], float vn[3],
+                                           float B[9]) {
+    float wr0[3];
+#pragma unroll
+    for (int o = 0; o < 3; ++o) wr0[o] = w[0][o] * rel[0][o];
+    float2 v01 = f2(0.f, 0.f);
+    float v2 = 0.f;
+    float2 c0_01 = f2(0.f, 0.f), c1_01 = f2(0.f, 0.f), c2_01 = f2(0.f, 0.f);
+    float c0_2 = 0.f, c1_2 = 0.f, c2_2 = 0.f;
+#pragma unroll
+    for (int dk = 0; dk < 3; ++dk)
+#pragma unroll
+        for (int dj = 0; dj < 3; ++dj) {
+            float2 a01 = f2(0.f, 0.f), b01 = f2(0.f, 0.f);
+            float a2 = 0.f, b2 = 0.f;  // sum wx v_z, sum wx rx v_z
+#pragma unroll
+            for (int di = 0; di < 3; ++di) {
+                const int n = (dk * 3 + dj) * 3 + di;
+                const float wx = w[0][di], wr = wr0[di];
+                a01 = __ffma2_rn(f2(wx, wx), n01[n], a01);
+                b01 = __ffma2_rn(f2(wr, wr), n01[n], b01);
+                a2 = fmaf(wx, n2[n], a2);
+                b2 = fmaf(wr, n2[n], b2);
+            }
+            const float wyz = w[1][dj] * w[2][dk];
+            const float wy = wyz * rel[1][dj], wz = wyz * rel[2][dk];
+            v01 = __ffma2_rn(f2(wyz, wyz), a01, v01);
+            v2 = fmaf(wyz, a2, v2);
+            c0_01 = __ffma2_rn(f2(wyz, wyz), b01, c0_01);  // column 0: rel_x
+            c0_2 = fmaf(wyz, b2, c0_2);
+            c1_01 = __ffma2_rn(f2(wy, wy), a01, c1_01);    // column 1: rel_y
+            c1_2 = fmaf(wy, a2, c1_2);
+            c2_01 = __ffma2_rn(f2(wz, wz), a01, c2_01);    // column 2: rel_z
+            c2_2 = fmaf(wz, a2, c2_2);
+        }
+    vn[0] = v01.x; vn[1] = v01.y; vn[2] = v2;
+    // B row r = velocity component r, column c = rel component c
+    B[0] = c0_01.x; B[1] = c1_01.x; B[2] = c2_01.x;
+    B[3] = c0_01.y; B[4] = c1_01.y; B[5] = c2_01.y;
+    B[6] = c0_2;    B[7] = c1_2;    B[8] = c2_2;
+}
+
+// Push-out of one particle against the scene's shapes, in order (contact.hpp:140-179).
+__device__ __forceinline__ int pushout_particle(const Params& P, const SceneView& S, float x[3],
+                                                float v[3]) {
+    int pushed = 0;
+    const float clearance = FM(1e-4f, S.dx);
+    for (int si = P.scenes[S.scene].shape_begin; si < P.scenes[S.scene].shape_begin + P.scenes[S.scene].shape_count; ++si) {
+        const DevShape& sh = P.shapes[si];
+        const DevPose& pose = pose_of(P, si);
+        const Sdf s = sdf_query(sh, pose, P.verts, P.ints, mk(x[0], x[1], x[2]));
+        float move = 0.f;
+        if (s.region == REGION_SURFACE || s.region == REGION_SPINE) {
+            if (s.distance < 0.f) move = FA(-s.distance, clearance);
+        } else if (s.region == REGION_EDGE) {
+            const float target = FM(0.5f, sh.hw);
+            const float d = fabsf(s.distance);
+            if (d < target) move = FA(FS(target, d), clearance);
+        } else if (s.region == REGION_CURVE) {
+            const float target = FM(0.5f, sh.hw);
+            if (s.distance < target) move = FA(FS(target, s.distance), clearance);
+        }
+        if (move > 0.f) {
+            x[0] = FA(x[0], FM(s.normal.x, move));
+            x[1] = FA(x[1], FM(s.normal.y, move));
+            x[2] = FA(x[2], FM(s.normal.z, move));
+            const V3 vr = rigid_point_velocity(pose, mk(x[0], x[1], x[2]));
+            const float vn = dot(mk(v[0], v[1], v[2]) - vr, s.normal);
+            if (vn < 0.f) {
+                v[0] = FS(v[0], FM(s.normal.x, vn));
+                v[1] = FS(v[1], FM(s.normal.y, vn));
+                v[2] = FS(v[2], FM(s.normal.z, vn));
+            }
+            ++pushed;
+        }
+    }
+    return pushed;
+}
+
+// F <- (I + C dt) F  (solvers.hpp:194, 275).  F only feeds the stress (never a contact
+// or push-out decision), so it keeps FMA contraction: F + dt (C F).
+__device__ __forceinline__ void update_F(const float C[9], float dt, float F[9]) {
+    float Fn[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            Fn[3 * i + j] = fmaf(dt, fmaf(C[3 * i], F[j], fmaf(C[3 * i + 1], F[3 + j], C[3 * i + 2] * F[6 + j])),
+                                 F[3 * i + j]);
+#pragma unroll
+    for (int i = 0; i < 9; ++i) F[i] = Fn[i];
+}
+
+template <bool PB>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(const Params P) {
+    extern __shared__ float4 smem[];
+    constexpr int NP = PB ? 7 : 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t n_groups = *P.n_groups;
+    const uint32_t n_chunks = *P.n_chunks;
+    const uint32_t wpb = blockDim.x >> 5;
+    Stager<NP> st;
+    st.buf = smem + (threadIdx.x >> 5) * (kStages * NP * 32);
+    st.lane = lane;
+    st.lt = lanemask_lt();
+    for (uint32_t g = blockIdx.x * wpb + (threadIdx.x >> 5); g < n_groups; g += gridDim.x * wpb) {
+        const uint32_t c = g * 32u + lane;
+        st.len = c < n_chunks ? P.chunk_len[c] : 0;
+        st.slot0 = P.group_base[g];
+        st.off = 0;
+        const int kmax = __reduce_max_sync(0xffffffffu, st.len);
+        for (int k = 0; k < kStages - 1; ++k) st.issue(P, k);
+        float2 n01[27];
+        float n2[27];
+        int cb[3] = {INT_MIN, INT_MIN, INT_MIN};
+        int cscene = -1, my_scene = 0;
+        int n_inv = 0, n_fail = 0, n_push = 0, n_deact = 0;
+        uint32_t off_c = 0;
+        for (int k = 0; k < kmax; ++k) {
+            st.issue(P, k + kStages - 1);
+            const unsigned mk_ = __ballot_sync(0xffffffffu, st.len > k);
+            const uint32_t s = st.slot0 + off_c + __popc(mk_ & st.lt);
+            off_c += __popc(mk_);
+            cp_wait<kStages - 1>();
+            if (st.len <= k) continue;
+            const float4* src = st.buf + (k % kStages) * NP * 32 + lane;
+            float4 r = src[(NP - 1) * 32];
+            uint32_t flags = __float_as_uint(r.z);
+            if (!(flags & kActiveBit)) continue;
+            Part p;
+            {
+                const float4 q0 = src[0];
+                p.x[0] = q0.x; p.x[1] = q0.y; p.x[2] = q0.z;
+                if (PB) {
+                    const float4 q1 = src[32], q2 = src[64], q3 = src[96], q4 = src[128], q5 = src[160];
+                    p.C[0] = q1.z; p.C[1] = q1.w; p.C[2] = q2.x; p.C[3] = q2.y; p.C[4] = q2.z;
+                    p.C[5] = q2.w; p.C[6] = q3.x; p.C[7] = q3.y; p.C[8] = q3.z;
+                    p.F[0] = q3.w; p.F[1] = q4.x; p.F[2] = q4.y; p.F[3] = q4.z; p.F[4] = q4.w;
+                    p.F[5] = q5.x; p.F[6] = q5.y; p.F[7] = q5.z; p.F[8] = q5.w;
+                } else {
+                    const float4 q3 = src[32], q4 = src[64], q5 = src[96];
+                    p.F[0] = q3.w; p.F[1] = q4.x; p.F[2] = q4.y; p.F[3] = q4.z; p.F[4] = q4.w;
+                    p.F[5] = q5.x; p.F[6] = q5.y; p.F[7] = q5.z; p.F[8] = q5.w;
+                }
+            }
+            const int scene = static_cast<int>((flags >> kSceneShift) & kSceneMask);
+            my_scene = scene;
+            const SceneView S = scene_view(P, scene);
+            int b[3];
+            float fx[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                b[a] = stencil_base(p.x[a], S.origin[a], S.inv_dx, fx[a]);
+                b[a] = min(max(b[a], 0), S.dims[a] - 3);
+            }
+            if (b[0] != cb[0] || b[1] != cb[1] || b[2] != cb[2] || scene != cscene) {
+                g2p_load_nodes(P, S, b, n01, n2);
+                cb[0] = b[0]; cb[1] = b[1]; cb[2] = b[2];
+                cscene = scene;
+            }
+            float w[3][3], rel[3][3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                bspline_w(fx[a], w[a]);
+#pragma unroll
+                for (int o = 0; o < 3; ++o)
+                    rel[a][o] = (S.origin[a] + static_cast<float>(b[a] + o) * S.dx) - p.x[a];
+            }
+            float B[9];
+            g2p_gather(n01, n2, w, rel, p.v, B);
+            bool do_commit;
+            if (!PB) {  // solvers.hpp:191-195
+#pragma unroll
+                for (int i = 0; i < 9; ++i) p.C[i] = B[i] * S.m_inv;
+                do_commit = true;
+            } else {  // solvers.hpp:259-267
+                float Cc[9], Cn[9];
+#pragma unroll
+                for (int i = 0; i < 9; ++i) Cc[i] = B[i] * S.m_inv;
+                const float4 mat = material(P, flags & kMatMask);
+                if (corotational_project(p.F, Cc, P.dt, mat.w, Cn)) {
+#pragma unroll
+                    for (int i = 0; i < 9; ++i) p.C[i] = Cn[i];
+                } else {
+                    ++n_fail;
+                }
+                do_commit = P.commit != 0;
+            }
+            if (do_commit) {  // solvers.hpp:193-195 / 274-276
+                p.x[0] = FA(p.x[0], FM(p.v[0], P.dt));
+                p.x[1] = FA(p.x[1], FM(p.v[1], P.dt));
+                p.x[2] = FA(p.x[2], FM(p.v[2], P.dt));
+                update_F(p.C, P.dt, p.F);
+                if (det3(p.F) <= 0.f) ++n_inv;
+                if (P.pushout && P.scenes[S.scene].shape_count > 0) n_push += pushout_particle(P, S, p.x, p.v);
+                if (P.deactivate && !spline_in_domain(mk(p.x[0], p.x[1], p.x[2]), S)) {
+                    flags &= ~kActiveBit;
+                    r.z = __uint_as_float(flags);
+                    P.pl[PR][s] = r;
+                    ++n_deact;
+                }
+            }
+            store_part(P, s, p);
+        }
+        add_scene_counter(P.counters, my_scene, 0, n_inv);
+        add_scene_counter(P.counters, my_scene, 1, n_fail);
+        add_scene_counter(P.counters, my_scene, 2, n_push);
+        add_scene_counter(P.counters, my_scene, 3, n_deact);
+    }
+    cp_wait<0>();
+}
+
+// ================================================  standalone push-out / deactivation
+__global__ void k_pushout(const Params P) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < P.n_total; base += stride) {
+        const int64_t s = base + threadIdx.x;
+        int pushed = 0, scene = 0;
+        if (s < P.n_total) {
+            const float4 r = P.pl[PR][s];
+            const uint32_t flags = __float_as_uint(r.z);
+            if (flags & kActiveBit) {
+                scene = static_cast<int>((flags >> kSceneShift) & kSceneMask);
+                const SceneView S = scene_view(P, scene);
+                if (P.scenes[S.scene].shape_count > 0) {
+                    float4 a = P.pl[0][s], b = P.pl[1][s];
+                    float x[3] = {a.x, a.y, a.z}, v[3] = {a.w, b.x, b.y};
+                    pushed = pushout_particle(P, S, x, v);
+                    if (pushed) {
+                        P.pl[0][s] = make_float4(x[0], x[1], x[2], v[0]);
+                        P.pl[1][s] = make_float4(v[1], v[2], b.z, b.w);
+                    }
+                }
+            }
+        }
+        add_scene_counter(P.counters, scene, 2, pushed);
+    }
+}
+
+__global__ void k_deactivate(const Params P) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < P.n_total; base += stride) {
+        const int64_t s = base + threadIdx.x;
+        int d = 0, scene = 0;
+        if (s < P.n_total) {
+            float4 r = P.pl[PR][s];
+            uint32_t flags = __float_as_uint(r.z);
+            if (flags & kActiveBit) {
+                scene = static_cast<int>((flags >> kSceneShift) & kSceneMask);
+                const float4 a = P.pl[0][s];
+                if (!spline_in_domain(mk(a.x, a.y, a.z), scene_view(P, scene))) {
+                    r.z = __uint_as_float(flags & ~kActiveBit);
+                    P.pl[PR][s] = r;
+                    d = 1;
+                }
+            }
+        }
+        add_scene_counter(P.counters, scene, 3, d);
+    }
+}
+
+// ===================================================================  launchers
+static int grid_for(int64_t work, int threads, int max_blocks) {
+    int64_t b = (work + threads - 1) / threads;
+    if (b < 1) b = 1;
+    if (b > max_blocks) b = max_blocks;
+    return static_cast<int>(b);
+}
+
+// dynamic shared memory per block: 4 warps x 3 stages x <=7 planes x 32 x 16 B <= 43 KB
+// (below the 48 KB default, no opt-in attribute needed)
+void launch_p2g(const Params& P, bool mls, int64_t max_groups, cudaStream_t st) {
+    const int threads = kWarpsPerBlock * 32;
+    const int smem = kWarpsPerBlock * kStages * kPlanes * 32 * static_cast<int>(sizeof(float4));
+    const int blocks = grid_for(max_groups * 32, threads, 148 * 16);
+    if (mls) {
+        k_p2g<true><<<blocks, threads, smem, st>>>(P);
+    } else {
+        k_p2g<false><<<blocks, threads, smem, st>>>(P);
+    }
+}
+
+void launch_g2p(const Params& P, bool pb, int64_t max_groups, cudaStream_t st) {
+    const int threads = kWarpsPerBlock * 32;
+    const int blocks = grid_for(max_groups * 32, threads, 148 * 16);
+    if (pb) {
+        const int smem = kWarpsPerBlock * kStages * 7 * 32 * static_cast<int>(sizeof(float4));
+        k_g2p<true><<<blocks, threads, smem, st>>>(P);
+    } else {
+        const int smem = kWarpsPerBlock * kStages * 5 * 32 * static_cast<int>(sizeof(float4));
+        k_g2p<false><<<blocks, threads, smem, st>>>(P);
+    }
+}
+
+void launch_pushout(const Params& P, cudaStream_t st) {
+    k_pushout<<<grid_for(P.n_total, 256, 148 * 8), 256, 0, st>>>(P);
+}
+
+void launch_deactivate(const Params& P, cudaStream_t st) {
+    k_deactivate<<<grid_for(P.n_total, 256, 148 * 8), 256, 0, st>>>(P);
+}
+
+}  // namespace mpmb

@@ -32,7 +32,9 @@ constexpr int PR = 6;
 
 struct Params {
     float4* pl[kPlanes];
-    const DevScene* scenes;
+    Geo geo;                             // uniform geometry of all scenes
+    float4 mats_c[kMaxConstMats];        // {kind, mu, lambda, beta}, first kMaxConstMats materials
+    const DevScene* scenes;              // per scene: shape range (and host bookkeeping)
     const DevShape* shapes;
     const float* verts;
     const int* ints;
@@ -73,6 +75,38 @@ struct Params {
     int commit;
 };
 
+// Per-scene view of the uniform geometry: scene-dependent offsets are scene x stride.
+struct SceneView {
+    float origin[3];
+    float dx, inv_dx, m_inv;
+    int dims[3];
+    int nb[3];
+    uint64_t node_base;
+    uint32_t brick_base;
+    int scene;
+};
+
+__device__ __forceinline__ SceneView scene_view(const Params& P, int scene) {
+    SceneView s;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        s.origin[a] = P.geo.origin[a];
+        s.dims[a] = P.geo.dims[a];
+        s.nb[a] = P.geo.nb[a];
+    }
+    s.dx = P.geo.dx;
+    s.inv_dx = P.geo.inv_dx;
+    s.m_inv = P.geo.m_inv;
+    s.node_base = static_cast<uint64_t>(scene) * P.geo.nodes_per_scene;
+    s.brick_base = static_cast<uint32_t>(scene) * P.geo.bricks_per_scene;
+    s.scene = scene;
+    return s;
+}
+
+__device__ __forceinline__ float4 material(const Params& P, uint32_t id) {
+    return id < kMaxConstMats ? P.mats_c[id] : P.mats[id];
+}
+
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -111,7 +145,7 @@ __device__ __forceinline__ const DevPose& pose_of(const Params& P, int i) {
 
 // Offsets of the bricked node layout along each axis for stencil base b:
 // node index = tz[dk] + ty[dj] + tx[di] within the scene's node pool.
-__device__ __forceinline__ void node_offsets(const DevScene& S, const int b[3], uint32_t tx[3],
+__device__ __forceinline__ void node_offsets(const SceneView& S, const int b[3], uint32_t tx[3],
                                              uint32_t ty[3], uint32_t tz[3]) {
     const uint32_t sy = static_cast<uint32_t>(S.nb[0]) * kBrickNodes;
     const uint32_t sz = sy * static_cast<uint32_t>(S.nb[1]);
