@@ -53,11 +53,30 @@ def parse():
     return ap.parse_args()
 
 
+def shard_replicas(rank, replicas):
+    """Replica ids of this rank: a contiguous block of `replicas` (weak scaling; replica r
+    has seed 4242 + r and its own blade jitter, so the union over ranks is 0..N*R-1)."""
+    return list(range(rank * replicas, (rank + 1) * replicas))
+
+
 def workload_specs(name, rank, replicas):
     from paper_2502_18437_b200 import scenes
     if name == "c5":
-        return [scenes.c5_cutting_replica(rank * replicas + i) for i in range(replicas)]
+        return [scenes.c5_cutting_replica(r) for r in shard_replicas(rank, replicas)]
     return [{"c1": scenes.c1_cube_drop, "c2": scenes.c2_cutting, "c3": scenes.c3_suture}[name]()]
+
+
+def reduce_over_ranks(ms, ms_e2e, n_particles, world, device):
+    """Whole-job timing = MAX over ranks of the device-timed region; particle count = SUM."""
+    if world <= 1:
+        return ms, ms_e2e, float(n_particles)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([ms, ms_e2e], device=device, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    cnt = torch.tensor([float(n_particles)], device=device, dtype=torch.float64)
+    dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
+    return float(t[0]), float(t[1]), float(cnt[0])
 
 
 def workload_desc(name, replicas, n_per_gpu):
@@ -290,16 +309,7 @@ def run_ours(args, rank, world, local_rank):
     f1.synchronize()
     ms_e2e = f0.elapsed_time(f1)
 
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([ms, ms_e2e], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, ms_e2e = float(t[0]), float(t[1])
-        cnt = torch.tensor([float(n_particles)], device="cuda", dtype=torch.float64)
-        dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
-        n_total = float(cnt[0])
-    else:
-        n_total = float(n_particles)
+    ms, ms_e2e, n_total = reduce_over_ranks(ms, ms_e2e, n_particles, world, "cuda")
 
     ps = n_total * sub * args.steps
     value = ps / (ms / 1e3)
