@@ -196,6 +196,7 @@ extern "C" mpmb_status mpmb_state_create(const int32_t dims[3], float dx, const 
         }
         st->grid.dx = dx;
         st->eng = std::make_unique<Engine>(std::vector<SceneGrid>{st->grid});
+        st->eng->enable_grid_readback();  // the solver-layer API exposes the grid
         *out = st.release();
         return MPMB_OK;
     });

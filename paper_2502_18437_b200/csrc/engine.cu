@@ -80,6 +80,7 @@ struct Engine::Impl {
     DevBuf d_scenes;
     uint64_t total_nodes = 0;
     uint32_t total_bricks = 0;
+    DevBuf dead_mom;  // grid readback only (enable_grid_readback)
     DevBuf grid_acc, grid_vel, brick_flag, brick_stamp, active_bricks, brick_scene, misc;
     // misc u32 slots: [0] n_active_bricks
     int64_t n = 0;
@@ -87,8 +88,7 @@ struct Engine::Impl {
     int cur = 0;
     bool binned = false;
     DevBuf b_count, b_off, b_key, b_rank, b_cell, b_orig, e_orig, e_cell, e_src, b_tmp, g_orig,
-        g_src, g_cell, s_src, s_orig, s_rank, b_flag, c_start, c_len, g_base, b_counts, scan_tmp,
-        key_by_orig;
+        g_src, g_cell, s_src, s_orig, b_counts, scan_tmp, key_by_orig, order, group_nact;
     BinBuffers bb{};
     DevBuf mats;
     DevBuf shapes, verts, ints, free_pose, pose_table, pose_override;
@@ -171,14 +171,14 @@ struct Engine::Impl {
         P.mats = mats.as<float4>();
         P.grid_acc = grid_acc.as<float4>();
         P.grid_vel = grid_vel.as<float4>();
+        P.dead_mom = dead_mom.p ? dead_mom.as<float4>() : nullptr;
         P.brick_flag = brick_flag.as<uint32_t>();
         P.brick_stamp = brick_stamp.as<uint32_t>();
         P.active_bricks = active_bricks.as<uint32_t>();
         P.n_active_bricks = misc.as<uint32_t>();
         P.brick_scene = brick_scene.as<uint32_t>();
-        P.group_base = g_base.as<uint32_t>();
-        P.chunk_len = c_len.as<uint8_t>();
-        P.n_chunks = b_counts.as<uint32_t>();
+        P.order = order.as<uint8_t>();  // per-substep group order (k_transfer.cu)
+        P.group_nact = group_nact.as<uint32_t>();
         P.n_groups = b_counts.as<uint32_t>() + 1;
         P.n_active = b_counts.as<uint32_t>() + 2;
         P.n_total = n;
@@ -216,7 +216,8 @@ Engine::Engine(const std::vector<SceneGrid>& scenes) : impl_(new Impl), scenes_(
         d.node_base = node_base;
         d.brick_base = brick_base;
         const uint64_t nb = static_cast<uint64_t>(d.nb[0]) * d.nb[1] * d.nb[2];
-        if (brick_base + nb >= 0xFFFFFFF0ull) throw std::invalid_argument("engine: too many grid bricks");
+        // brick ids are 32-bit; the brick flags/stamps are one word per brick
+        if (brick_base + nb >= (1ull << 31)) throw std::invalid_argument("engine: too many grid bricks (>2^31)");
         node_base += nb * kBrickNodes;
         brick_base += static_cast<uint32_t>(nb);
         if (!I.hs.empty()) {
@@ -332,8 +333,9 @@ void Engine::upload_particles(int64_t n, const float* x, const float* v, const f
     I.b_key.alloc(4 * N); I.b_rank.alloc(4 * N); I.b_cell.alloc(N); I.b_orig.alloc(4 * N);
     I.e_orig.alloc(4 * N); I.e_cell.alloc(N); I.e_src.alloc(4 * N); I.b_tmp.alloc(4 * N);
     I.g_orig.alloc(4 * N); I.g_src.alloc(4 * N); I.g_cell.alloc(N); I.s_src.alloc(4 * N);
-    I.s_orig.alloc(4 * N); I.s_rank.alloc(4 * N); I.b_flag.alloc(4 * (N + 1));
-    I.c_start.alloc(4 * N); I.c_len.alloc(N); I.g_base.alloc(4 * (N / 32 + 2));
+    I.s_orig.alloc(4 * N);
+    const size_t n_groups = (N + kGroup - 1) / kGroup;
+    I.order.alloc(kGroup * n_groups); I.group_nact.alloc(4 * n_groups);
     const size_t nbk = static_cast<size_t>(I.total_bricks) + 1;
     I.b_count.alloc(4 * nbk);
     I.b_off.alloc(4 * (nbk + 1));
@@ -346,9 +348,8 @@ void Engine::upload_particles(int64_t n, const float* x, const float* v, const f
     B.orig = I.b_orig.as<uint32_t>(); B.e_orig = I.e_orig.as<uint32_t>(); B.e_cell = I.e_cell.as<uint8_t>();
     B.e_src = I.e_src.as<uint32_t>(); B.tmp = I.b_tmp.as<uint32_t>(); B.g_orig = I.g_orig.as<uint32_t>();
     B.g_src = I.g_src.as<uint32_t>(); B.g_cell = I.g_cell.as<uint8_t>(); B.sorted_src = I.s_src.as<uint32_t>();
-    B.sorted_orig = I.s_orig.as<uint32_t>(); B.rank_in_cell = I.s_rank.as<uint32_t>();
-    B.flag = I.b_flag.as<uint32_t>(); B.chunk_start = I.c_start.as<uint32_t>(); B.chunk_len = I.c_len.as<uint8_t>();
-    B.group_base = I.g_base.as<uint32_t>(); B.counts = I.b_counts.as<uint32_t>(); B.scan_tmp = I.scan_tmp.as<uint32_t>();
+    B.sorted_orig = I.s_orig.as<uint32_t>();
+    B.counts = I.b_counts.as<uint32_t>(); B.scan_tmp = I.scan_tmp.as<uint32_t>();
     B.key_by_orig = nullptr;
     if (n == 0) {
         I.binned = false;
@@ -540,7 +541,7 @@ void Engine::p2g(bool mls, float dt) {
     cudaMemsetAsync(I.misc.p, 0, sizeof(uint32_t), I.st);  // active brick count
     Params P = I.params();
     P.dt = dt;
-    launch_p2g(P, mls, (I.n + 31) / 32, I.st);
+    launch_p2g(P, mls, (I.n + kGroup - 1) / kGroup, I.st);
     launch_collect_bricks(P, I.total_bricks, I.st);
     I.counted(2);
     if (mls) I.use_stress_in = false;  // consumed by the first MLS P2G
@@ -575,7 +576,7 @@ void Engine::g2p_mls(int sub, float dt, bool pushout, bool deactivate) {
     P.pushout = pushout ? 1 : 0;
     P.deactivate = deactivate ? 1 : 0;
     P.commit = 1;
-    launch_g2p(P, false, (I.n + 31) / 32, I.st);
+    launch_g2p(P, false, (I.n + kGroup - 1) / kGroup, I.st);
     I.counted(1);
     I.end(CAT_G2P, ev);
 }
@@ -590,7 +591,7 @@ void Engine::g2p_pb(int sub, float dt, bool commit, bool pushout, bool deactivat
     P.commit = commit ? 1 : 0;
     P.pushout = pushout ? 1 : 0;
     P.deactivate = deactivate ? 1 : 0;
-    launch_g2p(P, true, (I.n + 31) / 32, I.st);
+    launch_g2p(P, true, (I.n + kGroup - 1) / kGroup, I.st);
     I.counted(1);
     I.end(CAT_G2P, ev);
 }
@@ -714,6 +715,13 @@ void Engine::snapshot(float* x, float* v, uint8_t* active, std::vector<double>& 
     totals.assign(5 * S, 0.0);
     check(cudaMemcpyAsync(totals.data(), I.io_tot.p, sizeof(double) * 5 * S, cudaMemcpyDeviceToHost, I.st), "d2h");
     check(cudaStreamSynchronize(I.st), "snapshot");
+}
+
+void Engine::enable_grid_readback() {
+    Impl& I = *impl_;
+    if (I.dead_mom.p) return;
+    I.dead_mom.alloc(sizeof(float4) * I.total_nodes);
+    check(cudaMemsetAsync(I.dead_mom.p, 0, sizeof(float4) * I.total_nodes, I.st), "memset");
 }
 
 void Engine::download_grid(int scene, float* mass, float* mom, float* vel) {

@@ -2,8 +2,8 @@
 //
 // One Engine holds a BATCH of independent scenes (1 for a plain Scene / SimState)
 // resident in HBM and advances all of them with one launch per kernel:
-//   particles  : 7 float4 planes per particle slot (112 B), cell-sorted, laid out
-//                warp-interleaved by chunk
+//   particles  : 7 float4 planes per particle slot (112 B), sorted by (brick, cell) at
+//                binning; P2G re-sorts each 256-slot group every substep
 //   grid       : per-scene dense virtual grid in 4x4x4-node bricks (float4 nodes),
 //                only bricks touched by P2G are updated/cleared
 //   shapes     : flattened shape table + per-substep pose table + free-body poses
@@ -84,7 +84,7 @@ class Engine {
     std::vector<DevPose> read_free_poses();
 
     // ---- hot path (enqueue only) ----
-    void bin();                                   // K1: keys, sort, chunks, gather
+    void bin();                                   // K1: keys, stable sort, gather
     void p2g(bool mls, float dt);                 // K2 / K5
     void grid_update(int sub, float dt, const float g[3], bool gravity, bool contact, int bc);
     void g2p_mls(int sub, float dt, bool pushout, bool deactivate);   // K4
@@ -107,6 +107,9 @@ class Engine {
     void snapshot(float* x, float* v, uint8_t* active, std::vector<double>& totals /*5 per scene*/);
     // dense grid of one scene (node-major i + nx*(j + ny*k)); for tests and the hook adapter
     void download_grid(int scene, float* mass, float* momentum, float* velocity);
+    // keep the momentum of nodes below kMassEps for download_grid (one more float4 per node;
+    // the batched hot path leaves it off)
+    void enable_grid_readback();
     void upload_grid_velocity(int scene, const float* mass, const float* momentum,
                               const float* velocity);
     // keys/perm of the binning stage (original indices), see mpmb_bin_particles

@@ -120,7 +120,8 @@ __global__ void k_stress(const Params P, float* out) {
 }
 
 // Dense node-major export of one scene's grid after the last update: nodes of bricks
-// updated in the current epoch carry {mass, velocity} (or {mass, momentum} below eps).
+// updated in the current epoch carry {mass, velocity}; below eps the momentum is in
+// dead_mom (allocated by Engine::enable_grid_readback).
 __global__ void k_grid_download(const Params P, DevScene S, int64_t n_nodes, float* mass,
                                 float* mom, float* vel) {
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -131,10 +132,11 @@ __global__ void k_grid_download(const Params P, DevScene S, int64_t n_nodes, flo
         const uint32_t local = ((k >> 2) * S.nb[1] + (j >> 2)) * S.nb[0] + (i >> 2);
         const uint32_t gb = S.brick_base + local;
         float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (P.brick_stamp[gb] == P.epoch)
-            a = P.grid_vel[S.node_base + static_cast<uint64_t>(local) * kBrickNodes +
-                           ((k & 3) << 4) + ((j & 3) << 2) + (i & 3)];
+        const uint64_t idx = S.node_base + static_cast<uint64_t>(local) * kBrickNodes + ((k & 3) << 4) +
+                             ((j & 3) << 2) + (i & 3);
+        if (P.brick_stamp[gb] == P.epoch) a = P.grid_vel[idx];
         const bool live = a.w > kMassEps;  // node = {x, y, z, mass}
+        if (!live && P.brick_stamp[gb] == P.epoch && P.dead_mom) a = P.dead_mom[idx];
         if (mass) mass[q] = a.w;
         if (vel) {
             vel[3 * q + 0] = live ? a.x : 0.f;
@@ -161,10 +163,11 @@ __global__ void k_grid_upload(const Params P, DevScene S, int64_t n_nodes, const
         if (P.brick_stamp[gb] != P.epoch) continue;
         const float m = mass[q];
         const bool live = m > kMassEps;
-        P.grid_vel[S.node_base + static_cast<uint64_t>(local) * kBrickNodes + ((k & 3) << 4) +
-                   ((j & 3) << 2) + (i & 3)] =
-            live ? make_float4(vel[3 * q], vel[3 * q + 1], vel[3 * q + 2], m)
-                 : make_float4(mom[3 * q], mom[3 * q + 1], mom[3 * q + 2], m);
+        const uint64_t idx = S.node_base + static_cast<uint64_t>(local) * kBrickNodes + ((k & 3) << 4) +
+                             ((j & 3) << 2) + (i & 3);
+        P.grid_vel[idx] = live ? make_float4(vel[3 * q], vel[3 * q + 1], vel[3 * q + 2], m)
+                               : make_float4(0.f, 0.f, 0.f, m);
+        if (!live && P.dead_mom) P.dead_mom[idx] = make_float4(mom[3 * q], mom[3 * q + 1], mom[3 * q + 2], m);
     }
 }
 

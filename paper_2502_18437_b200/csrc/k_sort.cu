@@ -1,5 +1,5 @@
-// k_sort.cu — K1: particle binning / stable sort by (brick, cell, original index) and the
-// warp-interleaved chunk layout consumed by P2G/G2P.  No reference function exists for
+// k_sort.cu — K1: particle binning / stable sort by (brick, cell, original index), run once
+// per frame (or per resort interval); P2G refines each 256-slot group every substep.  No reference function exists for
 // this stage (the reference transfers in particle-index order, solvers.hpp:151); the
 // key arithmetic is the reference's stencil base (math.hpp:219-223, bit-exact).
 //
@@ -8,9 +8,8 @@
 //   scan      bucket offsets (exclusive scan; the inactive bucket is last)
 //   scatter   entries to their bucket
 //   local     per bucket: counting sort by cell (64 bins) + rank by original index in
-//             the cell -> (brick, cell, original index) order, rank-in-cell
-//   chunks    chunk = run of <= KMAX particles of one cell; chunk starts by scan
-//   gather    physical permutation of the 7 planes into the chunk-interleaved layout
+//             the cell -> (brick, cell, original index) order
+//   gather    physical permutation of the 7 planes into that order
 #include <cuda_runtime.h>
 
 #include "launch.h"
@@ -182,7 +181,6 @@ __global__ void __launch_bounds__(256) k_bin_local(BinBuffers B) {
             for (uint32_t q = beg + threadIdx.x; q < end; q += blockDim.x) {
                 B.sorted_src[q] = B.e_src[q];
                 B.sorted_orig[q] = B.e_orig[q];
-                B.rank_in_cell[q] = 0u;
             }
             continue;
         }
@@ -220,73 +218,25 @@ __global__ void __launch_bounds__(256) k_bin_local(BinBuffers B) {
             for (uint32_t f = lo; f < hi; ++f) rk += B.g_orig[f] < o ? 1u : 0u;
             B.sorted_src[lo + rk] = B.g_src[q];
             B.sorted_orig[lo + rk] = o;
-            B.rank_in_cell[lo + rk] = rk;
         }
         __syncthreads();
     }
 }
 
-__global__ void __launch_bounds__(256) k_chunk_flags(BinBuffers B, int64_t n) {
-    const uint32_t n_active = B.bucket_off[B.n_buckets - 1];
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < n; q += stride)
-        B.tmp[q] = (q < n_active && (B.rank_in_cell[q] % KMAX) == 0u) ? 1u : 0u;
-}
-
-__global__ void __launch_bounds__(256) k_chunk_emit(BinBuffers B, int64_t n) {
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < n; q += stride)
-        if (B.tmp[q]) B.chunk_start[B.flag[q]] = static_cast<uint32_t>(q);
-}
-
-__global__ void __launch_bounds__(256) k_chunk_finalize(BinBuffers B, int64_t n) {
-    const uint32_t n_chunks = B.flag[n];
-    const uint32_t n_active = B.bucket_off[B.n_buckets - 1];
+// Physical permutation of the 7 planes into the sorted order (coalesced writes), and the
+// counts the transfers read: [0] n_active, [1] transfer groups, [2] n_active.
+__global__ void __launch_bounds__(256) k_bin_gather(const Params P, BinBuffers B, int64_t n_total,
+                                                    float4* n0, float4* n1, float4* n2, float4* n3,
+                                                    float4* n4, float4* n5, float4* n6) {
+    float4* np[kPlanes] = {n0, n1, n2, n3, n4, n5, n6};
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        B.counts[0] = n_chunks;
-        B.counts[1] = (n_chunks + 31u) / 32u;
+        const uint32_t n_active = B.bucket_off[B.n_buckets - 1];
+        B.counts[0] = n_active;
+        B.counts[1] = (n_active + kGroup - 1) / kGroup;
         B.counts[2] = n_active;
     }
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; c < n_chunks; c += stride) {
-        const uint32_t st = B.chunk_start[c];
-        const uint32_t en = (c + 1 < n_chunks) ? B.chunk_start[c + 1] : n_active;
-        B.chunk_len[c] = static_cast<uint8_t>(en - st);
-        if ((c & 31) == 0) B.group_base[c >> 5] = st;
-    }
-}
-
-// Warp per group of 32 chunks: the k-th particles of the group's chunks become adjacent.
-__global__ void __launch_bounds__(256) k_group_gather(const Params P, BinBuffers B, int64_t n_total,
-                                                      float4* n0, float4* n1, float4* n2, float4* n3,
-                                                      float4* n4, float4* n5, float4* n6) {
-    float4* np[kPlanes] = {n0, n1, n2, n3, n4, n5, n6};
-    const uint32_t n_chunks = B.counts[0], n_groups = B.counts[1], n_active = B.counts[2];
-    const int lane = threadIdx.x & 31;
-    const unsigned lt = lanemask_lt();
-    const uint32_t wpb = blockDim.x >> 5;
-    const uint32_t gw = blockIdx.x * wpb + (threadIdx.x >> 5), nw = gridDim.x * wpb;
-    for (uint32_t g = gw; g < n_groups; g += nw) {
-        const uint32_t c = g * 32u + lane;
-        const int len = c < n_chunks ? B.chunk_len[c] : 0;
-        const uint32_t st = c < n_chunks ? B.chunk_start[c] : 0u;
-        const uint32_t base = B.group_base[g];
-        uint32_t off = 0;
-        for (int k = 0; k < KMAX; ++k) {
-            const unsigned mask = __ballot_sync(0xffffffffu, len > k);
-            if (!mask) break;
-            if (len > k) {
-                const uint32_t src = B.sorted_src[st + k];
-                const uint32_t dst = base + off + __popc(mask & lt);
-#pragma unroll
-                for (int q = 0; q < kPlanes; ++q) np[q][dst] = P.pl[q][src];
-            }
-            off += __popc(mask);
-        }
-    }
-    // inactive tail keeps the bucket order
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t q = n_active + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < n_total; q += stride) {
+    for (int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < n_total; q += stride) {
         const uint32_t src = B.sorted_src[q];
 #pragma unroll
         for (int p = 0; p < kPlanes; ++p) np[p][q] = P.pl[p][src];
@@ -308,14 +258,10 @@ void launch_bin(const Params& P, const BinBuffers& B, float4* const new_planes[k
     launch_exclusive_scan(B.bucket_count, B.bucket_off, B.n_buckets, B.scan_tmp, st, launches);
     k_bin_scatter<<<blocks_for(n_total, 256, cap), 256, 0, st>>>(B, n_total);
     k_bin_local<<<blocks_for(static_cast<int64_t>(B.n_buckets) * 256, 256, 148 * 8), 256, 0, st>>>(B);
-    k_chunk_flags<<<blocks_for(n_total, 256, cap), 256, 0, st>>>(B, n_total);
-    launch_exclusive_scan(B.tmp, B.flag, n_total, B.scan_tmp, st, launches);
-    k_chunk_emit<<<blocks_for(n_total, 256, cap), 256, 0, st>>>(B, n_total);
-    k_chunk_finalize<<<blocks_for(n_total, 256, cap), 256, 0, st>>>(B, n_total);
-    k_group_gather<<<blocks_for(n_total, 256, cap), 256, 0, st>>>(
+    k_bin_gather<<<blocks_for(n_total, 256, cap), 256, 0, st>>>(
         P, B, n_total, new_planes[0], new_planes[1], new_planes[2], new_planes[3],
         new_planes[4], new_planes[5], new_planes[6]);
-    *launches += 7;
+    *launches += 4;
 }
 
 }  // namespace mpmb

@@ -89,7 +89,10 @@ __global__ void __launch_bounds__(256) k_grid_update(const Params P) {
             }
             P.grid_vel[idx] = make_float4(v.x, v.y, v.z, m);
         } else {
-            P.grid_vel[idx] = a;  // below kMassEps: velocity undefined, keep momentum
+            // below kMassEps: G2P skips the node (solvers.hpp:186) -- a zero velocity makes
+            // its contribution vanish without a per-node test; the momentum stays readable
+            P.grid_vel[idx] = make_float4(0.f, 0.f, 0.f, m);
+            if (P.dead_mom) P.dead_mom[idx] = a;
         }
     }
 }

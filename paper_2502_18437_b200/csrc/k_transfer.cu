@@ -2,10 +2,13 @@
 // K6 PB-MPM, with the F update, push-out and deactivation fused), plus standalone push-out
 // and deactivation for the solver-layer API.
 //
-// Work decomposition: one warp per GROUP of 32 chunks, one lane per chunk (a chunk is a
-// run of <= KMAX particles that shared a stencil base cell at binning time).  The k-th
-// particles of the group's chunks are adjacent in memory (chunk-interleaved layout,
-// k_sort.cu), so at every iteration k the warp's loads are one contiguous span.
+// Work decomposition: one warp per GROUP of kGroup (256) consecutive slots.  The slots were
+// ordered by (brick, cell) at the last binning (k_sort.cu), so a group covers a compact
+// region; particles drift during a frame, so the group is RE-SORTED every substep inside
+// P2G by its current stencil base: a warp counting sort over kBins shared-memory bins keyed
+// by (brick low bits, cell).  Lane L then takes sorted positions [8L, 8L+8): runs of equal
+// base are consecutive, whatever the drift since binning.  P2G stores the order (one byte
+// per position) and G2P of the same substep replays it (x is unchanged in between).
 //
 // Latency hiding: each lane stages its particles' planes into shared memory with
 // cp.async (LDGSTS) kStages-1 iterations ahead of use (per-lane ring, no cross-lane
@@ -23,6 +26,10 @@ namespace mpmb {
 
 constexpr int kStages = 3;
 constexpr int kWarpsPerBlock = 4;
+constexpr int kPer = kGroup / 32;  // sorted positions per lane
+constexpr int kBins = 512;         // sort bins: ((global brick & 7) << 6) | cell
+constexpr int kBinWords = kBins + kBins / 32;  // one pad word per 32 bins (conflict-free scan)
+static_assert(kPer == 8, "order bytes are read as one u64 per lane");
 // resident blocks per SM the register allocation targets (A/B-tuned)
 #ifndef MPMB_P2G_MINB
 #define MPMB_P2G_MINB 3
@@ -33,7 +40,7 @@ constexpr int kWarpsPerBlock = 4;
 
 __device__ __forceinline__ void cp_async16(float4* smem, const float4* gmem) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
@@ -53,47 +60,44 @@ struct PlaneSet<5> {  // P0 {x, vx}, P3 {C6..8, F0}, P4, P5 {F}, PR
     __device__ static constexpr int plane(int q) { return q == 0 ? 0 : (q == 4 ? PR : q + 2); }
 };
 
-// Per-lane producer of the staging ring: issues iteration k's plane copies (all lanes
-// call it; lanes without a k-th particle commit an empty group).
+// Per-lane producer of the staging ring: issues the planes of the lane's k-th sorted
+// particle (lanes past their count commit an empty group, keeping the wait counts uniform).
 template <int NP>
 struct Stager {
-    float4* buf;     // this warp's ring: [kStages][NP][32]
-    uint32_t slot0;  // first slot of the group
-    uint32_t off;    // particles of iterations < k already issued
-    int len;
+    float4* buf;        // this warp's ring: [kStages][NP][32]
+    uint32_t slot0;     // first slot of the group
+    uint64_t order;     // the lane's 8 sorted particles, one slot-in-group byte each
+    int cnt;            // how many of them exist
     int lane;
-    unsigned lt;
+    __device__ __forceinline__ uint32_t slot(int k) const {
+        return slot0 + static_cast<uint32_t>((order >> (8 * k)) & 0xFFu);
+    }
     __device__ __forceinline__ void issue(const Params& P, int k) {
-        const unsigned m = __ballot_sync(0xffffffffu, len > k);
-        if (len > k) {
-            const uint32_t s = slot0 + off + __popc(m & lt);
+        if (k < cnt) {
+            const uint32_t s = slot(k);
             float4* dst = buf + (k % kStages) * NP * 32 + lane;
 #pragma unroll
             for (int q = 0; q < NP; ++q) cp_async16(dst + q * 32, P.pl[PlaneSet<NP>::plane(q)] + s);
         }
-        off += __popc(m);
         cp_commit();
     }
 };
 
+// Warm L2 with the planes of the warp's NEXT group while this one computes: lane L
+// touches the 128-byte line of slots [8L, 8L+8) in each plane.
+template <int NP>
+__device__ __forceinline__ void prefetch_group(const Params& P, uint32_t g, uint32_t n_groups) {
+    if (g >= n_groups) return;
+    const uint32_t s = g * kGroup + (threadIdx.x & 31) * 8u;
+    if (s >= P.n_total) return;
+#pragma unroll
+    for (int q = 0; q < NP; ++q)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(P.pl[PlaneSet<NP>::plane(q)] + s));
+}
+
 // =====================================================================  P2G
-__device__ __forceinline__ void p2g_flush(const Params& P, const SceneView& S, const int cb[3],
-                                          float2 (&pa)[27], float2 (&pb)[27]) {
-    uint32_t tx[3], ty[3], tz[3];
-    node_offsets(S, cb, tx, ty, tz);
-    float4* g = P.grid_acc + S.node_base;
-#pragma unroll
-    for (int dk = 0; dk < 3; ++dk)
-#pragma unroll
-        for (int dj = 0; dj < 3; ++dj)
-#pragma unroll
-            for (int di = 0; di < 3; ++di) {
-                const int n = (dk * 3 + dj) * 3 + di;
-                atomicAdd(g + (tz[dk] + ty[dj] + tx[di]), make_float4(pa[n].x, pa[n].y, pb[n].x, pb[n].y));
-                pa[n] = f2(0.f, 0.f);
-                pb[n] = f2(0.f, 0.f);
-            }
-    // mark the <= 8 bricks this stencil touches: plain stores of 1 (benign races, no
+__device__ __forceinline__ void mark_bricks(const Params& P, const SceneView& S, const int cb[3]) {
+    // the <= 8 bricks a stencil at base cb touches: plain stores of 1 (benign races, no
     // dependent loads); k_collect_bricks compacts the marks into the active list
     const int bx0 = cb[0] >> 2, bx1 = (cb[0] + 2) >> 2;
     const int by0 = cb[1] >> 2, by1 = (cb[1] + 2) >> 2;
@@ -108,6 +112,67 @@ __device__ __forceinline__ void p2g_flush(const Params& P, const SceneView& S, c
     f[bz1 * sz + by0 * sy + bx1] = 1u;
     f[bz1 * sz + by1 * sy + bx0] = 1u;
     f[bz1 * sz + by1 * sy + bx1] = 1u;
+}
+
+__device__ __forceinline__ void p2g_flush(const Params& P, const SceneView& S, const int cb[3],
+                                          float2 (&pa)[27], float2 (&pb)[27]) {
+    uint32_t tx[3], ty[3], tz[3];
+    node_offsets(S, cb, tx, ty, tz);
+    float4* g = P.grid_acc + S.node_base;
+    asm("" : "+l"(g));  // one 64-bit base, 32-bit node offsets
+#pragma unroll
+    for (int dk = 0; dk < 3; ++dk)
+#pragma unroll
+        for (int dj = 0; dj < 3; ++dj)
+#pragma unroll
+            for (int di = 0; di < 3; ++di) {
+                const int n = (dk * 3 + dj) * 3 + di;
+                atomicAdd(g + (tz[dk] + ty[dj] + tx[di]), make_float4(pa[n].x, pa[n].y, pb[n].x, pb[n].y));
+                pa[n] = f2(0.f, 0.f);
+                pb[n] = f2(0.f, 0.f);
+            }
+    mark_bricks(P, S, cb);
+}
+
+// The 27 node contributions of one particle (solvers.hpp:157-168):
+//   momentum += w (m v + A (x_I - x_p)),  mass += w m,  w = w_x w_y w_z.
+// With u_jk = m v + A_col1 r_y + A_col2 r_z:  w (m v + A r) = w_x (w_yz u_jk) + (w_x r_x)(w_yz A_col0),
+// so each node costs two packed FFMA2 per pair with per-particle scalar broadcasts.
+// Pairs: (mom_x, mom_y) and (mom_z, mass) -- the .y lane of the second carries m through
+// u and 0 through A.
+__device__ __forceinline__ void p2g_nodes(const float w[3][3], const float rel[3][3], const float A[9],
+                                          float m, const float v[3], float2 (&pa)[27], float2 (&pb)[27]) {
+    const float2 A01_0 = f2(A[0], A[3]), A2m_0 = f2(A[6], 0.f);
+    const float2 A01_1 = f2(A[1], A[4]), A2m_1 = f2(A[7], 0.f);
+    const float2 A01_2 = f2(A[2], A[5]), A2m_2 = f2(A[8], 0.f);
+    const float2 mv01 = f2(v[0] * m, v[1] * m), mv2m = f2(v[2] * m, m);
+    float wr0[3];
+#pragma unroll
+    for (int di = 0; di < 3; ++di) wr0[di] = w[0][di] * rel[0][di];
+#pragma unroll
+    for (int dk = 0; dk < 3; ++dk) {
+        const float rz = rel[2][dk];
+        const float2 uz01 = __ffma2_rn(A01_2, f2(rz, rz), mv01);
+        const float2 uz2m = __ffma2_rn(A2m_2, f2(rz, rz), mv2m);
+#pragma unroll
+        for (int dj = 0; dj < 3; ++dj) {
+            const float ry = rel[1][dj];
+            const float wyz = w[1][dj] * w[2][dk];
+            const float2 U01 = __fmul2_rn(__ffma2_rn(A01_1, f2(ry, ry), uz01), f2(wyz, wyz));
+            const float2 U2m = __fmul2_rn(__ffma2_rn(A2m_1, f2(ry, ry), uz2m), f2(wyz, wyz));
+            const float2 G01 = __fmul2_rn(A01_0, f2(wyz, wyz));
+            const float2 G2m = __fmul2_rn(A2m_0, f2(wyz, wyz));
+#pragma unroll
+            for (int di = 0; di < 3; ++di) {
+                const int n = (dk * 3 + dj) * 3 + di;
+                const float wx = w[0][di], wr = wr0[di];
+                pa[n] = __ffma2_rn(f2(wx, wx), U01, pa[n]);
+                pa[n] = __ffma2_rn(f2(wr, wr), G01, pa[n]);
+                pb[n] = __ffma2_rn(f2(wx, wx), U2m, pb[n]);  // .y: mass += w m
+                pb[n] = __ffma2_rn(f2(wr, wr), G2m, pb[n]);
+            }
+        }
+    }
 }
 
 // Active-brick list from the P2G marks (warp-aggregated append; order is irrelevant).
@@ -137,24 +202,104 @@ void launch_collect_bricks(const Params& P, uint32_t n_bricks, cudaStream_t st) 
     k_collect_bricks<<<static_cast<int>(blocks), 256, 0, st>>>(P, n_bricks);
 }
 
+__device__ __forceinline__ uint32_t bin_word(uint32_t b) { return b + (b >> 5); }
+
+// Warp counting sort of group g by current stencil base.  Element e = lane + 32 i is slot
+// g*kGroup + e; inactive particles (and slots past the binned active range) are dropped.
+// Returns the lane's 8 sorted slot bytes and the group's active count; `bins` is kBinWords
+// words and `order_s` kGroup bytes of this warp's shared memory (both free on entry).
+__device__ __forceinline__ uint64_t group_sort(const Params& P, uint32_t g, uint32_t n_active,
+                                               uint32_t* bins, uint8_t* order_s, uint32_t& n_act) {
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const uint32_t slot0 = g * kGroup;
+    uint32_t bin[kPer];
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+        const uint32_t s = slot0 + lane + 32u * i;
+        bin[i] = 0xFFFFFFFFu;
+        if (s < n_active) {
+            const uint32_t flags = __float_as_uint(P.pl[PR][s].z);
+            if (flags & kActiveBit) {
+                const float4 a = P.pl[0][s];
+                const int scene = static_cast<int>((flags >> kSceneShift) & kSceneMask);
+                const float xa[3] = {a.x, a.y, a.z};
+                int b[3];
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    float fx;
+                    b[q] = stencil_base(xa[q], P.geo.origin[q], P.geo.inv_dx, fx);
+                    b[q] = min(max(b[q], 0), P.geo.dims[q] - 3);
+                }
+                const uint32_t brick = static_cast<uint32_t>(scene) * P.geo.bricks_per_scene +
+                                       (static_cast<uint32_t>(b[2] >> 2) * P.geo.nb[1] +
+                                        static_cast<uint32_t>(b[1] >> 2)) * P.geo.nb[0] +
+                                       static_cast<uint32_t>(b[0] >> 2);
+                bin[i] = ((brick & 7u) << 6) | static_cast<uint32_t>(((b[2] & 3) << 4) | ((b[1] & 3) << 2) | (b[0] & 3));
+            }
+        }
+    }
+    for (int w = lane; w < kBinWords; w += 32) bins[w] = 0u;
+    __syncwarp();
+    uint32_t rank[kPer];
+#pragma unroll
+    for (int i = 0; i < kPer; ++i)
+        if (bin[i] != 0xFFFFFFFFu) rank[i] = atomicAdd(&bins[bin_word(bin[i])], 1u);
+    __syncwarp();
+    // exclusive scan over bins in index order: lane L owns bins [16L, 16L+16)
+    constexpr int kOwn = kBins / 32;
+    uint32_t c[kOwn];
+    uint32_t tot = 0;
+#pragma unroll
+    for (int j = 0; j < kOwn; ++j) {
+        c[j] = bins[bin_word(kOwn * lane + j)];
+        tot += c[j];
+    }
+    uint32_t inc = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(full, inc, o);
+        if (lane >= o) inc += t;
+    }
+    n_act = __shfl_sync(full, inc, 31);
+    uint32_t run = inc - tot;
+#pragma unroll
+    for (int j = 0; j < kOwn; ++j) {
+        bins[bin_word(kOwn * lane + j)] = run;
+        run += c[j];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < kPer; ++i)
+        if (bin[i] != 0xFFFFFFFFu) order_s[bins[bin_word(bin[i])] + rank[i]] = static_cast<uint8_t>(lane + 32 * i);
+    __syncwarp();
+    const uint64_t mine = reinterpret_cast<const uint64_t*>(order_s)[lane];
+    __syncwarp();  // the caller reuses this shared memory for staging
+    return mine;
+}
+
 template <bool MLS>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_p2g(const Params P) {
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_p2g(const __grid_constant__ Params P) {
     extern __shared__ float4 smem[];
     constexpr int NP = kPlanes;
     const int lane = threadIdx.x & 31;
     const uint32_t n_groups = *P.n_groups;
-    const uint32_t n_chunks = *P.n_chunks;
+    const uint32_t n_active = *P.n_active;
     const uint32_t wpb = blockDim.x >> 5;
     Stager<NP> st;
     st.buf = smem + (threadIdx.x >> 5) * (kStages * NP * 32);
     st.lane = lane;
-    st.lt = lanemask_lt();
+    uint32_t* bins = reinterpret_cast<uint32_t*>(st.buf);  // sort scratch aliases the ring
+    uint8_t* order_s = reinterpret_cast<uint8_t*>(bins + kBinWords);
     for (uint32_t g = blockIdx.x * wpb + (threadIdx.x >> 5); g < n_groups; g += gridDim.x * wpb) {
-        const uint32_t c = g * 32u + lane;
-        st.len = c < n_chunks ? P.chunk_len[c] : 0;
-        st.slot0 = P.group_base[g];
-        st.off = 0;
-        const int kmax = __reduce_max_sync(0xffffffffu, st.len);
+        uint32_t n_act;
+        st.order = group_sort(P, g, n_active, bins, order_s, n_act);
+        st.slot0 = g * kGroup;
+        st.cnt = min(max(static_cast<int>(n_act) - kPer * lane, 0), kPer);
+        reinterpret_cast<uint64_t*>(P.order)[static_cast<uint64_t>(g) * 32 + lane] = st.order;
+        if (lane == 0) P.group_nact[g] = n_act;
+        prefetch_group<NP>(P, g + gridDim.x * wpb, n_groups);
+        const int kmax = min(static_cast<int>(n_act), kPer);  // lane 0 has the most
         for (int k = 0; k < kStages - 1; ++k) st.issue(P, k);
         float2 pa[27], pb[27];  // (mom_x, mom_y), (mom_z, mass) per stencil node
 #pragma unroll
@@ -167,11 +312,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_p2g(cons
         for (int k = 0; k < kmax; ++k) {
             st.issue(P, k + kStages - 1);
             cp_wait<kStages - 1>();
-            if (st.len <= k) continue;
+            if (k >= st.cnt) continue;
             const float4* src = st.buf + (k % kStages) * NP * 32 + lane;
             const float4 r = src[PR * 32];
             const uint32_t flags = __float_as_uint(r.z);
-            if (!(flags & kActiveBit)) continue;
             const float4 q0 = src[0], q1 = src[32], q2 = src[64], q3 = src[96], q4 = src[128], q5 = src[160];
             const float x[3] = {q0.x, q0.y, q0.z};
             const float v[3] = {q0.w, q1.x, q1.y};
@@ -184,11 +328,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_p2g(cons
             for (int a = 0; a < 3; ++a) {
                 b[a] = stencil_base(x[a], S.origin[a], S.inv_dx, fx[a]);
                 b[a] = min(max(b[a], 0), S.dims[a] - 3);  // memory guard only
-            }
-            if (b[0] != cb[0] || b[1] != cb[1] || b[2] != cb[2] || scene != cscene) {
-                if (cscene >= 0) p2g_flush(P, scene_view(P, cscene), cb, pa, pb);
-                cb[0] = b[0]; cb[1] = b[1]; cb[2] = b[2];
-                cscene = scene;
             }
             const float m = r.x;
             // affine = m C - dt V (4/dx^2) sigma  (solvers.hpp:154-156; PB: m C, :222)
@@ -221,75 +360,30 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_p2g(cons
                 for (int o = 0; o < 3; ++o)  // node_position - x (state.hpp:49-51)
                     rel[a][o] = (S.origin[a] + static_cast<float>(b[a] + o) * S.dx) - x[a];
             }
-            // node (di,dj,dk) receives w (m v + A (x_I - x_p)) and w m, with
-            //   w (m v + A r) = w_x (w_yz u_jk) + (w_x r_x) (w_yz A_col0),  u_jk = m v + A_col1 r_y + A_col2 r_z
-            // so every per-node op is an FFMA2 with a per-particle scalar broadcast (w_x or
-            // w_x r_x) and a per-row pair.  Pairs: (mom_x, mom_y) and (mom_z, mass) -- the .y
-            // lane of the second carries m through u and 0 through A.
-            const float2 A01_0 = f2(A[0], A[3]), A2m_0 = f2(A[6], 0.f);
-            const float2 A01_1 = f2(A[1], A[4]), A2m_1 = f2(A[7], 0.f);
-            const float2 A01_2 = f2(A[2], A[5]), A2m_2 = f2(A[8], 0.f);
-            const float2 mv01 = f2(v[0] * m, v[1] * m), mv2m = f2(v[2] * m, m);
-            float wr0[3];
-#pragma unroll
-            for (int di = 0; di < 3; ++di) wr0[di] = w[0][di] * rel[0][di];
-#pragma unroll
-            for (int dk = 0; dk < 3; ++dk) {
-                const float rz = rel[2][dk];
-                const float2 uz01 = __ffma2_rn(A01_2, f2(rz, rz), mv01);
-                const float2 uz2m = __ffma2_rn(A2m_2, f2(rz, rz), mv2m);
-#pragma unroll
-                for (int dj = 0; dj < 3; ++dj) {
-                    const float ry = rel[1][dj];
-                    const float wyz = w[1][dj] * w[2][dk];
-                    const float2 U01 = __fmul2_rn(__ffma2_rn(A01_1, f2(ry, ry), uz01), f2(wyz, wyz));
-                    const float2 U2m = __fmul2_rn(__ffma2_rn(A2m_1, f2(ry, ry), uz2m), f2(wyz, wyz));
-                    const float2 G01 = __fmul2_rn(A01_0, f2(wyz, wyz));
-                    const float2 G2m = __fmul2_rn(A2m_0, f2(wyz, wyz));
-#pragma unroll
-                    for (int di = 0; di < 3; ++di) {
-                        const int n = (dk * 3 + dj) * 3 + di;
-                        const float wx = w[0][di], wr = wr0[di];
-                        pa[n] = __ffma2_rn(f2(wx, wx), U01, pa[n]);
-                        pa[n] = __ffma2_rn(f2(wr, wr), G01, pa[n]);
-                        pb[n] = __ffma2_rn(f2(wx, wx), U2m, pb[n]);  // .y: mass += w m
-                        pb[n] = __ffma2_rn(f2(wr, wr), G2m, pb[n]);
-                    }
-                }
+            if (b[0] != cb[0] || b[1] != cb[1] || b[2] != cb[2] || scene != cscene) {
+                if (cscene >= 0) p2g_flush(P, scene_view(P, cscene), cb, pa, pb);
+                cb[0] = b[0]; cb[1] = b[1]; cb[2] = b[2];
+                cscene = scene;
             }
+            p2g_nodes(w, rel, A, m, v, pa, pb);
         }
         if (cscene >= 0) p2g_flush(P, scene_view(P, cscene), cb, pa, pb);
+        cp_wait<0>();
+        __syncwarp();  // the ring is the next group's sort scratch
     }
-    cp_wait<0>();
 }
 
 // ================================================================  G2P
-// grid_vel node = {v.x, v.y, v.z, mass}; nodes at or below kMassEps contribute nothing
-// (solvers.hpp:186).
-__device__ __forceinline__ void g2p_load_nodes(const Params& P, const SceneView& S, const int b[3],
-                                               float2 (&n01)[27], float (&n2)[27]) {
-    uint32_t tx[3], ty[3], tz[3];
-    node_offsets(S, b, tx, ty, tz);
-    const float4* g = P.grid_vel + S.node_base;
-#pragma unroll
-    for (int dk = 0; dk < 3; ++dk)
-#pragma unroll
-        for (int dj = 0; dj < 3; ++dj)
-#pragma unroll
-            for (int di = 0; di < 3; ++di) {
-                const int n = (dk * 3 + dj) * 3 + di;
-                const float4 q = __ldg(g + (tz[dk] + ty[dj] + tx[di]));
-                const bool live = q.w > kMassEps;
-                n01[n] = live ? f2(q.x, q.y) : f2(0.f, 0.f);
-                n2[n] = live ? q.z : 0.f;
-            }
-}
-
+// grid_vel node = {v.x, v.y, v.z, mass}; nodes at or below kMassEps carry v = 0 (grid
+// update), so they contribute nothing without a per-node test (solvers.hpp:186).
+//
 // v = sum w v_I,  B = sum (w v_I)(x_I - x_p)^T  (solvers.hpp:178-190), summed per row
-// (dk, dj) over di with the x-weights, then scaled by w_y w_z.
-__device__ __forceinline__ void g2p_gather(const float2 (&n01)[27], const float (&n2)[27],
-                                           const float w[3][3], const float rel[3][3], float vn[3],
-                                           float B[9]) {
+// (dk, dj) over di with the x-weights, then scaled by w_y w_z.  The 27 nodes are read
+// straight from L1: the warp's 32 lanes hold 32 consecutive sorted particles (a few
+// stencil bases), so each load instruction touches only a handful of lines.
+__device__ __forceinline__ void g2p_gather(const float4* g, const uint32_t tx[3], const uint32_t ty[3],
+                                           const uint32_t tz[3], const float w[3][3], const float rel[3][3],
+                                           float vn[3], float B[9]) {
     float wr0[3];
 #pragma unroll
     for (int o = 0; o < 3; ++o) wr0[o] = w[0][o] * rel[0][o];
@@ -298,19 +392,22 @@ __device__ __forceinline__ void g2p_gather(const float2 (&n01)[27], const float 
     float2 c0_01 = f2(0.f, 0.f), c1_01 = f2(0.f, 0.f), c2_01 = f2(0.f, 0.f);
     float c0_2 = 0.f, c1_2 = 0.f, c2_2 = 0.f;
 #pragma unroll
-    for (int dk = 0; dk < 3; ++dk)
+    for (int dk = 0; dk < 3; ++dk) {
+        float4 q[9];
+#pragma unroll
+        for (int n = 0; n < 9; ++n) q[n] = __ldg(g + (tz[dk] + ty[n / 3] + tx[n % 3]));
 #pragma unroll
         for (int dj = 0; dj < 3; ++dj) {
             float2 a01 = f2(0.f, 0.f), b01 = f2(0.f, 0.f);
             float a2 = 0.f, b2 = 0.f;  // sum wx v_z, sum wx rx v_z
 #pragma unroll
             for (int di = 0; di < 3; ++di) {
-                const int n = (dk * 3 + dj) * 3 + di;
+                const float4 nq = q[dj * 3 + di];
                 const float wx = w[0][di], wr = wr0[di];
-                a01 = __ffma2_rn(f2(wx, wx), n01[n], a01);
-                b01 = __ffma2_rn(f2(wr, wr), n01[n], b01);
-                a2 = fmaf(wx, n2[n], a2);
-                b2 = fmaf(wr, n2[n], b2);
+                a01 = __ffma2_rn(f2(wx, wx), f2(nq.x, nq.y), a01);
+                b01 = __ffma2_rn(f2(wr, wr), f2(nq.x, nq.y), b01);
+                a2 = fmaf(wx, nq.z, a2);
+                b2 = fmaf(wr, nq.z, b2);
             }
             const float wyz = w[1][dj] * w[2][dk];
             const float wy = wyz * rel[1][dj], wz = wyz * rel[2][dk];
@@ -323,6 +420,7 @@ __device__ __forceinline__ void g2p_gather(const float2 (&n01)[27], const float 
             c2_01 = __ffma2_rn(f2(wz, wz), a01, c2_01);    // column 2: rel_z
             c2_2 = fmaf(wz, a2, c2_2);
         }
+    }
     vn[0] = v01.x; vn[1] = v01.y; vn[2] = v2;
     // B row r = velocity component r, column c = rel component c
     B[0] = c0_01.x; B[1] = c1_01.x; B[2] = c2_01.x;
@@ -382,41 +480,42 @@ __device__ __forceinline__ void update_F(const float C[9], float dt, float F[9])
 }
 
 template <bool PB>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(const Params P) {
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(const __grid_constant__ Params P) {
     extern __shared__ float4 smem[];
     constexpr int NP = PB ? 7 : 5;
     const int lane = threadIdx.x & 31;
     const uint32_t n_groups = *P.n_groups;
-    const uint32_t n_chunks = *P.n_chunks;
     const uint32_t wpb = blockDim.x >> 5;
     Stager<NP> st;
     st.buf = smem + (threadIdx.x >> 5) * (kStages * NP * 32);
     st.lane = lane;
-    st.lt = lanemask_lt();
     for (uint32_t g = blockIdx.x * wpb + (threadIdx.x >> 5); g < n_groups; g += gridDim.x * wpb) {
-        const uint32_t c = g * 32u + lane;
-        st.len = c < n_chunks ? P.chunk_len[c] : 0;
-        st.slot0 = P.group_base[g];
-        st.off = 0;
-        const int kmax = __reduce_max_sync(0xffffffffu, st.len);
+        // replay the order P2G sorted this group into (positions are unchanged since);
+        // lane L takes sorted positions L + 32 k, so the warp's 32 lanes gather around a
+        // few neighbouring stencils at every iteration
+        const uint32_t n_act = P.group_nact[g];
+        {
+            const uint8_t* ob = P.order + static_cast<uint64_t>(g) * kGroup + lane;
+            uint64_t o = 0;
+#pragma unroll
+            for (int k = 0; k < kPer; ++k) o |= static_cast<uint64_t>(ob[32 * k]) << (8 * k);
+            st.order = o;
+        }
+        st.slot0 = g * kGroup;
+        prefetch_group<NP>(P, g + gridDim.x * wpb, n_groups);
+        st.cnt = static_cast<int>((n_act + 31u - static_cast<uint32_t>(lane)) / 32u);
+        const int kmax = static_cast<int>((n_act + 31u) / 32u);
         for (int k = 0; k < kStages - 1; ++k) st.issue(P, k);
-        float2 n01[27];
-        float n2[27];
-        int cb[3] = {INT_MIN, INT_MIN, INT_MIN};
-        int cscene = -1, my_scene = 0;
+        int my_scene = 0;
         int n_inv = 0, n_fail = 0, n_push = 0, n_deact = 0;
-        uint32_t off_c = 0;
         for (int k = 0; k < kmax; ++k) {
             st.issue(P, k + kStages - 1);
-            const unsigned mk_ = __ballot_sync(0xffffffffu, st.len > k);
-            const uint32_t s = st.slot0 + off_c + __popc(mk_ & st.lt);
-            off_c += __popc(mk_);
             cp_wait<kStages - 1>();
-            if (st.len <= k) continue;
+            if (k >= st.cnt) continue;
+            const uint32_t s = st.slot(k);
             const float4* src = st.buf + (k % kStages) * NP * 32 + lane;
             float4 r = src[(NP - 1) * 32];
             uint32_t flags = __float_as_uint(r.z);
-            if (!(flags & kActiveBit)) continue;
             Part p;
             {
                 const float4 q0 = src[0];
@@ -443,11 +542,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(cons
                 b[a] = stencil_base(p.x[a], S.origin[a], S.inv_dx, fx[a]);
                 b[a] = min(max(b[a], 0), S.dims[a] - 3);
             }
-            if (b[0] != cb[0] || b[1] != cb[1] || b[2] != cb[2] || scene != cscene) {
-                g2p_load_nodes(P, S, b, n01, n2);
-                cb[0] = b[0]; cb[1] = b[1]; cb[2] = b[2];
-                cscene = scene;
-            }
             float w[3][3], rel[3][3];
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
@@ -457,7 +551,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(cons
                     rel[a][o] = (S.origin[a] + static_cast<float>(b[a] + o) * S.dx) - p.x[a];
             }
             float B[9];
-            g2p_gather(n01, n2, w, rel, p.v, B);
+            {
+                uint32_t tx[3], ty[3], tz[3];
+                node_offsets(S, b, tx, ty, tz);
+                const float4* gv = P.grid_vel + S.node_base;
+                asm("" : "+l"(gv));  // one 64-bit base, 32-bit node offsets
+                g2p_gather(gv, tx, ty, tz, w, rel, p.v, B);
+            }
             bool do_commit;
             if (!PB) {  // solvers.hpp:191-195
 #pragma unroll

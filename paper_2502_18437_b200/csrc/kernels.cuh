@@ -1,8 +1,8 @@
 // kernels.cuh — sm_100a kernels of the MPM hot path.  See DESIGN.md §3 for the data
 // layout and the roofline of each kernel.
 //
-//   K1 k_bin_*         binning / stable sort by (brick, cell, original index) and the
-//                      warp-interleaved chunk layout (NEW stage; keys from math.hpp:219-223)
+//   K1 k_bin_*         binning / stable sort by (brick, cell, original index) (NEW stage;
+//                      keys from math.hpp:219-223); P2G re-sorts each group every substep
 //   K2 k_p2g<true>     MLS P2G with the stress impulse (solvers.hpp:151-169)
 //   K5 k_p2g<false>    PB-MPM P2G (solvers.hpp:218-235)
 //   K3 k_grid_update   v = p/m (+g dt), contact pass over the scene's shapes in order,
@@ -21,7 +21,8 @@
 
 namespace mpmb {
 
-constexpr int KMAX = 8;  // max particles per chunk (one chunk = one cell's run)
+// slots per transfer group: one warp re-sorts and processes one group per substep
+constexpr int kGroup = 256;
 
 // Particle slot = 7 float4 planes (112 B):
 //   P0 {x.x, x.y, x.z, v.x}   P1 {v.y, v.z, C0, C1}   P2 {C2, C3, C4, C5}
@@ -44,15 +45,15 @@ struct Params {
     int n_shapes;
     const float4* mats;  // {kind, mu, lambda, beta}
     float4* grid_acc;
-    float4* grid_vel;
+    float4* grid_vel;   // {v, m}; v = 0 at nodes of mass <= kMassEps
+    float4* dead_mom;   // optional: {momentum, m} of nodes of mass <= kMassEps (grid readback)
     uint32_t* brick_flag;
     uint32_t* brick_stamp;
     uint32_t* active_bricks;
     uint32_t* n_active_bricks;
     const uint32_t* brick_scene;
-    const uint32_t* group_base;
-    const uint8_t* chunk_len;
-    const uint32_t* n_chunks;
+    uint8_t* order;        // per group: kGroup bytes, slot-in-group by current stencil base
+    uint32_t* group_nact;  // per group: active particles (written by P2G, replayed by G2P)
     const uint32_t* n_groups;
     const uint32_t* n_active;
     int64_t n_total;

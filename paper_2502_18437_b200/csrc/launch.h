@@ -26,12 +26,7 @@ struct BinBuffers {
     uint8_t* g_cell;
     uint32_t* sorted_src;      // final sorted position -> old slot
     uint32_t* sorted_orig;     // final sorted position -> original index
-    uint32_t* rank_in_cell;
-    uint32_t* flag;            // chunk-start flags, then their exclusive scan (n+1)
-    uint32_t* chunk_start;     // [n_chunks]
-    uint8_t* chunk_len;
-    uint32_t* group_base;
-    uint32_t* counts;          // [0] n_chunks, [1] n_groups, [2] n_active
+    uint32_t* counts;          // [0] n_active, [1] transfer groups, [2] n_active
     uint32_t* scan_tmp;        // block sums for the scans
     uint32_t* key_by_orig;     // optional (binning readback), may be null
 };
@@ -41,7 +36,7 @@ void launch_bin(const Params& P, const BinBuffers& B, float4* const new_planes[k
 void launch_exclusive_scan(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* tmp,
                            cudaStream_t st, int64_t* launches);
 
-// ---- K2..K7 (k_step.cu) ----
+// ---- K2..K7 (k_transfer.cu, k_step.cu); max_groups = ceil(n / kGroup) ----
 void launch_p2g(const Params& P, bool mls, int64_t max_groups, cudaStream_t st);
 void launch_grid_update(const Params& P, int64_t max_bricks, cudaStream_t st);
 void launch_g2p(const Params& P, bool pb, int64_t max_groups, cudaStream_t st);
