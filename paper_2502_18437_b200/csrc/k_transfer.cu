@@ -83,18 +83,6 @@ struct Stager {
     }
 };
 
-// Warm L2 with the planes of the warp's NEXT group while this one computes: lane L
-// touches the 128-byte line of slots [8L, 8L+8) in each plane.
-template <int NP>
-__device__ __forceinline__ void prefetch_group(const Params& P, uint32_t g, uint32_t n_groups) {
-    if (g >= n_groups) return;
-    const uint32_t s = g * kGroup + (threadIdx.x & 31) * 8u;
-    if (s >= P.n_total) return;
-#pragma unroll
-    for (int q = 0; q < NP; ++q)
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(P.pl[PlaneSet<NP>::plane(q)] + s));
-}
-
 // =====================================================================  P2G
 __device__ __forceinline__ void mark_bricks(const Params& P, const SceneView& S, const int cb[3]) {
     // the <= 8 bricks a stencil at base cb touches: plain stores of 1 (benign races, no
@@ -114,6 +102,13 @@ __device__ __forceinline__ void mark_bricks(const Params& P, const SceneView& S,
     f[bz1 * sz + by1 * sy + bx1] = 1u;
 }
 
+// red.global.add.v4.f32: the explicit state space keeps the 64-bit base + 32-bit offset
+// addressing (a generic pointer would turn into a returning generic ATOM)
+__device__ __forceinline__ void red_add_v4(float4* p, float2 a, float2 b) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a.x), "f"(a.y), "f"(b.x),
+                 "f"(b.y));
+}
+
 __device__ __forceinline__ void p2g_flush(const Params& P, const SceneView& S, const int cb[3],
                                           float2 (&pa)[27], float2 (&pb)[27]) {
     uint32_t tx[3], ty[3], tz[3];
@@ -127,7 +122,7 @@ __device__ __forceinline__ void p2g_flush(const Params& P, const SceneView& S, c
 #pragma unroll
             for (int di = 0; di < 3; ++di) {
                 const int n = (dk * 3 + dj) * 3 + di;
-                atomicAdd(g + (tz[dk] + ty[dj] + tx[di]), make_float4(pa[n].x, pa[n].y, pb[n].x, pb[n].y));
+                red_add_v4(g + (tz[dk] + ty[dj] + tx[di]), pa[n], pb[n]);
                 pa[n] = f2(0.f, 0.f);
                 pb[n] = f2(0.f, 0.f);
             }
@@ -214,14 +209,23 @@ __device__ __forceinline__ uint64_t group_sort(const Params& P, uint32_t g, uint
     const int lane = threadIdx.x & 31;
     const uint32_t slot0 = g * kGroup;
     uint32_t bin[kPer];
+    // all 16 loads first (unconditional, clamped slot): one memory latency per group
+    float4 xa4[kPer];
+    uint32_t fl[kPer];
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+        const uint32_t s = min(slot0 + lane + 32u * i, n_active - 1u);
+        fl[i] = __float_as_uint(__ldg(&P.pl[PR][s].z));
+        xa4[i] = __ldg(&P.pl[0][s]);
+    }
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
         const uint32_t s = slot0 + lane + 32u * i;
         bin[i] = 0xFFFFFFFFu;
         if (s < n_active) {
-            const uint32_t flags = __float_as_uint(P.pl[PR][s].z);
+            const uint32_t flags = fl[i];
             if (flags & kActiveBit) {
-                const float4 a = P.pl[0][s];
+                const float4 a = xa4[i];
                 const int scene = static_cast<int>((flags >> kSceneShift) & kSceneMask);
                 const float xa[3] = {a.x, a.y, a.z};
                 int b[3];
@@ -298,7 +302,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_p2g(cons
         st.cnt = min(max(static_cast<int>(n_act) - kPer * lane, 0), kPer);
         reinterpret_cast<uint64_t*>(P.order)[static_cast<uint64_t>(g) * 32 + lane] = st.order;
         if (lane == 0) P.group_nact[g] = n_act;
-        prefetch_group<NP>(P, g + gridDim.x * wpb, n_groups);
         const int kmax = min(static_cast<int>(n_act), kPer);  // lane 0 has the most
         for (int k = 0; k < kStages - 1; ++k) st.issue(P, k);
         float2 pa[27], pb[27];  // (mom_x, mom_y), (mom_z, mass) per stencil node
@@ -502,7 +505,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(cons
             st.order = o;
         }
         st.slot0 = g * kGroup;
-        prefetch_group<NP>(P, g + gridDim.x * wpb, n_groups);
         st.cnt = static_cast<int>((n_act + 31u - static_cast<uint32_t>(lane)) / 32u);
         const int kmax = static_cast<int>((n_act + 31u) / 32u);
         for (int k = 0; k < kStages - 1; ++k) st.issue(P, k);
