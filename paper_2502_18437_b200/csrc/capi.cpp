@@ -444,8 +444,13 @@ struct Scene {
     int next_shape_id = 0, next_object_id = 0;
     // last FrameResult
     mpmb_frame_summary res{};
-    std::vector<float> rx, rv;
-    std::vector<uint8_t> ra;
+    // positions / velocities / active of the last fetch: views into the batch's pinned
+    // frame buffer (kept alive by `frame`; replaced only by the next fetch)
+    std::shared_ptr<void> frame;
+    const float* rx = nullptr;
+    const float* rv = nullptr;
+    const uint8_t* ra = nullptr;
+    size_t rn = 0;
     std::vector<int32_t> rid;
     std::vector<float> rimp, rtq;
     bool alive = true;
@@ -457,6 +462,8 @@ enum class Status { idle, advancing, results_ready };
 struct Batch {
     std::vector<Scene*> scenes;
     std::unique_ptr<Engine> eng;
+    std::shared_ptr<void> frame;  // pinned FrameResult buffer (x, v, active of all scenes)
+    size_t frame_bytes = 0;
     bool device_valid = false;   // device holds the newest particle state
     bool particles_dirty = true; // host changed: re-upload
     bool shapes_dirty = true;
@@ -718,10 +725,16 @@ void fetch(Batch& b) {
     Engine& e = *b.eng;
     size_t total = 0;
     for (Scene* s : b.scenes) total += s->count();
-    std::vector<float> x(3 * total), v(3 * total);
-    std::vector<uint8_t> a(total);
+    const size_t bytes = 24 * total + total + 16;
+    if (!b.frame || b.frame_bytes < bytes) {
+        b.frame = Engine::pinned_host(bytes);
+        b.frame_bytes = bytes;
+    }
+    float* x = static_cast<float*>(b.frame.get());
+    float* v = x + 3 * total;
+    uint8_t* a = reinterpret_cast<uint8_t*>(v + 3 * total);
     std::vector<double> totals;
-    e.snapshot(x.data(), v.data(), a.data(), totals);
+    e.snapshot(x, v, a, totals);
     std::vector<SceneCounters> cnt = e.read_counters();
     std::vector<double> imp, tq;
     std::vector<int32_t> cc;
@@ -729,9 +742,11 @@ void fetch(Batch& b) {
     for (size_t si = 0; si < b.scenes.size(); ++si) {
         Scene* s = b.scenes[si];
         const size_t o = b.offsets[si], n = s->count();
-        s->rx.assign(x.begin() + 3 * o, x.begin() + 3 * (o + n));
-        s->rv.assign(v.begin() + 3 * o, v.begin() + 3 * (o + n));
-        s->ra.assign(a.begin() + o, a.begin() + o + n);
+        s->frame = b.frame;
+        s->rx = x + 3 * o;
+        s->rv = v + 3 * o;
+        s->ra = a + o;
+        s->rn = n;
         mpmb_frame_summary& r = s->res;
         r = mpmb_frame_summary{};
         r.time = s->time;
@@ -1053,9 +1068,9 @@ extern "C" mpmb_status mpmb_result_copy(mpmb_handle sh, float* pos, float* vel, 
     return guarded([&]() -> mpmb_status {
         Scene* s = reg().scene(sh);
         if (!s) return MPMB_BAD_HANDLE;
-        if (pos) std::copy(s->rx.begin(), s->rx.end(), pos);
-        if (vel) std::copy(s->rv.begin(), s->rv.end(), vel);
-        if (active) std::copy(s->ra.begin(), s->ra.end(), active);
+        if (pos && s->rn) std::copy(s->rx, s->rx + 3 * s->rn, pos);
+        if (vel && s->rn) std::copy(s->rv, s->rv + 3 * s->rn, vel);
+        if (active && s->rn) std::copy(s->ra, s->ra + s->rn, active);
         if (ids) std::copy(s->rid.begin(), s->rid.end(), ids);
         if (imp) std::copy(s->rimp.begin(), s->rimp.end(), imp);
         if (tq) std::copy(s->rtq.begin(), s->rtq.end(), tq);

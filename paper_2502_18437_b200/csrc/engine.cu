@@ -717,6 +717,12 @@ void Engine::snapshot(float* x, float* v, uint8_t* active, std::vector<double>& 
     check(cudaStreamSynchronize(I.st), "snapshot");
 }
 
+std::shared_ptr<void> Engine::pinned_host(size_t bytes) {
+    void* p = nullptr;
+    check(cudaMallocHost(&p, bytes ? bytes : 16), "cudaMallocHost");
+    return std::shared_ptr<void>(p, [](void* q) { cudaFreeHost(q); });
+}
+
 void Engine::enable_grid_readback() {
     Impl& I = *impl_;
     if (I.dead_mom.p) return;

@@ -10,6 +10,7 @@
 // Every public method enqueues on the engine's stream; only the explicit download /
 // read_* methods synchronise.
 #pragma once
+#include <memory>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -105,6 +106,9 @@ class Engine {
     // FrameResult snapshot for all scenes: positions/velocities/active in original order
     // (device -> pinned host), totals per scene (double).  Enqueue + wait.
     void snapshot(float* x, float* v, uint8_t* active, std::vector<double>& totals /*5 per scene*/);
+    // page-locked host memory (cudaMallocHost) freed with the last reference: D2H of a
+    // FrameResult straight into it runs at link speed, with no staging copies
+    static std::shared_ptr<void> pinned_host(size_t bytes);
     // dense grid of one scene (node-major i + nx*(j + ny*k)); for tests and the hook adapter
     void download_grid(int scene, float* mass, float* momentum, float* velocity);
     // keep the momentum of nodes below kMassEps for download_grid (one more float4 per node;

@@ -12,23 +12,35 @@ namespace mpmb {
 // (it is the last reader), writes {mass, velocity} for G2P.  Contact shapes are applied
 // in order per node (last shape wins, contact.hpp:106-134); each warp reduces its
 // per-shape impulse/torque/count with shuffles and adds them in FP64.
+//
+// Latency: the per-brick chain (brick id -> accumulator -> shapes) is software-pipelined
+// over the grid-stride loop: brick ids are loaded two iterations ahead and accumulators
+// one ahead; the scene follows from the brick id arithmetically (uniform geometry).
 __global__ void __launch_bounds__(256) k_grid_update(const Params P) {
     const uint32_t n_bricks = *P.n_active_bricks;
     const int l = threadIdx.x & 63;
     const uint32_t per_block = blockDim.x >> 6;
     const int lane = threadIdx.x & 31;
-    for (uint32_t bi = blockIdx.x * per_block + (threadIdx.x >> 6); bi < n_bricks;
-         bi += gridDim.x * per_block) {
-        const uint32_t gb = P.active_bricks[bi];
-        const int scene = static_cast<int>(P.brick_scene[gb]);
+    const uint32_t bstride = gridDim.x * per_block;
+    uint32_t bi = blockIdx.x * per_block + (threadIdx.x >> 6);
+    uint32_t gb_next = bi < n_bricks ? P.active_bricks[bi] : 0u;
+    uint32_t gb_after = bi + bstride < n_bricks ? P.active_bricks[bi + bstride] : 0u;
+    float4 a_next = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (bi < n_bricks) a_next = P.grid_acc[static_cast<uint64_t>(gb_next) * kBrickNodes + l];
+    for (; bi < n_bricks; bi += bstride) {
+        const uint32_t gb = gb_next;
+        const float4 a = a_next;
+        if (bi + bstride < n_bricks) a_next = P.grid_acc[static_cast<uint64_t>(gb_after) * kBrickNodes + l];
+        gb_next = gb_after;
+        if (bi + 2 * bstride < n_bricks) gb_after = P.active_bricks[bi + 2 * bstride];
+        const int scene = static_cast<int>(gb / P.geo.bricks_per_scene);
         const SceneView S = scene_view(P, scene);
         const uint32_t local = gb - S.brick_base;
         const int bx = static_cast<int>(local % S.nb[0]);
         const int by = static_cast<int>((local / S.nb[0]) % S.nb[1]);
         const int bz = static_cast<int>(local / (static_cast<uint32_t>(S.nb[0]) * S.nb[1]));
         const int i = bx * 4 + (l & 3), j = by * 4 + ((l >> 2) & 3), k = bz * 4 + (l >> 4);
-        const uint64_t idx = S.node_base + static_cast<uint64_t>(local) * kBrickNodes + l;
-        const float4 a = P.grid_acc[idx];
+        const uint64_t idx = static_cast<uint64_t>(gb) * kBrickNodes + l;  // == node_base + local*64 + l
         P.grid_acc[idx] = make_float4(0.f, 0.f, 0.f, 0.f);
         if (l == 0) P.brick_stamp[gb] = P.epoch;
         const float m = a.w;
