@@ -83,7 +83,8 @@ struct Engine::Impl {
     DevBuf dead_mom;  // grid readback only (enable_grid_readback)
     DevBuf grid_acc, grid_vel, brick_flag, brick_stamp, active_bricks, brick_scene, misc;
     // misc u32 slots: [0] n_active_bricks
-    int64_t n = 0;
+    int64_t n = 0;      // particles
+    int64_t n_cap = 0;  // slots of each plane buffer: n + kGroup (group padding, holes)
     DevBuf planes[2][kPlanes];
     int cur = 0;
     bool binned = false;
@@ -155,7 +156,10 @@ struct Engine::Impl {
 
     Params params() {
         Params P{};
-        for (int q = 0; q < kPlanes; ++q) P.pl[q] = planes[cur][q].as<float4>();
+        for (int q = 0; q < kPlanes; ++q) {
+            P.pl[q] = planes[cur][q].as<float4>();
+            P.pl_out[q] = planes[1 - cur][q].as<float4>();
+        }
         P.geo = geo;
         for (size_t i = 0; i < hmats.size() && i < static_cast<size_t>(kMaxConstMats); ++i)
             P.mats_c[i] = make_float4(static_cast<float>(hmats[i].kind), hmats[i].mu, hmats[i].lambda,
@@ -181,7 +185,7 @@ struct Engine::Impl {
         P.group_nact = group_nact.as<uint32_t>();
         P.n_groups = b_counts.as<uint32_t>() + 1;
         P.n_active = b_counts.as<uint32_t>() + 2;
-        P.n_total = n;
+        P.n_total = n_cap;
         P.stress_in = stress_in.as<float>();
         P.use_stress_in = use_stress_in ? 1 : 0;
         P.acc_sub = acc_sub.as<double>();
@@ -324,19 +328,20 @@ void Engine::upload_particles(int64_t n, const float* x, const float* v, const f
     if (n >= 0x7FFFFFFF) throw std::invalid_argument("engine: particle count exceeds 2^31");
     check(cudaStreamSynchronize(I.st), "sync");
     I.n = n;
+    I.n_cap = n > 0 ? n + kGroup : 0;
     n_total_ = n;
     for (int b = 0; b < 2; ++b)
-        for (int q = 0; q < kPlanes; ++q) I.planes[b][q].alloc(sizeof(float4) * std::max<int64_t>(n, 1));
+        for (int q = 0; q < kPlanes; ++q) I.planes[b][q].alloc(sizeof(float4) * std::max<int64_t>(I.n_cap, 1));
     I.cur = 0;
-    // sort scratch
-    const size_t N = static_cast<size_t>(std::max<int64_t>(n, 1));
+    // sort scratch (per slot)
+    const size_t N = static_cast<size_t>(std::max<int64_t>(I.n_cap, 1));
     I.b_key.alloc(4 * N); I.b_rank.alloc(4 * N); I.b_cell.alloc(N); I.b_orig.alloc(4 * N);
     I.e_orig.alloc(4 * N); I.e_cell.alloc(N); I.e_src.alloc(4 * N); I.b_tmp.alloc(4 * N);
     I.g_orig.alloc(4 * N); I.g_src.alloc(4 * N); I.g_cell.alloc(N); I.s_src.alloc(4 * N);
     I.s_orig.alloc(4 * N);
     const size_t n_groups = (N + kGroup - 1) / kGroup;
     I.order.alloc(kGroup * n_groups); I.group_nact.alloc(4 * n_groups);
-    const size_t nbk = static_cast<size_t>(I.total_bricks) + 1;
+    const size_t nbk = static_cast<size_t>(I.total_bricks) + 2;  // + inactive, holes
     I.b_count.alloc(4 * nbk);
     I.b_off.alloc(4 * (nbk + 1));
     const size_t tiles = (std::max(N + 1, nbk + 1) + 4095) / 4096 + 2;
@@ -526,7 +531,7 @@ void Engine::bin() {
     float4* np[kPlanes];
     for (int q = 0; q < kPlanes; ++q) np[q] = I.planes[1 - I.cur][q].as<float4>();
     int64_t k = 0;
-    launch_bin(P, I.bb, np, I.n, I.st, &k);
+    launch_bin(P, I.bb, np, I.n_cap, I.st, &k);
     I.counted(k);
     I.cur = 1 - I.cur;
     I.binned = true;
@@ -578,6 +583,7 @@ void Engine::g2p_mls(int sub, float dt, bool pushout, bool deactivate) {
     P.commit = 1;
     launch_g2p(P, false, (I.n + kGroup - 1) / kGroup, I.st);
     I.counted(1);
+    I.cur = 1 - I.cur;  // G2P wrote the group-sorted state into the other buffer
     I.end(CAT_G2P, ev);
 }
 
@@ -593,6 +599,7 @@ void Engine::g2p_pb(int sub, float dt, bool commit, bool pushout, bool deactivat
     P.deactivate = deactivate ? 1 : 0;
     launch_g2p(P, true, (I.n + kGroup - 1) / kGroup, I.st);
     I.counted(1);
+    I.cur = 1 - I.cur;
     I.end(CAT_G2P, ev);
 }
 

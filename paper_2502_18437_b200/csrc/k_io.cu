@@ -14,10 +14,16 @@ static int blocks_for(int64_t n, int threads, int cap) {
     return static_cast<int>(b);
 }
 
-// Slot = original index (the layout before the first binning).
+// Slot = original index (the layout before the first binning); slots [n, n_total) are holes.
 __global__ void k_upload(const Params P, IoArrays in, int64_t n) {
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < P.n_total; i += stride) {
+        if (i >= n) {
+#pragma unroll
+            for (int q = 0; q < PR; ++q) P.pl[q][i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            P.pl[PR][i] = make_float4(0.f, 0.f, 0.f, __uint_as_float(kHoleOrig));
+            continue;
+        }
         Part p;
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
@@ -43,7 +49,9 @@ __global__ void k_download(const Params P, IoArrays out) {
     for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < P.n_total; s += stride) {
         const float4 r = P.pl[PR][s];
         const uint32_t flags = __float_as_uint(r.z);
-        const uint64_t o = __float_as_uint(r.w);
+        const uint32_t o32 = __float_as_uint(r.w);
+        if (o32 == kHoleOrig) continue;
+        const uint64_t o = o32;
         Part p;
         load_part(P, static_cast<uint32_t>(s), p);
         if (out.x) for (int a = 0; a < 3; ++a) out.x[3 * o + a] = p.x[a];
@@ -105,6 +113,7 @@ __global__ void k_stress(const Params P, float* out) {
     for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < P.n_total; s += stride) {
         const float4 r = P.pl[PR][s];
         const uint32_t flags = __float_as_uint(r.z);
+        if (__float_as_uint(r.w) == kHoleOrig) continue;
         const uint64_t o = __float_as_uint(r.w);
         if (P.use_stress_in) {
             for (int a = 0; a < 9; ++a) out[9 * o + a] = P.stress_in[9 * o + a];
@@ -132,8 +141,7 @@ __global__ void k_grid_download(const Params P, DevScene S, int64_t n_nodes, flo
         const uint32_t local = ((k >> 2) * S.nb[1] + (j >> 2)) * S.nb[0] + (i >> 2);
         const uint32_t gb = S.brick_base + local;
         float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-        const uint64_t idx = S.node_base + static_cast<uint64_t>(local) * kBrickNodes + ((k & 3) << 4) +
-                             ((j & 3) << 2) + (i & 3);
+        const uint64_t idx = S.node_base + node_linear(P.geo, i, j, k);
         if (P.brick_stamp[gb] == P.epoch) a = P.grid_vel[idx];
         const bool live = a.w > kMassEps;  // node = {x, y, z, mass}
         if (!live && P.brick_stamp[gb] == P.epoch && P.dead_mom) a = P.dead_mom[idx];
@@ -163,8 +171,7 @@ __global__ void k_grid_upload(const Params P, DevScene S, int64_t n_nodes, const
         if (P.brick_stamp[gb] != P.epoch) continue;
         const float m = mass[q];
         const bool live = m > kMassEps;
-        const uint64_t idx = S.node_base + static_cast<uint64_t>(local) * kBrickNodes + ((k & 3) << 4) +
-                             ((j & 3) << 2) + (i & 3);
+        const uint64_t idx = S.node_base + node_linear(P.geo, i, j, k);
         P.grid_vel[idx] = live ? make_float4(vel[3 * q], vel[3 * q + 1], vel[3 * q + 2], m)
                                : make_float4(0.f, 0.f, 0.f, m);
         if (!live && P.dead_mom) P.dead_mom[idx] = make_float4(mom[3 * q], mom[3 * q + 1], mom[3 * q + 2], m);

@@ -121,7 +121,9 @@ __global__ void __launch_bounds__(256) k_bin_keys(const Params P, BinBuffers B) 
             const float4 r = P.pl[PR][s];
             const uint32_t flags = __float_as_uint(r.z);
             orig = __float_as_uint(r.w);
-            if (flags & kActiveBit) {
+            if (orig == kHoleOrig) {
+                bucket = B.n_buckets - 1;  // empty slot: sorted last, never gathered
+            } else if (flags & kActiveBit) {
                 const int scene = static_cast<int>((flags >> kSceneShift) & kSceneMask);
                 const SceneView S = scene_view(P, scene);
                 const float4 a = P.pl[0][s];
@@ -140,7 +142,7 @@ __global__ void __launch_bounds__(256) k_bin_keys(const Params P, BinBuffers B) 
                 cell = static_cast<uint32_t>(((b[2] & 3) << 4) | ((b[1] & 3) << 2) | (b[0] & 3));
                 if (B.key_by_orig) B.key_by_orig[orig] = (local << 6) | cell;
             } else {
-                bucket = B.n_buckets - 1;
+                bucket = B.n_buckets - 2;
                 if (B.key_by_orig) B.key_by_orig[orig] = 0xFFFFFFFFu;
             }
         }
@@ -173,11 +175,11 @@ __global__ void __launch_bounds__(256) k_bin_scatter(BinBuffers B, int64_t n) {
 __global__ void __launch_bounds__(256) k_bin_local(BinBuffers B) {
     __shared__ uint32_t hist[64];
     __shared__ uint32_t cstart[64];
-    const uint32_t inactive = B.n_buckets - 1;
+    const uint32_t inactive = B.n_buckets - 2;  // then the hole bucket
     for (uint32_t b = blockIdx.x; b < B.n_buckets; b += gridDim.x) {
         const uint32_t beg = B.bucket_off[b], end = B.bucket_off[b + 1];
         if (beg == end) continue;
-        if (b == inactive) {
+        if (b >= inactive) {
             for (uint32_t q = beg + threadIdx.x; q < end; q += blockDim.x) {
                 B.sorted_src[q] = B.e_src[q];
                 B.sorted_orig[q] = B.e_orig[q];
@@ -223,23 +225,54 @@ __global__ void __launch_bounds__(256) k_bin_local(BinBuffers B) {
     }
 }
 
-// Physical permutation of the 7 planes into the sorted order (coalesced writes), and the
-// counts the transfers read: [0] n_active, [1] transfer groups, [2] n_active.
-__global__ void __launch_bounds__(256) k_bin_gather(const Params P, BinBuffers B, int64_t n_total,
+// Physical permutation of the 7 planes into the group layout (launch.h), and the counts
+// the transfers read: [0] n_active, [1] transfer groups G, [2] n_active, [3] tail start
+// G*kGroup.  Slots [0, G*kGroup): group g holds sorted entries g*kGroup + p at slot
+// g*kGroup + group_phys(p), holes past n_active; then the inactive particles; then holes.
+__global__ void __launch_bounds__(256) k_bin_gather(const Params P, BinBuffers B, int64_t n_cap,
                                                     float4* n0, float4* n1, float4* n2, float4* n3,
                                                     float4* n4, float4* n5, float4* n6) {
     float4* np[kPlanes] = {n0, n1, n2, n3, n4, n5, n6};
+    const uint32_t n_active = B.bucket_off[B.n_buckets - 2];
+    const uint32_t n_real = B.bucket_off[B.n_buckets - 1];
+    const uint32_t groups = (n_active + kGroup - 1) / kGroup;
+    const uint32_t tail = groups * kGroup;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        const uint32_t n_active = B.bucket_off[B.n_buckets - 1];
         B.counts[0] = n_active;
-        B.counts[1] = (n_active + kGroup - 1) / kGroup;
+        B.counts[1] = groups;
         B.counts[2] = n_active;
+        B.counts[3] = tail;
     }
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < n_total; q += stride) {
-        const uint32_t src = B.sorted_src[q];
+    for (int64_t d = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; d < n_cap; d += stride) {
+        uint32_t src = kHoleOrig;
+        if (d < tail) {
+            const uint32_t q = static_cast<uint32_t>(d / kGroup) * kGroup +
+                               group_pos(static_cast<uint32_t>(d % kGroup));
+            if (q < n_active) src = B.sorted_src[q];
+        } else if (d < static_cast<int64_t>(tail) + (n_real - n_active)) {
+            src = B.sorted_src[n_active + static_cast<uint32_t>(d - tail)];
+        }
+        if (src != kHoleOrig) {
 #pragma unroll
-        for (int p = 0; p < kPlanes; ++p) np[p][q] = P.pl[p][src];
+            for (int p = 0; p < kPlanes; ++p) np[p][d] = P.pl[p][src];
+        } else {
+#pragma unroll
+            for (int p = 0; p < PR; ++p) np[p][d] = make_float4(0.f, 0.f, 0.f, 0.f);
+            np[PR][d] = make_float4(0.f, 0.f, 0.f, __uint_as_float(kHoleOrig));
+        }
+    }
+}
+
+// The transfers rewrite only the grouped slots each substep (G2P into the other buffer);
+// the tail (inactive particles + holes) must be identical in both buffers.
+// Q.pl = the freshly gathered buffer, Q.pl_out = the other one.
+__global__ void __launch_bounds__(256) k_bin_tail(const Params Q, BinBuffers B, int64_t n_cap) {
+    const int64_t tail = B.counts[3];
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t d = tail + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; d < n_cap; d += stride) {
+#pragma unroll
+        for (int p = 0; p < kPlanes; ++p) Q.pl_out[p][d] = Q.pl[p][d];
     }
 }
 
@@ -252,6 +285,7 @@ static int blocks_for(int64_t n, int threads, int cap) {
 
 void launch_bin(const Params& P, const BinBuffers& B, float4* const new_planes[kPlanes],
                 int64_t n_total, cudaStream_t st, int64_t* launches) {
+    // n_total: slot capacity of both buffers (particles + holes)
     cudaMemsetAsync(B.bucket_count, 0, sizeof(uint32_t) * B.n_buckets, st);
     const int cap = 148 * 16;
     k_bin_keys<<<blocks_for(n_total, 256, cap), 256, 0, st>>>(P, B);
@@ -261,7 +295,13 @@ void launch_bin(const Params& P, const BinBuffers& B, float4* const new_planes[k
     k_bin_gather<<<blocks_for(n_total, 256, cap), 256, 0, st>>>(
         P, B, n_total, new_planes[0], new_planes[1], new_planes[2], new_planes[3],
         new_planes[4], new_planes[5], new_planes[6]);
-    *launches += 4;
+    Params Q = P;
+    for (int q = 0; q < kPlanes; ++q) {
+        Q.pl_out[q] = P.pl[q];
+        Q.pl[q] = new_planes[q];
+    }
+    k_bin_tail<<<blocks_for(n_total / 8, 256, cap), 256, 0, st>>>(Q, B, n_total);
+    *launches += 5;
 }
 
 }  // namespace mpmb

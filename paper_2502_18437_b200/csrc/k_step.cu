@@ -7,6 +7,17 @@
 
 namespace mpmb {
 
+// node l (0..63) of global brick gb in the linear node pool
+__device__ __forceinline__ uint64_t brick_node(const Params& P, uint32_t gb, int l) {
+    const uint32_t scene = gb / P.geo.bricks_per_scene;
+    const uint32_t local = gb - scene * P.geo.bricks_per_scene;
+    const uint32_t nb0 = static_cast<uint32_t>(P.geo.nb[0]), nb1 = static_cast<uint32_t>(P.geo.nb[1]);
+    const int i = static_cast<int>((local % nb0) * 4u) + (l & 3);
+    const int j = static_cast<int>(((local / nb0) % nb1) * 4u) + ((l >> 2) & 3);
+    const int k = static_cast<int>((local / (nb0 * nb1)) * 4u) + (l >> 4);
+    return static_cast<uint64_t>(scene) * P.geo.nodes_per_scene + node_linear(P.geo, i, j, k);
+}
+
 // ==============================================================  grid update
 // 64 threads per active brick (one node each).  Reads the P2G accumulator and zeroes it
 // (it is the last reader), writes {mass, velocity} for G2P.  Contact shapes are applied
@@ -26,11 +37,11 @@ __global__ void __launch_bounds__(256) k_grid_update(const Params P) {
     uint32_t gb_next = bi < n_bricks ? P.active_bricks[bi] : 0u;
     uint32_t gb_after = bi + bstride < n_bricks ? P.active_bricks[bi + bstride] : 0u;
     float4 a_next = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (bi < n_bricks) a_next = P.grid_acc[static_cast<uint64_t>(gb_next) * kBrickNodes + l];
+    if (bi < n_bricks) a_next = P.grid_acc[brick_node(P, gb_next, l)];
     for (; bi < n_bricks; bi += bstride) {
         const uint32_t gb = gb_next;
         const float4 a = a_next;
-        if (bi + bstride < n_bricks) a_next = P.grid_acc[static_cast<uint64_t>(gb_after) * kBrickNodes + l];
+        if (bi + bstride < n_bricks) a_next = P.grid_acc[brick_node(P, gb_after, l)];
         gb_next = gb_after;
         if (bi + 2 * bstride < n_bricks) gb_after = P.active_bricks[bi + 2 * bstride];
         const int scene = static_cast<int>(gb / P.geo.bricks_per_scene);
@@ -40,7 +51,7 @@ __global__ void __launch_bounds__(256) k_grid_update(const Params P) {
         const int by = static_cast<int>((local / S.nb[0]) % S.nb[1]);
         const int bz = static_cast<int>(local / (static_cast<uint32_t>(S.nb[0]) * S.nb[1]));
         const int i = bx * 4 + (l & 3), j = by * 4 + ((l >> 2) & 3), k = bz * 4 + (l >> 4);
-        const uint64_t idx = static_cast<uint64_t>(gb) * kBrickNodes + l;  // == node_base + local*64 + l
+        const uint64_t idx = S.node_base + node_linear(P.geo, i, j, k);
         P.grid_acc[idx] = make_float4(0.f, 0.f, 0.f, 0.f);
         if (l == 0) P.brick_stamp[gb] = P.epoch;
         const float m = a.w;
@@ -123,7 +134,7 @@ __global__ void __launch_bounds__(256) k_grid_bc(const Params P) {
         const int by = static_cast<int>((local / S.nb[0]) % S.nb[1]);
         const int bz = static_cast<int>(local / (static_cast<uint32_t>(S.nb[0]) * S.nb[1]));
         const int i = bx * 4 + (l & 3), j = by * 4 + ((l >> 2) & 3), k = bz * 4 + (l >> 4);
-        const uint64_t idx = S.node_base + static_cast<uint64_t>(local) * kBrickNodes + l;
+        const uint64_t idx = S.node_base + node_linear(P.geo, i, j, k);
         float4 a = P.grid_vel[idx];
         if (!(a.w > kMassEps)) continue;
         const bool bxm = i < 2 || i >= S.dims[0] - 2;

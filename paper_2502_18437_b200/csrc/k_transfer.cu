@@ -38,6 +38,14 @@ static_assert(kPer == 8, "order bytes are read as one u64 per lane");
 #define MPMB_G2P_MINB 3
 #endif
 
+// G2P position of lane L at iteration k.  LDGSTS costs one L1 wavefront per (8-lane phase,
+// source line): lanes 8j..8j+7 take positions 64 b + 8 c + a (c = L & 7) that group_phys
+// maps to ONE 128-byte line (8 (4a + b) + c), and the warp's 32 positions lie in a
+// 64-position window of the sorted order (gather locality).  Increasing in k.
+__device__ __forceinline__ uint32_t g2p_pos(int lane, int k) {
+    return 64u * (k >> 1) + 8u * (lane & 7) + 4u * (k & 1) + (lane >> 3);
+}
+
 __device__ __forceinline__ void cp_async16(float4* smem, const float4* gmem) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
@@ -111,21 +119,22 @@ __device__ __forceinline__ void red_add_v4(float4* p, float2 a, float2 b) {
 
 __device__ __forceinline__ void p2g_flush(const Params& P, const SceneView& S, const int cb[3],
                                           float2 (&pa)[27], float2 (&pb)[27]) {
-    uint32_t tx[3], ty[3], tz[3];
-    node_offsets(S, cb, tx, ty, tz);
-    float4* g = P.grid_acc + S.node_base;
-    asm("" : "+l"(g));  // one 64-bit base, 32-bit node offsets
+    uint32_t base, px, pxy;
+    stencil_rows(P.geo, cb, base, px, pxy);
+    float4* g = P.grid_acc + S.node_base + base;
 #pragma unroll
     for (int dk = 0; dk < 3; ++dk)
 #pragma unroll
-        for (int dj = 0; dj < 3; ++dj)
+        for (int dj = 0; dj < 3; ++dj) {
+            float4* row = g + (dk * pxy + dj * px);
 #pragma unroll
             for (int di = 0; di < 3; ++di) {
                 const int n = (dk * 3 + dj) * 3 + di;
-                red_add_v4(g + (tz[dk] + ty[dj] + tx[di]), pa[n], pb[n]);
+                red_add_v4(row + di, pa[n], pb[n]);
                 pa[n] = f2(0.f, 0.f);
                 pb[n] = f2(0.f, 0.f);
             }
+        }
     mark_bricks(P, S, cb);
 }
 
@@ -199,56 +208,65 @@ void launch_collect_bricks(const Params& P, uint32_t n_bricks, cudaStream_t st) 
 
 __device__ __forceinline__ uint32_t bin_word(uint32_t b) { return b + (b >> 5); }
 
-// Warp counting sort of group g by current stencil base.  Element e = lane + 32 i is slot
-// g*kGroup + e; inactive particles (and slots past the binned active range) are dropped.
-// Returns the lane's 8 sorted slot bytes and the group's active count; `bins` is kBinWords
-// words and `order_s` kGroup bytes of this warp's shared memory (both free on entry).
-__device__ __forceinline__ uint64_t group_sort(const Params& P, uint32_t g, uint32_t n_active,
-                                               uint32_t* bins, uint8_t* order_s, uint32_t& n_act) {
+// Warp counting sort of group g by current stencil base, STABLE in the previous order:
+// element (i, lane) is the particle of previous sorted position p = 32 i + lane (slot
+// g*kGroup + group_phys(p)), and equal bins are ranked in (i, lane) order (warp-aggregated
+// smem atomics).  Active particles come first in bin order, then inactive ones and holes
+// in previous order.  Writes all kGroup order bytes (slot-in-group of each position) to
+// order_s and returns the lane's 8 P2G positions [8L, 8L+8); `bins` is kBinWords words.
+__device__ __forceinline__ uint64_t group_sort(const Params& P, uint32_t g, uint32_t* bins, uint8_t* order_s,
+                                               uint32_t& n_act) {
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31;
+    const unsigned lt = lanemask_lt();
     const uint32_t slot0 = g * kGroup;
     uint32_t bin[kPer];
-    // all 16 loads first (unconditional, clamped slot): one memory latency per group
+    // all 16 loads first: one memory latency per group
     float4 xa4[kPer];
     uint32_t fl[kPer];
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
-        const uint32_t s = min(slot0 + lane + 32u * i, n_active - 1u);
+        const uint32_t s = slot0 + group_phys(32u * i + lane);
         fl[i] = __float_as_uint(__ldg(&P.pl[PR][s].z));
         xa4[i] = __ldg(&P.pl[0][s]);
     }
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
-        const uint32_t s = slot0 + lane + 32u * i;
         bin[i] = 0xFFFFFFFFu;
-        if (s < n_active) {
-            const uint32_t flags = fl[i];
-            if (flags & kActiveBit) {
-                const float4 a = xa4[i];
-                const int scene = static_cast<int>((flags >> kSceneShift) & kSceneMask);
-                const float xa[3] = {a.x, a.y, a.z};
-                int b[3];
+        const uint32_t flags = fl[i];
+        if (flags & kActiveBit) {
+            const float4 a = xa4[i];
+            const int scene = static_cast<int>((flags >> kSceneShift) & kSceneMask);
+            const float xa[3] = {a.x, a.y, a.z};
+            int b[3];
 #pragma unroll
-                for (int q = 0; q < 3; ++q) {
-                    float fx;
-                    b[q] = stencil_base(xa[q], P.geo.origin[q], P.geo.inv_dx, fx);
-                    b[q] = min(max(b[q], 0), P.geo.dims[q] - 3);
-                }
-                const uint32_t brick = static_cast<uint32_t>(scene) * P.geo.bricks_per_scene +
-                                       (static_cast<uint32_t>(b[2] >> 2) * P.geo.nb[1] +
-                                        static_cast<uint32_t>(b[1] >> 2)) * P.geo.nb[0] +
-                                       static_cast<uint32_t>(b[0] >> 2);
-                bin[i] = ((brick & 7u) << 6) | static_cast<uint32_t>(((b[2] & 3) << 4) | ((b[1] & 3) << 2) | (b[0] & 3));
+            for (int q = 0; q < 3; ++q) {
+                float fx;
+                b[q] = stencil_base(xa[q], P.geo.origin[q], P.geo.inv_dx, fx);
+                b[q] = min(max(b[q], 0), P.geo.dims[q] - 3);
             }
+            const uint32_t brick = static_cast<uint32_t>(scene) * P.geo.bricks_per_scene +
+                                   (static_cast<uint32_t>(b[2] >> 2) * P.geo.nb[1] +
+                                    static_cast<uint32_t>(b[1] >> 2)) * P.geo.nb[0] +
+                                   static_cast<uint32_t>(b[0] >> 2);
+            bin[i] = ((brick & 7u) << 6) | static_cast<uint32_t>(((b[2] & 3) << 4) | ((b[1] & 3) << 2) | (b[0] & 3));
         }
     }
     for (int w = lane; w < kBinWords; w += 32) bins[w] = 0u;
     __syncwarp();
     uint32_t rank[kPer];
+    uint32_t n_inact = 0;
 #pragma unroll
-    for (int i = 0; i < kPer; ++i)
-        if (bin[i] != 0xFFFFFFFFu) rank[i] = atomicAdd(&bins[bin_word(bin[i])], 1u);
+    for (int i = 0; i < kPer; ++i) {
+        const unsigned peers = __match_any_sync(full, bin[i]);
+        const int lead = __ffs(peers) - 1;
+        const unsigned inact = __ballot_sync(full, bin[i] == 0xFFFFFFFFu);
+        uint32_t base = 0;
+        if (bin[i] != 0xFFFFFFFFu && lane == lead) base = atomicAdd(&bins[bin_word(bin[i])], __popc(peers));
+        base = __shfl_sync(full, base, lead);
+        rank[i] = bin[i] != 0xFFFFFFFFu ? base + __popc(peers & lt) : n_inact + __popc(inact & lt);
+        n_inact += __popc(inact);
+    }
     __syncwarp();
     // exclusive scan over bins in index order: lane L owns bins [16L, 16L+16)
     constexpr int kOwn = kBins / 32;
@@ -274,8 +292,10 @@ __device__ __forceinline__ uint64_t group_sort(const Params& P, uint32_t g, uint
     }
     __syncwarp();
 #pragma unroll
-    for (int i = 0; i < kPer; ++i)
-        if (bin[i] != 0xFFFFFFFFu) order_s[bins[bin_word(bin[i])] + rank[i]] = static_cast<uint8_t>(lane + 32 * i);
+    for (int i = 0; i < kPer; ++i) {
+        const uint32_t pos = bin[i] != 0xFFFFFFFFu ? bins[bin_word(bin[i])] + rank[i] : n_act + rank[i];
+        order_s[pos] = static_cast<uint8_t>(group_phys(32u * i + lane));
+    }
     __syncwarp();
     const uint64_t mine = reinterpret_cast<const uint64_t*>(order_s)[lane];
     __syncwarp();  // the caller reuses this shared memory for staging
@@ -288,7 +308,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_p2g(cons
     constexpr int NP = kPlanes;
     const int lane = threadIdx.x & 31;
     const uint32_t n_groups = *P.n_groups;
-    const uint32_t n_active = *P.n_active;
     const uint32_t wpb = blockDim.x >> 5;
     Stager<NP> st;
     st.buf = smem + (threadIdx.x >> 5) * (kStages * NP * 32);
@@ -297,7 +316,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_p2g(cons
     uint8_t* order_s = reinterpret_cast<uint8_t*>(bins + kBinWords);
     for (uint32_t g = blockIdx.x * wpb + (threadIdx.x >> 5); g < n_groups; g += gridDim.x * wpb) {
         uint32_t n_act;
-        st.order = group_sort(P, g, n_active, bins, order_s, n_act);
+        st.order = group_sort(P, g, bins, order_s, n_act);
         st.slot0 = g * kGroup;
         st.cnt = min(max(static_cast<int>(n_act) - kPer * lane, 0), kPer);
         reinterpret_cast<uint64_t*>(P.order)[static_cast<uint64_t>(g) * 32 + lane] = st.order;
@@ -384,9 +403,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_p2g(cons
 // (dk, dj) over di with the x-weights, then scaled by w_y w_z.  The 27 nodes are read
 // straight from L1: the warp's 32 lanes hold 32 consecutive sorted particles (a few
 // stencil bases), so each load instruction touches only a handful of lines.
-__device__ __forceinline__ void g2p_gather(const float4* g, const uint32_t tx[3], const uint32_t ty[3],
-                                           const uint32_t tz[3], const float w[3][3], const float rel[3][3],
-                                           float vn[3], float B[9]) {
+__device__ __forceinline__ void g2p_gather(const float4* g, uint32_t px, uint32_t pxy, const float w[3][3],
+                                           const float rel[3][3], float vn[3], float B[9]) {
     float wr0[3];
 #pragma unroll
     for (int o = 0; o < 3; ++o) wr0[o] = w[0][o] * rel[0][o];
@@ -398,7 +416,7 @@ __device__ __forceinline__ void g2p_gather(const float4* g, const uint32_t tx[3]
     for (int dk = 0; dk < 3; ++dk) {
         float4 q[9];
 #pragma unroll
-        for (int n = 0; n < 9; ++n) q[n] = __ldg(g + (tz[dk] + ty[n / 3] + tx[n % 3]));
+        for (int n = 0; n < 9; ++n) q[n] = __ldg(g + (dk * pxy + (n / 3) * px) + (n % 3));
 #pragma unroll
         for (int dj = 0; dj < 3; ++dj) {
             float2 a01 = f2(0.f, 0.f), b01 = f2(0.f, 0.f);
@@ -468,6 +486,16 @@ __device__ __forceinline__ int pushout_particle(const Params& P, const SceneView
     return pushed;
 }
 
+__device__ __forceinline__ void store_part_out(const Params& P, uint32_t s, const Part& p, float4 r) {
+    P.pl_out[0][s] = make_float4(p.x[0], p.x[1], p.x[2], p.v[0]);
+    P.pl_out[1][s] = make_float4(p.v[1], p.v[2], p.C[0], p.C[1]);
+    P.pl_out[2][s] = make_float4(p.C[2], p.C[3], p.C[4], p.C[5]);
+    P.pl_out[3][s] = make_float4(p.C[6], p.C[7], p.C[8], p.F[0]);
+    P.pl_out[4][s] = make_float4(p.F[1], p.F[2], p.F[3], p.F[4]);
+    P.pl_out[5][s] = make_float4(p.F[5], p.F[6], p.F[7], p.F[8]);
+    P.pl_out[PR][s] = r;
+}
+
 // F <- (I + C dt) F  (solvers.hpp:194, 275).  F only feeds the stress (never a contact
 // or push-out decision), so it keeps FMA contraction: F + dt (C F).
 __device__ __forceinline__ void update_F(const float C[9], float dt, float F[9]) {
@@ -494,19 +522,23 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(cons
     st.lane = lane;
     for (uint32_t g = blockIdx.x * wpb + (threadIdx.x >> 5); g < n_groups; g += gridDim.x * wpb) {
         // replay the order P2G sorted this group into (positions are unchanged since);
-        // lane L takes sorted positions L + 32 k, so the warp's 32 lanes gather around a
-        // few neighbouring stencils at every iteration
+        // lane L takes positions g2p_pos(L, k): the warp's 32 lanes gather around a few
+        // neighbouring stencils at every iteration.  Every position is written to the other
+        // buffer at slot group_phys(pos): the state leaves G2P in the new order.
         const uint32_t n_act = P.group_nact[g];
+        st.cnt = 0;
         {
-            const uint8_t* ob = P.order + static_cast<uint64_t>(g) * kGroup + lane;
+            const uint8_t* ob = P.order + static_cast<uint64_t>(g) * kGroup;
             uint64_t o = 0;
 #pragma unroll
-            for (int k = 0; k < kPer; ++k) o |= static_cast<uint64_t>(ob[32 * k]) << (8 * k);
+            for (int k = 0; k < kPer; ++k) {
+                o |= static_cast<uint64_t>(ob[g2p_pos(lane, k)]) << (8 * k);
+                st.cnt += g2p_pos(lane, k) < n_act ? 1 : 0;
+            }
             st.order = o;
         }
         st.slot0 = g * kGroup;
-        st.cnt = static_cast<int>((n_act + 31u - static_cast<uint32_t>(lane)) / 32u);
-        const int kmax = static_cast<int>((n_act + 31u) / 32u);
+        const int kmax = __reduce_max_sync(0xffffffffu, st.cnt);
         for (int k = 0; k < kStages - 1; ++k) st.issue(P, k);
         int my_scene = 0;
         int n_inv = 0, n_fail = 0, n_push = 0, n_deact = 0;
@@ -514,7 +546,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(cons
             st.issue(P, k + kStages - 1);
             cp_wait<kStages - 1>();
             if (k >= st.cnt) continue;
-            const uint32_t s = st.slot(k);
+            const uint32_t so = st.slot0 + group_phys(g2p_pos(lane, k));
             const float4* src = st.buf + (k % kStages) * NP * 32 + lane;
             float4 r = src[(NP - 1) * 32];
             uint32_t flags = __float_as_uint(r.z);
@@ -554,11 +586,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(cons
             }
             float B[9];
             {
-                uint32_t tx[3], ty[3], tz[3];
-                node_offsets(S, b, tx, ty, tz);
-                const float4* gv = P.grid_vel + S.node_base;
-                asm("" : "+l"(gv));  // one 64-bit base, 32-bit node offsets
-                g2p_gather(gv, tx, ty, tz, w, rel, p.v, B);
+                uint32_t base, px, pxy;
+                stencil_rows(P.geo, b, base, px, pxy);
+                g2p_gather(P.grid_vel + S.node_base + base, px, pxy, w, rel, p.v, B);
             }
             bool do_commit;
             if (!PB) {  // solvers.hpp:191-195
@@ -588,11 +618,16 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(cons
                 if (P.deactivate && !spline_in_domain(mk(p.x[0], p.x[1], p.x[2]), S)) {
                     flags &= ~kActiveBit;
                     r.z = __uint_as_float(flags);
-                    P.pl[PR][s] = r;
                     ++n_deact;
                 }
             }
-            store_part(P, s, p);
+            store_part_out(P, so, p, r);
+        }
+        // inactive particles and holes of the group move to their new slots unchanged
+        for (int k = st.cnt; k < kPer; ++k) {
+            const uint32_t si = st.slot(k), so = st.slot0 + group_phys(g2p_pos(lane, k));
+#pragma unroll
+            for (int q = 0; q < kPlanes; ++q) P.pl_out[q][so] = P.pl[q][si];
         }
         add_scene_counter(P.counters, my_scene, 0, n_inv);
         add_scene_counter(P.counters, my_scene, 1, n_fail);

@@ -23,6 +23,14 @@ namespace mpmb {
 
 // slots per transfer group: one warp re-sorts and processes one group per substep
 constexpr int kGroup = 256;
+// Inside a group the particle of sorted position p lives at slot phys(p): lane L's k-th
+// particle of P2G (p = 8L + k) sits at 32k + L, so a stable order makes every P2G staging
+// load one contiguous 512-byte span, and G2P (p = L + 32k) touches 8 runs of 64 bytes.
+__host__ __device__ __forceinline__ uint32_t group_phys(uint32_t p) { return (p & 7u) * 32u + (p >> 3); }
+__host__ __device__ __forceinline__ uint32_t group_pos(uint32_t r) { return (r & 31u) * 8u + (r >> 5); }
+// original index of an empty slot (group padding / allocation tail): never active, never
+// downloaded
+constexpr uint32_t kHoleOrig = 0xFFFFFFFFu;
 
 // Particle slot = 7 float4 planes (112 B):
 //   P0 {x.x, x.y, x.z, v.x}   P1 {v.y, v.z, C0, C1}   P2 {C2, C3, C4, C5}
@@ -32,7 +40,8 @@ constexpr int kPlanes = 7;
 constexpr int PR = 6;
 
 struct Params {
-    float4* pl[kPlanes];
+    float4* pl[kPlanes];      // current particle planes (n_total slots)
+    float4* pl_out[kPlanes];  // the other buffer: G2P writes the group-sorted state there
     Geo geo;                             // uniform geometry of all scenes
     float4 mats_c[kMaxConstMats];        // {kind, mu, lambda, beta}, first kMaxConstMats materials
     const DevScene* scenes;              // per scene: shape range (and host bookkeeping)
@@ -56,7 +65,7 @@ struct Params {
     uint32_t* group_nact;  // per group: active particles (written by P2G, replayed by G2P)
     const uint32_t* n_groups;
     const uint32_t* n_active;
-    int64_t n_total;
+    int64_t n_total;          // slots (particles + holes), a fixed bound
     const float* stress_in;  // original-order uploaded sigma (first MLS P2G only)
     int use_stress_in;
     double* acc_sub;   // per shape: impulse[3], torque[3]
@@ -144,19 +153,19 @@ __device__ __forceinline__ const DevPose& pose_of(const Params& P, int i) {
                                                                          : P.pose_table[t];
 }
 
-// Offsets of the bricked node layout along each axis for stencil base b:
-// node index = tz[dk] + ty[dj] + tx[di] within the scene's node pool.
-__device__ __forceinline__ void node_offsets(const SceneView& S, const int b[3], uint32_t tx[3],
-                                             uint32_t ty[3], uint32_t tz[3]) {
-    const uint32_t sy = static_cast<uint32_t>(S.nb[0]) * kBrickNodes;
-    const uint32_t sz = sy * static_cast<uint32_t>(S.nb[1]);
-#pragma unroll
-    for (int o = 0; o < 3; ++o) {
-        const uint32_t ix = b[0] + o, iy = b[1] + o, iz = b[2] + o;
-        tx[o] = (ix >> 2) * kBrickNodes + (ix & 3u);
-        ty[o] = (iy >> 2) * sy + (iy & 3u) * 4u;
-        tz[o] = (iz >> 2) * sz + (iz & 3u) * 16u;
-    }
+// Node pool of a scene: LINEAR over the brick-padded dims (PX = 4 nb_x, PY = 4 nb_y):
+// node (i, j, k) = (k PY + j) PX + i.  Activity is tracked per 4x4x4 brick, but a
+// stencil's 27 nodes are 9 rows of 3 consecutive nodes (row bases + immediate offsets).
+__device__ __forceinline__ uint32_t node_linear(const Geo& G, int i, int j, int k) {
+    const uint32_t px = static_cast<uint32_t>(G.nb[0]) * 4u, py = static_cast<uint32_t>(G.nb[1]) * 4u;
+    return (static_cast<uint32_t>(k) * py + static_cast<uint32_t>(j)) * px + static_cast<uint32_t>(i);
+}
+// row (dk, dj) of the stencil at base b starts at node_linear(b) + dk PXY + dj PX
+__device__ __forceinline__ void stencil_rows(const Geo& G, const int b[3], uint32_t& base, uint32_t& px,
+                                             uint32_t& pxy) {
+    px = static_cast<uint32_t>(G.nb[0]) * 4u;
+    pxy = px * static_cast<uint32_t>(G.nb[1]) * 4u;
+    base = node_linear(G, b[0], b[1], b[2]);
 }
 
 // Warp-aggregated per-scene counter add; must be called by all 32 lanes.  Lanes of a
