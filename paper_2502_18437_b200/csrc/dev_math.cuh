@@ -94,8 +94,22 @@ __device__ __forceinline__ void bspline_w(float fx, float w[3]) {
     w[2] = 0.5f * c * c;
 }
 // Interior band test, DIVIDING by dx (math.hpp:203-213) as deactivation does.
+// in domain <=> 0.5 <= p < dims - 1.5 per axis; a multiply by 1/dx decides every particle
+// farther than a safe margin from both thresholds, the exact division the rest.
 template <class SceneT>
 __device__ __forceinline__ bool spline_in_domain(V3 pos, const SceneT& S) {
+    {
+        const float d[3] = {__fsub_rn(pos.x, S.origin[0]), __fsub_rn(pos.y, S.origin[1]),
+                            __fsub_rn(pos.z, S.origin[2])};
+        bool inside = true;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const float q = d[a] * S.inv_dx;
+            const float eps = 1e-3f + 1e-5f * static_cast<float>(S.dims[a]);
+            inside = inside && q > 0.5f + eps && q < static_cast<float>(S.dims[a]) - 1.5f - eps;
+        }
+        if (inside) return true;
+    }
     const float p[3] = {__fdiv_rn(__fsub_rn(pos.x, S.origin[0]), S.dx),
                         __fdiv_rn(__fsub_rn(pos.y, S.origin[1]), S.dx),
                         __fdiv_rn(__fsub_rn(pos.z, S.origin[2]), S.dx)};
@@ -321,6 +335,14 @@ __device__ __forceinline__ V3 closest_on_triangle(V3 a, V3 b, V3 c, V3 p) {
     }
     float denom = FD(1.f, FA(FA(va, vb), vc));
     return a + ab * FM(vb, denom) + ac * FM(vc, denom);
+}
+
+// False when the point is provably outside every contact / push-out band of the shape
+// (DevShape::bound2); the reference's query would return no effect there.
+__device__ __forceinline__ bool shape_may_touch(const DevShape& g, const DevPose& pose, V3 point) {
+    if (g.bound2 < 0.f) return true;
+    const float dx = point.x - pose.pos[0], dy = point.y - pose.pos[1], dz = point.z - pose.pos[2];
+    return fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= g.bound2;
 }
 
 // World-space SDF query (geometry.hpp:370-395) against one device shape.

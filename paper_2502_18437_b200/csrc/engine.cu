@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <cstring>
 #include <stdexcept>
@@ -59,6 +60,31 @@ struct PinnedBuf {
 enum Cat { CAT_SORT = 0, CAT_P2G, CAT_GRID, CAT_G2P, CAT_OTHER };
 
 }  // namespace
+
+// DevShape::bound2: the largest |p| (local frame) at which any region of the shape can
+// still act -- contact bands use hw, push-out bands 0.5 hw (contact.hpp:82-92, 140-179) --
+// plus a relative margin for the float rotation.  Planes are unbounded.
+float shape_bound2(const DevShape& d, const std::vector<float>& verts) {
+    double r = -1.0;
+    double vmax = 0.0;
+    for (size_t i = 0; i + 2 < verts.size(); i += 3)
+        vmax = std::max(vmax, std::sqrt(double(verts[i]) * verts[i] + double(verts[i + 1]) * verts[i + 1] +
+                                        double(verts[i + 2]) * verts[i + 2]));
+    const double hw = std::max(0.0, double(d.hw));
+    switch (d.geom) {
+        case GEOM_PLANE: return -1.f;
+        case GEOM_SPHERE: r = d.gp[0]; break;
+        case GEOM_BOX: r = std::sqrt(double(d.gp[0]) * d.gp[0] + double(d.gp[1]) * d.gp[1] + double(d.gp[2]) * d.gp[2]); break;
+        case GEOM_QUAD_SLICER:
+            r = std::sqrt(double(d.gp[0]) * d.gp[0] + double(d.gp[1]) * d.gp[1]) + std::max(double(d.gp[2]), hw);
+            break;
+        case GEOM_TRI_MESH_SLICER: r = vmax + std::max(double(d.gp[0]), hw); break;
+        case GEOM_ARC: r = double(d.gp[0]) + hw; break;
+        default: r = vmax + hw; break;  // polyline
+    }
+    r = r * 1.001 + 1e-5;
+    return static_cast<float>(r * r);
+}
 
 bool device_available() {
     int n = 0;
@@ -445,6 +471,7 @@ void Engine::set_shapes(const std::vector<std::vector<EngineShape>>& per_scene) 
             d.spine_begin = static_cast<int>(ints.size());
             d.n_spine = static_cast<int>(e.spine.size());
             ints.insert(ints.end(), e.spine.begin(), e.spine.end());
+            d.bound2 = shape_bound2(d, e.verts);
             ds.push_back(d);
             poses.push_back(e.pose);
         }

@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(256) k_grid_update(const Params P) {
                 const DevShape& sh = P.shapes[si];
                 V3 imp = mk(0.f, 0.f, 0.f), tq = mk(0.f, 0.f, 0.f);
                 int hit = 0;
-                if (live) {
+                if (live && shape_may_touch(sh, pose_of(P, si), xn)) {
                     const DevPose& pose = pose_of(P, si);
                     const Sdf s = sdf_query(sh, pose, P.verts, P.ints, xn);
                     if (node_in_contact(s, sh.hw)) {

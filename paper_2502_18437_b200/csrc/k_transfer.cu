@@ -24,7 +24,14 @@
 
 namespace mpmb {
 
-constexpr int kStages = 3;
+#ifndef MPMB_P2G_STAGES
+#define MPMB_P2G_STAGES 3
+#endif
+#ifndef MPMB_G2P_STAGES
+#define MPMB_G2P_STAGES 3
+#endif
+constexpr int kStages = MPMB_P2G_STAGES;     // P2G staging ring depth
+constexpr int kG2PStages = MPMB_G2P_STAGES;  // G2P: one more, so particle k+1 has landed while k computes
 constexpr int kWarpsPerBlock = 4;
 constexpr int kPer = kGroup / 32;  // sorted positions per lane
 constexpr int kBins = 512;         // sort bins: ((global brick & 7) << 6) | cell
@@ -50,6 +57,18 @@ __device__ __forceinline__ void cp_async16(float4* smem, const float4* gmem) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
 }
+// Warm L1 with the 9 stencil rows (3 nodes, 48 B: first and last node) of base b.
+__device__ __forceinline__ void prefetch_stencil_l1(const float4* g, uint32_t px, uint32_t pxy) {
+#pragma unroll
+    for (int dk = 0; dk < 3; ++dk)
+#pragma unroll
+        for (int dj = 0; dj < 3; ++dj) {
+            const float4* row = g + (dk * pxy + dj * px);
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(row));
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(row + 2));
+        }
+}
+
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
@@ -70,9 +89,9 @@ struct PlaneSet<5> {  // P0 {x, vx}, P3 {C6..8, F0}, P4, P5 {F}, PR
 
 // Per-lane producer of the staging ring: issues the planes of the lane's k-th sorted
 // particle (lanes past their count commit an empty group, keeping the wait counts uniform).
-template <int NP>
+template <int NP, int NS = kStages>
 struct Stager {
-    float4* buf;        // this warp's ring: [kStages][NP][32]
+    float4* buf;        // this warp's ring: [NS][NP][32]
     uint32_t slot0;     // first slot of the group
     uint64_t order;     // the lane's 8 sorted particles, one slot-in-group byte each
     int cnt;            // how many of them exist
@@ -83,7 +102,7 @@ struct Stager {
     __device__ __forceinline__ void issue(const Params& P, int k) {
         if (k < cnt) {
             const uint32_t s = slot(k);
-            float4* dst = buf + (k % kStages) * NP * 32 + lane;
+            float4* dst = buf + (k % NS) * NP * 32 + lane;
 #pragma unroll
             for (int q = 0; q < NP; ++q) cp_async16(dst + q * 32, P.pl[PlaneSet<NP>::plane(q)] + s);
         }
@@ -457,6 +476,7 @@ __device__ __forceinline__ int pushout_particle(const Params& P, const SceneView
     for (int si = P.scenes[S.scene].shape_begin; si < P.scenes[S.scene].shape_begin + P.scenes[S.scene].shape_count; ++si) {
         const DevShape& sh = P.shapes[si];
         const DevPose& pose = pose_of(P, si);
+        if (!shape_may_touch(sh, pose, mk(x[0], x[1], x[2]))) continue;
         const Sdf s = sdf_query(sh, pose, P.verts, P.ints, mk(x[0], x[1], x[2]));
         float move = 0.f;
         if (s.region == REGION_SURFACE || s.region == REGION_SPINE) {
@@ -517,8 +537,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(cons
     const int lane = threadIdx.x & 31;
     const uint32_t n_groups = *P.n_groups;
     const uint32_t wpb = blockDim.x >> 5;
-    Stager<NP> st;
-    st.buf = smem + (threadIdx.x >> 5) * (kStages * NP * 32);
+    constexpr int NS = kG2PStages;
+    Stager<NP, NS> st;
+    st.buf = smem + (threadIdx.x >> 5) * (NS * NP * 32);
     st.lane = lane;
     for (uint32_t g = blockIdx.x * wpb + (threadIdx.x >> 5); g < n_groups; g += gridDim.x * wpb) {
         // replay the order P2G sorted this group into (positions are unchanged since);
@@ -539,15 +560,28 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(cons
         }
         st.slot0 = g * kGroup;
         const int kmax = __reduce_max_sync(0xffffffffu, st.cnt);
-        for (int k = 0; k < kStages - 1; ++k) st.issue(P, k);
+        for (int k = 0; k < NS - 1; ++k) st.issue(P, k);
         int my_scene = 0;
         int n_inv = 0, n_fail = 0, n_push = 0, n_deact = 0;
         for (int k = 0; k < kmax; ++k) {
-            st.issue(P, k + kStages - 1);
-            cp_wait<kStages - 1>();
+            st.issue(P, k + NS - 1);
+            cp_wait<(NS > 3 ? NS - 2 : NS - 1)>();  // particles k (and k+1) have landed
             if (k >= st.cnt) continue;
+            if (NS > 3 && k + 1 < st.cnt) {  // warm L1 with the next particle's stencil rows
+                const float4 xn = st.buf[((k + 1) % NS) * NP * 32 + lane];
+                int bn[3];
+                float fn;
+                bn[0] = min(max(stencil_base(xn.x, P.geo.origin[0], P.geo.inv_dx, fn), 0), P.geo.dims[0] - 3);
+                bn[1] = min(max(stencil_base(xn.y, P.geo.origin[1], P.geo.inv_dx, fn), 0), P.geo.dims[1] - 3);
+                bn[2] = min(max(stencil_base(xn.z, P.geo.origin[2], P.geo.inv_dx, fn), 0), P.geo.dims[2] - 3);
+                const uint32_t sn = (__float_as_uint(st.buf[((k + 1) % NS) * NP * 32 + (NP - 1) * 32 + lane].z) >>
+                                     kSceneShift) & kSceneMask;
+                uint32_t base, px, pxy;
+                stencil_rows(P.geo, bn, base, px, pxy);
+                prefetch_stencil_l1(P.grid_vel + sn * P.geo.nodes_per_scene + base, px, pxy);
+            }
             const uint32_t so = st.slot0 + group_phys(g2p_pos(lane, k));
-            const float4* src = st.buf + (k % kStages) * NP * 32 + lane;
+            const float4* src = st.buf + (k % NS) * NP * 32 + lane;
             float4 r = src[(NP - 1) * 32];
             uint32_t flags = __float_as_uint(r.z);
             Part p;
@@ -700,6 +734,12 @@ void launch_p2g(const Params& P, bool mls, int64_t max_groups, cudaStream_t st) 
     const int threads = kWarpsPerBlock * 32;
     const int smem = kWarpsPerBlock * kStages * kPlanes * 32 * static_cast<int>(sizeof(float4));
     const int blocks = grid_for(max_groups * 32, threads, 148 * 16);
+    static bool attr = false;
+    if (!attr) {  // > 48 KB of dynamic shared memory needs the opt-in
+        cudaFuncSetAttribute(k_p2g<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_p2g<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = true;
+    }
     if (mls) {
         k_p2g<true><<<blocks, threads, smem, st>>>(P);
     } else {
@@ -711,10 +751,20 @@ void launch_g2p(const Params& P, bool pb, int64_t max_groups, cudaStream_t st) {
     const int threads = kWarpsPerBlock * 32;
     const int blocks = grid_for(max_groups * 32, threads, 148 * 16);
     if (pb) {
-        const int smem = kWarpsPerBlock * kStages * 7 * 32 * static_cast<int>(sizeof(float4));
+        const int smem = kWarpsPerBlock * kG2PStages * 7 * 32 * static_cast<int>(sizeof(float4));
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_g2p<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            attr = true;
+        }
         k_g2p<true><<<blocks, threads, smem, st>>>(P);
     } else {
-        const int smem = kWarpsPerBlock * kStages * 5 * 32 * static_cast<int>(sizeof(float4));
+        const int smem = kWarpsPerBlock * kG2PStages * 5 * 32 * static_cast<int>(sizeof(float4));
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_g2p<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            attr = true;
+        }
         k_g2p<false><<<blocks, threads, smem, st>>>(P);
     }
 }
