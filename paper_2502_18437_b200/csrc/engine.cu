@@ -118,7 +118,7 @@ struct Engine::Impl {
         g_src, g_cell, s_src, s_orig, b_counts, scan_tmp, key_by_orig, order, group_nact;
     BinBuffers bb{};
     DevBuf mats;
-    DevBuf shapes, verts, ints, free_pose, pose_table, pose_override;
+    DevBuf shapes, verts, ints, free_pose, pose_table, pose_override, cull;
     int n_shapes = 0;
     int table_subs = 1;
     PinnedBuf pin_table[2];
@@ -197,6 +197,7 @@ struct Engine::Impl {
         P.pose_table = pose_table.as<DevPose>();
         P.pose_override = pose_override.as<uint8_t>();
         P.free_pose = free_pose.as<DevPose>();
+        P.cull = cull.as<float4>();
         P.n_shapes = n_shapes;
         P.mats = mats.as<float4>();
         P.grid_acc = grid_acc.as<float4>();
@@ -484,6 +485,7 @@ void Engine::set_shapes(const std::vector<std::vector<EngineShape>>& per_scene) 
     I.verts.alloc(sizeof(float) * std::max<size_t>(3, verts.size()));
     I.ints.alloc(sizeof(int) * std::max<size_t>(1, ints.size()));
     I.free_pose.alloc(sizeof(DevPose) * ns);
+    I.cull.alloc(sizeof(float4) * ns);
     I.acc_sub.alloc(sizeof(double) * 6 * ns);
     I.acc_frame.alloc(sizeof(double) * 6 * ns);
     I.cnt_sub.alloc(sizeof(int) * ns);
@@ -593,6 +595,10 @@ void Engine::grid_update(int sub, float dt, const float g[3], bool gravity, bool
     P.gravity = gravity ? 1 : 0;
     P.contact = contact ? 1 : 0;
     P.bc = bc;
+    if (I.n_shapes > 0) {  // G2P push-out of this substep reuses the table
+        launch_shape_cull(P, I.st);
+        I.counted(1);
+    }
     launch_grid_update(P, I.total_bricks, I.st);
     I.counted(1);
     I.end(CAT_GRID, ev);

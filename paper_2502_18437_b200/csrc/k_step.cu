@@ -18,6 +18,17 @@ __device__ __forceinline__ uint64_t brick_node(const Params& P, uint32_t gb, int
     return static_cast<uint64_t>(scene) * P.geo.nodes_per_scene + node_linear(P.geo, i, j, k);
 }
 
+// Per-substep shape cull table (one block): the pose position this substep (kinematic
+// table or integrated free pose) and the shape's bound2.
+__global__ void k_shape_cull(const Params P) {
+    for (int i = threadIdx.x; i < P.n_shapes; i += blockDim.x) {
+        const DevPose& pose = pose_of(P, i);
+        P.cull[i] = make_float4(pose.pos[0], pose.pos[1], pose.pos[2], P.shapes[i].bound2);
+    }
+}
+
+void launch_shape_cull(const Params& P, cudaStream_t st) { k_shape_cull<<<1, 128, 0, st>>>(P); }
+
 // ==============================================================  grid update
 // 64 threads per active brick (one node each).  Reads the P2G accumulator and zeroes it
 // (it is the last reader), writes {mass, velocity} for G2P.  Contact shapes are applied
@@ -69,7 +80,7 @@ __global__ void __launch_bounds__(256) k_grid_update(const Params P) {
                 const DevShape& sh = P.shapes[si];
                 V3 imp = mk(0.f, 0.f, 0.f), tq = mk(0.f, 0.f, 0.f);
                 int hit = 0;
-                if (live && shape_may_touch(sh, pose_of(P, si), xn)) {
+                if (live && cull_may_touch(P, si, xn.x, xn.y, xn.z)) {
                     const DevPose& pose = pose_of(P, si);
                     const Sdf s = sdf_query(sh, pose, P.verts, P.ints, xn);
                     if (node_in_contact(s, sh.hw)) {

@@ -51,6 +51,7 @@ struct Params {
     const DevPose* pose_table;
     const uint8_t* pose_override;
     DevPose* free_pose;
+    float4* cull;   // per shape, this substep: {pose position, bound2} (k_shape_cull)
     int n_shapes;
     const float4* mats;  // {kind, mu, lambda, beta}
     float4* grid_acc;
@@ -166,6 +167,15 @@ __device__ __forceinline__ void stencil_rows(const Geo& G, const int b[3], uint3
     px = static_cast<uint32_t>(G.nb[0]) * 4u;
     pxy = px * static_cast<uint32_t>(G.nb[1]) * 4u;
     base = node_linear(G, b[0], b[1], b[2]);
+}
+
+// Cheap reject before an SDF query: false when x is provably outside every band of shape
+// si at this substep (DevShape::bound2 around the pose position; bound2 < 0: unbounded).
+__device__ __forceinline__ bool cull_may_touch(const Params& P, int si, float x, float y, float z) {
+    const float4 c = P.cull[si];
+    if (c.w < 0.f) return true;
+    const float dx = x - c.x, dy = y - c.y, dz = z - c.z;
+    return fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= c.w;
 }
 
 // Warp-aggregated per-scene counter add; must be called by all 32 lanes.  Lanes of a
