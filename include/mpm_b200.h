@@ -276,7 +276,8 @@ mpmb_status mpmb_scene_get_particles(mpmb_handle scene, float* x, float* v, floa
                                      uint8_t* active);
 
 /* Execution control: run on the caller's cudaStream_t (NULL = library stream), re-bin every
- * k substeps (0 = once per frame), profile kernel classes with CUDA events. */
+ * k substeps (0 = every 4 frames; binning only re-compacts the transfer groups, P2G re-sorts
+ * each group every substep), profile kernel classes with CUDA events. */
 mpmb_status mpmb_set_stream(mpmb_handle h, void* cuda_stream);
 mpmb_status mpmb_set_resort_interval(mpmb_handle h, int32_t substeps);
 mpmb_status mpmb_set_profiling(mpmb_handle h, int32_t on);

@@ -468,7 +468,8 @@ struct Batch {
     bool particles_dirty = true; // host changed: re-upload
     bool shapes_dirty = true;
     Status status = Status::idle;
-    int resort = 0;
+    int resort = 0;               // substeps between binnings (0: every 4 frames)
+    int64_t since_sort = 1 << 30; // substeps since the last binning (runs across frames)
     bool profiling = false;
     void* stream = nullptr;
     std::vector<size_t> offsets;  // per scene: first original index in the engine
@@ -685,10 +686,17 @@ void run_frame(Batch& b, float dt) {
     }
     e.reset_counters();
     e.reset_contact(true, true);
-    const int resort = b.resort > 0 ? b.resort : n_sub;
+    // binning restores the spatial compactness of the 256-slot groups; drift inside a group
+    // is absorbed by P2G's per-substep warp sort, so the full sort runs every 4 frames
+    // unless the caller chose an interval (mpmb_set_resort_interval)
+    const int resort = b.resort > 0 ? b.resort : 4 * n_sub;
     if (!pb) {
         for (int sub = 0; sub < n_sub; ++sub) {
-            if (sub % resort == 0) e.bin();
+            if (b.since_sort >= resort) {
+                e.bin();
+                b.since_sort = 0;
+            }
+            ++b.since_sort;
             e.p2g(true, dt_sub);
             e.grid_update(sub, dt_sub, cfg.gravity, true, true, cfg.boundary);
             e.g2p_mls(sub, dt_sub, true, true);

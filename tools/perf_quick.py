@@ -6,7 +6,10 @@ sys.path.insert(0, str(ROOT)); sys.path.insert(0, str(ROOT / "tests"))
 import bench
 R = int(sys.argv[1]) if len(sys.argv) > 1 else 256
 F = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+RS = int(sys.argv[3]) if len(sys.argv) > 3 else 0  # resort interval in substeps (0: once per frame)
 b = bench.build_batch(bench.workload_specs("c5", 0, R))
+if RS:
+    b.set_resort_interval(RS)
 n = sum(s.particle_count() for s in b.scenes)
 b.advance_frames(0.02, 2); b.fetch_results()
 b.set_profiling(True)
