@@ -1,0 +1,161 @@
+"""GPU parity at scale and on edge cases, through the C-ABI.
+
+Full-size runs cannot be checked against the serial oracle particle by particle in
+seconds, so they are checked through properties that do not depend on size, plus an
+oracle comparison of a sampled replica:
+
+  C5 batch replica r vs the oracle's replica r   max|dx| <= 1e-3 * dx (scene horizon bound)
+  per-scene mass / active count                   mass rel 1e-12 (FP64 totals), counts exact
+  binning at C2 size (262,144 p)                  keys + permutation bit-exact
+  resort interval 1 vs default                    max|dx| <= 1e-3 * dx (order-only change)
+  state round trip (n not a multiple of 256)      bit-exact
+  empty scene, single particle, all inactive      exact / oracle tolerance
+"""
+import numpy as np
+import pytest
+
+import backends
+from paper_2502_18437_b200 import api, capi, scenes
+
+pytestmark = pytest.mark.gpu
+F32 = np.float32
+
+
+def _batch(specs):
+    cfg = api.scene_config(**scenes.config_kwargs(specs[0]))
+    b = api.SceneBatch(cfg, len(specs))
+    for sc, sp in zip(b.scenes, specs):
+        scenes.populate(sc, sp)
+    return b
+
+
+def test_c5_batch_replicas_vs_oracle_and_conservation():
+    R, frames = 32, 2
+    specs = [scenes.c5_cutting_replica(r) for r in range(R)]
+    b = _batch(specs)
+    for _ in range(frames):
+        b.advance(specs[0]["dt_frame"])
+        res = b.fetch_results(arrays=True)
+    dx = specs[0]["grid"]["dx"]
+    for r in (0, 17, R - 1):
+        o = backends.make_scene("oracle", specs[r])
+        for _ in range(frames):
+            o.advance(specs[r]["dt_frame"])
+            ro = o.fetch_results()
+        rg = res[r]
+        assert ro["n_particles"] == rg["n_particles"] == 64800
+        assert np.array_equal(ro["active"], rg["active"])
+        both = ro["active"].astype(bool)
+        assert np.abs(ro["positions"][both] - rg["positions"][both]).max() <= 1e-3 * dx
+        assert abs(ro["total_mass"] - rg["total_mass"]) <= 1e-12 * ro["total_mass"]
+        np.testing.assert_allclose(rg["shape_impulses"], ro["shape_impulses"], rtol=0.05,
+                                   atol=1e-6 * max(1.0, float(np.abs(ro["shape_impulses"]).max())))
+    for rg in res:
+        assert np.isfinite(rg["positions"]).all() and np.isfinite(rg["velocities"]).all()
+
+
+def test_binning_bit_exact_c2_size():
+    spec = scenes.c2_cutting()  # C2 lattice: 262,144 particles on 128^3
+    dims, dx = tuple(spec["grid"]["dims"]), spec["grid"]["dx"]
+    ob = spec["particle_objects"][0]
+    o = backends.oracle()
+    n_cap = 300000
+    x, m, vol = np.zeros((n_cap, 3), F32), np.zeros(n_cap, F32), np.zeros(n_cap, F32)
+    n = o.mpmor_spawn_box((capi.i3)(*dims), dx, api._fp(np.zeros(3, F32)), api._fp(np.array(ob["box_min"], F32)),
+                          api._fp(np.array(ob["box_max"], F32)), 8, 1000.0, ob["seed"], n_cap, api._fp(x),
+                          api._fp(m), api._fp(vol))
+    assert n == 262144
+    p = api.empty_particles(n)
+    p["x"], p["mass"], p["volume0"] = x[:n].copy(), m[:n].copy(), vol[:n].copy()
+    rng = np.random.default_rng(5)
+    p["x"] += rng.uniform(-0.3 * dx, 0.3 * dx, p["x"].shape).astype(F32)
+    p["active"][::53] = 0
+    mats = [(capi.MAT_NEO_HOOKEAN, *scenes.lame(1e4, 0.3), 0.9)]
+    o = backends.state("oracle", dims, dx)
+    g = backends.state("gpu", dims, dx)
+    for s in (o, g):
+        s.set_materials(mats)
+        s.set_particles(p)
+    ko, po = o.bin()
+    kg, pg = g.bin()
+    assert np.array_equal(ko, kg)
+    assert np.array_equal(po, pg)
+
+
+def test_resort_interval_does_not_change_results():
+    spec = scenes.cutting()
+    a = backends.make_scene("gpu", spec)
+    b = backends.make_scene("gpu", spec)
+    assert b.lib.mpmb_set_resort_interval(b.h, 1) == capi.OK  # bin every substep
+    for _ in range(3):
+        a.advance(spec["dt_frame"])
+        b.advance(spec["dt_frame"])
+        ra, rb = a.fetch_results(), b.fetch_results()
+    assert np.array_equal(ra["active"], rb["active"])
+    live = ra["active"].astype(bool)
+    assert np.abs(ra["positions"][live] - rb["positions"][live]).max() <= 1e-3 * spec["grid"]["dx"]
+
+
+def test_state_round_trip_is_exact():
+    n = 1000  # not a multiple of the 256-slot group: exercises the hole padding
+    rng = np.random.default_rng(11)
+    p = api.empty_particles(n)
+    p["x"] = rng.uniform(0.3, 0.9, (n, 3)).astype(F32)
+    p["v"] = rng.normal(0, 0.1, (n, 3)).astype(F32)
+    p["F"] += rng.normal(0, 0.01, (n, 9)).astype(F32)
+    p["C"] = rng.normal(0, 0.1, (n, 9)).astype(F32)
+    p["mass"][:] = rng.uniform(0.5, 1.5, n).astype(F32)
+    p["volume0"][:] = 1e-3
+    p["active"][::7] = 0
+    g = backends.state("gpu", (24, 24, 24), 0.05)
+    g.set_materials([(capi.MAT_NEO_HOOKEAN, *scenes.lame(100.0, 0.3), 0.9)])
+    g.set_particles(p)
+    g.bin()  # the device layout is now grouped, padded and permuted
+    q = g.get_particles()
+    for k in ("x", "v", "F", "C", "mass", "volume0", "active"):
+        assert np.array_equal(np.asarray(q[k]).reshape(np.asarray(p[k]).shape), p[k]), k
+
+
+def test_empty_scene_advances():
+    spec = scenes.cube_drop(dims=(24, 24, 24))
+    spec["particle_objects"] = []
+    g = backends.make_scene("gpu", spec)
+    g.advance(spec["dt_frame"])
+    r = g.fetch_results()
+    assert r["n_particles"] == 0
+    assert r["total_mass"] == 0.0
+
+
+def test_single_particle_vs_oracle():
+    dims, dx = (16, 16, 16), 0.05
+    p = api.empty_particles(1)
+    p["x"][0] = (0.41, 0.43, 0.39)
+    p["v"][0] = (0.3, -0.2, 0.1)
+    p["mass"][0], p["volume0"][0] = 1.0, 1e-4
+    mats = [(capi.MAT_NEO_HOOKEAN, *scenes.lame(100.0, 0.3), 0.9)]
+    o = backends.state("oracle", dims, dx)
+    g = backends.state("gpu", dims, dx)
+    for s in (o, g):
+        s.set_materials(mats)
+        s.set_particles(p)
+        for _ in range(5):
+            s.step_mls(0.002, (0.0, -9.81, 0.0))
+    a, b = o.get_particles(), g.get_particles()
+    assert np.abs(a["x"] - b["x"]).max() <= 1e-5 * dx
+    assert np.abs(a["v"] - b["v"]).max() <= 1e-5 * np.abs(a["v"]).max() + 1e-7
+
+
+def test_all_inactive_particles_stay_put():
+    p = api.empty_particles(700)
+    rng = np.random.default_rng(4)
+    p["x"] = rng.uniform(0.3, 0.6, (700, 3)).astype(F32)
+    p["v"] = rng.normal(0, 1.0, (700, 3)).astype(F32)
+    p["mass"][:], p["volume0"][:] = 1.0, 1e-4
+    p["active"][:] = 0
+    g = backends.state("gpu", (24, 24, 24), 0.05)
+    g.set_materials([(capi.MAT_NEO_HOOKEAN, *scenes.lame(100.0, 0.3), 0.9)])
+    g.set_particles(p)
+    for _ in range(3):
+        g.step_mls(0.002, (0.0, -9.81, 0.0))
+    q = g.get_particles()
+    assert np.array_equal(q["x"], p["x"]) and np.array_equal(q["v"], p["v"])
