@@ -52,12 +52,17 @@ __global__ void k_download(const Params P, IoArrays out) {
         const uint32_t o32 = __float_as_uint(r.w);
         if (o32 == kHoleOrig) continue;
         const uint64_t o = o32;
-        Part p;
-        load_part(P, static_cast<uint32_t>(s), p);
-        if (out.x) for (int a = 0; a < 3; ++a) out.x[3 * o + a] = p.x[a];
-        if (out.v) for (int a = 0; a < 3; ++a) out.v[3 * o + a] = p.v[a];
-        if (out.F) for (int a = 0; a < 9; ++a) out.F[9 * o + a] = p.F[a];
-        if (out.C) for (int a = 0; a < 9; ++a) out.C[9 * o + a] = p.C[a];
+        if (out.x || out.v) {  // P0 {x, v.x}, P1 {v.y, v.z, ...}: the FrameResult planes only
+            const float4 a = P.pl[0][s], b = P.pl[1][s];
+            if (out.x) { out.x[3 * o] = a.x; out.x[3 * o + 1] = a.y; out.x[3 * o + 2] = a.z; }
+            if (out.v) { out.v[3 * o] = a.w; out.v[3 * o + 1] = b.x; out.v[3 * o + 2] = b.y; }
+        }
+        if (out.F || out.C) {
+            Part p;
+            load_part(P, static_cast<uint32_t>(s), p);
+            if (out.F) for (int a = 0; a < 9; ++a) out.F[9 * o + a] = p.F[a];
+            if (out.C) for (int a = 0; a < 9; ++a) out.C[9 * o + a] = p.C[a];
+        }
         if (out.mass) out.mass[o] = r.x;
         if (out.vol0) out.vol0[o] = r.y;
         if (out.mat) out.mat[o] = static_cast<int32_t>(flags & kMatMask);
@@ -67,43 +72,64 @@ __global__ void k_download(const Params P, IoArrays out) {
 }
 
 // Per-scene double totals: mass, momentum[3], kinetic energy (scene.hpp:258-266).
-__global__ void k_totals(const Params P, double* totals) {
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    const unsigned full = 0xffffffffu;
-    const int lane = threadIdx.x & 31;
-    for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < P.n_total; base += stride) {
-        const int64_t s = base + threadIdx.x;
+// Slots are grouped by scene, so a block's slots belong to very few scenes: threads
+// accumulate per "current scene" and the block reduces runs of equal scene through shared
+// memory before one FP64 atomic per (block, scene, value) -- same-address atomics from
+// every warp serialise in L2 and dominated the old per-warp version.
+constexpr int kTotThreads = 256;
+constexpr int kTotPerThread = 16;
+__global__ void __launch_bounds__(kTotThreads) k_totals(const Params P, double* totals) {
+    __shared__ double red[5][kTotThreads];
+    __shared__ int scn[kTotThreads];
+    const int64_t span = static_cast<int64_t>(kTotThreads) * kTotPerThread;
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * span; base < P.n_total;
+         base += static_cast<int64_t>(gridDim.x) * span) {
         double t[5] = {0, 0, 0, 0, 0};
         int scene = -1;
-        if (s < P.n_total) {
+        for (int i = 0; i < kTotPerThread; ++i) {  // coalesced: stride blockDim per step
+            const int64_t s = base + static_cast<int64_t>(i) * kTotThreads + threadIdx.x;
+            if (s >= P.n_total) break;
             const float4 r = P.pl[PR][s];
             const uint32_t flags = __float_as_uint(r.z);
-            if (flags & kActiveBit) {
-                scene = static_cast<int>((flags >> kSceneShift) & kSceneMask);
-                const float4 a = P.pl[0][s], b = P.pl[1][s];
-                const double m = r.x;
-                const float vx = a.w, vy = b.x, vz = b.y;
-                t[0] = m;
-                t[1] = m * vx;
-                t[2] = m * vy;
-                t[3] = m * vz;
-                t[4] = 0.5 * m * static_cast<double>(vx * vx + vy * vy + vz * vz);
+            if (!(flags & kActiveBit)) continue;
+            const int sc = static_cast<int>((flags >> kSceneShift) & kSceneMask);
+            if (sc != scene) {
+                if (scene >= 0)
+                    for (int q = 0; q < 5; ++q) atomicAdd(&totals[5 * scene + q], t[q]);
+                scene = sc;
+                for (int q = 0; q < 5; ++q) t[q] = 0.0;
             }
+            const float4 a = P.pl[0][s], b = P.pl[1][s];
+            const double m = r.x;
+            const float vx = a.w, vy = b.x, vz = b.y;
+            t[0] += m;
+            t[1] += m * vx;
+            t[2] += m * vy;
+            t[3] += m * vz;
+            t[4] += 0.5 * m * static_cast<double>(vx * vx + vy * vy + vz * vz);
         }
-        const unsigned has = __ballot_sync(full, scene >= 0);
-        if (!has) continue;
-        const int lead = __ffs(has) - 1;
-        const int s0 = __shfl_sync(full, scene, lead);
-        if (__all_sync(full, scene < 0 || scene == s0)) {
-#pragma unroll
-            for (int q = 0; q < 5; ++q)
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) t[q] += __shfl_xor_sync(full, t[q], o);
-            if (lane == lead)
-                for (int q = 0; q < 5; ++q) atomicAdd(&totals[5 * s0 + q], t[q]);
-        } else if (scene >= 0) {
-            for (int q = 0; q < 5; ++q) atomicAdd(&totals[5 * scene + q], t[q]);
+        // runs of equal scene across the block's threads are summed by thread 0
+        scn[threadIdx.x] = scene;
+        for (int q = 0; q < 5; ++q) red[q][threadIdx.x] = t[q];
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int cur = -1;
+            double acc[5] = {0, 0, 0, 0, 0};
+            for (int k = 0; k < kTotThreads; ++k) {
+                const int sc = scn[k];
+                if (sc < 0) continue;
+                if (sc != cur) {
+                    if (cur >= 0)
+                        for (int q = 0; q < 5; ++q) atomicAdd(&totals[5 * cur + q], acc[q]);
+                    cur = sc;
+                    for (int q = 0; q < 5; ++q) acc[q] = 0.0;
+                }
+                for (int q = 0; q < 5; ++q) acc[q] += red[q][k];
+            }
+            if (cur >= 0)
+                for (int q = 0; q < 5; ++q) atomicAdd(&totals[5 * cur + q], acc[q]);
         }
+        __syncthreads();
     }
 }
 
@@ -185,7 +211,7 @@ void launch_download(const Params& P, const IoArrays& out, cudaStream_t st) {
     k_download<<<blocks_for(P.n_total, 256, 148 * 16), 256, 0, st>>>(P, out);
 }
 void launch_totals(const Params& P, double* totals, cudaStream_t st) {
-    k_totals<<<blocks_for(P.n_total, 256, 148 * 16), 256, 0, st>>>(P, totals);
+    k_totals<<<blocks_for(P.n_total, kTotThreads * kTotPerThread, 148 * 8), kTotThreads, 0, st>>>(P, totals);
 }
 void launch_stress(const Params& P, float* stress_orig, cudaStream_t st) {
     k_stress<<<blocks_for(P.n_total, 256, 148 * 16), 256, 0, st>>>(P, stress_orig);
