@@ -39,6 +39,9 @@ struct DevScene {
 
 // Grid geometry shared by every scene of an engine (one SceneConfig per batch): kernels
 // read it from the parameter bank (constant cache), never per particle from memory.
+// origin / dims are the GLOBAL grid (keys, node positions, BC, deactivation are the
+// reference's arithmetic on global indices); the node STORAGE of a slab domain (slab
+// decomposition) covers global x nodes [goff, goff + lx) in nb bricks.
 struct Geo {
     float origin[3];
     float dx;
@@ -48,6 +51,9 @@ struct Geo {
     int nb[3];
     uint64_t nodes_per_scene;
     uint32_t bricks_per_scene;
+    int goff;            // global x index of local node 0 (0 without a slab)
+    int lx;              // local storage width in x (nodes)
+    int own_lo, own_hi;  // local x range of the nodes this domain owns (contact sums)
     int pad;
 };
 

@@ -236,10 +236,12 @@ Engine::Engine(const std::vector<SceneGrid>& scenes) : impl_(new Impl), scenes_(
     uint32_t brick_base = 0;
     for (const SceneGrid& g : scenes) {
         DevScene d{};
+        const bool slab = g.slab_hi > g.slab_lo;
+        const int lx = slab ? g.slab_hi - g.slab_lo + 2 * g.margin + 2 : g.dims[0];
         for (int a = 0; a < 3; ++a) {
             d.origin[a] = g.origin[a];
             d.dims[a] = g.dims[a];
-            d.nb[a] = (g.dims[a] + kBrick - 1) / kBrick;
+            d.nb[a] = ((a == 0 ? lx : g.dims[a]) + kBrick - 1) / kBrick;
         }
         d.dx = g.dx;
         d.inv_dx = 1.0f / g.dx;                 // math.hpp:219
@@ -272,6 +274,21 @@ Engine::Engine(const std::vector<SceneGrid>& scenes) : impl_(new Impl), scenes_(
         I.geo.m_inv = d0.m_inv;
         I.geo.bricks_per_scene = static_cast<uint32_t>(d0.nb[0]) * d0.nb[1] * d0.nb[2];
         I.geo.nodes_per_scene = static_cast<uint64_t>(I.geo.bricks_per_scene) * kBrickNodes;
+        const SceneGrid& g0 = scenes[0];
+        if (g0.slab_hi > g0.slab_lo) {
+            if (scenes.size() != 1) throw std::invalid_argument("engine: a slab domain holds one scene");
+            if (g0.slab_lo < 0 || g0.slab_hi > g0.dims[0] || g0.margin < 0)
+                throw std::invalid_argument("engine: slab outside the grid");
+            I.geo.goff = g0.slab_lo - g0.margin;
+            I.geo.lx = g0.slab_hi - g0.slab_lo + 2 * g0.margin + 2;
+            I.geo.own_lo = g0.margin;
+            I.geo.own_hi = g0.margin + (g0.slab_hi - g0.slab_lo);
+        } else {
+            I.geo.goff = 0;
+            I.geo.lx = d0.dims[0];
+            I.geo.own_lo = 0;
+            I.geo.own_hi = d0.dims[0];
+        }
     }
     I.total_nodes = node_base;
     I.total_bricks = brick_base;

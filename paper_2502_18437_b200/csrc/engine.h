@@ -24,6 +24,9 @@ struct SceneGrid {
     int dims[3];
     float dx;
     float origin[3];
+    // slab domain: this engine owns global x nodes [slab_lo, slab_hi) and
+    // stores [slab_lo - margin, slab_hi + 2 + margin); slab_hi <= slab_lo: the whole grid
+    int slab_lo = 0, slab_hi = 0, margin = 0;
 };
 
 struct EngineShape {            // host copy of one shape (per scene, in order)

@@ -129,12 +129,8 @@ __global__ void __launch_bounds__(256) k_bin_keys(const Params P, BinBuffers B) 
                 const float4 a = P.pl[0][s];
                 const float x[3] = {a.x, a.y, a.z};
                 int b[3];
-#pragma unroll
-                for (int q = 0; q < 3; ++q) {
-                    float fx;
-                    b[q] = stencil_base(x[q], S.origin[q], S.inv_dx, fx);
-                    b[q] = min(max(b[q], 0), S.dims[q] - 3);
-                }
+                float fx[3];
+                local_base(P.geo, x, b, fx);
                 const uint32_t local = (static_cast<uint32_t>(b[2] >> 2) * S.nb[1] +
                                         static_cast<uint32_t>(b[1] >> 2)) * S.nb[0] +
                                        static_cast<uint32_t>(b[0] >> 2);

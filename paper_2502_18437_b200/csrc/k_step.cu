@@ -63,6 +63,8 @@ __global__ void __launch_bounds__(256) k_grid_update(const Params P) {
         const int bz = static_cast<int>(local / (static_cast<uint32_t>(S.nb[0]) * S.nb[1]));
         const int i = bx * 4 + (l & 3), j = by * 4 + ((l >> 2) & 3), k = bz * 4 + (l >> 4);
         const uint64_t idx = S.node_base + node_linear(P.geo, i, j, k);
+        const bool own = i >= P.geo.own_lo && i < P.geo.own_hi;
+        const int ig = i + P.geo.goff;  // global x index (BC, node position)
         P.grid_acc[idx] = make_float4(0.f, 0.f, 0.f, 0.f);
         if (l == 0) P.brick_stamp[gb] = P.epoch;
         const float m = a.w;
@@ -73,14 +75,16 @@ __global__ void __launch_bounds__(256) k_grid_update(const Params P) {
             if (P.gravity) v = v + mk(P.g[0], P.g[1], P.g[2]) * P.dt;
         }
         if (P.contact && P.scenes[S.scene].shape_count > 0) {  // contact.hpp:97-136, shapes in order
-            const V3 xn = mk(FA(S.origin[0], FM(static_cast<float>(i), S.dx)),  // state.hpp:49-51
+            const V3 xn = mk(FA(S.origin[0], FM(static_cast<float>(i + P.geo.goff), S.dx)),  // state.hpp:49-51
                              FA(S.origin[1], FM(static_cast<float>(j), S.dx)),
                              FA(S.origin[2], FM(static_cast<float>(k), S.dx)));
             for (int si = P.scenes[S.scene].shape_begin; si < P.scenes[S.scene].shape_begin + P.scenes[S.scene].shape_count; ++si) {
                 const DevShape& sh = P.shapes[si];
                 V3 imp = mk(0.f, 0.f, 0.f), tq = mk(0.f, 0.f, 0.f);
                 int hit = 0;
-                if (live && cull_may_touch(P, si, xn.x, xn.y, xn.z)) {
+                // a slab domain sums contact only over the nodes it owns (ghosts are the
+                // neighbour's; their velocities are overwritten by the halo exchange)
+                if (live && own && cull_may_touch(P, si, xn.x, xn.y, xn.z)) {
                     const DevPose& pose = pose_of(P, si);
                     const Sdf s = sdf_query(sh, pose, P.verts, P.ints, xn);
                     if (node_in_contact(s, sh.hw)) {
@@ -109,7 +113,7 @@ __global__ void __launch_bounds__(256) k_grid_update(const Params P) {
             }
         }
         if (live) {  // solvers.hpp:30-50 (bc < 0: deferred to k_grid_bc, hook adapter)
-            const bool bxm = i < 2 || i >= S.dims[0] - 2;
+            const bool bxm = ig < 2 || ig >= S.dims[0] - 2;
             const bool bym = j < 2 || j >= S.dims[1] - 2;
             const bool bzm = k < 2 || k >= S.dims[2] - 2;
             if (P.bc >= 0 && (bxm || bym || bzm)) {
@@ -148,7 +152,7 @@ __global__ void __launch_bounds__(256) k_grid_bc(const Params P) {
         const uint64_t idx = S.node_base + node_linear(P.geo, i, j, k);
         float4 a = P.grid_vel[idx];
         if (!(a.w > kMassEps)) continue;
-        const bool bxm = i < 2 || i >= S.dims[0] - 2;
+        const bool bxm = i + P.geo.goff < 2 || i + P.geo.goff >= S.dims[0] - 2;
         const bool bym = j < 2 || j >= S.dims[1] - 2;
         const bool bzm = k < 2 || k >= S.dims[2] - 2;
         if (!(bxm || bym || bzm)) continue;

@@ -258,12 +258,8 @@ __device__ __forceinline__ uint64_t group_sort(const Params& P, uint32_t g, uint
             const int scene = static_cast<int>((flags >> kSceneShift) & kSceneMask);
             const float xa[3] = {a.x, a.y, a.z};
             int b[3];
-#pragma unroll
-            for (int q = 0; q < 3; ++q) {
-                float fx;
-                b[q] = stencil_base(xa[q], P.geo.origin[q], P.geo.inv_dx, fx);
-                b[q] = min(max(b[q], 0), P.geo.dims[q] - 3);
-            }
+            float fx[3];
+            local_base(P.geo, xa, b, fx);
             const uint32_t brick = static_cast<uint32_t>(scene) * P.geo.bricks_per_scene +
                                    (static_cast<uint32_t>(b[2] >> 2) * P.geo.nb[1] +
                                     static_cast<uint32_t>(b[1] >> 2)) * P.geo.nb[0] +
@@ -365,11 +361,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_p2g(cons
             const SceneView S = scene_view(P, scene);
             int b[3];
             float fx[3];
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                b[a] = stencil_base(x[a], S.origin[a], S.inv_dx, fx[a]);
-                b[a] = min(max(b[a], 0), S.dims[a] - 3);  // memory guard only
-            }
+            local_base(P.geo, x, b, fx);
             const float m = r.x;
             // affine = m C - dt V (4/dx^2) sigma  (solvers.hpp:154-156; PB: m C, :222)
             float A[9];
@@ -399,7 +391,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_p2g(cons
                 bspline_w(fx[a], w[a]);
 #pragma unroll
                 for (int o = 0; o < 3; ++o)  // node_position - x (state.hpp:49-51)
-                    rel[a][o] = (S.origin[a] + static_cast<float>(b[a] + o) * S.dx) - x[a];
+                    rel[a][o] = node_coord(P.geo, a, b[a] + o) - x[a];
             }
             if (b[0] != cb[0] || b[1] != cb[1] || b[2] != cb[2] || scene != cscene) {
                 if (cscene >= 0) p2g_flush(P, scene_view(P, cscene), cb, pa, pb);
@@ -584,10 +576,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(cons
             if (NS > 3 && k + 1 < st.cnt) {  // warm L1 with the next particle's stencil rows
                 const float4 xn = st.buf[((k + 1) % NS) * NP * 32 + lane];
                 int bn[3];
-                float fn;
-                bn[0] = min(max(stencil_base(xn.x, P.geo.origin[0], P.geo.inv_dx, fn), 0), P.geo.dims[0] - 3);
-                bn[1] = min(max(stencil_base(xn.y, P.geo.origin[1], P.geo.inv_dx, fn), 0), P.geo.dims[1] - 3);
-                bn[2] = min(max(stencil_base(xn.z, P.geo.origin[2], P.geo.inv_dx, fn), 0), P.geo.dims[2] - 3);
+                float fn[3];
+                const float xq[3] = {xn.x, xn.y, xn.z};
+                local_base(P.geo, xq, bn, fn);
                 const uint32_t sn = (__float_as_uint(st.buf[((k + 1) % NS) * NP * 32 + (NP - 1) * 32 + lane].z) >>
                                      kSceneShift) & kSceneMask;
                 uint32_t base, px, pxy;
@@ -619,18 +610,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(cons
             const SceneView S = scene_view(P, scene);
             int b[3];
             float fx[3];
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                b[a] = stencil_base(p.x[a], S.origin[a], S.inv_dx, fx[a]);
-                b[a] = min(max(b[a], 0), S.dims[a] - 3);
-            }
+            local_base(P.geo, p.x, b, fx);
             float w[3][3], rel[3][3];
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
                 bspline_w(fx[a], w[a]);
 #pragma unroll
                 for (int o = 0; o < 3; ++o)
-                    rel[a][o] = (S.origin[a] + static_cast<float>(b[a] + o) * S.dx) - p.x[a];
+                    rel[a][o] = node_coord(P.geo, a, b[a] + o) - p.x[a];
             }
             float B[9];
             {

@@ -90,8 +90,8 @@ struct Params {
 struct SceneView {
     float origin[3];
     float dx, inv_dx, m_inv;
-    int dims[3];
-    int nb[3];
+    int dims[3];   // global dims (BC, deactivation)
+    int nb[3];     // storage bricks
     uint64_t node_base;
     uint32_t brick_base;
     int scene;
@@ -112,6 +112,21 @@ __device__ __forceinline__ SceneView scene_view(const Params& P, int scene) {
     s.brick_base = static_cast<uint32_t>(scene) * P.geo.bricks_per_scene;
     s.scene = scene;
     return s;
+}
+
+// Stencil base in LOCAL storage coordinates: the reference's global base (math.hpp:219-224,
+// bit-exact, global origin) shifted by the slab offset in x and clamped to the storage
+// (memory guard only); fx is the reference's fractional coordinate.
+__device__ __forceinline__ void local_base(const Geo& G, const float x[3], int b[3], float fx[3]) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) b[a] = stencil_base(x[a], G.origin[a], G.inv_dx, fx[a]);
+    b[0] = min(max(b[0] - G.goff, 0), G.lx - 3);
+    b[1] = min(max(b[1], 0), G.dims[1] - 3);
+    b[2] = min(max(b[2], 0), G.dims[2] - 3);
+}
+// world coordinate of LOCAL node index i along axis a (state.hpp:49-51 on the global index)
+__device__ __forceinline__ float node_coord(const Geo& G, int a, int i) {
+    return G.origin[a] + static_cast<float>(i + (a == 0 ? G.goff : 0)) * G.dx;
 }
 
 __device__ __forceinline__ float4 material(const Params& P, uint32_t id) {
