@@ -235,6 +235,49 @@ mpmb_status mpmb_state_get_grid(mpmb_state st, float* mass, float* momentum, flo
  * by (key, original index), inactive last.  Any pointer may be NULL. */
 mpmb_status mpmb_bin_particles(mpmb_state st, uint32_t* keys, uint32_t* perm);
 
+/* ------------------------------------------- slab domain decomposition (DD)
+ * One large scene split along x into slabs, one per rank.
+ * A slab state owns global x nodes [slab_lo, slab_hi) and stores [slab_lo - margin,
+ * slab_hi + 2 + margin).  All arithmetic uses the GLOBAL grid (keys, node positions, BC,
+ * deactivation), so a DD run equals the single-domain run up to float summation order.
+ * Per substep the caller (the transport, e.g. paper_2502_18437_b200/dd.py over NCCL) runs
+ *   mpmb_dd_p2g -> pack_acc -> [exchange] -> unpack_acc -> mpmb_dd_grid -> pack_vel ->
+ *   [exchange] -> unpack_vel -> mpmb_dd_g2p
+ * and every `margin` substeps (CFL: <= 1 cell per substep) mpmb_dd_migrate_pack ->
+ * [exchange] -> mpmb_dd_migrate_unpack.  Exchange rule (both phases): send_lo goes to the
+ * lower neighbour's recv_hi, send_hi to the upper neighbour's recv_lo; a missing
+ * neighbour's recv buffer stays zero.  Free bodies are not supported in DD. */
+mpmb_status mpmb_state_create_slab(const int32_t dims[3], float dx, const float origin[3], int32_t slab_lo,
+                                   int32_t slab_hi, int32_t margin, int64_t capacity, mpmb_state* out);
+/* Particles with explicit original indices (global ids that travel with migration). */
+mpmb_status mpmb_state_set_particles_ids(mpmb_state st, int32_t n, const float* x, const float* v,
+                                         const float* mass, const float* volume0, const float* F,
+                                         const float* C, const int32_t* material_id, const uint8_t* active,
+                                         const uint32_t* ids);
+/* Stream the state's kernels run on (NULL = the library's own). */
+mpmb_status mpmb_state_set_stream(mpmb_state st, void* cuda_stream);
+mpmb_status mpmb_state_synchronize(mpmb_state st);
+/* Halo buffers (device, `bytes` each) and their layout: plane_bytes per x-plane; in the
+ * grid-sum phase send_lo carries `margin` planes and send_hi `2 + margin`, in the
+ * velocity phase the reverse. */
+mpmb_status mpmb_dd_halo_buffers(mpmb_state st, void** send_lo, void** send_hi, void** recv_lo, void** recv_hi,
+                                 int64_t* bytes, int64_t* plane_bytes, int32_t* margin);
+mpmb_status mpmb_dd_p2g(mpmb_state st, float dt);  /* bins if needed; MLS P2G */
+mpmb_status mpmb_dd_pack_acc(mpmb_state st);
+mpmb_status mpmb_dd_unpack_acc(mpmb_state st);
+mpmb_status mpmb_dd_grid(mpmb_state st, float dt, const float gravity[3], int32_t contact, int32_t boundary);
+mpmb_status mpmb_dd_pack_vel(mpmb_state st);
+mpmb_status mpmb_dd_unpack_vel(mpmb_state st);
+mpmb_status mpmb_dd_g2p(mpmb_state st, float dt, int32_t pushout, int32_t deactivate);
+/* Migration: synchronous counts; buffers hold `capacity` particles of 112 bytes. */
+mpmb_status mpmb_dd_migrate_pack(mpmb_state st, int64_t* n_to_lo, int64_t* n_to_hi);
+mpmb_status mpmb_dd_migrate_buffers(mpmb_state st, void** send_lo, void** send_hi, void** recv_lo, void** recv_hi,
+                                    int64_t* capacity);
+mpmb_status mpmb_dd_migrate_unpack(mpmb_state st, int64_t n_from_lo, int64_t n_from_hi);
+/* The slab's particles (any order): ids, x, v, active; n = how many (<= capacity). */
+mpmb_status mpmb_dd_download(mpmb_state st, int64_t capacity, uint32_t* ids, float* x, float* v, uint8_t* active,
+                             int64_t* n);
+
 /* --------------------------------------------------------- facade layer */
 typedef uint64_t mpmb_handle;
 #define MPMB_INVALID_HANDLE ((mpmb_handle)0)

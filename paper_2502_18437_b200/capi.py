@@ -89,6 +89,8 @@ ip = C.POINTER(C.c_int32)
 u8p = C.POINTER(C.c_uint8)
 u32p = C.POINTER(C.c_uint32)
 u64 = C.c_uint64
+VPP = C.POINTER(C.c_void_p)
+I64P = C.POINTER(C.c_int64)
 
 # name (without prefix) -> (restype, argtypes); shared by product / reference / oracle
 STATE_API = {
@@ -140,6 +142,24 @@ PRODUCT_API.update({
     "set_profiling": (C.c_int, [u64, C.c_int32]),
     "get_profile": (C.c_int, [u64, C.POINTER(Profile)]),
     "synchronize": (C.c_int, [u64]),
+    # slab domain decomposition (include/mpm_b200.h)
+    "state_create_slab": (C.c_int, [ip, C.c_float, fp, C.c_int32, C.c_int32, C.c_int32, C.c_int64,
+                                    C.POINTER(C.c_void_p)]),
+    "state_set_particles_ids": (C.c_int, [P, C.c_int32, fp, fp, fp, fp, fp, fp, ip, u8p, u32p]),
+    "state_set_stream": (C.c_int, [P, C.c_void_p]),
+    "state_synchronize": (C.c_int, [P]),
+    "dd_halo_buffers": (C.c_int, [P, VPP, VPP, VPP, VPP, I64P, I64P, ip]),
+    "dd_p2g": (C.c_int, [P, C.c_float]),
+    "dd_pack_acc": (C.c_int, [P]),
+    "dd_unpack_acc": (C.c_int, [P]),
+    "dd_grid": (C.c_int, [P, C.c_float, fp, C.c_int32, C.c_int32]),
+    "dd_pack_vel": (C.c_int, [P]),
+    "dd_unpack_vel": (C.c_int, [P]),
+    "dd_g2p": (C.c_int, [P, C.c_float, C.c_int32, C.c_int32]),
+    "dd_migrate_pack": (C.c_int, [P, I64P, I64P]),
+    "dd_migrate_buffers": (C.c_int, [P, VPP, VPP, VPP, VPP, I64P]),
+    "dd_migrate_unpack": (C.c_int, [P, C.c_int64, C.c_int64]),
+    "dd_download": (C.c_int, [P, C.c_int64, u32p, fp, fp, u8p, I64P]),
 })
 
 

@@ -232,6 +232,157 @@ extern "C" mpmb_status mpmb_state_set_particles(mpmb_state st, int32_t n, const 
     });
 }
 
+// ------------------------------------------------ slab domain decomposition
+extern "C" mpmb_status mpmb_state_create_slab(const int32_t dims[3], float dx, const float origin[3],
+                                              int32_t slab_lo, int32_t slab_hi, int32_t margin, int64_t capacity,
+                                              mpmb_state* out) {
+    return guarded([&] {
+        if (!dims || !origin || !out) fail(MPMB_INVALID_ARGUMENT, "null argument");
+        if (dims[0] < 4 || dims[1] < 4 || dims[2] < 4) fail(MPMB_INVALID_ARGUMENT, "grid: dims must be >= 4 per axis");
+        if (!(dx > 0)) fail(MPMB_INVALID_ARGUMENT, "grid: dx must be positive");
+        if (slab_lo < 0 || slab_hi > dims[0] || slab_hi - slab_lo < 2 + margin || margin < 1)
+            fail(MPMB_INVALID_ARGUMENT, "slab: need 0 <= lo, hi <= nx, hi - lo >= 2 + margin, margin >= 1");
+        if (capacity < 0) fail(MPMB_INVALID_ARGUMENT, "slab: negative capacity");
+        require_device();
+        auto st = std::make_unique<mpmb_state_s>();
+        for (int a = 0; a < 3; ++a) {
+            st->grid.dims[a] = dims[a];
+            st->grid.origin[a] = origin[a];
+        }
+        st->grid.dx = dx;
+        st->grid.slab_lo = slab_lo;
+        st->grid.slab_hi = slab_hi;
+        st->grid.margin = margin;
+        st->eng = std::make_unique<Engine>(std::vector<SceneGrid>{st->grid});
+        st->eng->set_capacity(capacity);
+        *out = st.release();
+        return MPMB_OK;
+    });
+}
+
+extern "C" mpmb_status mpmb_state_set_particles_ids(mpmb_state st, int32_t n, const float* x, const float* v,
+                                                    const float* mass, const float* vol0, const float* F,
+                                                    const float* C, const int32_t* mat, const uint8_t* active,
+                                                    const uint32_t* ids) {
+    return guarded([&] {
+        if (n < 0) fail(MPMB_INVALID_ARGUMENT, "negative particle count");
+        if (n > 0 && (!x || !v || !mass || !vol0 || !F || !C || !mat || !active || !ids))
+            fail(MPMB_INVALID_ARGUMENT, "null particle array");
+        std::vector<int32_t> scene(static_cast<size_t>(n), 0);
+        S(st)->eng->upload_particles(n, x, v, mass, vol0, F, C, nullptr, mat, active, scene.data(), ids);
+        st->n = n;
+        return MPMB_OK;
+    });
+}
+
+extern "C" mpmb_status mpmb_state_set_stream(mpmb_state st, void* stream) {
+    return guarded([&] {
+        S(st)->eng->set_stream(stream);
+        return MPMB_OK;
+    });
+}
+
+extern "C" mpmb_status mpmb_state_synchronize(mpmb_state st) {
+    return guarded([&] {
+        S(st)->eng->synchronize();
+        return MPMB_OK;
+    });
+}
+
+extern "C" mpmb_status mpmb_dd_halo_buffers(mpmb_state st, void** send_lo, void** send_hi, void** recv_lo,
+                                            void** recv_hi, int64_t* bytes, int64_t* plane_bytes,
+                                            int32_t* margin) {
+    return guarded([&] {
+        Engine& e = *S(st)->eng;
+        e.dd_halo_buffers(send_lo, send_hi, recv_lo, recv_hi, bytes);
+        if (margin) *margin = st->grid.margin;
+        if (plane_bytes) *plane_bytes = *bytes / (2 + st->grid.margin);
+        return MPMB_OK;
+    });
+}
+
+extern "C" mpmb_status mpmb_dd_p2g(mpmb_state st, float dt) {
+    return guarded([&] {
+        S(st)->eng->p2g(true, dt, false);
+        return MPMB_OK;
+    });
+}
+extern "C" mpmb_status mpmb_dd_pack_acc(mpmb_state st) {
+    return guarded([&] { S(st)->eng->dd_pack_acc(); return MPMB_OK; });
+}
+extern "C" mpmb_status mpmb_dd_unpack_acc(mpmb_state st) {
+    return guarded([&] { S(st)->eng->dd_unpack_acc(); return MPMB_OK; });
+}
+extern "C" mpmb_status mpmb_dd_grid(mpmb_state st, float dt, const float g[3], int32_t contact, int32_t bc) {
+    return guarded([&] {
+        Engine& e = *S(st)->eng;
+        e.collect_bricks();
+        e.grid_update(0, dt, g, true, contact != 0, bc);
+        return MPMB_OK;
+    });
+}
+extern "C" mpmb_status mpmb_dd_pack_vel(mpmb_state st) {
+    return guarded([&] { S(st)->eng->dd_pack_vel(); return MPMB_OK; });
+}
+extern "C" mpmb_status mpmb_dd_unpack_vel(mpmb_state st) {
+    return guarded([&] { S(st)->eng->dd_unpack_vel(); return MPMB_OK; });
+}
+extern "C" mpmb_status mpmb_dd_g2p(mpmb_state st, float dt, int32_t pushout, int32_t deactivate) {
+    return guarded([&] {
+        S(st)->eng->g2p_mls(0, dt, pushout != 0, deactivate != 0);
+        return MPMB_OK;
+    });
+}
+extern "C" mpmb_status mpmb_dd_migrate_pack(mpmb_state st, int64_t* n_lo, int64_t* n_hi) {
+    return guarded([&] {
+        if (!n_lo || !n_hi) fail(MPMB_INVALID_ARGUMENT, "null argument");
+        S(st)->eng->dd_migrate_pack(n_lo, n_hi);
+        return MPMB_OK;
+    });
+}
+extern "C" mpmb_status mpmb_dd_migrate_buffers(mpmb_state st, void** send_lo, void** send_hi, void** recv_lo,
+                                               void** recv_hi, int64_t* cap) {
+    return guarded([&] {
+        S(st)->eng->dd_migrate_buffers(send_lo, send_hi, recv_lo, recv_hi, cap);
+        return MPMB_OK;
+    });
+}
+extern "C" mpmb_status mpmb_dd_migrate_unpack(mpmb_state st, int64_t n_from_lo, int64_t n_from_hi) {
+    return guarded([&] {
+        if (n_from_lo < 0 || n_from_hi < 0) fail(MPMB_INVALID_ARGUMENT, "negative count");
+        Engine& e = *S(st)->eng;
+        e.dd_migrate_unpack(n_from_lo, n_from_hi);
+        st->n = e.n_particles();
+        return MPMB_OK;
+    });
+}
+extern "C" mpmb_status mpmb_dd_download(mpmb_state st, int64_t capacity, uint32_t* ids, float* x, float* v,
+                                        uint8_t* active, int64_t* n) {
+    return guarded([&] {
+        if (!ids || !x || !v || !active || !n) fail(MPMB_INVALID_ARGUMENT, "null argument");
+        Engine& e = *S(st)->eng;
+        const int64_t slots = e.slot_count();
+        std::vector<uint32_t> si(static_cast<size_t>(slots));
+        std::vector<float> sx(3 * static_cast<size_t>(slots)), sv(3 * static_cast<size_t>(slots));
+        std::vector<uint8_t> sa(static_cast<size_t>(slots));
+        if (slots > 0) e.download_slots(si.data(), sx.data(), sv.data(), sa.data());
+        int64_t k = 0;
+        for (int64_t s = 0; s < slots; ++s) {
+            if (si[s] == 0xFFFFFFFFu) continue;
+            if (k >= capacity) fail(MPMB_BUFFER_TOO_SMALL, "dd_download: capacity too small");
+            ids[k] = si[s];
+            for (int a = 0; a < 3; ++a) {
+                x[3 * k + a] = sx[3 * s + a];
+                v[3 * k + a] = sv[3 * s + a];
+            }
+            active[k] = sa[s];
+            ++k;
+        }
+        *n = k;
+        return MPMB_OK;
+    });
+}
+
 extern "C" mpmb_status mpmb_state_get_particles(mpmb_state st, int32_t n, float* x, float* v,
                                                 float* mass, float* vol0, float* F, float* C,
                                                 float* stress, int32_t* mat, uint8_t* active) {

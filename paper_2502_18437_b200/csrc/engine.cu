@@ -110,7 +110,16 @@ struct Engine::Impl {
     DevBuf grid_acc, grid_vel, brick_flag, brick_stamp, active_bricks, brick_scene, misc;
     // misc u32 slots: [0] n_active_bricks
     int64_t n = 0;      // particles
-    int64_t n_cap = 0;  // slots of each plane buffer: n + kGroup (group padding, holes)
+    int64_t n_cap = 0;  // slots of each plane buffer: max(n, cap_hint) + kGroup (padding, holes)
+    int64_t cap_hint = 0;
+    // slab domain decomposition
+    int slab_lo = 0, slab_hi = 0, margin = 0;
+    DevBuf halo[4];      // send_lo, send_hi, recv_lo, recv_hi
+    int64_t halo_bytes = 0;
+    DevBuf mig[4];       // particles: send_lo, send_hi, recv_lo, recv_hi
+    int64_t mig_cap = 0;
+    DevBuf mig_counts;
+    int64_t mig_sent = 0;
     DevBuf planes[2][kPlanes];
     int cur = 0;
     bool binned = false;
@@ -283,6 +292,9 @@ Engine::Engine(const std::vector<SceneGrid>& scenes) : impl_(new Impl), scenes_(
             I.geo.lx = g0.slab_hi - g0.slab_lo + 2 * g0.margin + 2;
             I.geo.own_lo = g0.margin;
             I.geo.own_hi = g0.margin + (g0.slab_hi - g0.slab_lo);
+            I.slab_lo = g0.slab_lo;
+            I.slab_hi = g0.slab_hi;
+            I.margin = g0.margin;
         } else {
             I.geo.goff = 0;
             I.geo.lx = d0.dims[0];
@@ -367,12 +379,13 @@ void Engine::set_materials(const std::vector<mpmb_material>& m) {
 
 void Engine::upload_particles(int64_t n, const float* x, const float* v, const float* mass,
                               const float* vol0, const float* F, const float* C, const float* stress,
-                              const int32_t* material, const uint8_t* active, const int32_t* scene) {
+                              const int32_t* material, const uint8_t* active, const int32_t* scene,
+                              const uint32_t* ids) {
     Impl& I = *impl_;
     if (n >= 0x7FFFFFFF) throw std::invalid_argument("engine: particle count exceeds 2^31");
     check(cudaStreamSynchronize(I.st), "sync");
     I.n = n;
-    I.n_cap = n > 0 ? n + kGroup : 0;
+    I.n_cap = (n > 0 || I.cap_hint > 0) ? std::max<int64_t>(n, I.cap_hint) + kGroup : 0;
     n_total_ = n;
     for (int b = 0; b < 2; ++b)
         for (int q = 0; q < kPlanes; ++q) I.planes[b][q].alloc(sizeof(float4) * std::max<int64_t>(I.n_cap, 1));
@@ -400,7 +413,7 @@ void Engine::upload_particles(int64_t n, const float* x, const float* v, const f
     B.sorted_orig = I.s_orig.as<uint32_t>();
     B.counts = I.b_counts.as<uint32_t>(); B.scan_tmp = I.scan_tmp.as<uint32_t>();
     B.key_by_orig = nullptr;
-    if (n == 0) {
+    if (I.n_cap == 0) {
         I.binned = false;
         return;
     }
@@ -417,8 +430,14 @@ void Engine::upload_particles(int64_t n, const float* x, const float* v, const f
     check(cudaMemcpyAsync(dmat.p, material, 4 * n, cudaMemcpyHostToDevice, I.st), "h2d");
     check(cudaMemcpyAsync(dact.p, active, n, cudaMemcpyHostToDevice, I.st), "h2d");
     check(cudaMemcpyAsync(dsc.p, scene, 4 * n, cudaMemcpyHostToDevice, I.st), "h2d");
+    DevBuf dids;
+    if (ids) {
+        dids.alloc(4 * N);
+        check(cudaMemcpyAsync(dids.p, ids, 4 * n, cudaMemcpyHostToDevice, I.st), "h2d");
+    }
     IoArrays io{dx.as<float>(), dv.as<float>(), dm.as<float>(), dvol.as<float>(), dF.as<float>(),
-                dC.as<float>(), dmat.as<int32_t>(), dact.as<uint8_t>(), dsc.as<int32_t>()};
+                dC.as<float>(), dmat.as<int32_t>(), dact.as<uint8_t>(), dsc.as<int32_t>(),
+                ids ? dids.as<uint32_t>() : nullptr};
     Params P = I.params();
     launch_upload(P, io, n, I.st);
     I.counted(1);
@@ -571,7 +590,7 @@ std::vector<DevPose> Engine::read_free_poses() {
 // --------------------------------------------------------------- hot path
 void Engine::bin() {
     Impl& I = *impl_;
-    if (I.n == 0) return;
+    if (I.n_cap == 0) return;
     auto ev = I.begin();
     Params P = I.params();
     float4* np[kPlanes];
@@ -584,24 +603,27 @@ void Engine::bin() {
     I.end(CAT_SORT, ev);
 }
 
-void Engine::p2g(bool mls, float dt) {
+void Engine::p2g(bool mls, float dt, bool collect) {
     Impl& I = *impl_;
-    if (I.n == 0) return;
+    if (I.n_cap == 0) return;
     if (!I.binned) bin();
     auto ev = I.begin();
     cudaMemsetAsync(I.misc.p, 0, sizeof(uint32_t), I.st);  // active brick count
     Params P = I.params();
     P.dt = dt;
     launch_p2g(P, mls, (I.n + kGroup - 1) / kGroup, I.st);
-    launch_collect_bricks(P, I.total_bricks, I.st);
-    I.counted(2);
+    I.counted(1);
+    if (collect) {
+        launch_collect_bricks(P, I.total_bricks, I.st);
+        I.counted(1);
+    }
     if (mls) I.use_stress_in = false;  // consumed by the first MLS P2G
     I.end(CAT_P2G, ev);
 }
 
 void Engine::grid_update(int sub, float dt, const float g[3], bool gravity, bool contact, int bc) {
     Impl& I = *impl_;
-    if (I.n == 0) return;
+    if (I.n_cap == 0) return;
     auto ev = I.begin();
     ++I.epoch;
     if (I.epoch == 0xFFFFFFFFu) I.epoch = 1;
@@ -623,7 +645,7 @@ void Engine::grid_update(int sub, float dt, const float g[3], bool gravity, bool
 
 void Engine::g2p_mls(int sub, float dt, bool pushout, bool deactivate) {
     Impl& I = *impl_;
-    if (I.n == 0) return;
+    if (I.n_cap == 0) return;
     auto ev = I.begin();
     Params P = I.params();
     P.sub = std::min(sub, I.table_subs - 1);
@@ -639,7 +661,7 @@ void Engine::g2p_mls(int sub, float dt, bool pushout, bool deactivate) {
 
 void Engine::g2p_pb(int sub, float dt, bool commit, bool pushout, bool deactivate) {
     Impl& I = *impl_;
-    if (I.n == 0) return;
+    if (I.n_cap == 0) return;
     auto ev = I.begin();
     Params P = I.params();
     P.sub = std::min(sub, I.table_subs - 1);
@@ -840,5 +862,154 @@ int64_t Engine::n_active_sorted() {
 }
 
 void Engine::synchronize() { check(cudaStreamSynchronize(impl_->st), "synchronize"); }
+
+// ------------------------------------------------ slab domain decomposition (k_dd.cu)
+void Engine::set_capacity(int64_t particles) { impl_->cap_hint = std::max<int64_t>(0, particles); }
+
+int64_t Engine::slot_count() const { return impl_->n_cap; }
+
+int Engine::dd_halo_planes(int side_send_hi, bool acc) const {
+    // acc: low ghosts M planes, high ghosts 2 + M; vel: the mirror image
+    const int M = impl_->margin;
+    return (side_send_hi != 0) == acc ? 2 + M : M;
+}
+
+void Engine::ensure_halo() {
+    Impl& I = *impl_;
+    if (I.slab_hi <= I.slab_lo) throw std::invalid_argument("engine: not a slab domain");
+    Params P = I.params();
+    const int64_t b = dd_plane_nodes(P) * (2 + I.margin) * static_cast<int64_t>(sizeof(float4));
+    if (I.halo_bytes != b) {
+        for (int q = 0; q < 4; ++q) {
+            I.halo[q].alloc(b);
+            check(cudaMemset(I.halo[q].p, 0, b), "memset");  // a missing neighbour sends zeros
+        }
+        I.halo_bytes = b;
+    }
+}
+
+void Engine::dd_halo_buffers(void** send_lo, void** send_hi, void** recv_lo, void** recv_hi, int64_t* bytes) {
+    Impl& I = *impl_;
+    ensure_halo();
+    const int64_t b = I.halo_bytes;
+    *send_lo = I.halo[0].p; *send_hi = I.halo[1].p; *recv_lo = I.halo[2].p; *recv_hi = I.halo[3].p;
+    *bytes = b;
+}
+
+void Engine::dd_pack_acc() {
+    Impl& I = *impl_;
+    ensure_halo();
+    Params P = I.params();
+    launch_halo(P, 0, P.grid_acc, I.halo[0].as<float4>(), 0, I.margin, I.st);
+    launch_halo(P, 0, P.grid_acc, I.halo[1].as<float4>(), P.geo.own_hi, 2 + I.margin, I.st);
+    I.counted(2);
+}
+
+void Engine::dd_unpack_acc() {
+    Impl& I = *impl_;
+    ensure_halo();
+    Params P = I.params();
+    launch_halo(P, 1, P.grid_acc, I.halo[3].as<float4>(), P.geo.own_hi - I.margin, I.margin, I.st);
+    launch_halo(P, 1, P.grid_acc, I.halo[2].as<float4>(), P.geo.own_lo, 2 + I.margin, I.st);
+    I.counted(2);
+}
+
+void Engine::dd_pack_vel() {
+    Impl& I = *impl_;
+    ensure_halo();
+    Params P = I.params();
+    launch_halo(P, 0, P.grid_vel, I.halo[0].as<float4>(), P.geo.own_lo, 2 + I.margin, I.st);
+    launch_halo(P, 0, P.grid_vel, I.halo[1].as<float4>(), P.geo.own_hi - I.margin, I.margin, I.st);
+    I.counted(2);
+}
+
+void Engine::dd_unpack_vel() {
+    Impl& I = *impl_;
+    ensure_halo();
+    Params P = I.params();
+    launch_halo(P, 2, P.grid_vel, I.halo[2].as<float4>(), 0, I.margin, I.st);
+    launch_halo(P, 2, P.grid_vel, I.halo[3].as<float4>(), P.geo.own_hi, 2 + I.margin, I.st);
+    I.counted(2);
+}
+
+void Engine::collect_bricks() {
+    Impl& I = *impl_;
+    if (I.n_cap == 0) return;
+    Params P = I.params();
+    launch_collect_bricks(P, I.total_bricks, I.st);
+    I.counted(1);
+}
+
+void Engine::dd_migrate_buffers(void** send_lo, void** send_hi, void** recv_lo, void** recv_hi, int64_t* cap) {
+    Impl& I = *impl_;
+    const int64_t c = std::max<int64_t>(1024, I.n_cap / 4);
+    if (I.mig_cap != c) {
+        for (int q = 0; q < 4; ++q) I.mig[q].alloc(static_cast<size_t>(c) * kPlanes * sizeof(float4));
+        I.mig_counts.alloc(2 * sizeof(uint32_t));
+        I.mig_cap = c;
+    }
+    *send_lo = I.mig[0].p; *send_hi = I.mig[1].p; *recv_lo = I.mig[2].p; *recv_hi = I.mig[3].p;
+    *cap = c;
+}
+
+void Engine::dd_migrate_pack(int64_t* n_lo, int64_t* n_hi) {
+    Impl& I = *impl_;
+    void* d[4];
+    int64_t cap;
+    dd_migrate_buffers(&d[0], &d[1], &d[2], &d[3], &cap);
+    uint32_t c[2] = {0, 0};
+    if (I.n_cap > 0) {
+        check(cudaMemsetAsync(I.mig_counts.p, 0, 2 * sizeof(uint32_t), I.st), "memset");
+        Params P = I.params();
+        launch_migrate_pack(P, I.slab_lo, I.slab_hi, I.mig[0].as<float4>(), I.mig[1].as<float4>(),
+                            static_cast<uint32_t>(cap), I.mig_counts.as<uint32_t>(), I.st);
+        I.counted(1);
+        check(cudaMemcpyAsync(c, I.mig_counts.p, sizeof(c), cudaMemcpyDeviceToHost, I.st), "d2h");
+        check(cudaStreamSynchronize(I.st), "migrate");
+    }
+    if (c[0] > cap || c[1] > cap) throw std::runtime_error("engine: migration buffer overflow");
+    *n_lo = c[0];
+    *n_hi = c[1];
+    I.mig_sent = c[0] + c[1];
+}
+
+void Engine::dd_migrate_unpack(int64_t n_from_lo, int64_t n_from_hi) {
+    Impl& I = *impl_;
+    if (n_from_lo > I.mig_cap || n_from_hi > I.mig_cap) throw std::invalid_argument("engine: migration count");
+    int64_t first = I.n;  // upload layout: particles then holes
+    if (I.binned) {       // binned layout: groups, then the inactive tail, then holes
+        uint32_t c[4] = {0, 0, 0, 0};
+        check(cudaMemcpyAsync(c, I.b_counts.p, sizeof(c), cudaMemcpyDeviceToHost, I.st), "d2h");
+        check(cudaStreamSynchronize(I.st), "migrate");
+        first = static_cast<int64_t>(c[3]) + (I.n - static_cast<int64_t>(c[2]));
+    }
+    if (first + n_from_lo + n_from_hi > I.n_cap) throw std::runtime_error("engine: slab capacity exceeded (set_capacity)");
+    Params P = I.params();
+    launch_migrate_unpack(P, I.mig[2].as<float4>(), static_cast<uint32_t>(n_from_lo), static_cast<uint32_t>(first), I.st);
+    launch_migrate_unpack(P, I.mig[3].as<float4>(), static_cast<uint32_t>(n_from_hi),
+                          static_cast<uint32_t>(first + n_from_lo), I.st);
+    I.counted(2);
+    I.n += n_from_lo + n_from_hi - I.mig_sent;
+    n_total_ = I.n;
+    I.mig_sent = 0;
+    I.binned = false;
+    bin();
+}
+
+void Engine::download_slots(uint32_t* ids, float* x, float* v, uint8_t* active) {
+    Impl& I = *impl_;
+    if (I.n_cap == 0) return;
+    const size_t N = static_cast<size_t>(I.n_cap);
+    DevBuf di, dx, dv, da;
+    di.alloc(4 * N); dx.alloc(12 * N); dv.alloc(12 * N); da.alloc(N);
+    Params P = I.params();
+    launch_download_slots(P, di.as<uint32_t>(), dx.as<float>(), dv.as<float>(), da.as<uint8_t>(), I.st);
+    I.counted(1);
+    check(cudaMemcpyAsync(ids, di.p, 4 * N, cudaMemcpyDeviceToHost, I.st), "d2h");
+    check(cudaMemcpyAsync(x, dx.p, 12 * N, cudaMemcpyDeviceToHost, I.st), "d2h");
+    check(cudaMemcpyAsync(v, dv.p, 12 * N, cudaMemcpyDeviceToHost, I.st), "d2h");
+    check(cudaMemcpyAsync(active, da.p, N, cudaMemcpyDeviceToHost, I.st), "d2h");
+    check(cudaStreamSynchronize(I.st), "download_slots");
+}
 
 }  // namespace mpmb

@@ -71,7 +71,8 @@ class Engine {
     // Particles in ORIGINAL order (scene ranges concatenated); stress may be null.
     void upload_particles(int64_t n, const float* x, const float* v, const float* mass,
                           const float* vol0, const float* F, const float* C, const float* stress,
-                          const int32_t* material, const uint8_t* active, const int32_t* scene);
+                          const int32_t* material, const uint8_t* active, const int32_t* scene,
+                          const uint32_t* ids = nullptr);
     // Synchronous download in original order (null pointers skipped).
     void download_particles(int64_t begin, int64_t count, float* x, float* v, float* mass,
                             float* vol0, float* F, float* C, float* stress, int32_t* material,
@@ -89,7 +90,8 @@ class Engine {
 
     // ---- hot path (enqueue only) ----
     void bin();                                   // K1: keys, stable sort, gather
-    void p2g(bool mls, float dt);                 // K2 / K5
+    void p2g(bool mls, float dt, bool collect = true);  // K2 / K5 (+ active-brick list)
+    void collect_bricks();
     void grid_update(int sub, float dt, const float g[3], bool gravity, bool contact, int bc);
     void g2p_mls(int sub, float dt, bool pushout, bool deactivate);   // K4
     void g2p_pb(int sub, float dt, bool commit, bool pushout, bool deactivate);  // K6
@@ -121,6 +123,26 @@ class Engine {
                               const float* velocity);
     // keys/perm of the binning stage (original indices), see mpmb_bin_particles
     void read_binning(uint32_t* keys, uint32_t* perm);
+
+    // ---- slab domain decomposition (k_dd.cu) ----
+    // Slots for particles that may arrive by migration; call before upload_particles.
+    void set_capacity(int64_t particles);
+    // Device halo buffers (each `bytes`): send/recv towards the lower / upper neighbour.
+    void dd_halo_buffers(void** send_lo, void** send_hi, void** recv_lo, void** recv_hi, int64_t* bytes);
+    void dd_pack_acc();     // after P2G: ghost sums -> send_lo (M planes), send_hi (2+M planes)
+    void dd_unpack_acc();   // add recv_hi (M planes) / recv_lo (2+M planes) into owned planes
+    void dd_pack_vel();     // after the grid update: owned boundary velocities -> send_lo / send_hi
+    void dd_unpack_vel();   // recv_lo -> low ghosts (M planes), recv_hi -> high ghosts (2+M)
+    int dd_halo_planes(int side_send_hi, bool acc) const;
+    void ensure_halo();
+    // Migration (synchronous): particles whose base left the slab are packed for the
+    // neighbours; returns their counts.  Buffers hold `cap` particles of 7 float4 each.
+    void dd_migrate_pack(int64_t* n_lo, int64_t* n_hi);
+    void dd_migrate_buffers(void** send_lo, void** send_hi, void** recv_lo, void** recv_hi, int64_t* cap);
+    void dd_migrate_unpack(int64_t n_from_lo, int64_t n_from_hi);  // appends, then bins
+    // Per slot: original index (0xFFFFFFFF = hole), x, v, active; n = slot count.
+    int64_t slot_count() const;
+    void download_slots(uint32_t* ids, float* x, float* v, uint8_t* active);
     int64_t n_active_sorted();
 
     void synchronize();

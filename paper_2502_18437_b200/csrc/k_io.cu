@@ -40,7 +40,7 @@ __global__ void k_upload(const Params P, IoArrays in, int64_t n) {
                          ((static_cast<uint32_t>(in.scene[i]) & kSceneMask) << kSceneShift);
         if (in.active[i]) flags |= kActiveBit;
         P.pl[PR][i] = make_float4(in.mass[i], in.vol0[i], __uint_as_float(flags),
-                                  __uint_as_float(static_cast<uint32_t>(i)));
+                                  __uint_as_float(in.ids ? in.ids[i] : static_cast<uint32_t>(i)));
     }
 }
 

@@ -47,10 +47,19 @@ void launch_deactivate(const Params& P, cudaStream_t st);
 void launch_free_bodies(const Params& P, bool integrate, bool merge, cudaStream_t st);
 void launch_grid_bc(const Params& P, int64_t max_bricks, cudaStream_t st);
 
+// ---- slab domain decomposition (k_dd.cu) ----
+int64_t dd_plane_nodes(const Params& P);
+void launch_halo(const Params& P, int mode, float4* pool, float4* buf, int x0, int w, cudaStream_t st);
+void launch_migrate_pack(const Params& P, int lo, int hi, float4* out_lo, float4* out_hi, uint32_t cap,
+                         uint32_t* counts, cudaStream_t st);
+void launch_migrate_unpack(const Params& P, const float4* in, uint32_t n, uint32_t first, cudaStream_t st);
+void launch_download_slots(const Params& P, uint32_t* ids, float* x, float* v, uint8_t* active, cudaStream_t st);
+
 // ---- I/O (k_io.cu) ----
 struct IoArrays {  // original-order device staging arrays (any may be null)
     float* x; float* v; float* mass; float* vol0; float* F; float* C; int32_t* mat;
     uint8_t* active; int32_t* scene;
+    uint32_t* ids;  // upload: original index per particle (null: the upload order)
 };
 void launch_upload(const Params& P, const IoArrays& in, int64_t n, cudaStream_t st);
 void launch_download(const Params& P, const IoArrays& out, cudaStream_t st);

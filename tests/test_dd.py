@@ -1,0 +1,127 @@
+"""Slab domain decomposition.
+
+GPU: K slabs in one process (LocalTransport: the exchange rule with device copies) vs the
+single-domain state on identical particles -- horizon tolerance max|dx| <= 1e-3 * dx,
+every particle present exactly once, migration exercised by a sideways velocity.
+CPU (gloo, world size 2): the neighbour exchange rule of DistTransport and the slab cuts.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from paper_2502_18437_b200 import api, capi, dd, scenes
+
+F32 = np.float32
+DIMS, DX = (64, 32, 40), 0.02
+GRAV = (0.0, -9.81, 0.0)
+
+
+def _slab_particles():
+    o = __import__("backends").oracle()
+    n_cap = 80000
+    x, m, vol = np.zeros((n_cap, 3), F32), np.zeros(n_cap, F32), np.zeros(n_cap, F32)
+    n = o.mpmor_spawn_box((capi.i3)(*DIMS), DX, api._fp(np.zeros(3, F32)), api._fp(np.array([0.2, 0.12, 0.2], F32)),
+                          api._fp(np.array([1.0, 0.3, 0.6], F32)), 8, 1000.0, 3, n_cap, api._fp(x), api._fp(m),
+                          api._fp(vol))
+    p = api.empty_particles(n)
+    p["x"], p["mass"], p["volume0"] = x[:n].copy(), m[:n].copy(), vol[:n].copy()
+    rng = np.random.default_rng(9)
+    p["v"][:] = (1.5, 0.0, 0.2)  # drift across the cut planes: migration happens
+    p["v"] += rng.normal(0, 0.05, p["v"].shape).astype(F32)
+    return p
+
+
+MATS = [(capi.MAT_NEO_HOOKEAN, *scenes.lame(2e4, 0.3), 0.9)]
+
+
+def _floor():
+    return api.ShapeSpec("plane", position=(0.64, 0.1, 0.4), mu_k=0.4, c_d=0.9, collision_halfwidth=0.03)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k", [2, 3])
+def test_slabs_match_single_domain(k):
+    p = _slab_particles()
+    n, sub, dt = len(p["x"]), 24, 1e-3
+    ref = api.SolverState(DIMS, DX, (0.0, 0.0, 0.0))
+    ref.set_materials(MATS)
+    ref.set_particles(p, with_stress=False)
+    ref.set_shapes([_floor()])
+    for _ in range(sub):
+        ref.step_mls(dt, GRAV, contact=True)
+    want = ref.get_particles()
+
+    bx = dd.base_x(p["x"][:, 0], 0.0, DX)
+    bounds = dd.slab_bounds(DIMS[0], k, np.bincount(np.clip(bx, 0, DIMS[0] - 1), minlength=DIMS[0]))
+    own = dd.owner_of(bx, bounds)
+    doms = []
+    for r, (lo, hi) in enumerate(bounds):
+        d = dd.SlabDomain(DIMS, DX, (0.0, 0.0, 0.0), lo, hi, margin=2, capacity=n)
+        d.set_materials(MATS)
+        d.set_shapes([_floor()])
+        sel = np.nonzero(own == r)[0]
+        d.set_particles({key: val[sel] for key, val in p.items()}, sel.astype(np.uint32))
+        doms.append(d)
+    dd.run_substeps(doms, dd.LocalTransport(), sub, dt, GRAV, contact=True, migrate_every=2)
+    got = [d.download() for d in doms]
+    ids = np.concatenate([g["ids"] for g in got])
+    assert len(ids) == n and np.array_equal(np.sort(ids), np.arange(n))
+    moved = sum(int(np.sum(dd.owner_of(dd.base_x(p["x"][g["ids"], 0], 0.0, DX), bounds) != r))
+                for r, g in enumerate(got))
+    assert moved > 0  # particles changed slab
+    x = np.zeros((n, 3), F32)
+    v = np.zeros((n, 3), F32)
+    for g in got:
+        x[g["ids"]], v[g["ids"]] = g["x"], g["v"]
+    assert np.abs(x - want["x"]).max() <= 1e-3 * DX
+    assert np.abs(v - want["v"]).max() <= 1e-3 * np.abs(want["v"]).max()
+
+
+def test_slab_bounds_balance_and_min_width():
+    w = np.zeros(64)
+    w[10:30] = 100.0
+    b = dd.slab_bounds(64, 4, w, margin=2)
+    assert b[0][0] == 0 and b[-1][1] == 64
+    assert all(hi - lo >= 4 for lo, hi in b)
+    assert all(b[i][1] == b[i + 1][0] for i in range(3))
+    mid = [(lo + hi) / 2 for lo, hi in b]
+    assert 10 <= mid[1] <= 30 and 10 <= mid[2] <= 30  # cuts follow the particles
+    own = dd.owner_of(np.array([0, 9, 63]), b)
+    assert own[0] == 0 and own[-1] == 3
+
+
+def _worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    t = dd.DistTransport(rank, world)
+    # grid-sum phase with M = 1, plane = 4 floats: down M planes, up 2 + M planes
+    down, up = 4, 12
+    send_lo = torch.full((down,), 10.0 * rank + 1)
+    send_hi = torch.full((up,), 10.0 * rank + 2)
+    recv_lo = torch.zeros(up)
+    recv_hi = torch.zeros(down)
+    t.exchange_tensors(send_lo if rank > 0 else None, send_hi if rank + 1 < world else None,
+                       recv_lo if rank > 0 else None, recv_hi if rank + 1 < world else None)
+    q.put((rank, recv_lo.tolist(), recv_hi.tolist()))
+    dist.destroy_process_group()
+
+
+def test_dist_transport_exchange_rule_gloo():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in ps:
+        pr.start()
+    res = dict((r, (lo, hi)) for r, lo, hi in [q.get(timeout=120) for _ in ps])
+    for pr in ps:
+        pr.join(timeout=60)
+    assert res[1][0] == [2.0] * 12   # rank 1's recv_lo = rank 0's send_hi (2 + M planes)
+    assert res[0][1] == [11.0] * 4   # rank 0's recv_hi = rank 1's send_lo (M planes)
