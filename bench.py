@@ -46,10 +46,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c5", choices=["c5", "c1", "c2", "c3"])
+    ap.add_argument("--workload", default="c5", choices=["c5", "c1", "c2", "c3", "c4"])
     ap.add_argument("--replicas", type=int, default=512, help="C5 replicas per GPU")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU-baseline sample length")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dd", action="store_true", help="c4 through slab DD even at N=1 (one slab)")
     return ap.parse_args()
 
 
@@ -63,7 +64,8 @@ def workload_specs(name, rank, replicas):
     from paper_2502_18437_b200 import scenes
     if name == "c5":
         return [scenes.c5_cutting_replica(r) for r in shard_replicas(rank, replicas)]
-    return [{"c1": scenes.c1_cube_drop, "c2": scenes.c2_cutting, "c3": scenes.c3_suture}[name]()]
+    return [{"c1": scenes.c1_cube_drop, "c2": scenes.c2_cutting, "c3": scenes.c3_suture,
+             "c4": scenes.c4_slab}[name]()]
 
 
 def reduce_over_ranks(ms, ms_e2e, n_particles, world, device):
@@ -84,6 +86,8 @@ def workload_desc(name, replicas, n_per_gpu):
         return (f"C5 shard: {replicas} independent cutting replicas x 64,800 p per GPU, 84^3 grid each, "
                 f"MLS 10 substeps/frame, quad-slicer blade (BASELINE.json configs[4])")
     return {"c1": "C1 cube drop, MLS, 32,768 p, 64^3", "c2": "C2 cutting, MLS, 262,144 p, 128^3",
+            "c4": "C4 tissue slab on a floor, MLS 20 substeps/frame, 8,388,608 p, 512^3 (slab DD over NCCL "
+                  "when N > 1)",
             "c3": "C3 suture, PB-MPM K=10, 262,144 p, 128^3, arc needle + 16 free thread capsules"}[name]
 
 
@@ -212,6 +216,23 @@ def cpu_threads():
 def run_reference(args, rank):
     if rank != 0:
         return None
+    if args.workload == "c4":
+        from paper_2502_18437_b200 import scenes
+        vals, t_total = [], 0.0
+        for _ in range(args.warmup):
+            time_reference_substeps(scenes.c4_slab(), args.cpu_seconds / max(args.steps, 1))
+        for _ in range(args.steps):
+            r, w, n, k = time_reference_substeps(scenes.c4_slab(), args.cpu_seconds / max(args.steps, 1))
+            vals.append(r)
+            t_total += w
+        value = statistics.median(vals)
+        return {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": 1e3 * t_total / max(args.steps, 1), "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+                "config": {"workload": workload_desc("c4", 0, None), "parallelism": "1 host thread"},
+                "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "reference",
+                                 "sample": f"{k} step_mls substeps per step on all {n} particles"},
+                "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     threads = cpu_threads() if args.workload == "c5" else 1
     fn = cpu_specs_fn(args.workload)
     # size one step to ~cpu_seconds/steps: probe one frame first
@@ -350,6 +371,117 @@ def run_ours(args, rank, world, local_rank):
     return line, batch
 
 
+def spawn_spec_particles(spec):
+    """Every particle of a single-object spec via the product's host spawner
+    (mpmb_spawn_box = the reference's create_particle_object lattice, bit-exact)."""
+    import ctypes as C
+    from paper_2502_18437_b200 import api, capi, scenes
+    lib = capi.load_product()
+    g = spec["grid"]
+    (ob,) = spec["particle_objects"]
+    cells = np.prod((np.array(ob["box_max"]) - np.array(ob["box_min"])) / g["dx"] + 2)
+    cap = int(cells * ob["particles_per_cell"]) + 1024
+    x, m, vol = np.zeros((cap, 3), np.float32), np.zeros(cap, np.float32), np.zeros(cap, np.float32)
+    n = C.c_int64()
+    api.check(lib.mpmb_spawn_box((capi.i3)(*g["dims"]), float(np.float32(g["dx"])), api._fp(np.array(g["origin"], np.float32)),
+                                 api._fp(np.array(ob["box_min"], np.float32)), api._fp(np.array(ob["box_max"], np.float32)),
+                                 ob["particles_per_cell"], float(np.float32(ob["density"])), ob["seed"], cap,
+                                 api._fp(x), api._fp(m), api._fp(vol), C.byref(n)), lib, "spawn_box")
+    k = n.value
+    p = api.empty_particles(k)
+    p["x"], p["mass"], p["volume0"] = x[:k].copy(), m[:k].copy(), vol[:k].copy()
+    mats = [scenes.material_params(ob["material"])]
+    shapes = [scenes.shape_spec(s, g["dx"]) for s in spec["shapes"]]
+    return p, mats, shapes
+
+
+def time_reference_substeps(spec, target_s):
+    """Bounded CPU sample for a scene too large for whole frames (C4: ~8 s per substep on
+    one core): the compiled reference's step_mls with the contact hook on the full particle
+    set, as many substeps as fit in ~target_s."""
+    import backends
+    g = spec["grid"]
+    p, mats, shapes = spawn_spec_particles(spec)
+    st = backends.state("ref", tuple(g["dims"]), g["dx"], tuple(g["origin"]))
+    st.set_materials(mats)
+    st.set_particles(p, with_stress=False)
+    st.set_shapes(shapes)
+    dt = spec["dt_frame"] / spec["substeps"]
+    t0 = time.time()
+    st.step_mls(dt, spec["gravity"], contact=True)
+    one = time.time() - t0
+    k = max(1, int(target_s / max(one, 1e-3)))
+    t0 = time.time()
+    for _ in range(k):
+        st.step_mls(dt, spec["gravity"], contact=True)
+    wall = time.time() - t0
+    n = len(p["mass"])
+    return n * k / wall, wall, n, k
+
+
+def run_ours_dd(args, rank, world, local_rank):
+    """C4 across N GPUs: one scene, slab domain decomposition (dd.py) over NCCL.  Strong
+    scaling: the same 8.4M particles whatever N; timing = max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2502_18437_b200 import dd, scenes
+    torch.cuda.set_device(local_rank)
+    spec = scenes.c4_slab()
+    g = spec["grid"]
+    dims, dx, origin = tuple(g["dims"]), g["dx"], tuple(g["origin"])
+    sub = spec["substeps"]
+    dt = spec["dt_frame"] / sub
+    t0 = time.time()
+    p, mats, shapes = spawn_spec_particles(spec)
+    n_all = len(p["mass"])
+    bx = dd.base_x(p["x"][:, 0], origin[0], dx)
+    bounds = dd.slab_bounds(dims[0], world, np.bincount(np.clip(bx, 0, dims[0] - 1), minlength=dims[0]), margin=2)
+    mine = np.nonzero(dd.owner_of(bx, bounds) == rank)[0]
+    lo, hi = bounds[rank]
+    d = dd.SlabDomain(dims, dx, origin, lo, hi, margin=2, capacity=int(1.5 * len(mine)) + 4096)
+    d.set_materials(mats)
+    d.set_shapes(shapes)
+    d.set_particles({k: v[mine] for k, v in p.items()}, mine.astype(np.uint32))
+    tr = dd.DistTransport(rank, world)
+    stream = torch.cuda.Stream()
+    setup_s = time.time() - t0
+    kw = dict(contact=True, boundary=0, pushout=True, deactivate=True)
+    with torch.cuda.stream(stream):
+        dd.run_substeps([d], tr, sub * max(args.warmup, 1), dt, spec["gravity"], **kw)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        dd.run_substeps([d], tr, sub * args.steps, dt, spec["gravity"], **kw)
+        e1.record(stream)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            dist.barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        d2h = 0
+        for _ in range(args.steps):
+            dd.run_substeps([d], tr, sub, dt, spec["gravity"], **kw)
+            r = d.download()
+            d2h = len(r["ids"]) * (4 + 12 + 12 + 1)
+        f1.record(stream)
+        f1.synchronize()
+        ms_e2e = f0.elapsed_time(f1)
+    ms, ms_e2e, _ = reduce_over_ranks(ms, ms_e2e, 0, world, "cuda")
+    ps = n_all * sub * args.steps
+    line = {"metric": METRIC, "value": ps / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": workload_desc("c4", 0, n_all), "particles_total": n_all,
+                       "substeps_per_step": sub, "parallelism": f"slab DD x{world} (NCCL halo + migration)",
+                       "slabs": bounds},
+            "e2e": {"value": ps / (ms_e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": d2h},
+            "setup_s": setup_s}
+    return line, None
+
+
 def cpu_baseline(args):
     if args.no_cpu_baseline:
         return None
@@ -357,6 +489,11 @@ def cpu_baseline(args):
     import backends
     if not backends.have_reference():
         return None
+    if args.workload == "c4":
+        rate, wall, n, k = time_reference_substeps(scenes.c4_slab(), args.cpu_seconds)
+        return {"value": rate, "unit": UNIT, "cores": 1, "kind": "reference",
+                "sample": f"C4 (1 core): {k} step_mls substeps with the contact hook on all {n} particles, "
+                          f"{wall:.1f} s wall"}
     threads = cpu_threads() if args.workload == "c5" else 1
     fn = cpu_specs_fn(args.workload)
     rate1, wall1, n, sub = time_reference(fn, threads, 1)
@@ -382,7 +519,10 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    line, batch = run_ours(args, rank, world, local_rank)
+    if args.workload == "c4" and (world > 1 or args.dd):
+        line, batch = run_ours_dd(args, rank, world, local_rank)
+    else:
+        line, batch = run_ours(args, rank, world, local_rank)
     if rank == 0:
         if world == 1:
             line["cpu_baseline"] = cpu_baseline(args)

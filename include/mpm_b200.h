@@ -249,6 +249,11 @@ mpmb_status mpmb_bin_particles(mpmb_state st, uint32_t* keys, uint32_t* perm);
  * neighbour's recv buffer stays zero.  Free bodies are not supported in DD. */
 mpmb_status mpmb_state_create_slab(const int32_t dims[3], float dx, const float origin[3], int32_t slab_lo,
                                    int32_t slab_hi, int32_t margin, int64_t capacity, mpmb_state* out);
+/* The reference's particle lattice of create_particle_object (state.hpp:101-149, host,
+ * bit-exact): jittered ppc-per-cell points in [box_min, box_max), mass and volume0. */
+mpmb_status mpmb_spawn_box(const int32_t dims[3], float dx, const float origin[3], const float box_min[3],
+                           const float box_max[3], int32_t ppc, float density, uint64_t seed, int64_t capacity,
+                           float* x, float* mass, float* volume0, int64_t* n);
 /* Particles with explicit original indices (global ids that travel with migration). */
 mpmb_status mpmb_state_set_particles_ids(mpmb_state st, int32_t n, const float* x, const float* v,
                                          const float* mass, const float* volume0, const float* F,

@@ -232,6 +232,24 @@ extern "C" mpmb_status mpmb_state_set_particles(mpmb_state st, int32_t n, const 
     });
 }
 
+extern "C" mpmb_status mpmb_spawn_box(const int32_t dims[3], float dx, const float origin[3], const float mn[3],
+                                      const float mx[3], int32_t ppc, float density, uint64_t seed, int64_t capacity,
+                                      float* x, float* mass, float* vol0, int64_t* n) {
+    return guarded([&] {
+        if (!dims || !origin || !mn || !mx || !n) fail(MPMB_INVALID_ARGUMENT, "null argument");
+        std::vector<float> px, pm, pv;
+        if (!host::spawn_box(dims, dx, host::v3(origin), host::v3(mn), host::v3(mx), ppc, density, seed, px, pm, pv))
+            fail(MPMB_INVALID_ARGUMENT, "spawn_box: invalid box");
+        const int64_t k = static_cast<int64_t>(pm.size());
+        *n = k;
+        if (k > capacity) fail(MPMB_BUFFER_TOO_SMALL, "spawn_box: capacity too small");
+        if (x) std::copy(px.begin(), px.end(), x);
+        if (mass) std::copy(pm.begin(), pm.end(), mass);
+        if (vol0) std::copy(pv.begin(), pv.end(), vol0);
+        return MPMB_OK;
+    });
+}
+
 // ------------------------------------------------ slab domain decomposition
 extern "C" mpmb_status mpmb_state_create_slab(const int32_t dims[3], float dx, const float origin[3],
                                               int32_t slab_lo, int32_t slab_hi, int32_t margin, int64_t capacity,
@@ -361,23 +379,7 @@ extern "C" mpmb_status mpmb_dd_download(mpmb_state st, int64_t capacity, uint32_
     return guarded([&] {
         if (!ids || !x || !v || !active || !n) fail(MPMB_INVALID_ARGUMENT, "null argument");
         Engine& e = *S(st)->eng;
-        const int64_t slots = e.slot_count();
-        std::vector<uint32_t> si(static_cast<size_t>(slots));
-        std::vector<float> sx(3 * static_cast<size_t>(slots)), sv(3 * static_cast<size_t>(slots));
-        std::vector<uint8_t> sa(static_cast<size_t>(slots));
-        if (slots > 0) e.download_slots(si.data(), sx.data(), sv.data(), sa.data());
-        int64_t k = 0;
-        for (int64_t s = 0; s < slots; ++s) {
-            if (si[s] == 0xFFFFFFFFu) continue;
-            if (k >= capacity) fail(MPMB_BUFFER_TOO_SMALL, "dd_download: capacity too small");
-            ids[k] = si[s];
-            for (int a = 0; a < 3; ++a) {
-                x[3 * k + a] = sx[3 * s + a];
-                v[3 * k + a] = sv[3 * s + a];
-            }
-            active[k] = sa[s];
-            ++k;
-        }
+        const int64_t k = e.download_compact(capacity, ids, x, v, active);
         *n = k;
         return MPMB_OK;
     });

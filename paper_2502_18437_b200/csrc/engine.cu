@@ -120,6 +120,7 @@ struct Engine::Impl {
     int64_t mig_cap = 0;
     DevBuf mig_counts;
     int64_t mig_sent = 0;
+    DevBuf dl_ids, dl_x, dl_v, dl_a, dl_cnt;  // download_compact staging (persistent)
     DevBuf planes[2][kPlanes];
     int cur = 0;
     bool binned = false;
@@ -996,20 +997,27 @@ void Engine::dd_migrate_unpack(int64_t n_from_lo, int64_t n_from_hi) {
     bin();
 }
 
-void Engine::download_slots(uint32_t* ids, float* x, float* v, uint8_t* active) {
+int64_t Engine::download_compact(int64_t capacity, uint32_t* ids, float* x, float* v, uint8_t* active) {
     Impl& I = *impl_;
-    if (I.n_cap == 0) return;
+    if (I.n_cap == 0) return 0;
     const size_t N = static_cast<size_t>(I.n_cap);
-    DevBuf di, dx, dv, da;
-    di.alloc(4 * N); dx.alloc(12 * N); dv.alloc(12 * N); da.alloc(N);
+    DevBuf &di = I.dl_ids, &dx = I.dl_x, &dv = I.dl_v, &da = I.dl_a, &dc = I.dl_cnt;
+    di.alloc(4 * N); dx.alloc(12 * N); dv.alloc(12 * N); da.alloc(N); dc.alloc(4);
+    check(cudaMemsetAsync(dc.p, 0, 4, I.st), "memset");
     Params P = I.params();
-    launch_download_slots(P, di.as<uint32_t>(), dx.as<float>(), dv.as<float>(), da.as<uint8_t>(), I.st);
+    launch_download_slots(P, di.as<uint32_t>(), dx.as<float>(), dv.as<float>(), da.as<uint8_t>(), dc.as<uint32_t>(),
+                          I.st);
     I.counted(1);
-    check(cudaMemcpyAsync(ids, di.p, 4 * N, cudaMemcpyDeviceToHost, I.st), "d2h");
-    check(cudaMemcpyAsync(x, dx.p, 12 * N, cudaMemcpyDeviceToHost, I.st), "d2h");
-    check(cudaMemcpyAsync(v, dv.p, 12 * N, cudaMemcpyDeviceToHost, I.st), "d2h");
-    check(cudaMemcpyAsync(active, da.p, N, cudaMemcpyDeviceToHost, I.st), "d2h");
-    check(cudaStreamSynchronize(I.st), "download_slots");
+    uint32_t k = 0;
+    check(cudaMemcpyAsync(&k, dc.p, 4, cudaMemcpyDeviceToHost, I.st), "d2h");
+    check(cudaStreamSynchronize(I.st), "download");
+    if (static_cast<int64_t>(k) > capacity) throw std::invalid_argument("download: capacity too small");
+    check(cudaMemcpyAsync(ids, di.p, 4ull * k, cudaMemcpyDeviceToHost, I.st), "d2h");
+    check(cudaMemcpyAsync(x, dx.p, 12ull * k, cudaMemcpyDeviceToHost, I.st), "d2h");
+    check(cudaMemcpyAsync(v, dv.p, 12ull * k, cudaMemcpyDeviceToHost, I.st), "d2h");
+    check(cudaMemcpyAsync(active, da.p, k, cudaMemcpyDeviceToHost, I.st), "d2h");
+    check(cudaStreamSynchronize(I.st), "download");
+    return k;
 }
 
 }  // namespace mpmb

@@ -140,9 +140,9 @@ class Engine {
     void dd_migrate_pack(int64_t* n_lo, int64_t* n_hi);
     void dd_migrate_buffers(void** send_lo, void** send_hi, void** recv_lo, void** recv_hi, int64_t* cap);
     void dd_migrate_unpack(int64_t n_from_lo, int64_t n_from_hi);  // appends, then bins
-    // Per slot: original index (0xFFFFFFFF = hole), x, v, active; n = slot count.
+    // The particles (any order): original index, x, v, active; returns how many (<= capacity).
     int64_t slot_count() const;
-    void download_slots(uint32_t* ids, float* x, float* v, uint8_t* active);
+    int64_t download_compact(int64_t capacity, uint32_t* ids, float* x, float* v, uint8_t* active);
     int64_t n_active_sorted();
 
     void synchronize();

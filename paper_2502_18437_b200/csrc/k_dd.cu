@@ -111,20 +111,35 @@ void launch_migrate_unpack(const Params& P, const float4* in, uint32_t n, uint32
     k_migrate_unpack<<<dd_blocks(n, 256), 256, 0, st>>>(P, in, n, first);
 }
 
-// Per slot (holes included): original index, x, v, active.
-__global__ void k_download_slots(const Params P, uint32_t* ids, float* x, float* v, uint8_t* active) {
+// The slab's particles compacted (warp-aggregated append, any order): original index, x,
+// v, active; *count = how many.
+__global__ void k_download_slots(const Params P, uint32_t* ids, float* x, float* v, uint8_t* active,
+                                 uint32_t* count) {
+    const unsigned full = 0xffffffffu;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < P.n_total; s += stride) {
-        const float4 r = P.pl[PR][s], a = P.pl[0][s], b = P.pl[1][s];
-        ids[s] = __float_as_uint(r.w);
-        x[3 * s] = a.x; x[3 * s + 1] = a.y; x[3 * s + 2] = a.z;
-        v[3 * s] = a.w; v[3 * s + 1] = b.x; v[3 * s + 2] = b.y;
-        active[s] = (__float_as_uint(r.z) & kActiveBit) ? 1 : 0;
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < P.n_total; base += stride) {
+        const int64_t s = base + threadIdx.x;
+        float4 r = make_float4(0.f, 0.f, 0.f, __uint_as_float(kHoleOrig));
+        if (s < P.n_total) r = P.pl[PR][s];
+        const bool real = __float_as_uint(r.w) != kHoleOrig;
+        const unsigned m = __ballot_sync(full, real);
+        if (!m) continue;
+        uint32_t start = 0;
+        if ((threadIdx.x & 31) == 0) start = atomicAdd(count, __popc(m));
+        start = __shfl_sync(full, start, 0);
+        if (!real) continue;
+        const uint64_t k = start + __popc(m & lanemask_lt());
+        const float4 a = P.pl[0][s], b = P.pl[1][s];
+        ids[k] = __float_as_uint(r.w);
+        x[3 * k] = a.x; x[3 * k + 1] = a.y; x[3 * k + 2] = a.z;
+        v[3 * k] = a.w; v[3 * k + 1] = b.x; v[3 * k + 2] = b.y;
+        active[k] = (__float_as_uint(r.z) & kActiveBit) ? 1 : 0;
     }
 }
 
-void launch_download_slots(const Params& P, uint32_t* ids, float* x, float* v, uint8_t* active, cudaStream_t st) {
-    k_download_slots<<<dd_blocks(P.n_total, 256), 256, 0, st>>>(P, ids, x, v, active);
+void launch_download_slots(const Params& P, uint32_t* ids, float* x, float* v, uint8_t* active, uint32_t* count,
+                           cudaStream_t st) {
+    k_download_slots<<<dd_blocks(P.n_total, 256), 256, 0, st>>>(P, ids, x, v, active, count);
 }
 
 }  // namespace mpmb

@@ -168,20 +168,24 @@ __global__ void __launch_bounds__(256) k_bin_scatter(BinBuffers B, int64_t n) {
 }
 
 // One block per bucket (grid-stride): counting sort by cell, then rank by original index.
+// Inactive particles keep their bucket order (grid-wide copy: the bucket can be large);
+// holes need no sorted entry (the gather fills everything past the real particles).
+__global__ void __launch_bounds__(256) k_bin_rest(BinBuffers B) {
+    const uint32_t beg = B.bucket_off[B.n_buckets - 2], end = B.bucket_off[B.n_buckets - 1];
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t q = beg + blockIdx.x * blockDim.x + threadIdx.x; q < end; q += stride) {
+        B.sorted_src[q] = B.e_src[q];
+        B.sorted_orig[q] = B.e_orig[q];
+    }
+}
+
 __global__ void __launch_bounds__(256) k_bin_local(BinBuffers B) {
     __shared__ uint32_t hist[64];
     __shared__ uint32_t cstart[64];
-    const uint32_t inactive = B.n_buckets - 2;  // then the hole bucket
-    for (uint32_t b = blockIdx.x; b < B.n_buckets; b += gridDim.x) {
+    const uint32_t inactive = B.n_buckets - 2;  // the inactive and hole buckets: k_bin_rest
+    for (uint32_t b = blockIdx.x; b < inactive; b += gridDim.x) {
         const uint32_t beg = B.bucket_off[b], end = B.bucket_off[b + 1];
         if (beg == end) continue;
-        if (b >= inactive) {
-            for (uint32_t q = beg + threadIdx.x; q < end; q += blockDim.x) {
-                B.sorted_src[q] = B.e_src[q];
-                B.sorted_orig[q] = B.e_orig[q];
-            }
-            continue;
-        }
         if (threadIdx.x < 64) hist[threadIdx.x] = 0u;
         __syncthreads();
         for (uint32_t q = beg + threadIdx.x; q < end; q += blockDim.x)
@@ -288,6 +292,7 @@ void launch_bin(const Params& P, const BinBuffers& B, float4* const new_planes[k
     launch_exclusive_scan(B.bucket_count, B.bucket_off, B.n_buckets, B.scan_tmp, st, launches);
     k_bin_scatter<<<blocks_for(n_total, 256, cap), 256, 0, st>>>(B, n_total);
     k_bin_local<<<blocks_for(static_cast<int64_t>(B.n_buckets) * 256, 256, 148 * 8), 256, 0, st>>>(B);
+    k_bin_rest<<<blocks_for(n_total, 256, cap), 256, 0, st>>>(B);
     k_bin_gather<<<blocks_for(n_total, 256, cap), 256, 0, st>>>(
         P, B, n_total, new_planes[0], new_planes[1], new_planes[2], new_planes[3],
         new_planes[4], new_planes[5], new_planes[6]);
@@ -297,7 +302,7 @@ void launch_bin(const Params& P, const BinBuffers& B, float4* const new_planes[k
         Q.pl[q] = new_planes[q];
     }
     k_bin_tail<<<blocks_for(n_total / 8, 256, cap), 256, 0, st>>>(Q, B, n_total);
-    *launches += 5;
+    *launches += 6;
 }
 
 }  // namespace mpmb

@@ -53,7 +53,8 @@ void launch_halo(const Params& P, int mode, float4* pool, float4* buf, int x0, i
 void launch_migrate_pack(const Params& P, int lo, int hi, float4* out_lo, float4* out_hi, uint32_t cap,
                          uint32_t* counts, cudaStream_t st);
 void launch_migrate_unpack(const Params& P, const float4* in, uint32_t n, uint32_t first, cudaStream_t st);
-void launch_download_slots(const Params& P, uint32_t* ids, float* x, float* v, uint8_t* active, cudaStream_t st);
+void launch_download_slots(const Params& P, uint32_t* ids, float* x, float* v, uint8_t* active, uint32_t* count,
+                           cudaStream_t st);
 
 // ---- I/O (k_io.cu) ----
 struct IoArrays {  // original-order device staging arrays (any may be null)
