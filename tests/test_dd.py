@@ -125,3 +125,22 @@ def test_dist_transport_exchange_rule_gloo():
         pr.join(timeout=60)
     assert res[1][0] == [2.0] * 12   # rank 1's recv_lo = rank 0's send_hi (2 + M planes)
     assert res[0][1] == [11.0] * 4   # rank 0's recv_hi = rank 1's send_lo (M planes)
+
+
+def test_product_spawn_matches_oracle():
+    """mpmb_spawn_box (host, used by the DD drivers) is the oracle's lattice bit for bit."""
+    import ctypes as C
+    lib = capi.load_product()
+    o = __import__("backends").oracle()
+    args = ((capi.i3)(*DIMS), DX, api._fp(np.zeros(3, F32)), api._fp(np.array([0.2, 0.12, 0.2], F32)),
+            api._fp(np.array([1.0, 0.3, 0.6], F32)), 8, 1000.0, 3)
+    cap = 80000
+    a = [np.zeros((cap, 3), F32), np.zeros(cap, F32), np.zeros(cap, F32)]
+    b = [np.zeros((cap, 3), F32), np.zeros(cap, F32), np.zeros(cap, F32)]
+    n = C.c_int64()
+    assert lib.mpmb_spawn_box(*args, cap, *[api._fp(q) for q in a], C.byref(n)) == capi.OK
+    k = o.mpmor_spawn_box(*args, cap, *[api._fp(q) for q in b])
+    assert n.value == k > 0
+    for qa, qb in zip(a, b):
+        assert np.array_equal(qa[:k], qb[:k])
+    assert lib.mpmb_spawn_box(*args, 10, *[api._fp(q) for q in a], C.byref(n)) == capi.BUFFER_TOO_SMALL
