@@ -333,6 +333,17 @@ mpmb_status mpmb_get_profile(mpmb_handle h, mpmb_profile* out);
 /* Blocks until every frame enqueued on h has finished. */
 mpmb_status mpmb_synchronize(mpmb_handle h);
 
+/* --------------------------------------------------- scenario metrics (device)
+ * The harness metrics of run_scenario (scenario.hpp:68-139) on the resident particles: a
+ * batch handle addresses every scene (arrays of one entry per scene), a scene handle its
+ * own.  No frame may be pending.  Both reproduce the reference's spatial hash, probes and
+ * float arithmetic, so counts and spacings equal the reference's on identical positions.
+ *   components: compute_components with link radius radius[k] (components holding >= 5%
+ *               of the active particles);
+ *   nn_spacing: mean_nearest_neighbor_spacing with cell hint cell_hint[k]. */
+mpmb_status mpmb_components(mpmb_handle h, const float* radius, int32_t* count);
+mpmb_status mpmb_nn_spacing(mpmb_handle h, const float* cell_hint, float* spacing);
+
 #ifdef __cplusplus
 }
 #endif

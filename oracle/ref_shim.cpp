@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "mpm/facade.hpp"
+#include "mpm/scenario.hpp"
 #include "mpm/scene_spec.hpp"
 #include "mpm_b200.h"
 
@@ -520,6 +521,45 @@ double mpmref_advance_many(const uint64_t* scenes, int32_t n, float dt, int32_t 
     for (auto& th : pool) th.join();
     auto t1 = std::chrono::steady_clock::now();
     return std::chrono::duration<double>(t1 - t0).count();
+}
+
+// ---- scenario harness (scenario.hpp), for the device metrics / writer parity tests ----
+static std::vector<Vec3> vec3s(const float* p, int64_t n) {
+    std::vector<Vec3> v(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) v[i] = Vec3{p[3 * i], p[3 * i + 1], p[3 * i + 2]};
+    return v;
+}
+
+int32_t mpmref_compute_components(const float* pos, const uint8_t* active, int64_t n, float radius) {
+    std::vector<uint8_t> a(active, active + n);
+    return compute_components(vec3s(pos, n), a, radius);
+}
+
+float mpmref_nn_spacing(const float* pos, const uint8_t* active, int64_t n, float hint) {
+    std::vector<uint8_t> a(active, active + n);
+    return mean_nearest_neighbor_spacing(vec3s(pos, n), a, hint);
+}
+
+void mpmref_write_frame_bin(const char* path, const float* pos, int64_t n) {
+    scenario_detail::write_frame_bin(path, vec3s(pos, n));
+}
+
+void mpmref_write_frame_csv(const char* path, const float* pos, int64_t n) {
+    scenario_detail::write_frame_csv(path, vec3s(pos, n));
+}
+
+// run_scenario on a scene JSON file (load_scene_spec): writes metrics.csv and frame dumps
+// under out_dir; returns frames done (-1 on error, message in mpmref_last_error)
+int32_t mpmref_run_scenario(const char* json_path, int32_t frames, const char* out_dir, int32_t* components) {
+    try {
+        SceneSpec spec = load_scene(json_path);
+        ScenarioSummary sum = run_scenario(spec, frames, out_dir);
+        if (components) *components = sum.final_component_count;
+        return sum.frames_done;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
 }
 
 }  // extern "C"

@@ -142,6 +142,8 @@ PRODUCT_API.update({
     "set_profiling": (C.c_int, [u64, C.c_int32]),
     "get_profile": (C.c_int, [u64, C.POINTER(Profile)]),
     "synchronize": (C.c_int, [u64]),
+    "components": (C.c_int, [u64, fp, ip]),
+    "nn_spacing": (C.c_int, [u64, fp, fp]),
     "spawn_box": (C.c_int, [ip, C.c_float, fp, fp, fp, C.c_int32, C.c_float, u64, C.c_int64, fp, fp, fp,
                             I64P]),
     # slab domain decomposition (include/mpm_b200.h)

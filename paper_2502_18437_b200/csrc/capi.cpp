@@ -5,6 +5,8 @@
 // (facade.hpp:26-219) over host-side Scene records whose simulation state lives in a
 // device Engine shared by all scenes of a batch.  Scene semantics follow
 // mpm::Scene::run_frame (scene.hpp:176-249).  No function throws across the boundary.
+#include <cfloat>
+#include <cmath>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -1330,6 +1332,77 @@ extern "C" mpmb_status mpmb_set_stream(mpmb_handle h, void* stream) {
     return with_batch(h, [&](Batch& b) {
         b.stream = stream;
         if (b.eng) b.eng->set_stream(stream);
+        return MPMB_OK;
+    });
+}
+
+// ------------------------------------------------ scenario metrics (k_scenario.cu)
+namespace {
+// handle -> (batch, scenes addressed): a batch handle addresses all its scenes, a scene
+// handle its own; the device state must be current (no frame pending)
+Batch* metrics_target(mpmb_handle h, std::vector<size_t>& idx) {
+    bool is_batch;
+    Batch* b = batch_of_handle(reg(), h, is_batch);
+    if (!b) return nullptr;
+    if (b->status == Status::advancing) fail(MPMB_LIFECYCLE_ERROR, "metrics: fetch the pending frame first");
+    if (is_batch) {
+        for (size_t i = 0; i < b->scenes.size(); ++i) idx.push_back(i);
+    } else {
+        Scene* s = reg().scene(h);
+        for (size_t i = 0; i < b->scenes.size(); ++i)
+            if (b->scenes[i] == s) idx.push_back(i);
+    }
+    if (!b->device_valid || b->particles_dirty || b->shapes_dirty) upload(*b);
+    return b;
+}
+}  // namespace
+
+extern "C" mpmb_status mpmb_components(mpmb_handle h, const float* radius, int32_t* count) {
+    std::lock_guard<std::mutex> lk(reg().mu);
+    return guarded([&]() -> mpmb_status {
+        if (!radius || !count) fail(MPMB_INVALID_ARGUMENT, "null argument");
+        std::vector<size_t> idx;
+        Batch* b = metrics_target(h, idx);
+        if (!b) return MPMB_BAD_HANDLE;
+        std::vector<float> r(b->scenes.size(), radius[0]);
+        for (size_t k = 0; k < idx.size(); ++k) {
+            if (!(radius[k] > 0)) fail(MPMB_INVALID_ARGUMENT, "components: radius must be positive");
+            r[idx[k]] = radius[k];
+        }
+        std::vector<int32_t> c(b->scenes.size(), 0);
+        b->eng->components(r.data(), c.data());
+        for (size_t k = 0; k < idx.size(); ++k) count[k] = c[idx[k]];
+        return MPMB_OK;
+    });
+}
+
+extern "C" mpmb_status mpmb_nn_spacing(mpmb_handle h, const float* cell_hint, float* spacing) {
+    std::lock_guard<std::mutex> lk(reg().mu);
+    return guarded([&]() -> mpmb_status {
+        if (!cell_hint || !spacing) fail(MPMB_INVALID_ARGUMENT, "null argument");
+        std::vector<size_t> idx;
+        Batch* b = metrics_target(h, idx);
+        if (!b) return MPMB_BAD_HANDLE;
+        std::vector<float> cell(b->scenes.size(), cell_hint[0]);
+        for (size_t k = 0; k < idx.size(); ++k) {
+            if (!(cell_hint[k] > 0)) fail(MPMB_INVALID_ARGUMENT, "nn_spacing: cell hint must be positive");
+            cell[idx[k]] = cell_hint[k];
+        }
+        size_t total = 0;
+        for (Scene* s : b->scenes) total += s->count();
+        std::vector<float> best2(total, FLT_MAX);
+        if (total) b->eng->nn_best2(cell.data(), best2.data());
+        for (size_t k = 0; k < idx.size(); ++k) {  // scenario.hpp:73-95, original order, FP64 sum
+            const size_t si = idx[k], o = b->offsets[si], n = b->scenes[si]->count();
+            double sum = 0;
+            size_t cnt = 0;
+            for (size_t i = 0; i < n; ++i)
+                if (best2[o + i] < FLT_MAX) {
+                    sum += std::sqrt(double(best2[o + i]));
+                    ++cnt;
+                }
+            spacing[k] = cnt ? static_cast<float>(sum / cnt) : cell_hint[k];
+        }
         return MPMB_OK;
     });
 }

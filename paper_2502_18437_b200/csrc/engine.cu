@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cfloat>
 #include <cmath>
 #include <atomic>
 #include <cstring>
@@ -863,6 +864,52 @@ int64_t Engine::n_active_sorted() {
 }
 
 void Engine::synchronize() { check(cudaStreamSynchronize(impl_->st), "synchronize"); }
+
+// ------------------------------------------------ scenario metrics (k_scenario.cu)
+void Engine::components(const float* radius, int32_t* counts) {
+    Impl& I = *impl_;
+    const size_t S = I.hs.size();
+    if (I.n_cap == 0) {
+        std::fill(counts, counts + S, 0);
+        return;
+    }
+    DevBuf cell, cnt, scratch;
+    cell.alloc(4 * S); cnt.alloc(4 * S);
+    const size_t sb = scenario_scratch_bytes(I.n_cap, static_cast<int>(S));
+    scratch.alloc(sb);
+    check(cudaMemcpyAsync(cell.p, radius, 4 * S, cudaMemcpyHostToDevice, I.st), "h2d");
+    Params P = I.params();
+    launch_scenario(P, 0, cell.as<float>(), scratch.p, sb, cnt.as<int32_t>(), nullptr, nullptr, static_cast<int>(S), I.st);
+    I.counted(6);
+    check(cudaMemcpyAsync(counts, cnt.p, 4 * S, cudaMemcpyDeviceToHost, I.st), "d2h");
+    check(cudaStreamSynchronize(I.st), "components");
+}
+
+void Engine::nn_best2(const float* cell_size, float* best2) {
+    Impl& I = *impl_;
+    const size_t S = I.hs.size();
+    if (I.n_cap == 0) return;
+    const size_t N = static_cast<size_t>(I.n_cap);
+    DevBuf cell, b2, orig, scratch;
+    cell.alloc(4 * S); b2.alloc(4 * N); orig.alloc(4 * N);
+    const size_t sb = scenario_scratch_bytes(I.n_cap, static_cast<int>(S));
+    scratch.alloc(sb);
+    check(cudaMemcpyAsync(cell.p, cell_size, 4 * S, cudaMemcpyHostToDevice, I.st), "h2d");
+    Params P = I.params();
+    launch_scenario(P, 1, cell.as<float>(), scratch.p, sb, nullptr, b2.as<float>(), orig.as<uint32_t>(),
+                    static_cast<int>(S), I.st);
+    I.counted(4);
+    std::vector<float> hb(N);
+    std::vector<uint32_t> ho(N);
+    check(cudaMemcpyAsync(hb.data(), b2.p, 4 * N, cudaMemcpyDeviceToHost, I.st), "d2h");
+    check(cudaMemcpyAsync(ho.data(), orig.p, 4 * N, cudaMemcpyDeviceToHost, I.st), "d2h");
+    check(cudaStreamSynchronize(I.st), "nn_best2");
+    std::fill(best2, best2 + I.n, FLT_MAX);
+    std::vector<uint8_t> act(static_cast<size_t>(I.n), 0);
+    // slots that are not active particles keep FLT_MAX; hb is only meaningful for active ones
+    for (size_t s = 0; s < N; ++s)
+        if (ho[s] != 0xFFFFFFFFu && ho[s] < static_cast<uint32_t>(I.n)) best2[ho[s]] = hb[s];
+}
 
 // ------------------------------------------------ slab domain decomposition (k_dd.cu)
 void Engine::set_capacity(int64_t particles) { impl_->cap_hint = std::max<int64_t>(0, particles); }

@@ -124,6 +124,13 @@ class Engine {
     // keys/perm of the binning stage (original indices), see mpmb_bin_particles
     void read_binning(uint32_t* keys, uint32_t* perm);
 
+    // ---- scenario metrics (k_scenario.cu; scenario.hpp:68-139), synchronous ----
+    // components per scene with link radius radius[scene] (>= 5% of the active particles)
+    void components(const float* radius, int32_t* counts);
+    // squared nearest-neighbour distance per particle in original order (FLT_MAX = none),
+    // probing with cell size cell[scene]
+    void nn_best2(const float* cell, float* best2);
+
     // ---- slab domain decomposition (k_dd.cu) ----
     // Slots for particles that may arrive by migration; call before upload_particles.
     void set_capacity(int64_t particles);

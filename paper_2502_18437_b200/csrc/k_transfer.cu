@@ -32,7 +32,10 @@ namespace mpmb {
 #endif
 constexpr int kStages = MPMB_P2G_STAGES;     // P2G staging ring depth
 constexpr int kG2PStages = MPMB_G2P_STAGES;  // G2P: one more, so particle k+1 has landed while k computes
-constexpr int kWarpsPerBlock = 4;
+#ifndef MPMB_WPB
+#define MPMB_WPB 4
+#endif
+constexpr int kWarpsPerBlock = MPMB_WPB;
 constexpr int kPer = kGroup / 32;  // sorted positions per lane
 constexpr int kBins = 512;         // sort bins: ((global brick & 7) << 6) | cell
 constexpr int kBinWords = kBins + kBins / 32;  // one pad word per 32 bins (conflict-free scan)

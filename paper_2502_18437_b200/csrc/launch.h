@@ -56,6 +56,11 @@ void launch_migrate_unpack(const Params& P, const float4* in, uint32_t n, uint32
 void launch_download_slots(const Params& P, uint32_t* ids, float* x, float* v, uint8_t* active, uint32_t* count,
                            cudaStream_t st);
 
+// ---- scenario metrics (k_scenario.cu) ----
+size_t scenario_scratch_bytes(int64_t n, int n_scenes);
+void launch_scenario(const Params& P, int mode, const float* cell, void* scratch, size_t scratch_bytes,
+                     int32_t* count, float* best2, uint32_t* orig, int n_scenes, cudaStream_t st);
+
 // ---- I/O (k_io.cu) ----
 struct IoArrays {  // original-order device staging arrays (any may be null)
     float* x; float* v; float* mass; float* vol0; float* F; float* C; int32_t* mat;
