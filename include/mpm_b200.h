@@ -208,6 +208,9 @@ mpmb_status mpmb_state_reset_contact(mpmb_state st);
 /* step_mls; contact != 0 installs apply_contact_pass over the state's shapes as the hook. */
 mpmb_status mpmb_step_mls(mpmb_state st, float dt, const float gravity[3], int32_t contact,
                           int32_t boundary, mpmb_step_stats* stats);
+/* step_standard (solvers.hpp:80-138): PIC transfers, nodal force -dt V sigma grad w. */
+mpmb_status mpmb_step_standard(mpmb_state st, float dt, const float gravity[3], int32_t contact,
+                               int32_t boundary, mpmb_step_stats* stats);
 /* step_pbmpm with PbmpmConfig{iterations}. */
 mpmb_status mpmb_step_pbmpm(mpmb_state st, float dt, const float gravity[3], int32_t iterations,
                             int32_t contact, int32_t boundary, mpmb_step_stats* stats);

@@ -1063,6 +1063,60 @@ static void g2p_gather(const Grid* grid, V3 x, V3* vnew, M3* B) {
             }
 }
 
+/* ref: solvers.hpp:80-138 (standard MPM: PIC transfers, nodal force -dt V sigma grad w) */
+mpmb_status mpmor_step_standard(mpmor_state st, float dt, const float gr[3], int32_t contact, int32_t bc,
+                                mpmb_step_stats* stats) {
+    int inverted = 0;
+    Particles* p = &st->p;
+    Grid* grid = &st->grid;
+    grid_clear(grid);
+    for (size_t ii = 0; ii < p->n; ++ii) {
+        const size_t i = g_order_mode == 1 ? p->n - 1 - ii : ii;
+        if (!p->active[i]) continue;
+        SW sw = spline_weights(p->x[i], grid->origin, grid->dx);
+        float volume = mdet(p->F[i]) * p->vol0[i];
+        M3 impulse_m = mscale(p->stress[i], -dt * volume);
+        for (int dk = 0; dk < 3; ++dk)
+            for (int dj = 0; dj < 3; ++dj)
+                for (int di = 0; di < 3; ++di) {
+                    float w = sw.w[0][di] * sw.w[1][dj] * sw.w[2][dk];
+                    V3 grad = v3(sw.dw[0][di] * sw.w[1][dj] * sw.w[2][dk], sw.w[0][di] * sw.dw[1][dj] * sw.w[2][dk],
+                                 sw.w[0][di] * sw.w[1][dj] * sw.dw[2][dk]);
+                    Node* node = &grid->nodes[gindex(grid, sw.base[0] + di, sw.base[1] + dj, sw.base[2] + dk)];
+                    node->mass += w * p->mass[i];
+                    node->mom = vadd(node->mom, vadd(vmul(p->v[i], w * p->mass[i]), mmulv(impulse_m, grad)));
+                }
+    }
+    grid_velocity_update(st, v3p(gr), dt, contact, bc, 1);
+    for (size_t i = 0; i < p->n; ++i) {
+        if (!p->active[i]) continue;
+        SW sw = spline_weights(p->x[i], grid->origin, grid->dx);
+        V3 vnew = v3(0, 0, 0);
+        M3 L = mzero();
+        for (int dk = 0; dk < 3; ++dk)
+            for (int dj = 0; dj < 3; ++dj)
+                for (int di = 0; di < 3; ++di) {
+                    float w = sw.w[0][di] * sw.w[1][dj] * sw.w[2][dk];
+                    V3 grad = v3(sw.dw[0][di] * sw.w[1][dj] * sw.w[2][dk], sw.w[0][di] * sw.dw[1][dj] * sw.w[2][dk],
+                                 sw.w[0][di] * sw.w[1][dj] * sw.dw[2][dk]);
+                    const Node* node =
+                        &grid->nodes[gindex(grid, sw.base[0] + di, sw.base[1] + dj, sw.base[2] + dk)];
+                    if (node->mass <= kMassEps) continue;
+                    vnew = vadd(vnew, vmul(node->vel, w));
+                    maddto(&L, mouter(node->vel, grad));
+                }
+        p->v[i] = vnew;
+        p->x[i] = vadd(p->x[i], vmul(vnew, dt));
+        p->F[i] = mmul(madd(mident(), mscale(L, dt)), p->F[i]);
+        update_stress(st, i, &inverted);
+    }
+    if (stats) {
+        stats->inverted_f = inverted;
+        stats->projection_failures = 0;
+    }
+    return MPMB_OK;
+}
+
 /* ref: solvers.hpp:141-198 */
 mpmb_status mpmor_step_mls(mpmor_state st, float dt, const float gr[3], int32_t contact,
                            int32_t bc, mpmb_step_stats* stats) {
@@ -1492,6 +1546,8 @@ mpmb_status mpmor_scene_advance(mpmor_scene s, float dt) {
         if (pb)
             mpmor_step_pbmpm(&s->st, dt_sub, s->cfg.gravity, s->cfg.iterations, 1,
                              s->cfg.boundary, &stt);
+        else if (s->cfg.solver == MPMB_SOLVER_STANDARD)  /* scene.hpp:200-203 */
+            mpmor_step_standard(&s->st, dt_sub, s->cfg.gravity, 1, s->cfg.boundary, &stt);
         else
             mpmor_step_mls(&s->st, dt_sub, s->cfg.gravity, 1, s->cfg.boundary, &stt);
         s->inverted += stt.inverted_f;

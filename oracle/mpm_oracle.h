@@ -40,6 +40,8 @@ mpmb_status mpmor_state_get_shape_poses(mpmor_state st, mpmb_pose* out, int32_t 
 mpmb_status mpmor_state_get_contact(mpmor_state st, float* imp, float* tq, int32_t* cnt,
                                     int32_t n);
 mpmb_status mpmor_state_reset_contact(mpmor_state st);
+mpmb_status mpmor_step_standard(mpmor_state st, float dt, const float g[3], int32_t contact,
+                                int32_t boundary, mpmb_step_stats* stats);
 mpmb_status mpmor_step_mls(mpmor_state st, float dt, const float g[3], int32_t contact,
                            int32_t bc, mpmb_step_stats* stats);
 mpmb_status mpmor_step_pbmpm(mpmor_state st, float dt, const float g[3], int32_t iterations,

@@ -267,6 +267,17 @@ mpmb_status mpmref_step_mls(void* st, float dt, const float g[3], int32_t contac
     return MPMB_OK;
 }
 
+mpmb_status mpmref_step_standard(void* st, float dt, const float g[3], int32_t contact, int32_t bc,
+                                 mpmb_step_stats* stats) {
+    auto* s = static_cast<RefState*>(st);
+    GridHook hook = nullptr;
+    if (contact) hook = [s](Grid& grid) { apply_contact_pass(grid, s->shapes, s->acc); };
+    StepStats r = step_standard(s->sim, dt, v3(g), hook,
+                                bc == MPMB_BC_STICKY ? BoundaryKind::sticky : BoundaryKind::slip);
+    if (stats) { stats->inverted_f = r.inverted_f; stats->projection_failures = r.projection_failures; }
+    return MPMB_OK;
+}
+
 mpmb_status mpmref_step_pbmpm(void* st, float dt, const float g[3], int32_t iters,
                               int32_t contact, int32_t bc, mpmb_step_stats* stats) {
     auto* s = static_cast<RefState*>(st);

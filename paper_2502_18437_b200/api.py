@@ -208,6 +208,13 @@ class SolverState:
               self.lib, "step_mls")
         return st.inverted_f, st.projection_failures
 
+    def step_standard(self, dt, g=(0.0, 0.0, 0.0), contact=False, bc=capi.BC_SLIP):
+        st = capi.StepStats()
+        gg = np.array(g, F32)
+        check(self._f("step_standard")(self.h, float(F32(dt)), _fp(gg), int(contact), bc, C.byref(st)),
+              self.lib, "step_standard")
+        return st.inverted_f, st.projection_failures
+
     def step_pbmpm(self, dt, g=(0.0, 0.0, 0.0), iterations=10, contact=False, bc=capi.BC_SLIP):
         st = capi.StepStats()
         gg = np.array(g, F32)

@@ -106,6 +106,7 @@ STATE_API = {
     "step_mls": (C.c_int, [P, C.c_float, fp, C.c_int32, C.c_int32, C.POINTER(StepStats)]),
     "step_pbmpm": (C.c_int, [P, C.c_float, fp, C.c_int32, C.c_int32, C.c_int32,
                              C.POINTER(StepStats)]),
+    "step_standard": (C.c_int, [P, C.c_float, fp, C.c_int32, C.c_int32, C.POINTER(StepStats)]),
     "particle_pushout": (C.c_int, [P, ip]),
     "deactivate_out_of_domain": (C.c_int, [P, ip]),
     "integrate_free_bodies": (C.c_int, [P, fp, C.c_float]),

@@ -477,6 +477,20 @@ extern "C" mpmb_status mpmb_step_mls(mpmb_state st, float dt, const float g[3], 
     });
 }
 
+extern "C" mpmb_status mpmb_step_standard(mpmb_state st, float dt, const float g[3], int32_t contact,
+                                          int32_t bc, mpmb_step_stats* stats) {
+    return guarded([&] {
+        Engine& e = *S(st)->eng;
+        e.reset_counters();
+        e.bin();
+        e.p2g(true, dt, true, true);
+        e.grid_update(0, dt, g, true, contact != 0, bc);
+        e.g2p_standard(0, dt, false, false);
+        fill_stats(e, stats);
+        return MPMB_OK;
+    });
+}
+
 extern "C" mpmb_status mpmb_step_pbmpm(mpmb_state st, float dt, const float g[3], int32_t iters,
                                        int32_t contact, int32_t bc, mpmb_step_stats* stats) {
     return guarded([&] {
@@ -852,9 +866,11 @@ void run_frame(Batch& b, float dt) {
                 b.since_sort = 0;
             }
             ++b.since_sort;
-            e.p2g(true, dt_sub);
+            const bool standard = cfg.solver == MPMB_SOLVER_STANDARD;  // scene.hpp:200-207
+            e.p2g(true, dt_sub, true, standard);
             e.grid_update(sub, dt_sub, cfg.gravity, true, true, cfg.boundary);
-            e.g2p_mls(sub, dt_sub, true, true);
+            if (standard) e.g2p_standard(sub, dt_sub, true, true);
+            else e.g2p_mls(sub, dt_sub, true, true);
             if (ns > 0) e.free_bodies(sub, dt_sub, cfg.gravity, any_free, true);
         }
     } else {

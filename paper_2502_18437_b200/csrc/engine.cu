@@ -605,7 +605,7 @@ void Engine::bin() {
     I.end(CAT_SORT, ev);
 }
 
-void Engine::p2g(bool mls, float dt, bool collect) {
+void Engine::p2g(bool mls, float dt, bool collect, bool standard) {
     Impl& I = *impl_;
     if (I.n_cap == 0) return;
     if (!I.binned) bin();
@@ -613,13 +613,13 @@ void Engine::p2g(bool mls, float dt, bool collect) {
     cudaMemsetAsync(I.misc.p, 0, sizeof(uint32_t), I.st);  // active brick count
     Params P = I.params();
     P.dt = dt;
-    launch_p2g(P, mls, (I.n + kGroup - 1) / kGroup, I.st);
+    launch_p2g(P, mls || standard, (I.n + kGroup - 1) / kGroup, I.st, standard);
     I.counted(1);
     if (collect) {
         launch_collect_bricks(P, I.total_bricks, I.st);
         I.counted(1);
     }
-    if (mls) I.use_stress_in = false;  // consumed by the first MLS P2G
+    if (mls || standard) I.use_stress_in = false;  // consumed by the first stress-using P2G
     I.end(CAT_P2G, ev);
 }
 
@@ -658,6 +658,22 @@ void Engine::g2p_mls(int sub, float dt, bool pushout, bool deactivate) {
     launch_g2p(P, false, (I.n + kGroup - 1) / kGroup, I.st);
     I.counted(1);
     I.cur = 1 - I.cur;  // G2P wrote the group-sorted state into the other buffer
+    I.end(CAT_G2P, ev);
+}
+
+void Engine::g2p_standard(int sub, float dt, bool pushout, bool deactivate) {
+    Impl& I = *impl_;
+    if (I.n_cap == 0) return;
+    auto ev = I.begin();
+    Params P = I.params();
+    P.sub = std::min(sub, I.table_subs - 1);
+    P.dt = dt;
+    P.pushout = pushout ? 1 : 0;
+    P.deactivate = deactivate ? 1 : 0;
+    P.commit = 1;
+    launch_g2p(P, false, (I.n + kGroup - 1) / kGroup, I.st, true);
+    I.counted(1);
+    I.cur = 1 - I.cur;
     I.end(CAT_G2P, ev);
 }
 

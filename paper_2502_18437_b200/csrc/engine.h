@@ -90,10 +90,12 @@ class Engine {
 
     // ---- hot path (enqueue only) ----
     void bin();                                   // K1: keys, stable sort, gather
-    void p2g(bool mls, float dt, bool collect = true);  // K2 / K5 (+ active-brick list)
+    // K2 / K5 (+ active-brick list); standard: the standard-MPM force transfer (mls = true)
+    void p2g(bool mls, float dt, bool collect = true, bool standard = false);
     void collect_bricks();
     void grid_update(int sub, float dt, const float g[3], bool gravity, bool contact, int bc);
     void g2p_mls(int sub, float dt, bool pushout, bool deactivate);   // K4
+    void g2p_standard(int sub, float dt, bool pushout, bool deactivate);  // K4, PIC (solvers.hpp:107-135)
     void g2p_pb(int sub, float dt, bool commit, bool pushout, bool deactivate);  // K6
     void free_bodies(int sub, float dt, const float g[3], bool integrate, bool merge);  // K7
     void bc_pass(int bc);                         // BC alone (hook adapter)

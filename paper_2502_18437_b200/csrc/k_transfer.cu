@@ -201,6 +201,44 @@ __device__ __forceinline__ void p2g_nodes(const float w[3][3], const float rel[3
     }
 }
 
+// Standard MPM (solvers.hpp:96-103): momentum += v (w m) + M grad w, mass += w m, with the
+// impulse matrix M = -dt V sigma and grad w = (dw_x w_y w_z, w_x dw_y w_z, w_x w_y dw_z).
+// Per row (dj, dk): a = w_y w_z, b = dw_y w_z, c = w_y dw_z, U = m v a + M_col1 b + M_col2 c,
+// G = M_col0 a; per node: w_x U + dw_x G -- the FFMA2 shape of p2g_nodes.
+__device__ __forceinline__ void p2g_nodes_std(const float w[3][3], const float dw[3][3], const float M[9], float m,
+                                              const float v[3], float2 (&pa)[27], float2 (&pb)[27]) {
+    const float2 M0_01 = f2(M[0], M[3]), M0_2m = f2(M[6], 0.f);
+    const float2 M1_01 = f2(M[1], M[4]), M1_2m = f2(M[7], 0.f);
+    const float2 M2_01 = f2(M[2], M[5]), M2_2m = f2(M[8], 0.f);
+    const float2 mv01 = f2(v[0] * m, v[1] * m), mv2m = f2(v[2] * m, m);
+#pragma unroll
+    for (int dk = 0; dk < 3; ++dk)
+#pragma unroll
+        for (int dj = 0; dj < 3; ++dj) {
+            const float a = w[1][dj] * w[2][dk], b = dw[1][dj] * w[2][dk], c = w[1][dj] * dw[2][dk];
+            const float2 U01 = __ffma2_rn(M2_01, f2(c, c), __ffma2_rn(M1_01, f2(b, b), __fmul2_rn(mv01, f2(a, a))));
+            const float2 U2m = __ffma2_rn(M2_2m, f2(c, c), __ffma2_rn(M1_2m, f2(b, b), __fmul2_rn(mv2m, f2(a, a))));
+            const float2 G01 = __fmul2_rn(M0_01, f2(a, a));
+            const float2 G2m = __fmul2_rn(M0_2m, f2(a, a));
+#pragma unroll
+            for (int di = 0; di < 3; ++di) {
+                const int n = (dk * 3 + dj) * 3 + di;
+                const float wx = w[0][di], dx = dw[0][di];
+                pa[n] = __ffma2_rn(f2(wx, wx), U01, pa[n]);
+                pa[n] = __ffma2_rn(f2(dx, dx), G01, pa[n]);
+                pb[n] = __ffma2_rn(f2(wx, wx), U2m, pb[n]);  // .y: mass += w m
+                pb[n] = __ffma2_rn(f2(dx, dx), G2m, pb[n]);
+            }
+        }
+}
+
+// quadratic B-spline weight derivatives (math.hpp:229-231)
+__device__ __forceinline__ void bspline_dw(float fx, float inv_dx, float dw[3]) {
+    dw[0] = (fx - 1.5f) * inv_dx;
+    dw[1] = -2.f * (fx - 1.f) * inv_dx;
+    dw[2] = (fx - 0.5f) * inv_dx;
+}
+
 // Active-brick list from the P2G marks (warp-aggregated append; order is irrelevant).
 // Marks are reset here, so the next P2G starts from a clean slate.
 __global__ void __launch_bounds__(256) k_collect_bricks(const Params P, uint32_t n_bricks) {
@@ -320,7 +358,9 @@ __device__ __forceinline__ uint64_t group_sort(const Params& P, uint32_t g, uint
     return mine;
 }
 
-template <bool MLS>
+// MLS: stress impulse from F (MLS-MPM, solvers.hpp:151-169; with STD: standard MPM's force
+// transfer, solvers.hpp:88-104); !MLS: PB-MPM (A = m C, solvers.hpp:218-235)
+template <bool MLS, bool STD = false>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_p2g(const __grid_constant__ Params P) {
     extern __shared__ float4 smem[];
     constexpr int NP = kPlanes;
@@ -381,27 +421,38 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_p2g(cons
                     const float4 mat = material(P, flags & kMatMask);
                     J = neo_hookean_f32(F, mat.y, mat.z, sig);
                 }
-                const float sc = -P.dt * (J * r.y) * S.m_inv;
+                if (STD) {  // impulse_m = sigma (-dt V), V = det(F) V0 (solvers.hpp:91-92)
+                    const float sc = -P.dt * (J * r.y);
 #pragma unroll
-                for (int i = 0; i < 9; ++i) A[i] = fmaf(Cm[i], m, sig[i] * sc);
+                    for (int i = 0; i < 9; ++i) A[i] = sig[i] * sc;
+                } else {
+                    const float sc = -P.dt * (J * r.y) * S.m_inv;
+#pragma unroll
+                    for (int i = 0; i < 9; ++i) A[i] = fmaf(Cm[i], m, sig[i] * sc);
+                }
             } else {
 #pragma unroll
                 for (int i = 0; i < 9; ++i) A[i] = Cm[i] * m;
             }
-            float w[3][3], rel[3][3];
+            float w[3][3], rel[3][3];  // STD: rel holds the weight derivatives
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
                 bspline_w(fx[a], w[a]);
+                if (STD) {
+                    bspline_dw(fx[a], S.inv_dx, rel[a]);
+                } else {
 #pragma unroll
-                for (int o = 0; o < 3; ++o)  // node_position - x (state.hpp:49-51)
-                    rel[a][o] = node_coord(P.geo, a, b[a] + o) - x[a];
+                    for (int o = 0; o < 3; ++o)  // node_position - x (state.hpp:49-51)
+                        rel[a][o] = node_coord(P.geo, a, b[a] + o) - x[a];
+                }
             }
             if (b[0] != cb[0] || b[1] != cb[1] || b[2] != cb[2] || scene != cscene) {
                 if (cscene >= 0) p2g_flush(P, scene_view(P, cscene), cb, pa, pb);
                 cb[0] = b[0]; cb[1] = b[1]; cb[2] = b[2];
                 cscene = scene;
             }
-            p2g_nodes(w, rel, A, m, v, pa, pb);
+            if (STD) p2g_nodes_std(w, rel, A, m, v, pa, pb);
+            else p2g_nodes(w, rel, A, m, v, pa, pb);
         }
         if (cscene >= 0) p2g_flush(P, scene_view(P, cscene), cb, pa, pb);
         cp_wait<0>();
@@ -461,6 +512,51 @@ __device__ __forceinline__ void g2p_gather(const float4* g, uint32_t px, uint32_
     B[0] = c0_01.x; B[1] = c1_01.x; B[2] = c2_01.x;
     B[3] = c0_01.y; B[4] = c1_01.y; B[5] = c2_01.y;
     B[6] = c0_2;    B[7] = c1_2;    B[8] = c2_2;
+}
+
+// Standard MPM gather (solvers.hpp:112-128): v = sum w v_I, L = sum v_I (x) grad w, the
+// same separable row sums as g2p_gather with dw_x in place of w_x r_x and the row factors
+// (w_y w_z, dw_y w_z, w_y dw_z) for the three gradient columns.
+__device__ __forceinline__ void g2p_gather_std(const float4* g, uint32_t px, uint32_t pxy, const float w[3][3],
+                                               const float dw[3][3], float vn[3], float L[9]) {
+    float2 v01 = f2(0.f, 0.f);
+    float v2 = 0.f;
+    float2 c0_01 = f2(0.f, 0.f), c1_01 = f2(0.f, 0.f), c2_01 = f2(0.f, 0.f);
+    float c0_2 = 0.f, c1_2 = 0.f, c2_2 = 0.f;
+#pragma unroll
+    for (int dk = 0; dk < 3; ++dk) {
+        float4 q[9];
+#pragma unroll
+        for (int n = 0; n < 9; ++n) q[n] = __ldg(g + (dk * pxy + (n / 3) * px) + (n % 3));
+#pragma unroll
+        for (int dj = 0; dj < 3; ++dj) {
+            float2 a01 = f2(0.f, 0.f), d01 = f2(0.f, 0.f);
+            float a2 = 0.f, d2 = 0.f;
+#pragma unroll
+            for (int di = 0; di < 3; ++di) {
+                const float4 nq = q[dj * 3 + di];
+                const float wx = w[0][di], dx = dw[0][di];
+                a01 = __ffma2_rn(f2(wx, wx), f2(nq.x, nq.y), a01);
+                d01 = __ffma2_rn(f2(dx, dx), f2(nq.x, nq.y), d01);
+                a2 = fmaf(wx, nq.z, a2);
+                d2 = fmaf(dx, nq.z, d2);
+            }
+            const float wyz = w[1][dj] * w[2][dk];
+            const float gy = dw[1][dj] * w[2][dk], gz = w[1][dj] * dw[2][dk];
+            v01 = __ffma2_rn(f2(wyz, wyz), a01, v01);
+            v2 = fmaf(wyz, a2, v2);
+            c0_01 = __ffma2_rn(f2(wyz, wyz), d01, c0_01);  // column 0: dw_x w_y w_z
+            c0_2 = fmaf(wyz, d2, c0_2);
+            c1_01 = __ffma2_rn(f2(gy, gy), a01, c1_01);    // column 1: w_x dw_y w_z
+            c1_2 = fmaf(gy, a2, c1_2);
+            c2_01 = __ffma2_rn(f2(gz, gz), a01, c2_01);    // column 2: w_x w_y dw_z
+            c2_2 = fmaf(gz, a2, c2_2);
+        }
+    }
+    vn[0] = v01.x; vn[1] = v01.y; vn[2] = v2;
+    L[0] = c0_01.x; L[1] = c1_01.x; L[2] = c2_01.x;
+    L[3] = c0_01.y; L[4] = c1_01.y; L[5] = c2_01.y;
+    L[6] = c0_2;    L[7] = c1_2;    L[8] = c2_2;
 }
 
 // Push-out of one particle against the scene's shapes, in order (contact.hpp:140-179).
@@ -537,10 +633,12 @@ __device__ __forceinline__ void update_F(const float C[9], float dt, float F[9])
     for (int i = 0; i < 9; ++i) F[i] = Fn[i];
 }
 
-template <bool PB>
+// PB: PB-MPM (solvers.hpp:240-277); STD: standard MPM, PIC velocity + L (solvers.hpp:107-135,
+// C travels unchanged); neither: MLS-MPM (solvers.hpp:173-196)
+template <bool PB, bool STD = false>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(const __grid_constant__ Params P) {
     extern __shared__ float4 smem[];
-    constexpr int NP = PB ? 7 : 5;
+    constexpr int NP = (PB || STD) ? 7 : 5;
     const int lane = threadIdx.x & 31;
     const uint32_t n_groups = *P.n_groups;
     const uint32_t wpb = blockDim.x >> 5;
@@ -596,7 +694,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(cons
             {
                 const float4 q0 = src[0];
                 p.x[0] = q0.x; p.x[1] = q0.y; p.x[2] = q0.z;
-                if (PB) {
+                if (PB || STD) {
                     const float4 q1 = src[32], q2 = src[64], q3 = src[96], q4 = src[128], q5 = src[160];
                     p.C[0] = q1.z; p.C[1] = q1.w; p.C[2] = q2.x; p.C[3] = q2.y; p.C[4] = q2.z;
                     p.C[5] = q2.w; p.C[6] = q3.x; p.C[7] = q3.y; p.C[8] = q3.z;
@@ -614,22 +712,29 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(cons
             int b[3];
             float fx[3];
             local_base(P.geo, p.x, b, fx);
-            float w[3][3], rel[3][3];
+            float w[3][3], rel[3][3];  // STD: rel holds the weight derivatives
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
                 bspline_w(fx[a], w[a]);
+                if (STD) {
+                    bspline_dw(fx[a], S.inv_dx, rel[a]);
+                } else {
 #pragma unroll
-                for (int o = 0; o < 3; ++o)
-                    rel[a][o] = node_coord(P.geo, a, b[a] + o) - p.x[a];
+                    for (int o = 0; o < 3; ++o)
+                        rel[a][o] = node_coord(P.geo, a, b[a] + o) - p.x[a];
+                }
             }
-            float B[9];
+            float B[9];  // STD: the velocity gradient L
             {
                 uint32_t base, px, pxy;
                 stencil_rows(P.geo, b, base, px, pxy);
-                g2p_gather(P.grid_vel + S.node_base + base, px, pxy, w, rel, p.v, B);
+                if (STD) g2p_gather_std(P.grid_vel + S.node_base + base, px, pxy, w, rel, p.v, B);
+                else g2p_gather(P.grid_vel + S.node_base + base, px, pxy, w, rel, p.v, B);
             }
             bool do_commit;
-            if (!PB) {  // solvers.hpp:191-195
+            if (STD) {  // solvers.hpp:130-134: x += v dt, F = (I + L dt) F; C unchanged
+                do_commit = true;
+            } else if (!PB) {  // solvers.hpp:191-195
 #pragma unroll
                 for (int i = 0; i < 9; ++i) p.C[i] = B[i] * S.m_inv;
                 do_commit = true;
@@ -650,7 +755,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(cons
                 p.x[0] = FA(p.x[0], FM(p.v[0], P.dt));
                 p.x[1] = FA(p.x[1], FM(p.v[1], P.dt));
                 p.x[2] = FA(p.x[2], FM(p.v[2], P.dt));
-                update_F(p.C, P.dt, p.F);
+                update_F(STD ? B : p.C, P.dt, p.F);
                 if (det3(p.F) <= 0.f) ++n_inv;
                 if (P.pushout) {
                     if (scene != cs_scene) {  // per-lane cache of the scene's shape range
@@ -741,45 +846,44 @@ static int grid_for(int64_t work, int threads, int max_blocks) {
     return static_cast<int>(b);
 }
 
-// dynamic shared memory per block: 4 warps x 3 stages x <=7 planes x 32 x 16 B <= 43 KB
-// (below the 48 KB default, no opt-in attribute needed)
-void launch_p2g(const Params& P, bool mls, int64_t max_groups, cudaStream_t st) {
+// dynamic shared memory per block: warps x stages x planes x 32 lanes x 16 B; kernels above
+// 48 KB opt in once
+template <class K>
+static void opt_in_smem(K kernel, int bytes) {
+    if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+void launch_p2g(const Params& P, bool mls, int64_t max_groups, cudaStream_t st, bool standard) {
     const int threads = kWarpsPerBlock * 32;
     const int smem = kWarpsPerBlock * kStages * kPlanes * 32 * static_cast<int>(sizeof(float4));
     const int blocks = grid_for(max_groups * 32, threads, 148 * 16);
     static bool attr = false;
-    if (!attr) {  // > 48 KB of dynamic shared memory needs the opt-in
-        cudaFuncSetAttribute(k_p2g<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(k_p2g<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (!attr) {
+        opt_in_smem(k_p2g<true>, smem);
+        opt_in_smem(k_p2g<false>, smem);
+        opt_in_smem(k_p2g<true, true>, smem);
         attr = true;
     }
-    if (mls) {
-        k_p2g<true><<<blocks, threads, smem, st>>>(P);
-    } else {
-        k_p2g<false><<<blocks, threads, smem, st>>>(P);
-    }
+    if (standard) k_p2g<true, true><<<blocks, threads, smem, st>>>(P);
+    else if (mls) k_p2g<true><<<blocks, threads, smem, st>>>(P);
+    else k_p2g<false><<<blocks, threads, smem, st>>>(P);
 }
 
-void launch_g2p(const Params& P, bool pb, int64_t max_groups, cudaStream_t st) {
+void launch_g2p(const Params& P, bool pb, int64_t max_groups, cudaStream_t st, bool standard) {
     const int threads = kWarpsPerBlock * 32;
     const int blocks = grid_for(max_groups * 32, threads, 148 * 16);
-    if (pb) {
-        const int smem = kWarpsPerBlock * kG2PStages * 7 * 32 * static_cast<int>(sizeof(float4));
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k_g2p<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-            attr = true;
-        }
-        k_g2p<true><<<blocks, threads, smem, st>>>(P);
-    } else {
-        const int smem = kWarpsPerBlock * kG2PStages * 5 * 32 * static_cast<int>(sizeof(float4));
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k_g2p<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-            attr = true;
-        }
-        k_g2p<false><<<blocks, threads, smem, st>>>(P);
+    const int smem7 = kWarpsPerBlock * kG2PStages * 7 * 32 * static_cast<int>(sizeof(float4));
+    const int smem5 = kWarpsPerBlock * kG2PStages * 5 * 32 * static_cast<int>(sizeof(float4));
+    static bool attr = false;
+    if (!attr) {
+        opt_in_smem(k_g2p<true>, smem7);
+        opt_in_smem(k_g2p<false, true>, smem7);
+        opt_in_smem(k_g2p<false>, smem5);
+        attr = true;
     }
+    if (standard) k_g2p<false, true><<<blocks, threads, smem7, st>>>(P);
+    else if (pb) k_g2p<true><<<blocks, threads, smem7, st>>>(P);
+    else k_g2p<false><<<blocks, threads, smem5, st>>>(P);
 }
 
 void launch_pushout(const Params& P, cudaStream_t st) {

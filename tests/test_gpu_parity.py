@@ -80,6 +80,30 @@ def test_mls_single_step_grid_and_particles():
     assert np.abs(a["stress"] - b["stress"]).max() <= 1e-4 * np.abs(a["stress"]).max() + 1e-6
 
 
+def test_standard_single_step():
+    """step_standard (solvers.hpp:80-138): PIC + nodal force; same tolerances as MLS."""
+    p = block_particles()
+    rng = np.random.default_rng(12)
+    p["v"] = rng.uniform(-0.1, 0.1, p["v"].shape).astype(F32)
+    p["F"] += rng.uniform(-0.02, 0.02, p["F"].shape).astype(F32)
+    p["C"] = rng.uniform(-0.5, 0.5, p["C"].shape).astype(F32)
+    o, g = pair((24, 24, 24), 0.05, p, NEO)
+    for s in (o, g):
+        for _ in range(3):
+            s.step_standard(0.002, (0.0, -9.81, 0.0))
+    mo, _, vo = o.grid()
+    mg, _, vg = g.grid()
+    assert np.abs(mo - mg).max() <= 1e-6 * mo.max()
+    live = mo > 1e-9
+    assert np.abs(vo[live] - vg[live]).max() <= 1e-5 * np.abs(vo[live]).max() + 1e-7
+    a, b = o.get_particles(), g.get_particles()
+    assert np.abs(a["x"] - b["x"]).max() <= 1e-5 * 0.05
+    assert np.abs(a["v"] - b["v"]).max() <= 1e-5 * np.abs(a["v"]).max() + 1e-7
+    assert np.array_equal(a["C"], b["C"])  # standard MPM leaves C alone
+    assert np.abs(a["F"] - b["F"]).max() <= 1e-4 * np.abs(a["F"]).max()
+    assert np.abs(a["stress"] - b["stress"]).max() <= 1e-4 * np.abs(a["stress"]).max() + 1e-6
+
+
 def test_pbmpm_single_step():
     p = block_particles()
     rng = np.random.default_rng(3)
@@ -124,6 +148,7 @@ def _scene_pair(spec):
 @pytest.mark.parametrize("name,spec_fn,frames", [
     ("cube_drop", scenes.cube_drop, 5),
     ("cube_drop_pbmpm", lambda: scenes.cube_drop(solver="pbmpm"), 3),
+    ("cube_drop_standard", lambda: scenes.cube_drop(solver="standard"), 5),
     ("cutting", scenes.cutting, 5),
     ("needle_lateral", lambda: scenes.needle(True), 3),
     ("mesh_slicer", scenes.mesh_slicer_scene, 4),

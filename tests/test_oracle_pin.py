@@ -54,6 +54,8 @@ def run_solver_case_on(kind, backend):
     for _ in range(3):
         if kind == "pbmpm":
             stats.append(s.step_pbmpm(0.01, grav, iterations=4, contact=True))
+        elif kind == "standard":
+            stats.append(s.step_standard(0.002, grav, contact=True))
         else:
             stats.append(s.step_mls(0.002, grav, contact=True))
         stats.append((s.pushout(), s.deactivate()))
@@ -61,7 +63,7 @@ def run_solver_case_on(kind, backend):
     return g, s, np.array(stats, np.int32)
 
 
-@pytest.mark.parametrize("kind", ["mls", "pbmpm"])
+@pytest.mark.parametrize("kind", ["mls", "pbmpm", "standard"])
 def test_golden_solver_sequence_reproduced_bitwise(kind):
     g, s, stats = run_solver_case_on(kind, "oracle")
     out = s.get_particles()
@@ -108,6 +110,7 @@ def test_golden_scene_reproduced_bitwise(name):
     ("needle_tangent", lambda: scenes.needle(False)),
     ("suture_pbmpm_thread", lambda: scenes.suture(solver="pbmpm", n_thread=4)),
     ("cutting_blunt_like", lambda: scenes.cutting(blade_dx=0.02)),
+    ("cube_drop_standard", lambda: scenes.cube_drop(solver="standard")),
 ])
 def test_oracle_vs_reference_live(name, fn):
     spec = fn()

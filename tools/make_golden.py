@@ -63,6 +63,8 @@ def solver_case(kind):
     for _ in range(3):
         if kind == "pbmpm":
             stats.append(s.step_pbmpm(0.01, g, iterations=4, contact=True))
+        elif kind == "standard":
+            stats.append(s.step_standard(0.002, g, contact=True))
         else:
             stats.append(s.step_mls(0.002, g, contact=True))
         stats.append((s.pushout(), s.deactivate()))
@@ -83,6 +85,7 @@ def solver_case(kind):
 SCENE_CASES = {
     "cube_drop": (scenes.cube_drop, 3),
     "cube_drop_pbmpm": (lambda: scenes.cube_drop(solver="pbmpm"), 2),
+    "cube_drop_standard": (lambda: scenes.cube_drop(solver="standard"), 3),
     "cutting": (scenes.cutting, 3),
     "needle_lateral": (lambda: scenes.needle(True), 2),
     "rigid_coupling": (scenes.rigid_coupling, 3),
@@ -110,7 +113,7 @@ def scene_case(name):
 
 def main():
     OUT.mkdir(parents=True, exist_ok=True)
-    for kind in ("mls", "pbmpm"):
+    for kind in ("mls", "pbmpm", "standard"):
         np.savez_compressed(OUT / f"solver_{kind}.npz", **solver_case(kind))
         print("wrote", OUT / f"solver_{kind}.npz")
     for name in SCENE_CASES:
