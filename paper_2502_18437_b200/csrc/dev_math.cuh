@@ -338,11 +338,15 @@ __device__ __forceinline__ V3 closest_on_triangle(V3 a, V3 b, V3 c, V3 p) {
 }
 
 // False when the point is provably outside every contact / push-out band of the shape
-// (DevShape::bound2); the reference's query would return no effect there.
+// (DevShape::lbox, tested in the shape's frame); the reference's query would return no
+// effect there.  The substep pipeline uses the precomputed world boxes (cull_may_touch).
 __device__ __forceinline__ bool shape_may_touch(const DevShape& g, const DevPose& pose, V3 point) {
-    if (g.bound2 < 0.f) return true;
-    const float dx = point.x - pose.pos[0], dy = point.y - pose.pos[1], dz = point.z - pose.pos[2];
-    return fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= g.bound2;
+    if (g.lbox_h[0] < 0.f) return true;
+    Q4 q{pose.rot[0], pose.rot[1], pose.rot[2], pose.rot[3]};
+    const V3 p = qrotate_inv(q, point - mk(pose.pos[0], pose.pos[1], pose.pos[2]));
+    const float m = 1.001f;
+    return fabsf(p.x - g.lbox_c[0]) <= g.lbox_h[0] * m + 1e-5f && fabsf(p.y - g.lbox_c[1]) <= g.lbox_h[1] * m + 1e-5f &&
+           fabsf(p.z - g.lbox_c[2]) <= g.lbox_h[2] * m + 1e-5f;
 }
 
 // World-space SDF query (geometry.hpp:370-395) against one device shape.

@@ -70,10 +70,11 @@ struct DevShape {
     float mu_k, c_d, hw, body_mass;
     float inertia[3];
     int scene;
-    // squared radius around the pose origin outside which the shape can neither contact a
-    // node nor push a particle (every region's band included, conservative margin); < 0
-    // for unbounded shapes (plane).  A cull, never a change of result.
-    float bound2;
+    // local-frame box (center, half extents) outside which the shape can neither contact a
+    // node nor push a particle (every region's band included, conservative margin);
+    // lbox_h[0] < 0 for unbounded shapes (plane).  A cull, never a change of result.
+    float lbox_c[3];
+    float lbox_h[3];
 };
 
 // mpm::ShapePose (geometry.hpp:14-27), padded to 64 B.

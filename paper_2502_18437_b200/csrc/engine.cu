@@ -62,29 +62,57 @@ enum Cat { CAT_SORT = 0, CAT_P2G, CAT_GRID, CAT_G2P, CAT_OTHER };
 
 }  // namespace
 
-// DevShape::bound2: the largest |p| (local frame) at which any region of the shape can
-// still act -- contact bands use hw, push-out bands 0.5 hw (contact.hpp:82-92, 140-179) --
-// plus a relative margin for the float rotation.  Planes are unbounded.
-float shape_bound2(const DevShape& d, const std::vector<float>& verts) {
-    double r = -1.0;
-    double vmax = 0.0;
-    for (size_t i = 0; i + 2 < verts.size(); i += 3)
-        vmax = std::max(vmax, std::sqrt(double(verts[i]) * verts[i] + double(verts[i + 1]) * verts[i + 1] +
-                                        double(verts[i + 2]) * verts[i + 2]));
+// DevShape::lbox: the local-frame box holding every point where a region of the shape can
+// still act -- contact bands use hw, push-out bands 0.5 hw (contact.hpp:82-92, 140-179),
+// spines their radius -- with a relative margin for the float rotation.  Planes are
+// unbounded.
+void shape_lbox(DevShape& d, const std::vector<float>& verts) {
+    double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
     const double hw = std::max(0.0, double(d.hw));
+    auto vbox = [&](double pad) {
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = 1e300;
+            hi[a] = -1e300;
+        }
+        for (size_t i = 0; i + 2 < verts.size(); i += 3)
+            for (int a = 0; a < 3; ++a) {
+                lo[a] = std::min(lo[a], double(verts[i + a]));
+                hi[a] = std::max(hi[a], double(verts[i + a]));
+            }
+        for (int a = 0; a < 3; ++a) {
+            lo[a] -= pad;
+            hi[a] += pad;
+        }
+    };
+    auto sym = [&](double x, double y, double z) {
+        lo[0] = -x; lo[1] = -y; lo[2] = -z;
+        hi[0] = x; hi[1] = y; hi[2] = z;
+    };
     switch (d.geom) {
-        case GEOM_PLANE: return -1.f;
-        case GEOM_SPHERE: r = d.gp[0]; break;
-        case GEOM_BOX: r = std::sqrt(double(d.gp[0]) * d.gp[0] + double(d.gp[1]) * d.gp[1] + double(d.gp[2]) * d.gp[2]); break;
-        case GEOM_QUAD_SLICER:
-            r = std::sqrt(double(d.gp[0]) * d.gp[0] + double(d.gp[1]) * d.gp[1]) + std::max(double(d.gp[2]), hw);
+        case GEOM_PLANE:
+            d.lbox_h[0] = d.lbox_h[1] = d.lbox_h[2] = -1.f;
+            d.lbox_c[0] = d.lbox_c[1] = d.lbox_c[2] = 0.f;
+            return;
+        case GEOM_SPHERE: sym(d.gp[0], d.gp[0], d.gp[0]); break;
+        case GEOM_BOX: sym(d.gp[0], d.gp[1], d.gp[2]); break;
+        case GEOM_QUAD_SLICER: {  // spine along x at y = hh (radius sr), blade plane z = 0
+            const double hl = d.gp[0], hh = d.gp[1], sr = d.gp[2], b = std::max(sr, hw);
+            lo[0] = -(hl + sr); hi[0] = hl + sr;
+            lo[1] = -hh; hi[1] = hh + sr;
+            lo[2] = -b; hi[2] = b;
             break;
-        case GEOM_TRI_MESH_SLICER: r = vmax + std::max(double(d.gp[0]), hw); break;
-        case GEOM_ARC: r = double(d.gp[0]) + hw; break;
-        default: r = vmax + hw; break;  // polyline
+        }
+        case GEOM_TRI_MESH_SLICER: vbox(std::max(double(d.gp[0]), hw)); break;
+        case GEOM_ARC: sym(double(d.gp[0]) + hw, double(d.gp[0]) + hw, hw); break;
+        default: vbox(hw); break;  // polyline
     }
-    r = r * 1.001 + 1e-5;
-    return static_cast<float>(r * r);
+    double ext = 0;
+    for (int a = 0; a < 3; ++a) ext = std::max(ext, std::max(std::fabs(lo[a]), std::fabs(hi[a])));
+    const double m = 1e-3 * ext + 1e-5;
+    for (int a = 0; a < 3; ++a) {
+        d.lbox_c[a] = static_cast<float>(0.5 * (lo[a] + hi[a]));
+        d.lbox_h[a] = static_cast<float>(0.5 * (hi[a] - lo[a]) + m);
+    }
 }
 
 bool device_available() {
@@ -510,7 +538,7 @@ void Engine::set_shapes(const std::vector<std::vector<EngineShape>>& per_scene) 
             d.spine_begin = static_cast<int>(ints.size());
             d.n_spine = static_cast<int>(e.spine.size());
             ints.insert(ints.end(), e.spine.begin(), e.spine.end());
-            d.bound2 = shape_bound2(d, e.verts);
+            shape_lbox(d, e.verts);
             ds.push_back(d);
             poses.push_back(e.pose);
         }
@@ -523,7 +551,7 @@ void Engine::set_shapes(const std::vector<std::vector<EngineShape>>& per_scene) 
     I.verts.alloc(sizeof(float) * std::max<size_t>(3, verts.size()));
     I.ints.alloc(sizeof(int) * std::max<size_t>(1, ints.size()));
     I.free_pose.alloc(sizeof(DevPose) * ns);
-    I.cull.alloc(sizeof(float4) * ns);
+    I.cull.alloc(2 * sizeof(float4) * ns);
     I.acc_sub.alloc(sizeof(double) * 6 * ns);
     I.acc_frame.alloc(sizeof(double) * 6 * ns);
     I.cnt_sub.alloc(sizeof(int) * ns);

@@ -18,12 +18,31 @@ __device__ __forceinline__ uint64_t brick_node(const Params& P, uint32_t gb, int
     return static_cast<uint64_t>(scene) * P.geo.nodes_per_scene + node_linear(P.geo, i, j, k);
 }
 
-// Per-substep shape cull table (one block): the pose position this substep (kinematic
-// table or integrated free pose) and the shape's bound2.
+// Per-substep shape cull table (one block): the world AABB of each shape's local box
+// (DevShape::lbox) under this substep's pose (kinematic table or integrated free pose):
+// cull[2i] = {min, bounded ? 1 : -1}, cull[2i+1] = {max, 0}.
 __global__ void k_shape_cull(const Params P) {
     for (int i = threadIdx.x; i < P.n_shapes; i += blockDim.x) {
+        const DevShape& sh = P.shapes[i];
+        if (sh.lbox_h[0] < 0.f) {
+            P.cull[2 * i] = make_float4(0.f, 0.f, 0.f, -1.f);
+            P.cull[2 * i + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+            continue;
+        }
         const DevPose& pose = pose_of(P, i);
-        P.cull[i] = make_float4(pose.pos[0], pose.pos[1], pose.pos[2], P.shapes[i].bound2);
+        const float x = pose.rot[0], y = pose.rot[1], z = pose.rot[2], w = pose.rot[3];
+        const float R[3][3] = {{1.f - 2.f * (y * y + z * z), 2.f * (x * y - z * w), 2.f * (x * z + y * w)},
+                               {2.f * (x * y + z * w), 1.f - 2.f * (x * x + z * z), 2.f * (y * z - x * w)},
+                               {2.f * (x * z - y * w), 2.f * (y * z + x * w), 1.f - 2.f * (x * x + y * y)}};
+        float c[3], h[3];
+        for (int a = 0; a < 3; ++a) {
+            c[a] = pose.pos[a] + R[a][0] * sh.lbox_c[0] + R[a][1] * sh.lbox_c[1] + R[a][2] * sh.lbox_c[2];
+            // |R| h, widened for a not-quite-unit quaternion and float rounding
+            h[a] = (fabsf(R[a][0]) * sh.lbox_h[0] + fabsf(R[a][1]) * sh.lbox_h[1] + fabsf(R[a][2]) * sh.lbox_h[2]) *
+                       1.001f + 1e-5f;
+        }
+        P.cull[2 * i] = make_float4(c[0] - h[0], c[1] - h[1], c[2] - h[2], 1.f);
+        P.cull[2 * i + 1] = make_float4(c[0] + h[0], c[1] + h[1], c[2] + h[2], 0.f);
     }
 }
 

@@ -561,21 +561,19 @@ __device__ __forceinline__ void g2p_gather_std(const float4* g, uint32_t px, uin
 
 // Push-out of one particle against the scene's shapes, in order (contact.hpp:140-179).
 // Shapes [begin, begin + count) of the particle's scene, in order.  kCull: this substep's
-// cull table is valid (inside the substep pipeline, after the grid update; cull0 = its
-// entry for the first shape, cached per lane); the standalone push-out tests the shape
+// cull table is valid (inside the substep pipeline, after the grid update; lo0 / hi0 = the
+// first shape's world box, cached per lane); the standalone push-out tests the shape
 // directly.
 template <bool kCull>
 __device__ __forceinline__ int pushout_particle(const Params& P, const SceneView& S, float x[3], float v[3],
-                                                int begin, int count, float4 cull0) {
+                                                int begin, int count, float4 lo0, float4 hi0) {
     int pushed = 0;
     const float clearance = FM(1e-4f, S.dx);
     for (int si = begin; si < begin + count; ++si) {
         if (kCull) {
-            const float4 c = si == begin ? cull0 : P.cull[si];
-            if (c.w >= 0.f) {
-                const float dx = x[0] - c.x, dy = x[1] - c.y, dz = x[2] - c.z;
-                if (fmaf(dx, dx, fmaf(dy, dy, dz * dz)) > c.w) continue;
-            }
+            const bool near = si == begin ? aabb_may_touch(lo0, hi0, x[0], x[1], x[2])
+                                          : cull_may_touch(P, si, x[0], x[1], x[2]);
+            if (!near) continue;
         }
         const DevShape& sh = P.shapes[si];
         const DevPose& pose = pose_of(P, si);
@@ -668,7 +666,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(cons
         for (int k = 0; k < NS - 1; ++k) st.issue(P, k);
         int my_scene = 0;
         int cs_scene = -1, cs_begin = 0, cs_count = 0;
-        float4 cs_cull0 = make_float4(0.f, 0.f, 0.f, -1.f);
+        float4 cs_lo = make_float4(0.f, 0.f, 0.f, -1.f), cs_hi = cs_lo;
         int n_inv = 0, n_fail = 0, n_push = 0, n_deact = 0;
         for (int k = 0; k < kmax; ++k) {
             st.issue(P, k + NS - 1);
@@ -762,9 +760,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(cons
                         cs_scene = scene;
                         cs_begin = P.scenes[scene].shape_begin;
                         cs_count = P.scenes[scene].shape_count;
-                        if (cs_count > 0) cs_cull0 = P.cull[cs_begin];
+                        if (cs_count > 0) {
+                            cs_lo = P.cull[2 * cs_begin];
+                            cs_hi = P.cull[2 * cs_begin + 1];
+                        }
                     }
-                    if (cs_count > 0) n_push += pushout_particle<true>(P, S, p.x, p.v, cs_begin, cs_count, cs_cull0);
+                    if (cs_count > 0)
+                        n_push += pushout_particle<true>(P, S, p.x, p.v, cs_begin, cs_count, cs_lo, cs_hi);
                 }
                 if (P.deactivate && !spline_in_domain(mk(p.x[0], p.x[1], p.x[2]), S)) {
                     flags &= ~kActiveBit;
@@ -803,8 +805,9 @@ __global__ void k_pushout(const Params P) {
                 if (P.scenes[S.scene].shape_count > 0) {
                     float4 a = P.pl[0][s], b = P.pl[1][s];
                     float x[3] = {a.x, a.y, a.z}, v[3] = {a.w, b.x, b.y};
+                    const float4 none = make_float4(0.f, 0.f, 0.f, -1.f);
                     pushed = pushout_particle<false>(P, S, x, v, P.scenes[S.scene].shape_begin,
-                                                     P.scenes[S.scene].shape_count, make_float4(0.f, 0.f, 0.f, -1.f));
+                                                     P.scenes[S.scene].shape_count, none, none);
                     if (pushed) {
                         P.pl[0][s] = make_float4(x[0], x[1], x[2], v[0]);
                         P.pl[1][s] = make_float4(v[1], v[2], b.z, b.w);

@@ -51,7 +51,7 @@ struct Params {
     const DevPose* pose_table;
     const uint8_t* pose_override;
     DevPose* free_pose;
-    float4* cull;   // per shape, this substep: {pose position, bound2} (k_shape_cull)
+    float4* cull;   // per shape, this substep: world AABB {min, bounded}, {max, 0} (k_shape_cull)
     int n_shapes;
     const float4* mats;  // {kind, mu, lambda, beta}
     float4* grid_acc;
@@ -185,12 +185,12 @@ __device__ __forceinline__ void stencil_rows(const Geo& G, const int b[3], uint3
 }
 
 // Cheap reject before an SDF query: false when x is provably outside every band of shape
-// si at this substep (DevShape::bound2 around the pose position; bound2 < 0: unbounded).
+// si at this substep (the world AABB of DevShape::lbox; unbounded shapes never cull).
+__device__ __forceinline__ bool aabb_may_touch(float4 lo, float4 hi, float x, float y, float z) {
+    return lo.w < 0.f || (x >= lo.x && x <= hi.x && y >= lo.y && y <= hi.y && z >= lo.z && z <= hi.z);
+}
 __device__ __forceinline__ bool cull_may_touch(const Params& P, int si, float x, float y, float z) {
-    const float4 c = P.cull[si];
-    if (c.w < 0.f) return true;
-    const float dx = x - c.x, dy = y - c.y, dz = z - c.z;
-    return fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= c.w;
+    return aabb_may_touch(P.cull[2 * si], P.cull[2 * si + 1], x, y, z);
 }
 
 // Warp-aggregated per-scene counter add; must be called by all 32 lanes.  Lanes of a
