@@ -137,6 +137,7 @@ struct Engine::Impl {
     uint32_t total_bricks = 0;
     DevBuf dead_mom;  // grid readback only (enable_grid_readback)
     DevBuf grid_acc, grid_vel, brick_flag, brick_stamp, active_bricks, brick_scene, misc;
+    int flag_parity = 0;  // which half of brick_flag P2G marks (flips at every collect)
     // misc u32 slots: [0] n_active_bricks
     int64_t n = 0;      // particles
     int64_t n_cap = 0;  // slots of each plane buffer: max(n, cap_hint) + kGroup (padding, holes)
@@ -242,7 +243,8 @@ struct Engine::Impl {
         P.grid_acc = grid_acc.as<float4>();
         P.grid_vel = grid_vel.as<float4>();
         P.dead_mom = dead_mom.p ? dead_mom.as<float4>() : nullptr;
-        P.brick_flag = brick_flag.as<uint32_t>();
+        P.brick_flag = brick_flag.as<uint32_t>() + static_cast<size_t>(flag_parity) * total_bricks;
+        P.brick_flag_next = brick_flag.as<uint32_t>() + static_cast<size_t>(1 - flag_parity) * total_bricks;
         P.brick_stamp = brick_stamp.as<uint32_t>();
         P.active_bricks = active_bricks.as<uint32_t>();
         P.n_active_bricks = misc.as<uint32_t>();
@@ -340,10 +342,10 @@ Engine::Engine(const std::vector<SceneGrid>& scenes) : impl_(new Impl), scenes_(
     I.grid_vel.alloc(sizeof(float4) * I.total_nodes);
     check(cudaMemset(I.grid_acc.p, 0, sizeof(float4) * I.total_nodes), "memset");
     check(cudaMemset(I.grid_vel.p, 0, sizeof(float4) * I.total_nodes), "memset");
-    I.brick_flag.alloc(sizeof(uint32_t) * I.total_bricks);
+    I.brick_flag.alloc(2 * sizeof(uint32_t) * I.total_bricks);  // alternating mark arrays
     I.brick_stamp.alloc(sizeof(uint32_t) * I.total_bricks);
     I.active_bricks.alloc(sizeof(uint32_t) * I.total_bricks);
-    check(cudaMemset(I.brick_flag.p, 0, sizeof(uint32_t) * I.total_bricks), "memset");
+    check(cudaMemset(I.brick_flag.p, 0, 2 * sizeof(uint32_t) * I.total_bricks), "memset");
     check(cudaMemset(I.brick_stamp.p, 0xFF, sizeof(uint32_t) * I.total_bricks), "memset");
     std::vector<uint32_t> bs(I.total_bricks);
     for (size_t s = 0; s < I.hs.size(); ++s) {
@@ -646,6 +648,7 @@ void Engine::p2g(bool mls, float dt, bool collect, bool standard) {
     if (collect) {
         launch_collect_bricks(P, I.total_bricks, I.st);
         I.counted(1);
+        I.flag_parity = 1 - I.flag_parity;
     }
     if (mls || standard) I.use_stress_in = false;  // consumed by the first stress-using P2G
     I.end(CAT_P2G, ev);
@@ -1030,6 +1033,7 @@ void Engine::collect_bricks() {
     Params P = I.params();
     launch_collect_bricks(P, I.total_bricks, I.st);
     I.counted(1);
+    I.flag_parity = 1 - I.flag_parity;
 }
 
 void Engine::dd_migrate_buffers(void** send_lo, void** send_hi, void** recv_lo, void** recv_hi, int64_t* cap) {

@@ -44,8 +44,9 @@ __global__ void k_halo(const Params P, float4* pool, float4* buf, int x0, int w)
                 float4 a = pool[idx];
                 a.x += q.x; a.y += q.y; a.z += q.z; a.w += q.w;
                 pool[idx] = a;
-                P.brick_flag[(static_cast<uint32_t>(z >> 2) * P.geo.nb[1] + static_cast<uint32_t>(y >> 2)) * P.geo.nb[0] +
-                             static_cast<uint32_t>(x >> 2)] = 1u;
+                atomicOr(&P.brick_flag[(static_cast<uint32_t>(z >> 2) * P.geo.nb[1] + static_cast<uint32_t>(y >> 2)) *
+                                           P.geo.nb[0] + static_cast<uint32_t>(x >> 2)],
+                         8u);  // the node's own brick (mark_bricks encoding)
             }
         } else {
             pool[idx] = buf[e];

@@ -115,21 +115,13 @@ struct Stager {
 
 // =====================================================================  P2G
 __device__ __forceinline__ void mark_bricks(const Params& P, const SceneView& S, const int cb[3]) {
-    // the <= 8 bricks a stencil at base cb touches: plain stores of 1 (benign races, no
-    // dependent loads); k_collect_bricks compacts the marks into the active list
-    const int bx0 = cb[0] >> 2, bx1 = (cb[0] + 2) >> 2;
-    const int by0 = cb[1] >> 2, by1 = (cb[1] + 2) >> 2;
-    const int bz0 = cb[2] >> 2, bz1 = (cb[2] + 2) >> 2;
-    uint32_t* f = P.brick_flag + S.brick_base;
-    const int sy = S.nb[0], sz = S.nb[0] * S.nb[1];
-    f[bz0 * sz + by0 * sy + bx0] = 1u;
-    f[bz0 * sz + by0 * sy + bx1] = 1u;
-    f[bz0 * sz + by1 * sy + bx0] = 1u;
-    f[bz0 * sz + by1 * sy + bx1] = 1u;
-    f[bz1 * sz + by0 * sy + bx0] = 1u;
-    f[bz1 * sz + by0 * sy + bx1] = 1u;
-    f[bz1 * sz + by1 * sy + bx0] = 1u;
-    f[bz1 * sz + by1 * sy + bx1] = 1u;
+    // ONE fire-and-forget red.or on the brick of the stencil base: bit 3 = touched, bit a =
+    // the stencil crosses into the +a neighbour brick (base & 3 >= 2); k_collect_bricks
+    // expands the marks to exactly the <= 8 bricks the stencils touch
+    const uint32_t m = 8u | ((cb[0] & 3) >= 2 ? 1u : 0u) | ((cb[1] & 3) >= 2 ? 2u : 0u) | ((cb[2] & 3) >= 2 ? 4u : 0u);
+    uint32_t* f = P.brick_flag + S.brick_base +
+                  ((cb[2] >> 2) * S.nb[1] + (cb[1] >> 2)) * S.nb[0] + (cb[0] >> 2);
+    asm volatile("red.global.or.b32 [%0], %1;" ::"l"(f), "r"(m) : "memory");
 }
 
 // red.global.add.v4.f32: the explicit state space keeps the 64-bit base + 32-bit offset
@@ -240,22 +232,35 @@ __device__ __forceinline__ void bspline_dw(float fx, float inv_dx, float dw[3]) 
 }
 
 // Active-brick list from the P2G marks (warp-aggregated append; order is irrelevant).
-// Marks are reset here, so the next P2G starts from a clean slate.
+// Brick X is active when some X - d, d in {0,1}^3 (same scene), is marked with every bit of
+// d set (mark_bricks).  The marks are read across neighbours, so they cannot be cleared
+// here: the flag arrays alternate per substep and this pass zeroes the OTHER one, which
+// the next P2G marks.
 __global__ void __launch_bounds__(256) k_collect_bricks(const Params P, uint32_t n_bricks) {
     const unsigned full = 0xffffffffu;
     const uint32_t stride = gridDim.x * blockDim.x;
+    const uint32_t nb0 = P.geo.nb[0], nb1 = P.geo.nb[1], bps = P.geo.bricks_per_scene;
     for (uint32_t base = blockIdx.x * blockDim.x; base < n_bricks; base += stride) {
         const uint32_t b = base + threadIdx.x;
-        const bool on = b < n_bricks && P.brick_flag[b] != 0u;
+        bool on = false;
+        if (b < n_bricks) {
+            P.brick_flag_next[b] = 0u;
+            const uint32_t local = b % bps;
+            const uint32_t bx = local % nb0, by = (local / nb0) % nb1, bz = local / (nb0 * nb1);
+#pragma unroll
+            for (int d = 0; d < 8; ++d) {
+                const uint32_t dx = d & 1, dy = (d >> 1) & 1, dz = d >> 2;
+                if (bx < dx || by < dy || bz < dz) continue;
+                const uint32_t f = P.brick_flag[b - dx - dy * nb0 - dz * nb0 * nb1];
+                on = on || ((f & 8u) && (f & static_cast<uint32_t>(d)) == static_cast<uint32_t>(d));
+            }
+        }
         const unsigned m = __ballot_sync(full, on);
         if (m == 0u) continue;
         uint32_t start = 0;
         if ((threadIdx.x & 31) == 0) start = atomicAdd(P.n_active_bricks, __popc(m));
         start = __shfl_sync(full, start, 0);
-        if (on) {
-            P.active_bricks[start + __popc(m & lanemask_lt())] = b;
-            P.brick_flag[b] = 0u;
-        }
+        if (on) P.active_bricks[start + __popc(m & lanemask_lt())] = b;
     }
 }
 

@@ -57,7 +57,8 @@ struct Params {
     float4* grid_acc;
     float4* grid_vel;   // {v, m}; v = 0 at nodes of mass <= kMassEps
     float4* dead_mom;   // optional: {momentum, m} of nodes of mass <= kMassEps (grid readback)
-    uint32_t* brick_flag;
+    uint32_t* brick_flag;       // P2G marks of this substep (mark_bricks)
+    uint32_t* brick_flag_next;  // the other array: zeroed by k_collect_bricks for the next P2G
     uint32_t* brick_stamp;
     uint32_t* active_bricks;
     uint32_t* n_active_bricks;
