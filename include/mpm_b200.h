@@ -262,6 +262,8 @@ mpmb_status mpmb_state_set_particles_ids(mpmb_state st, int32_t n, const float* 
                                          const float* mass, const float* volume0, const float* F,
                                          const float* C, const int32_t* material_id, const uint8_t* active,
                                          const uint32_t* ids);
+/* Exact mode for the solver layer (see mpmb_set_exact). */
+mpmb_status mpmb_state_set_exact(mpmb_state st, int32_t on);
 /* Stream the state's kernels run on (NULL = the library's own). */
 mpmb_status mpmb_state_set_stream(mpmb_state st, void* cuda_stream);
 mpmb_status mpmb_state_synchronize(mpmb_state st);
@@ -332,6 +334,10 @@ mpmb_status mpmb_scene_get_particles(mpmb_handle scene, float* x, float* v, floa
 mpmb_status mpmb_set_stream(mpmb_handle h, void* cuda_stream);
 mpmb_status mpmb_set_resort_interval(mpmb_handle h, int32_t substeps);
 mpmb_status mpmb_set_profiling(mpmb_handle h, int32_t on);
+/* Exact mode (MLS): every substep in the reference's float arithmetic and summation order --
+ * bit-identical to the reference and run to run (SPEC.md:252 deterministic mode), several
+ * times slower than the default fast mode (float atomics). */
+mpmb_status mpmb_set_exact(mpmb_handle h, int32_t on);
 mpmb_status mpmb_get_profile(mpmb_handle h, mpmb_profile* out);
 /* Blocks until every frame enqueued on h has finished. */
 mpmb_status mpmb_synchronize(mpmb_handle h);

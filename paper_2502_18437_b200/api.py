@@ -208,6 +208,10 @@ class SolverState:
               self.lib, "step_mls")
         return st.inverted_f, st.projection_failures
 
+    def set_exact(self, on: bool = True):
+        """Exact mode (product only): the reference's float order and arithmetic."""
+        check(self._f("state_set_exact")(self.h, int(on)), self.lib, "set_exact")
+
     def step_standard(self, dt, g=(0.0, 0.0, 0.0), contact=False, bc=capi.BC_SLIP):
         st = capi.StepStats()
         gg = np.array(g, F32)
@@ -312,6 +316,11 @@ class Scene:
     def set_shape_pose_target(self, shape, position, orientation):
         p, q = np.array(position, F32), np.array(orientation, F32)
         check(self.lib.mpmb_set_shape_pose_target(self.h, shape, _fp(p), _fp(q)), self.lib, "pose target")
+
+    def set_exact(self, on: bool = True):
+        """Exact mode: the reference's float arithmetic and summation order (MLS solver),
+        bit-identical frames; slower (ordered reductions, host totals)."""
+        check(self.lib.mpmb_set_exact(self.h, int(on)), self.lib, "set_exact")
 
     def advance(self, dt):
         check(self.lib.mpmb_advance(self.h, float(F32(dt))), self.lib, "advance")

@@ -152,6 +152,8 @@ PRODUCT_API.update({
                                     C.POINTER(C.c_void_p)]),
     "state_set_particles_ids": (C.c_int, [P, C.c_int32, fp, fp, fp, fp, fp, fp, ip, u8p, u32p]),
     "state_set_stream": (C.c_int, [P, C.c_void_p]),
+    "state_set_exact": (C.c_int, [P, C.c_int32]),
+    "set_exact": (C.c_int, [u64, C.c_int32]),
     "state_synchronize": (C.c_int, [P]),
     "dd_halo_buffers": (C.c_int, [P, VPP, VPP, VPP, VPP, I64P, I64P, ip]),
     "dd_p2g": (C.c_int, [P, C.c_float]),

@@ -295,6 +295,13 @@ extern "C" mpmb_status mpmb_state_set_particles_ids(mpmb_state st, int32_t n, co
     });
 }
 
+extern "C" mpmb_status mpmb_state_set_exact(mpmb_state st, int32_t on) {
+    return guarded([&] {
+        S(st)->eng->set_exact(on != 0);
+        return MPMB_OK;
+    });
+}
+
 extern "C" mpmb_status mpmb_state_set_stream(mpmb_state st, void* stream) {
     return guarded([&] {
         S(st)->eng->set_stream(stream);
@@ -638,6 +645,7 @@ struct Batch {
     bool shapes_dirty = true;
     Status status = Status::idle;
     int resort = 0;               // substeps between binnings (0: every 4 frames)
+    bool exact = false;           // exact mode (Engine::set_exact)
     int64_t since_sort = 1 << 30; // substeps since the last binning (runs across frames)
     bool profiling = false;
     void* stream = nullptr;
@@ -735,6 +743,7 @@ void ensure_engine(Batch& b) {
     b.eng = std::make_unique<Engine>(grids);
     if (b.stream) b.eng->set_stream(b.stream);
     b.eng->set_profiling(b.profiling);
+    b.eng->set_exact(b.exact);
 }
 
 void upload(Batch& b) {
@@ -914,6 +923,25 @@ void fetch(Batch& b) {
     uint8_t* a = reinterpret_cast<uint8_t*>(v + 3 * total);
     std::vector<double> totals;
     e.snapshot(x, v, a, totals);
+    if (b.exact) {  // make_result (scene.hpp:256-266): FP64 sums in particle order, on the host
+        for (size_t si = 0; si < b.scenes.size(); ++si) {
+            const Scene* s = b.scenes[si];
+            const size_t o = b.offsets[si];
+            double t[5] = {0, 0, 0, 0, 0};
+            for (size_t i = 0; i < s->count(); ++i) {
+                if (!a[o + i]) continue;
+                const double m = s->mass[i];
+                const float* vi = v + 3 * (o + i);
+                t[0] += m;
+                t[1] += m * vi[0];
+                t[2] += m * vi[1];
+                t[3] += m * vi[2];
+                const float n2 = vi[0] * vi[0] + vi[1] * vi[1] + vi[2] * vi[2];
+                t[4] += 0.5 * m * static_cast<double>(n2);
+            }
+            for (int q = 0; q < 5; ++q) totals[5 * si + q] = t[q];
+        }
+    }
     std::vector<SceneCounters> cnt = e.read_counters();
     std::vector<double> imp, tq;
     std::vector<int32_t> cc;
@@ -1419,6 +1447,14 @@ extern "C" mpmb_status mpmb_nn_spacing(mpmb_handle h, const float* cell_hint, fl
                 }
             spacing[k] = cnt ? static_cast<float>(sum / cnt) : cell_hint[k];
         }
+        return MPMB_OK;
+    });
+}
+
+extern "C" mpmb_status mpmb_set_exact(mpmb_handle h, int32_t on) {
+    return with_batch(h, [&](Batch& b) {
+        b.exact = on != 0;
+        if (b.eng) b.eng->set_exact(b.exact);
         return MPMB_OK;
     });
 }

@@ -131,30 +131,27 @@ __device__ __forceinline__ float det3(const float a[9]) {  // math.hpp:273-277
 // Cauchy stress (materials.hpp:35-54), FP64 internally, J clamped >= 1e-6.
 // b = F F^T is symmetric; the 6 unique entries are computed once.
 __device__ __forceinline__ void neo_hookean(const float F[9], float mu, float lambda, float s[9]) {
+    // the reference's own operation order, every FP64 op round-to-nearest and unfused, and a
+    // true division by Jc: bit-identical to the cached stress of solvers.hpp:69-74
     double f[9];
 #pragma unroll
     for (int i = 0; i < 9; ++i) f[i] = static_cast<double>(F[i]);
-    double J = f[0] * (f[4] * f[8] - f[5] * f[7]) - f[1] * (f[3] * f[8] - f[5] * f[6]) +
-               f[2] * (f[3] * f[7] - f[4] * f[6]);
-    double Jc = J < 1e-6 ? 1e-6 : J;
-    double d = static_cast<double>(lambda) * log(Jc);
-    double inv = 1.0 / Jc;
-    double mu_d = static_cast<double>(mu);
-    double b00 = f[0] * f[0] + f[1] * f[1] + f[2] * f[2];
-    double b11 = f[3] * f[3] + f[4] * f[4] + f[5] * f[5];
-    double b22 = f[6] * f[6] + f[7] * f[7] + f[8] * f[8];
-    double b01 = f[0] * f[3] + f[1] * f[4] + f[2] * f[5];
-    double b02 = f[0] * f[6] + f[1] * f[7] + f[2] * f[8];
-    double b12 = f[3] * f[6] + f[4] * f[7] + f[5] * f[8];
-    s[0] = static_cast<float>((mu_d * (b00 - 1.0) + d) * inv);
-    s[4] = static_cast<float>((mu_d * (b11 - 1.0) + d) * inv);
-    s[8] = static_cast<float>((mu_d * (b22 - 1.0) + d) * inv);
-    float o01 = static_cast<float>(mu_d * b01 * inv);
-    float o02 = static_cast<float>(mu_d * b02 * inv);
-    float o12 = static_cast<float>(mu_d * b12 * inv);
-    s[1] = o01; s[3] = o01;
-    s[2] = o02; s[6] = o02;
-    s[5] = o12; s[7] = o12;
+    const double J = __dadd_rn(
+        __dsub_rn(__dmul_rn(f[0], __dsub_rn(__dmul_rn(f[4], f[8]), __dmul_rn(f[5], f[7]))),
+                  __dmul_rn(f[1], __dsub_rn(__dmul_rn(f[3], f[8]), __dmul_rn(f[5], f[6])))),
+        __dmul_rn(f[2], __dsub_rn(__dmul_rn(f[3], f[7]), __dmul_rn(f[4], f[6]))));
+    const double Jc = J < 1e-6 ? 1e-6 : J;
+    const double d = __dmul_rn(static_cast<double>(lambda), log(Jc));
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            const double b = __dadd_rn(__dadd_rn(__dmul_rn(f[3 * i], f[3 * j]), __dmul_rn(f[3 * i + 1], f[3 * j + 1])),
+                                       __dmul_rn(f[3 * i + 2], f[3 * j + 2]));
+            double v = __dmul_rn(static_cast<double>(mu), __dsub_rn(b, i == j ? 1.0 : 0.0));
+            if (i == j) v = __dadd_rn(v, d);
+            s[3 * i + j] = static_cast<float>(__ddiv_rn(v, Jc));
+        }
 }
 
 // The same Cauchy stress in FP32 without cancellation, for the P2G hot loop:

@@ -16,7 +16,10 @@ enum : int { BC_SLIP = 0, BC_STICKY = 1 };
 constexpr uint32_t kActiveBit = 0x80000000u;
 constexpr uint32_t kMatMask = 0xFFu;
 constexpr int kSceneShift = 8;
-constexpr uint32_t kSceneMask = 0x7FFFFFu;
+constexpr uint32_t kSceneMask = 0x3FFFFFu;
+// set at upload on a particle given inactive together with an explicit stress: the reference
+// never updates an inactive particle's cached stress, so downloads return the uploaded value
+constexpr uint32_t kKeepStressBit = 0x40000000u;
 
 constexpr float kMassEps = 1e-9f;  // state.hpp:13
 constexpr int kBrick = 4;          // nodes (and cells) per brick edge

@@ -138,6 +138,11 @@ struct Engine::Impl {
     DevBuf dead_mom;  // grid readback only (enable_grid_readback)
     DevBuf grid_acc, grid_vel, brick_flag, brick_stamp, active_bricks, brick_scene, misc;
     int flag_parity = 0;  // which half of brick_flag P2G marks (flips at every collect)
+    bool exact = false;   // exact mode (k_exact.cu): the reference's arithmetic and order
+    DevBuf ex_scratch, ex_bidx;
+    uint32_t ex_epoch = 0;
+    DevBuf ex_ckey, ex_crec, ex_cn, ex_cscratch;  // exact contact records (k_exact.cu)
+    PinnedBuf ex_cn_host;
     // misc u32 slots: [0] n_active_bricks
     int64_t n = 0;      // particles
     int64_t n_cap = 0;  // slots of each plane buffer: max(n, cap_hint) + kGroup (padding, holes)
@@ -262,6 +267,7 @@ struct Engine::Impl {
         P.cnt_frame = cnt_frame.as<int>();
         P.counters = counters.as<int>();
         P.epoch = epoch;
+        P.exact = exact ? 1 : 0;
         return P;
     }
 };
@@ -469,7 +475,7 @@ void Engine::upload_particles(int64_t n, const float* x, const float* v, const f
     }
     IoArrays io{dx.as<float>(), dv.as<float>(), dm.as<float>(), dvol.as<float>(), dF.as<float>(),
                 dC.as<float>(), dmat.as<int32_t>(), dact.as<uint8_t>(), dsc.as<int32_t>(),
-                ids ? dids.as<uint32_t>() : nullptr};
+                ids ? dids.as<uint32_t>() : nullptr, stress != nullptr};
     Params P = I.params();
     launch_upload(P, io, n, I.st);
     I.counted(1);
@@ -643,6 +649,21 @@ void Engine::p2g(bool mls, float dt, bool collect, bool standard) {
     cudaMemsetAsync(I.misc.p, 0, sizeof(uint32_t), I.st);  // active brick count
     Params P = I.params();
     P.dt = dt;
+    if (I.exact) {
+        if (standard || !mls) throw std::invalid_argument("engine: exact mode covers the MLS solver");
+        const size_t sb = exact_scratch_bytes(I.n_cap, I.total_bricks);
+        if (I.ex_scratch.bytes < sb) I.ex_scratch.alloc(sb);
+        if (!I.ex_bidx.p) {
+            I.ex_bidx.alloc(sizeof(uint2) * I.total_bricks);
+            check(cudaMemsetAsync(I.ex_bidx.p, 0, sizeof(uint2) * I.total_bricks, I.st), "memset");
+        }
+        launch_exact_p2g(P, mls, I.ex_scratch.p, I.ex_bidx.as<uint2>(), ++I.ex_epoch, I.total_bricks, I.st);
+        I.counted(8);
+        I.flag_parity = 1 - I.flag_parity;  // the collect ran inside
+        if (mls) I.use_stress_in = false;
+        I.end(CAT_P2G, ev);
+        return;
+    }
     launch_p2g(P, mls || standard, (I.n + kGroup - 1) / kGroup, I.st, standard);
     I.counted(1);
     if (collect) {
@@ -671,8 +692,31 @@ void Engine::grid_update(int sub, float dt, const float g[3], bool gravity, bool
         launch_shape_cull(P, I.st);
         I.counted(1);
     }
+    const bool ex_contact = I.exact && contact && I.n_shapes > 0;
+    if (ex_contact) {  // one record per contacting (node, shape): at most nodes x shapes
+        const uint64_t cap64 = I.total_nodes * static_cast<uint64_t>(I.n_shapes);
+        const uint32_t cap = static_cast<uint32_t>(std::min<uint64_t>(cap64, 0x7FFFFFFFull));
+        I.ex_ckey.alloc(8ull * cap);
+        I.ex_crec.alloc(24ull * cap);
+        I.ex_cn.alloc(4);
+        I.ex_cn_host.alloc(4);
+        check(cudaMemsetAsync(I.ex_cn.p, 0, 4, I.st), "memset");
+        P.ex_ckey = I.ex_ckey.as<uint64_t>();
+        P.ex_crec = I.ex_crec.as<float>();
+        P.ex_cn = I.ex_cn.as<uint32_t>();
+        P.ex_ccap = cap;
+    }
     launch_grid_update(P, I.total_bricks, I.st);
     I.counted(1);
+    if (ex_contact) {  // ordered float sums need the record count on the host (CUB sizes)
+        check(cudaMemcpyAsync(I.ex_cn_host.p, I.ex_cn.p, 4, cudaMemcpyDeviceToHost, I.st), "d2h");
+        check(cudaStreamSynchronize(I.st), "exact contact");
+        const uint32_t n = *static_cast<uint32_t*>(I.ex_cn_host.p);
+        if (n > P.ex_ccap) throw std::runtime_error("engine: exact contact records overflow");
+        I.ex_cscratch.alloc(exact_contact_scratch_bytes(n));
+        launch_exact_contact(P, n, I.ex_cscratch.p, I.st);
+        I.counted(3);
+    }
     I.end(CAT_GRID, ev);
 }
 
@@ -686,15 +730,33 @@ void Engine::g2p_mls(int sub, float dt, bool pushout, bool deactivate) {
     P.pushout = pushout ? 1 : 0;
     P.deactivate = deactivate ? 1 : 0;
     P.commit = 1;
+    if (I.exact) {  // in place, reference order; push-out / deactivation as separate passes
+        launch_exact_g2p(P, I.st);
+        I.counted(1);
+        if (pushout && I.n_shapes > 0) {
+            launch_pushout(P, I.st);
+            I.counted(1);
+        }
+        if (deactivate) {
+            launch_deactivate(P, I.st);
+            I.counted(1);
+        }
+        I.end(CAT_G2P, ev);
+        return;
+    }
     launch_g2p(P, false, (I.n + kGroup - 1) / kGroup, I.st);
     I.counted(1);
     I.cur = 1 - I.cur;  // G2P wrote the group-sorted state into the other buffer
     I.end(CAT_G2P, ev);
 }
 
+void Engine::set_exact(bool on) { impl_->exact = on; }
+bool Engine::exact() const { return impl_->exact; }
+
 void Engine::g2p_standard(int sub, float dt, bool pushout, bool deactivate) {
     Impl& I = *impl_;
     if (I.n_cap == 0) return;
+    if (I.exact) throw std::invalid_argument("engine: exact mode covers the MLS solver");
     auto ev = I.begin();
     Params P = I.params();
     P.sub = std::min(sub, I.table_subs - 1);
@@ -711,6 +773,7 @@ void Engine::g2p_standard(int sub, float dt, bool pushout, bool deactivate) {
 void Engine::g2p_pb(int sub, float dt, bool commit, bool pushout, bool deactivate) {
     Impl& I = *impl_;
     if (I.n_cap == 0) return;
+    if (I.exact) throw std::invalid_argument("engine: exact mode covers the MLS solver");
     auto ev = I.begin();
     Params P = I.params();
     P.sub = std::min(sub, I.table_subs - 1);

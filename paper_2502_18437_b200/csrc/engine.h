@@ -96,6 +96,10 @@ class Engine {
     void grid_update(int sub, float dt, const float g[3], bool gravity, bool contact, int bc);
     void g2p_mls(int sub, float dt, bool pushout, bool deactivate);   // K4
     void g2p_standard(int sub, float dt, bool pushout, bool deactivate);  // K4, PIC (solvers.hpp:107-135)
+    // exact mode (k_exact.cu): MLS substeps in the reference's float order and arithmetic,
+    // bit-identical to the reference and run to run; much slower than the default fast mode
+    void set_exact(bool on);
+    bool exact() const;
     void g2p_pb(int sub, float dt, bool commit, bool pushout, bool deactivate);  // K6
     void free_bodies(int sub, float dt, const float g[3], bool integrate, bool merge);  // K7
     void bc_pass(int bc);                         // BC alone (hook adapter)

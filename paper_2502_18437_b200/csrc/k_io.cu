@@ -39,6 +39,7 @@ __global__ void k_upload(const Params P, IoArrays in, int64_t n) {
         uint32_t flags = (static_cast<uint32_t>(in.mat[i]) & kMatMask) |
                          ((static_cast<uint32_t>(in.scene[i]) & kSceneMask) << kSceneShift);
         if (in.active[i]) flags |= kActiveBit;
+        else if (in.keep_stress) flags |= kKeepStressBit;
         P.pl[PR][i] = make_float4(in.mass[i], in.vol0[i], __uint_as_float(flags),
                                   __uint_as_float(in.ids ? in.ids[i] : static_cast<uint32_t>(i)));
     }
@@ -141,8 +142,9 @@ __global__ void k_stress(const Params P, float* out) {
         const uint32_t flags = __float_as_uint(r.z);
         if (__float_as_uint(r.w) == kHoleOrig) continue;
         const uint64_t o = __float_as_uint(r.w);
-        if (P.use_stress_in) {
-            for (int a = 0; a < 9; ++a) out[9 * o + a] = P.stress_in[9 * o + a];
+        if (P.use_stress_in || (flags & kKeepStressBit)) {
+            if (out != P.stress_in)
+                for (int a = 0; a < 9; ++a) out[9 * o + a] = P.stress_in[9 * o + a];
             continue;
         }
         Part p;

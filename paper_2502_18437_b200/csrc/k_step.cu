@@ -114,10 +114,20 @@ __global__ void __launch_bounds__(256) k_grid_update(const Params P) {
                             imp = delta * (-m);
                             tq = cross(xn - mk(pose.pos[0], pose.pos[1], pose.pos[2]), imp);
                             hit = 1;
+                            if (P.ex_ckey) {
+                                const uint32_t r = atomicAdd(P.ex_cn, 1u);
+                                if (r < P.ex_ccap) {
+                                    P.ex_ckey[r] = (static_cast<uint64_t>(si) << 40) |
+                                                   ((static_cast<uint64_t>(k) * S.dims[1] + j) * S.dims[0] + ig);
+                                    float* o = P.ex_crec + 6ull * r;
+                                    o[0] = imp.x; o[1] = imp.y; o[2] = imp.z;
+                                    o[3] = tq.x; o[4] = tq.y; o[5] = tq.z;
+                                }
+                            }
                         }
                     }
                 }
-                if (__any_sync(0xffffffffu, hit)) {
+                if (!P.ex_ckey && __any_sync(0xffffffffu, hit)) {
                     float r[7] = {imp.x, imp.y, imp.z, tq.x, tq.y, tq.z, static_cast<float>(hit)};
 #pragma unroll
                     for (int o = 16; o > 0; o >>= 1)
@@ -250,7 +260,11 @@ __global__ void k_free_bodies(const Params P, int integrate, int merge) {
         if (merge) {
 #pragma unroll
             for (int q = 0; q < 6; ++q) {
-                P.acc_frame[6 * i + q] += P.acc_sub[6 * i + q];
+                if (P.exact)  // the reference's float frame sums (scene.hpp:228-231)
+                    P.acc_frame[6 * i + q] = static_cast<double>(
+                        __fadd_rn(static_cast<float>(P.acc_frame[6 * i + q]), static_cast<float>(P.acc_sub[6 * i + q])));
+                else
+                    P.acc_frame[6 * i + q] += P.acc_sub[6 * i + q];
                 P.acc_sub[6 * i + q] = 0.0;
             }
             P.cnt_frame[i] += P.cnt_sub[i];

@@ -75,6 +75,14 @@ struct Params {
     double* acc_frame;
     int* cnt_frame;
     int* counters;     // per scene: inverted, proj failures, pushed, deactivated
+    // exact mode: contact terms as records {key = shape << 40 | reference node index,
+    // impulse[3], torque[3]} for the ordered float sums of contact.hpp:127-129 (k_exact.cu);
+    // null in the default mode (FP64 atomics)
+    uint64_t* ex_ckey;
+    float* ex_crec;
+    uint32_t* ex_cn;
+    uint32_t ex_ccap;
+    int exact;  // exact mode: frame accumulators merge in float (scene.hpp:228-231)
     uint32_t epoch;
     float dt;
     float g[3];

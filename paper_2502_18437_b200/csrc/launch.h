@@ -56,6 +56,14 @@ void launch_migrate_unpack(const Params& P, const float4* in, uint32_t n, uint32
 void launch_download_slots(const Params& P, uint32_t* ids, float* x, float* v, uint8_t* active, uint32_t* count,
                            cudaStream_t st);
 
+// ---- exact mode (k_exact.cu) ----
+size_t exact_scratch_bytes(int64_t n, int64_t n_bricks);
+void launch_exact_p2g(const Params& P, bool mls, void* scratch, uint2* brick_idx, uint32_t epoch, int64_t n_bricks,
+                      cudaStream_t st);
+void launch_exact_g2p(const Params& P, cudaStream_t st);
+size_t exact_contact_scratch_bytes(uint32_t n);
+void launch_exact_contact(const Params& P, uint32_t n, void* scratch, cudaStream_t st);
+
 // ---- scenario metrics (k_scenario.cu) ----
 size_t scenario_scratch_bytes(int64_t n, int n_scenes);
 void launch_scenario(const Params& P, int mode, const float* cell, void* scratch, size_t scratch_bytes,
@@ -66,6 +74,7 @@ struct IoArrays {  // original-order device staging arrays (any may be null)
     float* x; float* v; float* mass; float* vol0; float* F; float* C; int32_t* mat;
     uint8_t* active; int32_t* scene;
     uint32_t* ids;  // upload: original index per particle (null: the upload order)
+    int keep_stress;  // upload: a stress array accompanies the particles (kKeepStressBit)
 };
 void launch_upload(const Params& P, const IoArrays& in, int64_t n, cudaStream_t st);
 void launch_download(const Params& P, const IoArrays& out, cudaStream_t st);
