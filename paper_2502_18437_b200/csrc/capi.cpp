@@ -639,6 +639,12 @@ struct Batch {
     std::vector<Scene*> scenes;
     std::unique_ptr<Engine> eng;
     std::shared_ptr<void> frame;  // pinned FrameResult buffer (x, v, active of all scenes)
+    ~Batch() {  // the frame buffer goes before the engine: finish its copy first
+        try {
+            if (eng) eng->wait_results();
+        } catch (...) {  // at process exit the driver may already be gone
+        }
+    }
     size_t frame_bytes = 0;
     bool device_valid = false;   // device holds the newest particle state
     bool particles_dirty = true; // host changed: re-upload
@@ -915,15 +921,24 @@ void fetch(Batch& b) {
     for (Scene* s : b.scenes) total += s->count();
     const size_t bytes = 24 * total + total + 16;
     if (!b.frame || b.frame_bytes < bytes) {
+        e.wait_results();  // the previous frame's copy may still target the old buffer
         b.frame = Engine::pinned_host(bytes);
         b.frame_bytes = bytes;
     }
     float* x = static_cast<float*>(b.frame.get());
     float* v = x + 3 * total;
     uint8_t* a = reinterpret_cast<uint8_t*>(v + 3 * total);
+    // counters and contact first: a device->host copy issued after the arrays' would queue
+    // behind them on the copy engine
+    std::vector<SceneCounters> cnt = e.read_counters();
+    std::vector<double> imp, tq;
+    std::vector<int32_t> cc;
+    e.read_contact(1, imp, tq, cc);
     std::vector<double> totals;
-    e.snapshot(x, v, a, totals);
-    if (b.exact) {  // make_result (scene.hpp:256-266): FP64 sums in particle order, on the host
+    // the arrays' D2H overlaps the next frame; mpmb_result_copy waits for it
+    e.snapshot(x, v, a, totals, true);
+    if (b.exact) {
+        e.wait_results();  // make_result (scene.hpp:256-266): FP64 sums in particle order, on the host
         for (size_t si = 0; si < b.scenes.size(); ++si) {
             const Scene* s = b.scenes[si];
             const size_t o = b.offsets[si];
@@ -942,10 +957,6 @@ void fetch(Batch& b) {
             for (int q = 0; q < 5; ++q) totals[5 * si + q] = t[q];
         }
     }
-    std::vector<SceneCounters> cnt = e.read_counters();
-    std::vector<double> imp, tq;
-    std::vector<int32_t> cc;
-    e.read_contact(1, imp, tq, cc);
     for (size_t si = 0; si < b.scenes.size(); ++si) {
         Scene* s = b.scenes[si];
         const size_t o = b.offsets[si], n = s->count();
@@ -1275,6 +1286,7 @@ extern "C" mpmb_status mpmb_result_copy(mpmb_handle sh, float* pos, float* vel, 
     return guarded([&]() -> mpmb_status {
         Scene* s = reg().scene(sh);
         if (!s) return MPMB_BAD_HANDLE;
+        if ((pos || vel || active) && s->rn && s->batch && s->batch->eng) s->batch->eng->wait_results();
         if (pos && s->rn) std::copy(s->rx, s->rx + 3 * s->rn, pos);
         if (vel && s->rn) std::copy(s->rv, s->rv + 3 * s->rn, vel);
         if (active && s->rn) std::copy(s->ra, s->ra + s->rn, active);

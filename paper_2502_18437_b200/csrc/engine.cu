@@ -168,12 +168,16 @@ struct Engine::Impl {
     int table_subs = 1;
     PinnedBuf pin_table[2];
     cudaEvent_t pin_done[2] = {nullptr, nullptr};
+    cudaStream_t copy_st = nullptr;  // snapshot D2H (Engine::snapshot async)
+    cudaEvent_t ev_dl = nullptr, ev_copy = nullptr;
+    bool copy_pending = false;
     int pin_slot = 0;
     DevBuf acc_sub, cnt_sub, acc_frame, cnt_frame, counters;
     DevBuf stress_in;
     bool use_stress_in = false;
     uint32_t epoch = 0;
     DevBuf io_x, io_v, io_a, io_tot;
+    PinnedBuf io_tot_h;
     PinnedBuf pin_io;
     // profiling
     bool profiling = false;
@@ -376,6 +380,12 @@ Engine::Engine(const std::vector<SceneGrid>& scenes) : impl_(new Impl), scenes_(
 Engine::~Engine() {
     Impl& I = *impl_;
     cudaStreamSynchronize(I.st);
+    if (I.copy_st) {
+        cudaStreamSynchronize(I.copy_st);
+        cudaStreamDestroy(I.copy_st);
+        cudaEventDestroy(I.ev_dl);
+        cudaEventDestroy(I.ev_copy);
+    }
     for (auto& e : I.events) {
         cudaEventDestroy(e.second.first);
         cudaEventDestroy(e.second.second);
@@ -884,10 +894,19 @@ void Engine::read_contact(int which, std::vector<double>& imp, std::vector<doubl
         }
 }
 
-void Engine::snapshot(float* x, float* v, uint8_t* active, std::vector<double>& totals) {
+void Engine::snapshot(float* x, float* v, uint8_t* active, std::vector<double>& totals, bool async) {
     Impl& I = *impl_;
     const size_t N = static_cast<size_t>(std::max<int64_t>(I.n, 1));
     const size_t S = I.hs.size();
+    if (I.copy_pending && (I.io_x.bytes < 12 * N || I.io_v.bytes < 12 * N || I.io_a.bytes < N))
+        wait_results();  // the staging is about to be reallocated
+    if (I.copy_pending) check(cudaStreamWaitEvent(I.st, I.ev_copy, 0), "wait copy");  // staging reuse
+    if (async && !I.copy_st) {
+        check(cudaStreamCreateWithFlags(&I.copy_st, cudaStreamNonBlocking), "cudaStreamCreate");
+        check(cudaEventCreateWithFlags(&I.ev_dl, cudaEventDisableTiming), "event");
+        check(cudaEventCreateWithFlags(&I.ev_copy, cudaEventDisableTiming), "event");
+    }
+    cudaStream_t cs = async ? I.copy_st : I.st;
     I.io_tot.alloc(sizeof(double) * 5 * std::max<size_t>(S, 1));
     check(cudaMemsetAsync(I.io_tot.p, 0, I.io_tot.bytes, I.st), "memset");
     Params P = I.params();
@@ -899,13 +918,27 @@ void Engine::snapshot(float* x, float* v, uint8_t* active, std::vector<double>& 
         launch_download(P, io, I.st);
         launch_totals(P, I.io_tot.as<double>(), I.st);
         I.counted(2);
-        if (x) check(cudaMemcpyAsync(x, I.io_x.p, 12 * I.n, cudaMemcpyDeviceToHost, I.st), "d2h");
-        if (v) check(cudaMemcpyAsync(v, I.io_v.p, 12 * I.n, cudaMemcpyDeviceToHost, I.st), "d2h");
-        if (active) check(cudaMemcpyAsync(active, I.io_a.p, I.n, cudaMemcpyDeviceToHost, I.st), "d2h");
     }
-    totals.assign(5 * S, 0.0);
-    check(cudaMemcpyAsync(totals.data(), I.io_tot.p, sizeof(double) * 5 * S, cudaMemcpyDeviceToHost, I.st), "d2h");
+    // the small totals copy goes first: queued behind the arrays on the same copy engine it
+    // would hold the host for the whole transfer
+    I.io_tot_h.alloc(sizeof(double) * 5 * std::max<size_t>(S, 1));
+    check(cudaMemcpyAsync(I.io_tot_h.p, I.io_tot.p, sizeof(double) * 5 * S, cudaMemcpyDeviceToHost, I.st), "d2h");
+    if (I.n > 0) {
+        if (async) {
+            check(cudaEventRecord(I.ev_dl, I.st), "event");
+            check(cudaStreamWaitEvent(cs, I.ev_dl, 0), "wait download");
+        }
+        if (x) check(cudaMemcpyAsync(x, I.io_x.p, 12 * I.n, cudaMemcpyDeviceToHost, cs), "d2h");
+        if (v) check(cudaMemcpyAsync(v, I.io_v.p, 12 * I.n, cudaMemcpyDeviceToHost, cs), "d2h");
+        if (active) check(cudaMemcpyAsync(active, I.io_a.p, I.n, cudaMemcpyDeviceToHost, cs), "d2h");
+        if (async) {
+            check(cudaEventRecord(I.ev_copy, cs), "event");
+            I.copy_pending = true;
+        }
+    }
     check(cudaStreamSynchronize(I.st), "snapshot");
+    const double* th = static_cast<const double*>(I.io_tot_h.p);
+    totals.assign(th, th + 5 * S);
 }
 
 std::shared_ptr<void> Engine::pinned_host(size_t bytes) {
@@ -973,7 +1006,17 @@ int64_t Engine::n_active_sorted() {
     return c[2];
 }
 
-void Engine::synchronize() { check(cudaStreamSynchronize(impl_->st), "synchronize"); }
+void Engine::wait_results() {
+    Impl& I = *impl_;
+    if (!I.copy_pending) return;
+    I.copy_pending = false;
+    check(cudaEventSynchronize(I.ev_copy), "snapshot copy");
+}
+
+void Engine::synchronize() {
+    check(cudaStreamSynchronize(impl_->st), "synchronize");
+    wait_results();
+}
 
 // ------------------------------------------------ scenario metrics (k_scenario.cu)
 void Engine::components(const float* radius, int32_t* counts) {

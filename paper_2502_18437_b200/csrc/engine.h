@@ -116,7 +116,13 @@ class Engine {
                       std::vector<int32_t>& count);
     // FrameResult snapshot for all scenes: positions/velocities/active in original order
     // (device -> pinned host), totals per scene (double).  Enqueue + wait.
-    void snapshot(float* x, float* v, uint8_t* active, std::vector<double>& totals /*5 per scene*/);
+    // Frame snapshot: totals are ready on return.  async: the x / v / active D2H runs on a
+    // copy stream and overlaps whatever the caller enqueues next (the next frame); the host
+    // arrays are valid after wait_results().  The next snapshot reuses the device staging
+    // only after that copy (stream wait, no host sync).
+    void snapshot(float* x, float* v, uint8_t* active, std::vector<double>& totals /*5 per scene*/,
+                  bool async = false);
+    void wait_results();
     // page-locked host memory (cudaMallocHost) freed with the last reference: D2H of a
     // FrameResult straight into it runs at link speed, with no staging copies
     static std::shared_ptr<void> pinned_host(size_t bytes);
@@ -158,7 +164,7 @@ class Engine {
     int64_t download_compact(int64_t capacity, uint32_t* ids, float* x, float* v, uint8_t* active);
     int64_t n_active_sorted();
 
-    void synchronize();
+    void synchronize();  // the engine stream and any snapshot copy in flight
     int64_t launches() const { return launches_total_; }
 
   private:

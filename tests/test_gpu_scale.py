@@ -159,3 +159,24 @@ def test_all_inactive_particles_stay_put():
         g.step_mls(0.002, (0.0, -9.81, 0.0))
     q = g.get_particles()
     assert np.array_equal(q["x"], p["x"]) and np.array_equal(q["v"], p["v"])
+
+
+@pytest.mark.gpu
+def test_fetch_arrays_survive_next_advance():
+    """fetch_results' array D2H overlaps the next frame (copy stream): results read after the
+    next advance are still the fetched frame's, and equal a blocking re-read of that frame."""
+    spec = scenes.cube_drop(dims=(56, 56, 56))
+    a = backends.make_scene("gpu", spec)
+    b = backends.make_scene("gpu", spec)
+    for s in (a, b):
+        s.set_exact(True)  # deterministic: the two scenes agree bitwise
+        s.advance(spec["dt_frame"])
+    ra = a.fetch_results()                       # arrays read right away
+    summ = (capi.FrameSummary * 1)()
+    assert b.lib.mpmb_fetch_results(b.h, summ) == capi.OK
+    b.advance(spec["dt_frame"])                  # next frame enqueued while the copy runs
+    rb = b._result(api._summary_dict(summ[0]))   # waits for the copy, then reads frame 1
+    assert np.array_equal(ra["positions"], rb["positions"])
+    assert np.array_equal(ra["velocities"], rb["velocities"])
+    assert np.array_equal(ra["active"], rb["active"])
+    b.fetch_results()
