@@ -56,10 +56,19 @@ __device__ __forceinline__ uint32_t g2p_pos(int lane, int k) {
     return 64u * (k >> 1) + 8u * (lane & 7) + 4u * (k & 1) + (lane >> 3);
 }
 
+// CG: bypass L1 (the staged particle stream would evict the grid lines G2P gathers)
+template <bool CG>
 __device__ __forceinline__ void cp_async16(float4* smem, const float4* gmem) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+    if (CG) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+    else asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
 }
+#ifndef MPMB_P2G_CG
+#define MPMB_P2G_CG 0
+#endif
+#ifndef MPMB_G2P_CG
+#define MPMB_G2P_CG 1  // A/B on C5: G2P -5%; P2G +1% with CG (its L1 holds nothing else)
+#endif
 // Warm L1 with the 9 stencil rows (3 nodes, 48 B: first and last node) of base b.
 __device__ __forceinline__ void prefetch_stencil_l1(const float4* g, uint32_t px, uint32_t pxy) {
 #pragma unroll
@@ -92,7 +101,7 @@ struct PlaneSet<5> {  // P0 {x, vx}, P3 {C6..8, F0}, P4, P5 {F}, PR
 
 // Per-lane producer of the staging ring: issues the planes of the lane's k-th sorted
 // particle (lanes past their count commit an empty group, keeping the wait counts uniform).
-template <int NP, int NS = kStages>
+template <int NP, int NS = kStages, bool CG = false>
 struct Stager {
     float4* buf;        // this warp's ring: [NS][NP][32]
     uint32_t slot0;     // first slot of the group
@@ -107,7 +116,7 @@ struct Stager {
             const uint32_t s = slot(k);
             float4* dst = buf + (k % NS) * NP * 32 + lane;
 #pragma unroll
-            for (int q = 0; q < NP; ++q) cp_async16(dst + q * 32, P.pl[PlaneSet<NP>::plane(q)] + s);
+            for (int q = 0; q < NP; ++q) cp_async16<CG>(dst + q * 32, P.pl[PlaneSet<NP>::plane(q)] + s);
         }
         cp_commit();
     }
@@ -372,7 +381,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_p2g(cons
     const int lane = threadIdx.x & 31;
     const uint32_t n_groups = *P.n_groups;
     const uint32_t wpb = blockDim.x >> 5;
-    Stager<NP> st;
+    Stager<NP, kStages, MPMB_P2G_CG != 0> st;
     st.buf = smem + (threadIdx.x >> 5) * (kStages * NP * 32);
     st.lane = lane;
     uint32_t* bins = reinterpret_cast<uint32_t*>(st.buf);  // sort scratch aliases the ring
@@ -646,7 +655,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(cons
     const uint32_t n_groups = *P.n_groups;
     const uint32_t wpb = blockDim.x >> 5;
     constexpr int NS = kG2PStages;
-    Stager<NP, NS> st;
+    Stager<NP, NS, MPMB_G2P_CG != 0> st;
     st.buf = smem + (threadIdx.x >> 5) * (NS * NP * 32);
     st.lane = lane;
     for (uint32_t g = blockIdx.x * wpb + (threadIdx.x >> 5); g < n_groups; g += gridDim.x * wpb) {

@@ -19,5 +19,5 @@ for r in rows:
     L.append((e, st, f"{fname}:{r[0]}", r[1].strip()[:80]))
 te, ts = sum(x[0] for x in L) or 1, sum(x[1] for x in L) or 1
 print("inst%  stall%  line")
-for e, st, loc, s in sorted(L, key=lambda x: -x[0])[:top]:
+for e, st, loc, s in sorted(L, key=lambda x: -x[1 if len(sys.argv) > 4 else 0])[:top]:
     print("%5.1f  %5.1f  %-22s %s" % (100 * e / te, 100 * st / ts, loc, s))
