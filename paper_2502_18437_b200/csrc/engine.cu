@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cfloat>
 #include <cmath>
 #include <atomic>
@@ -141,7 +142,8 @@ struct Engine::Impl {
     bool exact = false;   // exact mode (k_exact.cu): the reference's arithmetic and order
     DevBuf ex_scratch, ex_bidx;
     uint32_t ex_epoch = 0;
-    DevBuf ex_ckey, ex_crec, ex_cn, ex_cscratch;  // exact contact records (k_exact.cu)
+    DevBuf ex_ckey, ex_crec, ex_cn, ex_cscratch;
+    bool wide = false;  // thread-per-slot G2P (small problems, launch_g2p)  // exact contact records (k_exact.cu)
     PinnedBuf ex_cn_host;
     // misc u32 slots: [0] n_active_bricks
     int64_t n = 0;      // particles
@@ -275,6 +277,16 @@ struct Engine::Impl {
         return P;
     }
 };
+
+// Below this many slots G2P runs one thread per slot: one warp per 256-slot group
+// would leave most of the 148 SMs idle (MPMB_WIDE_MAX overrides; measured).
+static int64_t wide_max_slots() {
+    static const int64_t v = [] {
+        const char* e = std::getenv("MPMB_WIDE_MAX");
+        return e ? std::atoll(e) : static_cast<int64_t>(kWideMaxSlots);
+    }();
+    return v;
+}
 
 Engine::Engine(const std::vector<SceneGrid>& scenes) : impl_(new Impl), scenes_(scenes) {
     Impl& I = *impl_;
@@ -434,6 +446,7 @@ void Engine::upload_particles(int64_t n, const float* x, const float* v, const f
     check(cudaStreamSynchronize(I.st), "sync");
     I.n = n;
     I.n_cap = (n > 0 || I.cap_hint > 0) ? std::max<int64_t>(n, I.cap_hint) + kGroup : 0;
+    I.wide = I.n_cap > 0 && I.n_cap <= wide_max_slots();
     n_total_ = n;
     for (int b = 0; b < 2; ++b)
         for (int q = 0; q < kPlanes; ++q) I.planes[b][q].alloc(sizeof(float4) * std::max<int64_t>(I.n_cap, 1));
@@ -754,7 +767,7 @@ void Engine::g2p_mls(int sub, float dt, bool pushout, bool deactivate) {
         I.end(CAT_G2P, ev);
         return;
     }
-    launch_g2p(P, false, (I.n + kGroup - 1) / kGroup, I.st);
+    launch_g2p(P, false, (I.n + kGroup - 1) / kGroup, I.st, false, I.wide);
     I.counted(1);
     I.cur = 1 - I.cur;  // G2P wrote the group-sorted state into the other buffer
     I.end(CAT_G2P, ev);
@@ -774,7 +787,7 @@ void Engine::g2p_standard(int sub, float dt, bool pushout, bool deactivate) {
     P.pushout = pushout ? 1 : 0;
     P.deactivate = deactivate ? 1 : 0;
     P.commit = 1;
-    launch_g2p(P, false, (I.n + kGroup - 1) / kGroup, I.st, true);
+    launch_g2p(P, false, (I.n + kGroup - 1) / kGroup, I.st, true, I.wide);
     I.counted(1);
     I.cur = 1 - I.cur;
     I.end(CAT_G2P, ev);
@@ -791,7 +804,7 @@ void Engine::g2p_pb(int sub, float dt, bool commit, bool pushout, bool deactivat
     P.commit = commit ? 1 : 0;
     P.pushout = pushout ? 1 : 0;
     P.deactivate = deactivate ? 1 : 0;
-    launch_g2p(P, true, (I.n + kGroup - 1) / kGroup, I.st);
+    launch_g2p(P, true, (I.n + kGroup - 1) / kGroup, I.st, false, I.wide);
     I.counted(1);
     I.cur = 1 - I.cur;
     I.end(CAT_G2P, ev);

@@ -372,6 +372,63 @@ __device__ __forceinline__ uint64_t group_sort(const Params& P, uint32_t g, uint
     return mine;
 }
 
+// One particle's P2G inputs (solvers.hpp:151-169 / 88-104 / 218-235) from its 7 planes:
+// scene, stencil base b, weights w, rel = node - x (STD: the weight derivatives), the
+// affine / impulse matrix A, mass m and velocity v.
+template <bool MLS, bool STD>
+__device__ __forceinline__ void p2g_prepare(const Params& P, const float4 q0, const float4 q1, const float4 q2,
+                                            const float4 q3, const float4 q4, const float4 q5, const float4 r,
+                                            int& scene, int b[3], float w[3][3], float rel[3][3], float A[9],
+                                            float& m, float v[3]) {
+    const uint32_t flags = __float_as_uint(r.z);
+    const float x[3] = {q0.x, q0.y, q0.z};
+    v[0] = q0.w; v[1] = q1.x; v[2] = q1.y;
+    const float Cm[9] = {q1.z, q1.w, q2.x, q2.y, q2.z, q2.w, q3.x, q3.y, q3.z};
+    scene = static_cast<int>((flags >> kSceneShift) & kSceneMask);
+    const SceneView S = scene_view(P, scene);
+    float fx[3];
+    local_base(P.geo, x, b, fx);
+    m = r.x;
+    // affine = m C - dt V (4/dx^2) sigma  (solvers.hpp:154-156; PB: m C, :222)
+    if (MLS) {
+        const float F[9] = {q3.w, q4.x, q4.y, q4.z, q4.w, q5.x, q5.y, q5.z, q5.w};
+        float sig[9];
+        float J;  // det F (solvers.hpp:154)
+        if (P.use_stress_in) {  // explicitly uploaded stress cache (solvers.hpp:156)
+            const float* s9 = P.stress_in + 9ull * __float_as_uint(r.w);
+#pragma unroll
+            for (int i = 0; i < 9; ++i) sig[i] = s9[i];
+            J = det3(F);
+        } else {  // cached stress == sigma(F) of the last G2P (solvers.hpp:69-74)
+            const float4 mat = material(P, flags & kMatMask);
+            J = neo_hookean_f32(F, mat.y, mat.z, sig);
+        }
+        if (STD) {  // impulse_m = sigma (-dt V), V = det(F) V0 (solvers.hpp:91-92)
+            const float sc = -P.dt * (J * r.y);
+#pragma unroll
+            for (int i = 0; i < 9; ++i) A[i] = sig[i] * sc;
+        } else {
+            const float sc = -P.dt * (J * r.y) * S.m_inv;
+#pragma unroll
+            for (int i = 0; i < 9; ++i) A[i] = fmaf(Cm[i], m, sig[i] * sc);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 9; ++i) A[i] = Cm[i] * m;
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        bspline_w(fx[a], w[a]);
+        if (STD) {
+            bspline_dw(fx[a], S.inv_dx, rel[a]);
+        } else {
+#pragma unroll
+            for (int o = 0; o < 3; ++o)  // node_position - x (state.hpp:49-51)
+                rel[a][o] = node_coord(P.geo, a, b[a] + o) - x[a];
+        }
+    }
+}
+
 // MLS: stress impulse from F (MLS-MPM, solvers.hpp:151-169; with STD: standard MPM's force
 // transfer, solvers.hpp:88-104); !MLS: PB-MPM (A = m C, solvers.hpp:218-235)
 template <bool MLS, bool STD = false>
@@ -409,57 +466,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_p2g(cons
             if (k >= st.cnt) continue;
             const float4* src = st.buf + (k % kStages) * NP * 32 + lane;
             const float4 r = src[PR * 32];
-            const uint32_t flags = __float_as_uint(r.z);
             const float4 q0 = src[0], q1 = src[32], q2 = src[64], q3 = src[96], q4 = src[128], q5 = src[160];
-            const float x[3] = {q0.x, q0.y, q0.z};
-            const float v[3] = {q0.w, q1.x, q1.y};
-            const float Cm[9] = {q1.z, q1.w, q2.x, q2.y, q2.z, q2.w, q3.x, q3.y, q3.z};
-            const int scene = static_cast<int>((flags >> kSceneShift) & kSceneMask);
-            const SceneView S = scene_view(P, scene);
-            int b[3];
-            float fx[3];
-            local_base(P.geo, x, b, fx);
-            const float m = r.x;
-            // affine = m C - dt V (4/dx^2) sigma  (solvers.hpp:154-156; PB: m C, :222)
-            float A[9];
-            if (MLS) {
-                const float F[9] = {q3.w, q4.x, q4.y, q4.z, q4.w, q5.x, q5.y, q5.z, q5.w};
-                float sig[9];
-                float J;  // det F (solvers.hpp:154)
-                if (P.use_stress_in) {  // explicitly uploaded stress cache (solvers.hpp:156)
-                    const float* s9 = P.stress_in + 9ull * __float_as_uint(r.w);
-#pragma unroll
-                    for (int i = 0; i < 9; ++i) sig[i] = s9[i];
-                    J = det3(F);
-                } else {  // cached stress == sigma(F) of the last G2P (solvers.hpp:69-74)
-                    const float4 mat = material(P, flags & kMatMask);
-                    J = neo_hookean_f32(F, mat.y, mat.z, sig);
-                }
-                if (STD) {  // impulse_m = sigma (-dt V), V = det(F) V0 (solvers.hpp:91-92)
-                    const float sc = -P.dt * (J * r.y);
-#pragma unroll
-                    for (int i = 0; i < 9; ++i) A[i] = sig[i] * sc;
-                } else {
-                    const float sc = -P.dt * (J * r.y) * S.m_inv;
-#pragma unroll
-                    for (int i = 0; i < 9; ++i) A[i] = fmaf(Cm[i], m, sig[i] * sc);
-                }
-            } else {
-#pragma unroll
-                for (int i = 0; i < 9; ++i) A[i] = Cm[i] * m;
-            }
-            float w[3][3], rel[3][3];  // STD: rel holds the weight derivatives
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                bspline_w(fx[a], w[a]);
-                if (STD) {
-                    bspline_dw(fx[a], S.inv_dx, rel[a]);
-                } else {
-#pragma unroll
-                    for (int o = 0; o < 3; ++o)  // node_position - x (state.hpp:49-51)
-                        rel[a][o] = node_coord(P.geo, a, b[a] + o) - x[a];
-                }
-            }
+            int scene, b[3];
+            float w[3][3], rel[3][3], A[9], m, v[3];  // STD: rel holds the weight derivatives
+            p2g_prepare<MLS, STD>(P, q0, q1, q2, q3, q4, q5, r, scene, b, w, rel, A, m, v);
             if (b[0] != cb[0] || b[1] != cb[1] || b[2] != cb[2] || scene != cscene) {
                 if (cscene >= 0) p2g_flush(P, scene_view(P, cscene), cb, pa, pb);
                 cb[0] = b[0]; cb[1] = b[1]; cb[2] = b[2];
@@ -645,6 +655,91 @@ __device__ __forceinline__ void update_F(const float C[9], float dt, float F[9])
     for (int i = 0; i < 9; ++i) F[i] = Fn[i];
 }
 
+// Per-lane G2P state: the shape-range cache of the last scene and the counters.
+struct G2PLane {
+    int my_scene = 0;
+    int cs_scene = -1, cs_begin = 0, cs_count = 0;
+    float4 cs_lo = make_float4(0.f, 0.f, 0.f, -1.f), cs_hi = make_float4(0.f, 0.f, 0.f, -1.f);
+    int n_inv = 0, n_fail = 0, n_push = 0, n_deact = 0;
+};
+
+// One particle's G2P (MLS solvers.hpp:173-196; PB :240-277; STD :107-135) with the F update,
+// push-out and deactivation; p holds x, F (PB/STD: C) on entry, the new state on exit.
+template <bool PB, bool STD>
+__device__ __forceinline__ void g2p_particle(const Params& P, Part& p, float4& r, G2PLane& L) {
+    uint32_t flags = __float_as_uint(r.z);
+    const int scene = static_cast<int>((flags >> kSceneShift) & kSceneMask);
+    L.my_scene = scene;
+    const SceneView S = scene_view(P, scene);
+    int b[3];
+    float fx[3];
+    local_base(P.geo, p.x, b, fx);
+    float w[3][3], rel[3][3];  // STD: rel holds the weight derivatives
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        bspline_w(fx[a], w[a]);
+        if (STD) {
+            bspline_dw(fx[a], S.inv_dx, rel[a]);
+        } else {
+#pragma unroll
+            for (int o = 0; o < 3; ++o)
+                rel[a][o] = node_coord(P.geo, a, b[a] + o) - p.x[a];
+        }
+    }
+    float B[9];  // STD: the velocity gradient L
+    {
+        uint32_t base, px, pxy;
+        stencil_rows(P.geo, b, base, px, pxy);
+        if (STD) g2p_gather_std(P.grid_vel + S.node_base + base, px, pxy, w, rel, p.v, B);
+        else g2p_gather(P.grid_vel + S.node_base + base, px, pxy, w, rel, p.v, B);
+    }
+    bool do_commit;
+    if (STD) {  // solvers.hpp:130-134: x += v dt, F = (I + L dt) F; C unchanged
+        do_commit = true;
+    } else if (!PB) {  // solvers.hpp:191-195
+#pragma unroll
+        for (int i = 0; i < 9; ++i) p.C[i] = B[i] * S.m_inv;
+        do_commit = true;
+    } else {  // solvers.hpp:259-267
+        float Cc[9], Cn[9];
+#pragma unroll
+        for (int i = 0; i < 9; ++i) Cc[i] = B[i] * S.m_inv;
+        const float4 mat = material(P, flags & kMatMask);
+        if (corotational_project(p.F, Cc, P.dt, mat.w, Cn)) {
+#pragma unroll
+            for (int i = 0; i < 9; ++i) p.C[i] = Cn[i];
+        } else {
+            ++L.n_fail;
+        }
+        do_commit = P.commit != 0;
+    }
+    if (do_commit) {  // solvers.hpp:193-195 / 274-276
+        p.x[0] = FA(p.x[0], FM(p.v[0], P.dt));
+        p.x[1] = FA(p.x[1], FM(p.v[1], P.dt));
+        p.x[2] = FA(p.x[2], FM(p.v[2], P.dt));
+        update_F(STD ? B : p.C, P.dt, p.F);
+        if (det3(p.F) <= 0.f) ++L.n_inv;
+        if (P.pushout) {
+            if (scene != L.cs_scene) {  // per-lane cache of the scene's shape range
+                L.cs_scene = scene;
+                L.cs_begin = P.scenes[scene].shape_begin;
+                L.cs_count = P.scenes[scene].shape_count;
+                if (L.cs_count > 0) {
+                    L.cs_lo = P.cull[2 * L.cs_begin];
+                    L.cs_hi = P.cull[2 * L.cs_begin + 1];
+                }
+            }
+            if (L.cs_count > 0)
+                L.n_push += pushout_particle<true>(P, S, p.x, p.v, L.cs_begin, L.cs_count, L.cs_lo, L.cs_hi);
+        }
+        if (P.deactivate && !spline_in_domain(mk(p.x[0], p.x[1], p.x[2]), S)) {
+            flags &= ~kActiveBit;
+            r.z = __uint_as_float(flags);
+            ++L.n_deact;
+        }
+    }
+}
+
 // PB: PB-MPM (solvers.hpp:240-277); STD: standard MPM, PIC velocity + L (solvers.hpp:107-135,
 // C travels unchanged); neither: MLS-MPM (solvers.hpp:173-196)
 template <bool PB, bool STD = false>
@@ -678,10 +773,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(cons
         st.slot0 = g * kGroup;
         const int kmax = __reduce_max_sync(0xffffffffu, st.cnt);
         for (int k = 0; k < NS - 1; ++k) st.issue(P, k);
-        int my_scene = 0;
-        int cs_scene = -1, cs_begin = 0, cs_count = 0;
-        float4 cs_lo = make_float4(0.f, 0.f, 0.f, -1.f), cs_hi = cs_lo;
-        int n_inv = 0, n_fail = 0, n_push = 0, n_deact = 0;
+        G2PLane L;
         for (int k = 0; k < kmax; ++k) {
             st.issue(P, k + NS - 1);
             cp_wait<(NS > 3 ? NS - 2 : NS - 1)>();  // particles k (and k+1) have landed
@@ -701,7 +793,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(cons
             const uint32_t so = st.slot0 + group_phys(g2p_pos(lane, k));
             const float4* src = st.buf + (k % NS) * NP * 32 + lane;
             float4 r = src[(NP - 1) * 32];
-            uint32_t flags = __float_as_uint(r.z);
             Part p;
             {
                 const float4 q0 = src[0];
@@ -718,76 +809,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(cons
                     p.F[5] = q5.x; p.F[6] = q5.y; p.F[7] = q5.z; p.F[8] = q5.w;
                 }
             }
-            const int scene = static_cast<int>((flags >> kSceneShift) & kSceneMask);
-            my_scene = scene;
-            const SceneView S = scene_view(P, scene);
-            int b[3];
-            float fx[3];
-            local_base(P.geo, p.x, b, fx);
-            float w[3][3], rel[3][3];  // STD: rel holds the weight derivatives
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                bspline_w(fx[a], w[a]);
-                if (STD) {
-                    bspline_dw(fx[a], S.inv_dx, rel[a]);
-                } else {
-#pragma unroll
-                    for (int o = 0; o < 3; ++o)
-                        rel[a][o] = node_coord(P.geo, a, b[a] + o) - p.x[a];
-                }
-            }
-            float B[9];  // STD: the velocity gradient L
-            {
-                uint32_t base, px, pxy;
-                stencil_rows(P.geo, b, base, px, pxy);
-                if (STD) g2p_gather_std(P.grid_vel + S.node_base + base, px, pxy, w, rel, p.v, B);
-                else g2p_gather(P.grid_vel + S.node_base + base, px, pxy, w, rel, p.v, B);
-            }
-            bool do_commit;
-            if (STD) {  // solvers.hpp:130-134: x += v dt, F = (I + L dt) F; C unchanged
-                do_commit = true;
-            } else if (!PB) {  // solvers.hpp:191-195
-#pragma unroll
-                for (int i = 0; i < 9; ++i) p.C[i] = B[i] * S.m_inv;
-                do_commit = true;
-            } else {  // solvers.hpp:259-267
-                float Cc[9], Cn[9];
-#pragma unroll
-                for (int i = 0; i < 9; ++i) Cc[i] = B[i] * S.m_inv;
-                const float4 mat = material(P, flags & kMatMask);
-                if (corotational_project(p.F, Cc, P.dt, mat.w, Cn)) {
-#pragma unroll
-                    for (int i = 0; i < 9; ++i) p.C[i] = Cn[i];
-                } else {
-                    ++n_fail;
-                }
-                do_commit = P.commit != 0;
-            }
-            if (do_commit) {  // solvers.hpp:193-195 / 274-276
-                p.x[0] = FA(p.x[0], FM(p.v[0], P.dt));
-                p.x[1] = FA(p.x[1], FM(p.v[1], P.dt));
-                p.x[2] = FA(p.x[2], FM(p.v[2], P.dt));
-                update_F(STD ? B : p.C, P.dt, p.F);
-                if (det3(p.F) <= 0.f) ++n_inv;
-                if (P.pushout) {
-                    if (scene != cs_scene) {  // per-lane cache of the scene's shape range
-                        cs_scene = scene;
-                        cs_begin = P.scenes[scene].shape_begin;
-                        cs_count = P.scenes[scene].shape_count;
-                        if (cs_count > 0) {
-                            cs_lo = P.cull[2 * cs_begin];
-                            cs_hi = P.cull[2 * cs_begin + 1];
-                        }
-                    }
-                    if (cs_count > 0)
-                        n_push += pushout_particle<true>(P, S, p.x, p.v, cs_begin, cs_count, cs_lo, cs_hi);
-                }
-                if (P.deactivate && !spline_in_domain(mk(p.x[0], p.x[1], p.x[2]), S)) {
-                    flags &= ~kActiveBit;
-                    r.z = __uint_as_float(flags);
-                    ++n_deact;
-                }
-            }
+            g2p_particle<PB, STD>(P, p, r, L);
             store_part_out(P, so, p, r);
         }
         // inactive particles and holes of the group move to their new slots unchanged
@@ -796,12 +818,50 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(cons
 #pragma unroll
             for (int q = 0; q < kPlanes; ++q) P.pl_out[q][so] = P.pl[q][si];
         }
-        add_scene_counter(P.counters, my_scene, 0, n_inv);
-        add_scene_counter(P.counters, my_scene, 1, n_fail);
-        add_scene_counter(P.counters, my_scene, 2, n_push);
-        add_scene_counter(P.counters, my_scene, 3, n_deact);
+        add_scene_counter(P.counters, L.my_scene, 0, L.n_inv);
+        add_scene_counter(P.counters, L.my_scene, 1, L.n_fail);
+        add_scene_counter(P.counters, L.my_scene, 2, L.n_push);
+        add_scene_counter(P.counters, L.my_scene, 3, L.n_deact);
     }
     cp_wait<0>();
+}
+
+// Wide G2P for small problems, where one warp per group would leave most SMs idle: one
+// thread per slot, written to the same slot of the other buffer (inactive particles and
+// holes copied unchanged).  The slot layout stays as binned; P2G's group sort is stable on
+// any input order, so it pairs with the grouped P2G (a thread-per-slot P2G loses its
+// register accumulation to L2 atomic contention: measured 1.8x slower at C2).
+template <bool PB, bool STD = false>
+__global__ void __launch_bounds__(128) k_g2p_wide(const __grid_constant__ Params P) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < P.n_total; base += stride) {
+        const int64_t s = base + threadIdx.x;  // the warp stays converged for the counters
+        G2PLane L;
+        if (s < P.n_total) {
+            float4 r = P.pl[PR][s];
+            if (__float_as_uint(r.w) == kHoleOrig || !(__float_as_uint(r.z) & kActiveBit)) {
+#pragma unroll
+                for (int q = 0; q < kPlanes; ++q) P.pl_out[q][s] = P.pl[q][s];
+            } else {
+                Part p;
+                const float4 q0 = P.pl[0][s], q3 = P.pl[3][s], q4 = P.pl[4][s], q5 = P.pl[5][s];
+                p.x[0] = q0.x; p.x[1] = q0.y; p.x[2] = q0.z;
+                p.F[0] = q3.w; p.F[1] = q4.x; p.F[2] = q4.y; p.F[3] = q4.z; p.F[4] = q4.w;
+                p.F[5] = q5.x; p.F[6] = q5.y; p.F[7] = q5.z; p.F[8] = q5.w;
+                if (PB || STD) {
+                    const float4 q1 = P.pl[1][s], q2 = P.pl[2][s];
+                    p.C[0] = q1.z; p.C[1] = q1.w; p.C[2] = q2.x; p.C[3] = q2.y; p.C[4] = q2.z;
+                    p.C[5] = q2.w; p.C[6] = q3.x; p.C[7] = q3.y; p.C[8] = q3.z;
+                }
+                g2p_particle<PB, STD>(P, p, r, L);
+                store_part_out(P, static_cast<uint32_t>(s), p, r);
+            }
+        }
+        add_scene_counter(P.counters, L.my_scene, 0, L.n_inv);
+        add_scene_counter(P.counters, L.my_scene, 1, L.n_fail);
+        add_scene_counter(P.counters, L.my_scene, 2, L.n_push);
+        add_scene_counter(P.counters, L.my_scene, 3, L.n_deact);
+    }
 }
 
 // ================================================  standalone push-out / deactivation
@@ -886,7 +946,14 @@ void launch_p2g(const Params& P, bool mls, int64_t max_groups, cudaStream_t st, 
     else k_p2g<false><<<blocks, threads, smem, st>>>(P);
 }
 
-void launch_g2p(const Params& P, bool pb, int64_t max_groups, cudaStream_t st, bool standard) {
+void launch_g2p(const Params& P, bool pb, int64_t max_groups, cudaStream_t st, bool standard, bool wide) {
+    if (wide) {
+        const int b = grid_for(P.n_total, 128, 148 * 16);
+        if (standard) k_g2p_wide<false, true><<<b, 128, 0, st>>>(P);
+        else if (pb) k_g2p_wide<true><<<b, 128, 0, st>>>(P);
+        else k_g2p_wide<false><<<b, 128, 0, st>>>(P);
+        return;
+    }
     const int threads = kWarpsPerBlock * 32;
     const int blocks = grid_for(max_groups * 32, threads, 148 * 16);
     const int smem7 = kWarpsPerBlock * kG2PStages * 7 * 32 * static_cast<int>(sizeof(float4));

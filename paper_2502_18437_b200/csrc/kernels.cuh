@@ -23,6 +23,7 @@ namespace mpmb {
 
 // slots per transfer group: one warp re-sorts and processes one group per substep
 constexpr int kGroup = 256;
+constexpr int64_t kWideMaxSlots = 600000;  // engine: thread-per-slot G2P at or below this (A/B)
 // Inside a group the particle of sorted position p lives at slot phys(p): lane L's k-th
 // particle of P2G (p = 8L + k) sits at 32k + L, so a stable order makes every P2G staging
 // load one contiguous 512-byte span, and G2P (p = L + 32k) touches 8 runs of 64 bytes.

@@ -38,9 +38,12 @@ void launch_exclusive_scan(const uint32_t* in, uint32_t* out, int64_t n, uint32_
 
 // ---- K2..K7 (k_transfer.cu, k_step.cu); max_groups = ceil(n / kGroup) ----
 void launch_p2g(const Params& P, bool mls, int64_t max_groups, cudaStream_t st, bool standard = false);
+// wide: one thread per slot (k_g2p_wide) for problems too small to fill the GPU with one warp
+// per group
 void launch_grid_update(const Params& P, int64_t max_bricks, cudaStream_t st);
 void launch_shape_cull(const Params& P, cudaStream_t st);
-void launch_g2p(const Params& P, bool pb, int64_t max_groups, cudaStream_t st, bool standard = false);
+void launch_g2p(const Params& P, bool pb, int64_t max_groups, cudaStream_t st, bool standard = false,
+                bool wide = false);
 void launch_collect_bricks(const Params& P, uint32_t n_bricks, cudaStream_t st);
 void launch_pushout(const Params& P, cudaStream_t st);
 void launch_deactivate(const Params& P, cudaStream_t st);
