@@ -22,6 +22,7 @@ __device__ __forceinline__ uint64_t brick_node(const Params& P, uint32_t gb, int
 // (DevShape::lbox) under this substep's pose (kinematic table or integrated free pose):
 // cull[2i] = {min, bounded ? 1 : -1}, cull[2i+1] = {max, 0}.
 __global__ void k_shape_cull(const Params P) {
+    pdl_enter();
     for (int i = threadIdx.x; i < P.n_shapes; i += blockDim.x) {
         const DevShape& sh = P.shapes[i];
         if (sh.lbox_h[0] < 0.f) {
@@ -46,7 +47,7 @@ __global__ void k_shape_cull(const Params P) {
     }
 }
 
-void launch_shape_cull(const Params& P, cudaStream_t st) { k_shape_cull<<<1, 128, 0, st>>>(P); }
+void launch_shape_cull(const Params& P, cudaStream_t st) { launch_chain(k_shape_cull, 1, 128, 0, st, P); }
 
 // ==============================================================  grid update
 // 64 threads per active brick (one node each).  Reads the P2G accumulator and zeroes it
@@ -58,6 +59,7 @@ void launch_shape_cull(const Params& P, cudaStream_t st) { k_shape_cull<<<1, 128
 // over the grid-stride loop: brick ids are loaded two iterations ahead and accumulators
 // one ahead; the scene follows from the brick id arithmetically (uniform geometry).
 __global__ void __launch_bounds__(256) k_grid_update(const Params P) {
+    pdl_enter();
     const uint32_t n_bricks = *P.n_active_bricks;
     const int l = threadIdx.x & 63;
     const uint32_t per_block = blockDim.x >> 6;
@@ -200,6 +202,7 @@ __global__ void __launch_bounds__(256) k_grid_bc(const Params P) {
 // integrate_free_body (rigid_dynamics.hpp:82-103) with this substep's impulse, then merge
 // the substep accumulators into the frame accumulators (scene.hpp:220-232).
 __global__ void k_free_bodies(const Params P, int integrate, int merge) {
+    pdl_enter();
     for (int i = threadIdx.x; i < P.n_shapes; i += blockDim.x) {
         const DevShape& sh = P.shapes[i];
         if (integrate && sh.motion == MOTION_FREE) {
@@ -285,14 +288,14 @@ static int grid_for(int64_t work, int threads, int max_blocks) {
 void launch_grid_update(const Params& P, int64_t max_bricks, cudaStream_t st) {
     const int threads = 256;
     const int blocks = grid_for(max_bricks * 64, threads, 148 * 8);
-    k_grid_update<<<blocks, threads, 0, st>>>(P);
+    launch_chain(k_grid_update, blocks, threads, 0, st, P);
 }
 
 
 
 
 void launch_free_bodies(const Params& P, bool integrate, bool merge, cudaStream_t st) {
-    k_free_bodies<<<1, 128, 0, st>>>(P, integrate ? 1 : 0, merge ? 1 : 0);
+    launch_chain(k_free_bodies, 1, 128, 0, st, P, integrate ? 1 : 0, merge ? 1 : 0);
 }
 
 void launch_grid_bc(const Params& P, int64_t max_bricks, cudaStream_t st) {

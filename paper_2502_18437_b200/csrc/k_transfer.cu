@@ -246,6 +246,7 @@ __device__ __forceinline__ void bspline_dw(float fx, float inv_dx, float dw[3]) 
 // here: the flag arrays alternate per substep and this pass zeroes the OTHER one, which
 // the next P2G marks.
 __global__ void __launch_bounds__(256) k_collect_bricks(const Params P, uint32_t n_bricks) {
+    pdl_enter();
     const unsigned full = 0xffffffffu;
     const uint32_t stride = gridDim.x * blockDim.x;
     const uint32_t nb0 = P.geo.nb[0], nb1 = P.geo.nb[1], bps = P.geo.bricks_per_scene;
@@ -277,7 +278,7 @@ void launch_collect_bricks(const Params& P, uint32_t n_bricks, cudaStream_t st) 
     int64_t blocks = (static_cast<int64_t>(n_bricks) + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
     if (blocks < 1) blocks = 1;
-    k_collect_bricks<<<static_cast<int>(blocks), 256, 0, st>>>(P, n_bricks);
+    launch_chain(k_collect_bricks, static_cast<int>(blocks), 256, 0, st, P, n_bricks);
 }
 
 __device__ __forceinline__ uint32_t bin_word(uint32_t b) { return b + (b >> 5); }
@@ -433,6 +434,7 @@ __device__ __forceinline__ void p2g_prepare(const Params& P, const float4 q0, co
 // transfer, solvers.hpp:88-104); !MLS: PB-MPM (A = m C, solvers.hpp:218-235)
 template <bool MLS, bool STD = false>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_p2g(const __grid_constant__ Params P) {
+    pdl_enter();
     extern __shared__ float4 smem[];
     constexpr int NP = kPlanes;
     const int lane = threadIdx.x & 31;
@@ -744,6 +746,7 @@ __device__ __forceinline__ void g2p_particle(const Params& P, Part& p, float4& r
 // C travels unchanged); neither: MLS-MPM (solvers.hpp:173-196)
 template <bool PB, bool STD = false>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(const __grid_constant__ Params P) {
+    pdl_enter();
     extern __shared__ float4 smem[];
     constexpr int NP = (PB || STD) ? 7 : 5;
     const int lane = threadIdx.x & 31;
@@ -833,6 +836,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(cons
 // register accumulation to L2 atomic contention: measured 1.8x slower at C2).
 template <bool PB, bool STD = false>
 __global__ void __launch_bounds__(128) k_g2p_wide(const __grid_constant__ Params P) {
+    pdl_enter();
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < P.n_total; base += stride) {
         const int64_t s = base + threadIdx.x;  // the warp stays converged for the counters
@@ -941,17 +945,17 @@ void launch_p2g(const Params& P, bool mls, int64_t max_groups, cudaStream_t st, 
         opt_in_smem(k_p2g<true, true>, smem);
         attr = true;
     }
-    if (standard) k_p2g<true, true><<<blocks, threads, smem, st>>>(P);
-    else if (mls) k_p2g<true><<<blocks, threads, smem, st>>>(P);
-    else k_p2g<false><<<blocks, threads, smem, st>>>(P);
+    if (standard) launch_chain(k_p2g<true, true>, blocks, threads, smem, st, P);
+    else if (mls) launch_chain(k_p2g<true>, blocks, threads, smem, st, P);
+    else launch_chain(k_p2g<false>, blocks, threads, smem, st, P);
 }
 
 void launch_g2p(const Params& P, bool pb, int64_t max_groups, cudaStream_t st, bool standard, bool wide) {
     if (wide) {
         const int b = grid_for(P.n_total, 128, 148 * 16);
-        if (standard) k_g2p_wide<false, true><<<b, 128, 0, st>>>(P);
-        else if (pb) k_g2p_wide<true><<<b, 128, 0, st>>>(P);
-        else k_g2p_wide<false><<<b, 128, 0, st>>>(P);
+        if (standard) launch_chain(k_g2p_wide<false, true>, b, 128, 0, st, P);
+        else if (pb) launch_chain(k_g2p_wide<true>, b, 128, 0, st, P);
+        else launch_chain(k_g2p_wide<false>, b, 128, 0, st, P);
         return;
     }
     const int threads = kWarpsPerBlock * 32;
@@ -965,9 +969,9 @@ void launch_g2p(const Params& P, bool pb, int64_t max_groups, cudaStream_t st, b
         opt_in_smem(k_g2p<false>, smem5);
         attr = true;
     }
-    if (standard) k_g2p<false, true><<<blocks, threads, smem7, st>>>(P);
-    else if (pb) k_g2p<true><<<blocks, threads, smem7, st>>>(P);
-    else k_g2p<false><<<blocks, threads, smem5, st>>>(P);
+    if (standard) launch_chain(k_g2p<false, true>, blocks, threads, smem7, st, P);
+    else if (pb) launch_chain(k_g2p<true>, blocks, threads, smem7, st, P);
+    else launch_chain(k_g2p<false>, blocks, threads, smem5, st, P);
 }
 
 void launch_pushout(const Params& P, cudaStream_t st) {

@@ -16,6 +16,8 @@
 #pragma once
 #include <climits>
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 
 #include "dev_math.cuh"
 
@@ -218,6 +220,39 @@ __device__ __forceinline__ void add_scene_counter(int* counters, int scene, int 
     } else if (value != 0) {
         atomicAdd(&counters[4 * scene + slot], value);
     }
+}
+
+// ---- programmatic dependent launch (PDL) for the per-substep kernel chain -------------
+// A chain kernel is launched with programmatic stream serialisation: its grid may start while
+// the previous kernel's last blocks drain, and waits at entry (griddepcontrol.wait) until that
+// kernel has completed and its writes are visible.  Waiting first thing keeps every RAW / WAR
+// order of the plain stream; what overlaps is the launch latency and block rasterisation.
+// Launched without the attribute (MPMB_PDL=0) both instructions are no-ops.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+inline bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("MPMB_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+template <typename... Exp, typename... Act>
+inline void launch_chain(void (*kernel)(Exp...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                         Act&&... args) {
+    cudaLaunchConfig_t c{};
+    c.gridDim = grid;
+    c.blockDim = block;
+    c.dynamicSmemBytes = smem;
+    c.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    c.attrs = at;
+    c.numAttrs = pdl_enabled() ? 1 : 0;
+    cudaLaunchKernelEx(&c, kernel, std::forward<Act>(args)...);
 }
 
 }  // namespace mpmb

@@ -13,6 +13,10 @@ spec = scenes.cutting(dims=(128, 128, 128), dx=1.4 / 128, box=((0.3, 0.075, 0.3)
 b = bench.build_batch([spec])
 n = b.scenes[0].particle_count()
 b.advance_frames(0.02, 3); b.fetch_results()
+b.synchronize()
+t = time.time(); b.advance_frames(0.02, F); b.synchronize(); wall0 = time.time() - t
+b.fetch_results()
+print(f"1M scene, profiling off: {n * 10 * F / wall0:.3g} p-substeps/s ({1e3 * wall0 / (10 * F):.3f} ms/substep)")
 b.set_profiling(True)
 t = time.time(); b.advance_frames(0.02, F); b.synchronize(); wall = time.time() - t
 p = b.profile(); b.fetch_results()
