@@ -886,7 +886,7 @@ void run_frame(Batch& b, float dt) {
             e.grid_update(sub, dt_sub, cfg.gravity, true, true, cfg.boundary);
             if (standard) e.g2p_standard(sub, dt_sub, true, true);
             else e.g2p_mls(sub, dt_sub, true, true);
-            if (ns > 0) e.free_bodies(sub, dt_sub, cfg.gravity, any_free, true);
+            if (ns > 0) e.free_bodies(sub, dt_sub, cfg.gravity, any_free, true, sub + 1 < n_sub ? sub + 1 : -1);
         }
     } else {
         e.bin();

@@ -143,7 +143,8 @@ struct Engine::Impl {
     DevBuf ex_scratch, ex_bidx;
     uint32_t ex_epoch = 0;
     DevBuf ex_ckey, ex_crec, ex_cn, ex_cscratch;
-    bool wide = false;  // thread-per-slot G2P (small problems, launch_g2p)  // exact contact records (k_exact.cu)
+    bool wide = false;  // thread-per-slot G2P (small problems, launch_g2p)
+    int cull_sub = -1;  // the substep whose shape cull table is current (-1: none)  // exact contact records (k_exact.cu)
     PinnedBuf ex_cn_host;
     // misc u32 slots: [0] n_active_bricks
     int64_t n = 0;      // particles
@@ -548,6 +549,7 @@ void Engine::download_particles(int64_t begin, int64_t count, float* x, float* v
 }
 
 void Engine::set_shapes(const std::vector<std::vector<EngineShape>>& per_scene) {
+    impl_->cull_sub = -1;
     Impl& I = *impl_;
     check(cudaStreamSynchronize(I.st), "sync");
     std::vector<DevShape> ds;
@@ -610,6 +612,7 @@ void Engine::set_shapes(const std::vector<std::vector<EngineShape>>& per_scene) 
 
 void Engine::set_pose_table(int n_sub, const std::vector<DevPose>& poses,
                             const std::vector<uint8_t>& ovr) {
+    impl_->cull_sub = -1;
     Impl& I = *impl_;
     if (I.n_shapes == 0) return;
     const size_t np = static_cast<size_t>(n_sub) * I.n_shapes;
@@ -634,6 +637,7 @@ void Engine::set_pose_table(int n_sub, const std::vector<DevPose>& poses,
 }
 
 void Engine::set_free_pose(int shape, const DevPose& pose) {
+    impl_->cull_sub = -1;
     Impl& I = *impl_;
     check(cudaStreamSynchronize(I.st), "sync");
     check(cudaMemcpy(I.free_pose.as<DevPose>() + shape, &pose, sizeof(DevPose), cudaMemcpyHostToDevice), "pose");
@@ -711,9 +715,10 @@ void Engine::grid_update(int sub, float dt, const float g[3], bool gravity, bool
     P.gravity = gravity ? 1 : 0;
     P.contact = contact ? 1 : 0;
     P.bc = bc;
-    if (I.n_shapes > 0) {  // G2P push-out of this substep reuses the table
+    if (I.n_shapes > 0 && I.cull_sub != P.sub) {  // G2P push-out of this substep reuses the table
         launch_shape_cull(P, I.st);
         I.counted(1);
+        I.cull_sub = P.sub;
     }
     const bool ex_contact = I.exact && contact && I.n_shapes > 0;
     if (ex_contact) {  // one record per contacting (node, shape): at most nodes x shapes
@@ -810,7 +815,7 @@ void Engine::g2p_pb(int sub, float dt, bool commit, bool pushout, bool deactivat
     I.end(CAT_G2P, ev);
 }
 
-void Engine::free_bodies(int sub, float dt, const float g[3], bool integrate, bool merge) {
+void Engine::free_bodies(int sub, float dt, const float g[3], bool integrate, bool merge, int cull_next) {
     Impl& I = *impl_;
     if (I.n_shapes == 0) return;
     auto ev = I.begin();
@@ -818,7 +823,10 @@ void Engine::free_bodies(int sub, float dt, const float g[3], bool integrate, bo
     P.sub = std::min(sub, I.table_subs - 1);
     P.dt = dt;
     P.g[0] = g[0]; P.g[1] = g[1]; P.g[2] = g[2];
-    launch_free_bodies(P, integrate, merge, I.st);
+    const int next = cull_next >= 0 ? std::min(cull_next, I.table_subs - 1) : -1;
+    launch_free_bodies(P, integrate, merge, I.st, next);
+    if (next >= 0) I.cull_sub = next;
+    else if (integrate) I.cull_sub = -1;  // the free bodies moved
     I.counted(1);
     I.end(CAT_OTHER, ev);
 }

@@ -101,7 +101,8 @@ class Engine {
     void set_exact(bool on);
     bool exact() const;
     void g2p_pb(int sub, float dt, bool commit, bool pushout, bool deactivate);  // K6
-    void free_bodies(int sub, float dt, const float g[3], bool integrate, bool merge);  // K7
+    // cull_next >= 0: also build that substep's shape cull table (saves its k_shape_cull)
+    void free_bodies(int sub, float dt, const float g[3], bool integrate, bool merge, int cull_next = -1);  // K7
     void bc_pass(int bc);                         // BC alone (hook adapter)
     void materialize_stress();                    // sigma(F) -> cached stress array
     void pushout(int sub);

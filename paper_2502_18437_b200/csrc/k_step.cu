@@ -21,16 +21,15 @@ __device__ __forceinline__ uint64_t brick_node(const Params& P, uint32_t gb, int
 // Per-substep shape cull table (one block): the world AABB of each shape's local box
 // (DevShape::lbox) under this substep's pose (kinematic table or integrated free pose):
 // cull[2i] = {min, bounded ? 1 : -1}, cull[2i+1] = {max, 0}.
-__global__ void k_shape_cull(const Params P) {
-    pdl_enter();
-    for (int i = threadIdx.x; i < P.n_shapes; i += blockDim.x) {
+__device__ __forceinline__ void cull_shape(const Params& P, int i, int sub) {
+    {
         const DevShape& sh = P.shapes[i];
         if (sh.lbox_h[0] < 0.f) {
             P.cull[2 * i] = make_float4(0.f, 0.f, 0.f, -1.f);
             P.cull[2 * i + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
-            continue;
+            return;
         }
-        const DevPose& pose = pose_of(P, i);
+        const DevPose& pose = pose_of_sub(P, i, sub);
         const float x = pose.rot[0], y = pose.rot[1], z = pose.rot[2], w = pose.rot[3];
         const float R[3][3] = {{1.f - 2.f * (y * y + z * z), 2.f * (x * y - z * w), 2.f * (x * z + y * w)},
                                {2.f * (x * y + z * w), 1.f - 2.f * (x * x + z * z), 2.f * (y * z - x * w)},
@@ -45,6 +44,11 @@ __global__ void k_shape_cull(const Params P) {
         P.cull[2 * i] = make_float4(c[0] - h[0], c[1] - h[1], c[2] - h[2], 1.f);
         P.cull[2 * i + 1] = make_float4(c[0] + h[0], c[1] + h[1], c[2] + h[2], 0.f);
     }
+}
+
+__global__ void k_shape_cull(const Params P) {
+    pdl_enter();
+    for (int i = threadIdx.x; i < P.n_shapes; i += blockDim.x) cull_shape(P, i, P.sub);
 }
 
 void launch_shape_cull(const Params& P, cudaStream_t st) { launch_chain(k_shape_cull, 1, 128, 0, st, P); }
@@ -201,7 +205,9 @@ __global__ void __launch_bounds__(256) k_grid_bc(const Params P) {
 // ==========================================================  free bodies (K7)
 // integrate_free_body (rigid_dynamics.hpp:82-103) with this substep's impulse, then merge
 // the substep accumulators into the frame accumulators (scene.hpp:220-232).
-__global__ void k_free_bodies(const Params P, int integrate, int merge) {
+// next_sub >= 0: also build the cull table of that substep (its poses are final once the free
+// bodies have moved), saving the next substep's k_shape_cull launch.
+__global__ void k_free_bodies(const Params P, int integrate, int merge, int next_sub) {
     pdl_enter();
     for (int i = threadIdx.x; i < P.n_shapes; i += blockDim.x) {
         const DevShape& sh = P.shapes[i];
@@ -273,6 +279,7 @@ __global__ void k_free_bodies(const Params P, int integrate, int merge) {
             P.cnt_frame[i] += P.cnt_sub[i];
             P.cnt_sub[i] = 0;
         }
+        if (next_sub >= 0) cull_shape(P, i, next_sub);
     }
 }
 
@@ -294,8 +301,8 @@ void launch_grid_update(const Params& P, int64_t max_bricks, cudaStream_t st) {
 
 
 
-void launch_free_bodies(const Params& P, bool integrate, bool merge, cudaStream_t st) {
-    launch_chain(k_free_bodies, 1, 128, 0, st, P, integrate ? 1 : 0, merge ? 1 : 0);
+void launch_free_bodies(const Params& P, bool integrate, bool merge, cudaStream_t st, int next_sub) {
+    launch_chain(k_free_bodies, 1, 128, 0, st, P, integrate ? 1 : 0, merge ? 1 : 0, next_sub);
 }
 
 void launch_grid_bc(const Params& P, int64_t max_bricks, cudaStream_t st) {

@@ -175,6 +175,11 @@ __device__ __forceinline__ void store_part(const Params& P, uint32_t s, const Pa
     P.pl[5][s] = make_float4(p.F[5], p.F[6], p.F[7], p.F[8]);
 }
 
+__device__ __forceinline__ const DevPose& pose_of_sub(const Params& P, int i, int sub) {
+    const int t = sub * P.n_shapes + i;
+    return (P.shapes[i].motion == MOTION_FREE && !P.pose_override[t]) ? P.free_pose[i]
+                                                                         : P.pose_table[t];
+}
 __device__ __forceinline__ const DevPose& pose_of(const Params& P, int i) {
     const int t = P.sub * P.n_shapes + i;
     return (P.shapes[i].motion == MOTION_FREE && !P.pose_override[t]) ? P.free_pose[i]

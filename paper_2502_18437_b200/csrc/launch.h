@@ -47,7 +47,7 @@ void launch_g2p(const Params& P, bool pb, int64_t max_groups, cudaStream_t st, b
 void launch_collect_bricks(const Params& P, uint32_t n_bricks, cudaStream_t st);
 void launch_pushout(const Params& P, cudaStream_t st);
 void launch_deactivate(const Params& P, cudaStream_t st);
-void launch_free_bodies(const Params& P, bool integrate, bool merge, cudaStream_t st);
+void launch_free_bodies(const Params& P, bool integrate, bool merge, cudaStream_t st, int next_sub = -1);
 void launch_grid_bc(const Params& P, int64_t max_bricks, cudaStream_t st);
 
 // ---- slab domain decomposition (k_dd.cu) ----

@@ -25,7 +25,10 @@ for _ in range(3):
     t2 = time.time()
     print(f"advance {1e3 * (t1 - t0):.2f} ms  fetch {1e3 * (t2 - t1):.2f} ms  ({25 * n / 1e6:.0f} MB)")
 # the e2e loop itself: advance + fetch back to back (the arrays' copy overlaps the next frame)
-for _ in range(8):
+import subprocess
+smi = subprocess.Popen(["nvidia-smi", "--query-gpu=clocks.sm,power.draw,clocks_event_reasons.active",
+                        "--format=csv,noheader", "-lms", "100"], stdout=subprocess.PIPE, text=True)
+for _ in range(20):
     t0 = time.time()
     b.advance(0.02)
     t1 = time.time()
@@ -34,6 +37,8 @@ for _ in range(8):
     print(f"pipelined: advance enqueue {1e3 * (t1 - t0):.2f} ms  fetch {1e3 * (t2 - t1):.2f} ms  "
           f"frame {1e3 * (t2 - t0):.2f} ms")
 b.synchronize()
+smi.terminate()
+print("clocks during the pipelined loop:", [l.strip() for l in smi.stdout.read().splitlines()][:40])
 host = torch.empty(25 * n, dtype=torch.uint8, pin_memory=True)
 dev = torch.empty(25 * n, dtype=torch.uint8, device="cuda")
 for _ in range(3):
