@@ -36,7 +36,9 @@ METRIC = "particle-substeps/sec"
 UNIT = "particle-substeps/s"
 DT_FRAME = 0.02
 # algorithmic bytes per particle per launch
-ALG_BYTES = {"p2g": 108.0, "g2p": 148.0, "grid": 0.0, "sort": 224.0}
+# per particle per launch.  fused = k_g2p2g (G2P of substep s + P2G of s+1):
+# one substep of compulsory state turnover, the §8d per-substep figure.
+ALG_BYTES = {"p2g": 108.0, "g2p": 148.0, "grid": 0.0, "sort": 224.0, "fused": 204.0}
 SUBSTEP_BYTES = 204.0
 
 
@@ -347,9 +349,14 @@ def run_ours(args, rank, world, local_rank):
     e2e = ps / (ms_e2e / 1e3)
     peak, peak_src = measured_peak()
     # dominant kernel class and its roofline (per-launch averages over the timed region)
-    launches_per_class = {"p2g": sub * args.steps, "g2p": sub * args.steps, "grid": sub * args.steps,
-                          "sort": args.steps if specs[0]["solver"] != "pbmpm" else args.steps}
-    cls_ms = {"p2g": prof["ms_p2g"], "g2p": prof["ms_g2p"], "grid": prof["ms_grid"], "sort": prof["ms_sort"]}
+    # with substep fusion (mpmb_set_fusion) the frame runs P2G and G2P alone once each and
+    # k_g2p2g sub-1 times
+    fused = prof["ms_fused"] > 0.0
+    n_sep = args.steps if fused else sub * args.steps
+    launches_per_class = {"p2g": n_sep, "g2p": n_sep, "grid": sub * args.steps, "sort": args.steps,
+                          "fused": (sub - 1) * args.steps if fused else 0}
+    cls_ms = {"p2g": prof["ms_p2g"], "g2p": prof["ms_g2p"], "grid": prof["ms_grid"], "sort": prof["ms_sort"],
+              "fused": prof["ms_fused"]}
     dom = max(cls_ms, key=lambda k: cls_ms[k])
     per_launch_ms = cls_ms[dom] / max(launches_per_class[dom], 1)
     alg = ALG_BYTES[dom] * n_particles

@@ -168,6 +168,7 @@ typedef struct {
     double ms_other;
     int64_t launches;            /* kernels launched by the library while profiling */
     int64_t particle_substeps;   /* active particles x substeps (PB: x iterations) */
+    double ms_fused;             /* k_g2p2g: G2P of substep s fused with P2G of s+1 (+ collect) */
 } mpmb_profile;
 
 /* ------------------------------------------------------------------ library */
@@ -338,6 +339,11 @@ mpmb_status mpmb_set_profiling(mpmb_handle h, int32_t on);
  * bit-identical to the reference and run to run (SPEC.md:252 deterministic mode), several
  * times slower than the default fast mode (float atomics). */
 mpmb_status mpmb_set_exact(mpmb_handle h, int32_t on);
+/* Substep fusion inside run_frame (Scene::run_frame, scene.hpp:199-235, MLS / standard):
+ * G2P of substep s and P2G of s+1 run as one kernel.  0 off, 1 (default) when the engine
+ * runs one warp per particle group, 2 always.  Results are the same up to float atomic
+ * order either way. */
+mpmb_status mpmb_set_fusion(mpmb_handle h, int32_t mode);
 mpmb_status mpmb_get_profile(mpmb_handle h, mpmb_profile* out);
 /* Blocks until every frame enqueued on h has finished. */
 mpmb_status mpmb_synchronize(mpmb_handle h);

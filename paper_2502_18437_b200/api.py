@@ -325,6 +325,18 @@ class Scene:
     def advance(self, dt):
         check(self.lib.mpmb_advance(self.h, float(F32(dt))), self.lib, "advance")
 
+    def set_fusion(self, mode: int):
+        """0 off, 1 (default) when G2P runs one warp per group, 2 always (mpmb_set_fusion)."""
+        check(self.lib.mpmb_set_fusion(self.h, mode), self.lib, "fusion")
+
+    def set_profiling(self, on: bool):
+        check(self.lib.mpmb_set_profiling(self.h, int(on)), self.lib, "profiling")
+
+    def profile(self) -> dict:
+        p = capi.Profile()
+        check(self.lib.mpmb_get_profile(self.h, C.byref(p)), self.lib, "profile")
+        return {k: getattr(p, k) for k, _ in capi.Profile._fields_}
+
     def fetch_results(self) -> dict:
         s = capi.FrameSummary()
         check(self.lib.mpmb_fetch_results(self.h, C.byref(s)), self.lib, "fetch")
@@ -394,6 +406,10 @@ class SceneBatch:
 
     def set_stream(self, stream_ptr: int):
         check(self.lib.mpmb_set_stream(self.h, C.c_void_p(stream_ptr)), self.lib, "set_stream")
+
+    def set_fusion(self, mode: int):
+        """0 off, 1 (default) when G2P runs one warp per group, 2 always (mpmb_set_fusion)."""
+        check(self.lib.mpmb_set_fusion(self.h, mode), self.lib, "fusion")
 
     def set_resort_interval(self, k: int):
         check(self.lib.mpmb_set_resort_interval(self.h, k), self.lib, "resort")

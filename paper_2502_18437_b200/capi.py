@@ -77,7 +77,7 @@ class FrameSummary(C.Structure):
 class Profile(C.Structure):
     _fields_ = [("ms_sort", C.c_double), ("ms_p2g", C.c_double), ("ms_grid", C.c_double),
                 ("ms_g2p", C.c_double), ("ms_other", C.c_double), ("launches", C.c_int64),
-                ("particle_substeps", C.c_int64)]
+                ("particle_substeps", C.c_int64), ("ms_fused", C.c_double)]
 
 
 GridHook = C.CFUNCTYPE(None, C.c_void_p, C.c_int32, C.POINTER(C.c_float),
@@ -140,6 +140,7 @@ PRODUCT_API.update({
     "scene_get_particles": (C.c_int, [u64, fp, fp, fp, fp, u8p]),
     "set_stream": (C.c_int, [u64, C.c_void_p]),
     "set_resort_interval": (C.c_int, [u64, C.c_int32]),
+    "set_fusion": (C.c_int, [u64, C.c_int32]),
     "set_profiling": (C.c_int, [u64, C.c_int32]),
     "get_profile": (C.c_int, [u64, C.POINTER(Profile)]),
     "synchronize": (C.c_int, [u64]),

@@ -651,6 +651,7 @@ struct Batch {
     bool shapes_dirty = true;
     Status status = Status::idle;
     int resort = 0;               // substeps between binnings (0: every 4 frames)
+    int fusion = 1;               // Engine::set_fusion (mpmb_set_fusion)
     bool exact = false;           // exact mode (Engine::set_exact)
     int64_t since_sort = 1 << 30; // substeps since the last binning (runs across frames)
     bool profiling = false;
@@ -750,6 +751,7 @@ void ensure_engine(Batch& b) {
     if (b.stream) b.eng->set_stream(b.stream);
     b.eng->set_profiling(b.profiling);
     b.eng->set_exact(b.exact);
+    b.eng->set_fusion(b.fusion);
 }
 
 void upload(Batch& b) {
@@ -875,18 +877,25 @@ void run_frame(Batch& b, float dt) {
     // unless the caller chose an interval (mpmb_set_resort_interval)
     const int resort = b.resort > 0 ? b.resort : 4 * n_sub;
     if (!pb) {
+        // inside the frame, G2P of substep s and P2G of s+1 run as one kernel (k_g2p2g)
+        // unless a binning falls between them
+        const bool standard = cfg.solver == MPMB_SOLVER_STANDARD;  // scene.hpp:200-207
+        const bool can_fuse = e.fuse_ok();
+        bool fused_in = false;  // P2G of this substep already ran inside the previous kernel
         for (int sub = 0; sub < n_sub; ++sub) {
             if (b.since_sort >= resort) {
                 e.bin();
                 b.since_sort = 0;
             }
             ++b.since_sort;
-            const bool standard = cfg.solver == MPMB_SOLVER_STANDARD;  // scene.hpp:200-207
-            e.p2g(true, dt_sub, true, standard);
+            if (!fused_in) e.p2g(true, dt_sub, true, standard);
             e.grid_update(sub, dt_sub, cfg.gravity, true, true, cfg.boundary);
-            if (standard) e.g2p_standard(sub, dt_sub, true, true);
+            const bool fuse = can_fuse && sub + 1 < n_sub && b.since_sort < resort;
+            if (fuse) e.g2p2g(sub, dt_sub, standard);
+            else if (standard) e.g2p_standard(sub, dt_sub, true, true);
             else e.g2p_mls(sub, dt_sub, true, true);
             if (ns > 0) e.free_bodies(sub, dt_sub, cfg.gravity, any_free, true, sub + 1 < n_sub ? sub + 1 : -1);
+            fused_in = fuse;
         }
     } else {
         e.bin();
@@ -1471,6 +1480,15 @@ extern "C" mpmb_status mpmb_set_exact(mpmb_handle h, int32_t on) {
     });
 }
 
+extern "C" mpmb_status mpmb_set_fusion(mpmb_handle h, int32_t mode) {
+    return with_batch(h, [&](Batch& b) {
+        if (mode < 0 || mode > 2) return MPMB_INVALID_ARGUMENT;
+        b.fusion = mode;
+        if (b.eng) b.eng->set_fusion(mode);
+        return MPMB_OK;
+    });
+}
+
 extern "C" mpmb_status mpmb_set_resort_interval(mpmb_handle h, int32_t k) {
     return with_batch(h, [&](Batch& b) {
         if (k < 0) return MPMB_INVALID_ARGUMENT;
@@ -1502,6 +1520,7 @@ extern "C" mpmb_status mpmb_get_profile(mpmb_handle h, mpmb_profile* out) {
             out->ms_g2p = t.ms_g2p;
             out->ms_other = t.ms_other;
             out->launches = t.launches;
+            out->ms_fused = t.ms_fused;
         }
         return MPMB_OK;
     });

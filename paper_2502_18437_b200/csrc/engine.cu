@@ -59,7 +59,7 @@ struct PinnedBuf {
     }
 };
 
-enum Cat { CAT_SORT = 0, CAT_P2G, CAT_GRID, CAT_G2P, CAT_OTHER };
+enum Cat { CAT_SORT = 0, CAT_P2G, CAT_GRID, CAT_G2P, CAT_OTHER, CAT_FUSED };
 
 }  // namespace
 
@@ -144,6 +144,7 @@ struct Engine::Impl {
     uint32_t ex_epoch = 0;
     DevBuf ex_ckey, ex_crec, ex_cn, ex_cscratch;
     bool wide = false;  // thread-per-slot G2P (small problems, launch_g2p)
+    int fusion = 1;     // k_g2p2g inside frames: 0 off, 1 unless wide, 2 always
     int cull_sub = -1;  // the substep whose shape cull table is current (-1: none)  // exact contact records (k_exact.cu)
     PinnedBuf ex_cn_host;
     // misc u32 slots: [0] n_active_bricks
@@ -219,6 +220,7 @@ struct Engine::Impl {
                           : e.first == CAT_P2G ? &times.ms_p2g
                           : e.first == CAT_GRID ? &times.ms_grid
                           : e.first == CAT_G2P ? &times.ms_g2p
+                          : e.first == CAT_FUSED ? &times.ms_fused
                                                : &times.ms_other;
             *dst += ms;
             event_pool.push_back(e.second.first);
@@ -776,6 +778,34 @@ void Engine::g2p_mls(int sub, float dt, bool pushout, bool deactivate) {
     I.counted(1);
     I.cur = 1 - I.cur;  // G2P wrote the group-sorted state into the other buffer
     I.end(CAT_G2P, ev);
+}
+
+// G2P(sub) + P2G(sub+1) in one launch (k_g2p2g), then the brick collect of sub+1.  The
+// caller runs free_bodies(sub) after it (its shape cull for sub+1 would overwrite the
+// table the fused push-out of sub still reads).
+void Engine::g2p2g(int sub, float dt, bool standard) {
+    Impl& I = *impl_;
+    if (I.n_cap == 0) return;
+    auto ev = I.begin();
+    cudaMemsetAsync(I.misc.p, 0, sizeof(uint32_t), I.st);  // active brick count of sub+1
+    Params P = I.params();
+    P.sub = std::min(sub, I.table_subs - 1);
+    P.dt = dt;
+    P.pushout = 1;
+    P.deactivate = 1;
+    P.commit = 1;
+    launch_g2p2g(P, (I.n + kGroup - 1) / kGroup, I.st, standard);
+    launch_collect_bricks(P, I.total_bricks, I.st);
+    I.counted(2);
+    I.flag_parity = 1 - I.flag_parity;
+    I.cur = 1 - I.cur;  // the state of sub+1 is in the other buffer
+    I.end(CAT_FUSED, ev);
+}
+
+void Engine::set_fusion(int mode) { impl_->fusion = mode; }
+bool Engine::fuse_ok() const {
+    const Impl& I = *impl_;
+    return !I.exact && I.n_cap > 0 && (I.fusion == 2 || (I.fusion == 1 && !I.wide));
 }
 
 void Engine::set_exact(bool on) { impl_->exact = on; }

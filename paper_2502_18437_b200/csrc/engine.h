@@ -46,6 +46,7 @@ struct SceneCounters {          // per scene, summed since reset_counters()
 
 struct KernelTimes {
     double ms_sort = 0, ms_p2g = 0, ms_grid = 0, ms_g2p = 0, ms_other = 0;
+    double ms_fused = 0;  // k_g2p2g (G2P of substep s + P2G of s+1) + its brick collect
     int64_t launches = 0;
 };
 
@@ -96,6 +97,12 @@ class Engine {
     void grid_update(int sub, float dt, const float g[3], bool gravity, bool contact, int bc);
     void g2p_mls(int sub, float dt, bool pushout, bool deactivate);   // K4
     void g2p_standard(int sub, float dt, bool pushout, bool deactivate);  // K4, PIC (solvers.hpp:107-135)
+    // K4 of substep `sub` fused with K2 of sub+1 (MLS or standard; push-out and deactivation
+    // on), followed by the brick collect of sub+1: replaces g2p_* then p2g inside a frame
+    void g2p2g(int sub, float dt, bool standard);
+    // fusion policy: 0 off, 1 when G2P runs one warp per group (default), 2 always
+    void set_fusion(int mode);
+    bool fuse_ok() const;
     // exact mode (k_exact.cu): MLS substeps in the reference's float order and arithmetic,
     // bit-identical to the reference and run to run; much slower than the default fast mode
     void set_exact(bool on);

@@ -101,7 +101,7 @@ struct PlaneSet<5> {  // P0 {x, vx}, P3 {C6..8, F0}, P4, P5 {F}, PR
 
 // Per-lane producer of the staging ring: issues the planes of the lane's k-th sorted
 // particle (lanes past their count commit an empty group, keeping the wait counts uniform).
-template <int NP, int NS = kStages, bool CG = false>
+template <int NP, int NS = kStages, bool CG = false, bool OUT = false>
 struct Stager {
     float4* buf;        // this warp's ring: [NS][NP][32]
     uint32_t slot0;     // first slot of the group
@@ -116,7 +116,8 @@ struct Stager {
             const uint32_t s = slot(k);
             float4* dst = buf + (k % NS) * NP * 32 + lane;
 #pragma unroll
-            for (int q = 0; q < NP; ++q) cp_async16<CG>(dst + q * 32, P.pl[PlaneSet<NP>::plane(q)] + s);
+            for (int q = 0; q < NP; ++q)
+                cp_async16<CG>(dst + q * 32, (OUT ? P.pl_out : P.pl)[PlaneSet<NP>::plane(q)] + s);
         }
         cp_commit();
     }
@@ -144,18 +145,22 @@ __device__ __forceinline__ void p2g_flush(const Params& P, const SceneView& S, c
                                           float2 (&pa)[27], float2 (&pb)[27]) {
     uint32_t base, px, pxy;
     stencil_rows(P.geo, cb, base, px, pxy);
-    float4* g = P.grid_acc + S.node_base + base;
+    // one 64-bit stencil pointer; the 9 row offsets are warp-uniform byte counts (uniform
+    // datapath), so each row costs one 64-bit add instead of an index-to-address chain
+    char* g = reinterpret_cast<char*>(P.grid_acc + S.node_base + base);
+    const uint32_t pxb = px * 16u, pxyb = pxy * 16u;
+    const float2 zero2 = f2(P.zero, P.zero);
 #pragma unroll
     for (int dk = 0; dk < 3; ++dk)
 #pragma unroll
         for (int dj = 0; dj < 3; ++dj) {
-            float4* row = g + (dk * pxy + dj * px);
+            float4* row = reinterpret_cast<float4*>(g + (dk * pxyb + dj * pxb));
 #pragma unroll
             for (int di = 0; di < 3; ++di) {
                 const int n = (dk * 3 + dj) * 3 + di;
                 red_add_v4(row + di, pa[n], pb[n]);
-                pa[n] = f2(0.f, 0.f);
-                pb[n] = f2(0.f, 0.f);
+                pa[n] = __fmul2_rn(pa[n], zero2);  // one FFMA-pipe op per pair (a plain
+                pb[n] = __fmul2_rn(pb[n], zero2);  // zero costs ptxas one MOV per register)
             }
         }
     mark_bricks(P, S, cb);
@@ -289,6 +294,7 @@ __device__ __forceinline__ uint32_t bin_word(uint32_t b) { return b + (b >> 5); 
 // smem atomics).  Active particles come first in bin order, then inactive ones and holes
 // in previous order.  Writes all kGroup order bytes (slot-in-group of each position) to
 // order_s and returns the lane's 8 P2G positions [8L, 8L+8); `bins` is kBinWords words.
+template <bool OUT>
 __device__ __forceinline__ uint64_t group_sort(const Params& P, uint32_t g, uint32_t* bins, uint8_t* order_s,
                                                uint32_t& n_act) {
     const unsigned full = 0xffffffffu;
@@ -302,8 +308,13 @@ __device__ __forceinline__ uint64_t group_sort(const Params& P, uint32_t g, uint
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
         const uint32_t s = slot0 + group_phys(32u * i + lane);
-        fl[i] = __float_as_uint(__ldg(&P.pl[PR][s].z));
-        xa4[i] = __ldg(&P.pl[0][s]);
+        if (OUT) {  // written earlier in this kernel by the same warp: coherent L2 loads
+            fl[i] = __float_as_uint(__ldcg(&P.pl_out[PR][s].z));
+            xa4[i] = __ldcg(&P.pl_out[0][s]);
+        } else {
+            fl[i] = __float_as_uint(__ldg(&P.pl[PR][s].z));
+            xa4[i] = __ldg(&P.pl[0][s]);
+        }
     }
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
@@ -430,60 +441,68 @@ __device__ __forceinline__ void p2g_prepare(const Params& P, const float4 q0, co
     }
 }
 
-// MLS: stress impulse from F (MLS-MPM, solvers.hpp:151-169; with STD: standard MPM's force
-// transfer, solvers.hpp:88-104); !MLS: PB-MPM (A = m C, solvers.hpp:218-235)
+// P2G of group g (MLS: stress impulse from F, solvers.hpp:151-169; with STD: standard MPM's
+// force transfer, solvers.hpp:88-104; !MLS: PB-MPM, A = m C, solvers.hpp:218-235).  `ring` is
+// this warp's staging ring (kStages x kPlanes x 32 float4), also the sort scratch.  OUT: the
+// group's particles are in the other buffer (pl_out), written by this warp's G2P of the
+// previous substep inside the fused kernel (k_g2p2g).
+template <bool MLS, bool STD, bool OUT>
+__device__ __forceinline__ void p2g_group(const Params& P, uint32_t g, float4* ring, int lane) {
+    constexpr int NP = kPlanes;
+    Stager<NP, kStages, OUT || MPMB_P2G_CG != 0, OUT> st;
+    st.buf = ring;
+    st.lane = lane;
+    uint32_t* bins = reinterpret_cast<uint32_t*>(ring);  // sort scratch aliases the ring
+    uint8_t* order_s = reinterpret_cast<uint8_t*>(bins + kBinWords);
+    uint32_t n_act;
+    st.order = group_sort<OUT>(P, g, bins, order_s, n_act);
+    st.slot0 = g * kGroup;
+    st.cnt = min(max(static_cast<int>(n_act) - kPer * lane, 0), kPer);
+    reinterpret_cast<uint64_t*>(P.order)[static_cast<uint64_t>(g) * 32 + lane] = st.order;
+    if (lane == 0) P.group_nact[g] = n_act;
+    const int kmax = min(static_cast<int>(n_act), kPer);  // lane 0 has the most
+    for (int k = 0; k < kStages - 1; ++k) st.issue(P, k);
+    float2 pa[27], pb[27];  // (mom_x, mom_y), (mom_z, mass) per stencil node
+#pragma unroll
+    for (int n = 0; n < 27; ++n) {
+        pa[n] = f2(0.f, 0.f);
+        pb[n] = f2(0.f, 0.f);
+    }
+    int cb[3] = {INT_MIN, INT_MIN, INT_MIN};
+    int cscene = -1;
+    for (int k = 0; k < kmax; ++k) {
+        st.issue(P, k + kStages - 1);
+        cp_wait<kStages - 1>();
+        if (k >= st.cnt) continue;
+        const float4* src = st.buf + (k % kStages) * NP * 32 + lane;
+        const float4 r = src[PR * 32];
+        const float4 q0 = src[0], q1 = src[32], q2 = src[64], q3 = src[96], q4 = src[128], q5 = src[160];
+        int scene, b[3];
+        float w[3][3], rel[3][3], A[9], m, v[3];  // STD: rel holds the weight derivatives
+        p2g_prepare<MLS, STD>(P, q0, q1, q2, q3, q4, q5, r, scene, b, w, rel, A, m, v);
+        if (b[0] != cb[0] || b[1] != cb[1] || b[2] != cb[2] || scene != cscene) {
+            if (cscene >= 0) p2g_flush(P, scene_view(P, cscene), cb, pa, pb);
+            cb[0] = b[0]; cb[1] = b[1]; cb[2] = b[2];
+            cscene = scene;
+        }
+        if (STD) p2g_nodes_std(w, rel, A, m, v, pa, pb);
+        else p2g_nodes(w, rel, A, m, v, pa, pb);
+    }
+    if (cscene >= 0) p2g_flush(P, scene_view(P, cscene), cb, pa, pb);
+    cp_wait<0>();
+    __syncwarp();  // the ring is the next group's sort scratch
+}
+
 template <bool MLS, bool STD = false>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_p2g(const __grid_constant__ Params P) {
     pdl_enter();
     extern __shared__ float4 smem[];
-    constexpr int NP = kPlanes;
     const int lane = threadIdx.x & 31;
     const uint32_t n_groups = *P.n_groups;
     const uint32_t wpb = blockDim.x >> 5;
-    Stager<NP, kStages, MPMB_P2G_CG != 0> st;
-    st.buf = smem + (threadIdx.x >> 5) * (kStages * NP * 32);
-    st.lane = lane;
-    uint32_t* bins = reinterpret_cast<uint32_t*>(st.buf);  // sort scratch aliases the ring
-    uint8_t* order_s = reinterpret_cast<uint8_t*>(bins + kBinWords);
-    for (uint32_t g = blockIdx.x * wpb + (threadIdx.x >> 5); g < n_groups; g += gridDim.x * wpb) {
-        uint32_t n_act;
-        st.order = group_sort(P, g, bins, order_s, n_act);
-        st.slot0 = g * kGroup;
-        st.cnt = min(max(static_cast<int>(n_act) - kPer * lane, 0), kPer);
-        reinterpret_cast<uint64_t*>(P.order)[static_cast<uint64_t>(g) * 32 + lane] = st.order;
-        if (lane == 0) P.group_nact[g] = n_act;
-        const int kmax = min(static_cast<int>(n_act), kPer);  // lane 0 has the most
-        for (int k = 0; k < kStages - 1; ++k) st.issue(P, k);
-        float2 pa[27], pb[27];  // (mom_x, mom_y), (mom_z, mass) per stencil node
-#pragma unroll
-        for (int n = 0; n < 27; ++n) {
-            pa[n] = f2(0.f, 0.f);
-            pb[n] = f2(0.f, 0.f);
-        }
-        int cb[3] = {INT_MIN, INT_MIN, INT_MIN};
-        int cscene = -1;
-        for (int k = 0; k < kmax; ++k) {
-            st.issue(P, k + kStages - 1);
-            cp_wait<kStages - 1>();
-            if (k >= st.cnt) continue;
-            const float4* src = st.buf + (k % kStages) * NP * 32 + lane;
-            const float4 r = src[PR * 32];
-            const float4 q0 = src[0], q1 = src[32], q2 = src[64], q3 = src[96], q4 = src[128], q5 = src[160];
-            int scene, b[3];
-            float w[3][3], rel[3][3], A[9], m, v[3];  // STD: rel holds the weight derivatives
-            p2g_prepare<MLS, STD>(P, q0, q1, q2, q3, q4, q5, r, scene, b, w, rel, A, m, v);
-            if (b[0] != cb[0] || b[1] != cb[1] || b[2] != cb[2] || scene != cscene) {
-                if (cscene >= 0) p2g_flush(P, scene_view(P, cscene), cb, pa, pb);
-                cb[0] = b[0]; cb[1] = b[1]; cb[2] = b[2];
-                cscene = scene;
-            }
-            if (STD) p2g_nodes_std(w, rel, A, m, v, pa, pb);
-            else p2g_nodes(w, rel, A, m, v, pa, pb);
-        }
-        if (cscene >= 0) p2g_flush(P, scene_view(P, cscene), cb, pa, pb);
-        cp_wait<0>();
-        __syncwarp();  // the ring is the next group's sort scratch
-    }
+    float4* ring = smem + (threadIdx.x >> 5) * (kStages * kPlanes * 32);
+    for (uint32_t g = blockIdx.x * wpb + (threadIdx.x >> 5); g < n_groups; g += gridDim.x * wpb)
+        p2g_group<MLS, STD, false>(P, g, ring, lane);
 }
 
 // ================================================================  G2P
@@ -507,7 +526,9 @@ __device__ __forceinline__ void g2p_gather(const float4* g, uint32_t px, uint32_
     for (int dk = 0; dk < 3; ++dk) {
         float4 q[9];
 #pragma unroll
-        for (int n = 0; n < 9; ++n) q[n] = __ldg(g + (dk * pxy + (n / 3) * px) + (n % 3));
+        for (int n = 0; n < 9; ++n)
+            q[n] = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const char*>(g) +
+                                                         (dk * pxy + (n / 3) * px) * 16u) + (n % 3));
 #pragma unroll
         for (int dj = 0; dj < 3; ++dj) {
             float2 a01 = f2(0.f, 0.f), b01 = f2(0.f, 0.f);
@@ -553,7 +574,9 @@ __device__ __forceinline__ void g2p_gather_std(const float4* g, uint32_t px, uin
     for (int dk = 0; dk < 3; ++dk) {
         float4 q[9];
 #pragma unroll
-        for (int n = 0; n < 9; ++n) q[n] = __ldg(g + (dk * pxy + (n / 3) * px) + (n % 3));
+        for (int n = 0; n < 9; ++n)
+            q[n] = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const char*>(g) +
+                                                         (dk * pxy + (n / 3) * px) * 16u) + (n % 3));
 #pragma unroll
         for (int dj = 0; dj < 3; ++dj) {
             float2 a01 = f2(0.f, 0.f), d01 = f2(0.f, 0.f);
@@ -742,8 +765,87 @@ __device__ __forceinline__ void g2p_particle(const Params& P, Part& p, float4& r
     }
 }
 
-// PB: PB-MPM (solvers.hpp:240-277); STD: standard MPM, PIC velocity + L (solvers.hpp:107-135,
-// C travels unchanged); neither: MLS-MPM (solvers.hpp:173-196)
+// G2P of group g (PB: PB-MPM, solvers.hpp:240-277; STD: standard MPM, PIC velocity + L,
+// solvers.hpp:107-135, C travels unchanged; neither: MLS-MPM, solvers.hpp:173-196).  Replays
+// the order P2G sorted this group into (positions are unchanged since); lane L takes
+// positions g2p_pos(L, k): the warp's 32 lanes gather around a few neighbouring stencils at
+// every iteration.  Every position is written to the other buffer at slot
+// group_phys(pos): the state leaves G2P in the new order.  `ring`: this warp's staging ring.
+template <bool PB, bool STD>
+__device__ __forceinline__ void g2p_group(const Params& P, uint32_t g, float4* ring, int lane) {
+    constexpr int NP = (PB || STD) ? 7 : 5;
+    constexpr int NS = kG2PStages;
+    Stager<NP, NS, MPMB_G2P_CG != 0> st;
+    st.buf = ring;
+    st.lane = lane;
+    const uint32_t n_act = P.group_nact[g];
+    st.cnt = 0;
+    {
+        const uint8_t* ob = P.order + static_cast<uint64_t>(g) * kGroup;
+        uint64_t o = 0;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            o |= static_cast<uint64_t>(ob[g2p_pos(lane, k)]) << (8 * k);
+            st.cnt += g2p_pos(lane, k) < n_act ? 1 : 0;
+        }
+        st.order = o;
+    }
+    st.slot0 = g * kGroup;
+    const int kmax = __reduce_max_sync(0xffffffffu, st.cnt);
+    for (int k = 0; k < NS - 1; ++k) st.issue(P, k);
+    G2PLane L;
+    for (int k = 0; k < kmax; ++k) {
+        st.issue(P, k + NS - 1);
+        cp_wait<(NS > 3 ? NS - 2 : NS - 1)>();  // particles k (and k+1) have landed
+        if (k >= st.cnt) continue;
+        if (NS > 3 && k + 1 < st.cnt) {  // warm L1 with the next particle's stencil rows
+            const float4 xn = st.buf[((k + 1) % NS) * NP * 32 + lane];
+            int bn[3];
+            float fn[3];
+            const float xq[3] = {xn.x, xn.y, xn.z};
+            local_base(P.geo, xq, bn, fn);
+            const uint32_t sn = (__float_as_uint(st.buf[((k + 1) % NS) * NP * 32 + (NP - 1) * 32 + lane].z) >>
+                                 kSceneShift) & kSceneMask;
+            uint32_t base, px, pxy;
+            stencil_rows(P.geo, bn, base, px, pxy);
+            prefetch_stencil_l1(P.grid_vel + sn * P.geo.nodes_per_scene + base, px, pxy);
+        }
+        const uint32_t so = st.slot0 + group_phys(g2p_pos(lane, k));
+        const float4* src = st.buf + (k % NS) * NP * 32 + lane;
+        float4 r = src[(NP - 1) * 32];
+        Part p;
+        {
+            const float4 q0 = src[0];
+            p.x[0] = q0.x; p.x[1] = q0.y; p.x[2] = q0.z;
+            if (PB || STD) {
+                const float4 q1 = src[32], q2 = src[64], q3 = src[96], q4 = src[128], q5 = src[160];
+                p.C[0] = q1.z; p.C[1] = q1.w; p.C[2] = q2.x; p.C[3] = q2.y; p.C[4] = q2.z;
+                p.C[5] = q2.w; p.C[6] = q3.x; p.C[7] = q3.y; p.C[8] = q3.z;
+                p.F[0] = q3.w; p.F[1] = q4.x; p.F[2] = q4.y; p.F[3] = q4.z; p.F[4] = q4.w;
+                p.F[5] = q5.x; p.F[6] = q5.y; p.F[7] = q5.z; p.F[8] = q5.w;
+            } else {
+                const float4 q3 = src[32], q4 = src[64], q5 = src[96];
+                p.F[0] = q3.w; p.F[1] = q4.x; p.F[2] = q4.y; p.F[3] = q4.z; p.F[4] = q4.w;
+                p.F[5] = q5.x; p.F[6] = q5.y; p.F[7] = q5.z; p.F[8] = q5.w;
+            }
+        }
+        g2p_particle<PB, STD>(P, p, r, L);
+        store_part_out(P, so, p, r);
+    }
+    // inactive particles and holes of the group move to their new slots unchanged
+    for (int k = st.cnt; k < kPer; ++k) {
+        const uint32_t si = st.slot(k), so = st.slot0 + group_phys(g2p_pos(lane, k));
+#pragma unroll
+        for (int q = 0; q < kPlanes; ++q) P.pl_out[q][so] = P.pl[q][si];
+    }
+    add_scene_counter(P.counters, L.my_scene, 0, L.n_inv);
+    add_scene_counter(P.counters, L.my_scene, 1, L.n_fail);
+    add_scene_counter(P.counters, L.my_scene, 2, L.n_push);
+    add_scene_counter(P.counters, L.my_scene, 3, L.n_deact);
+    cp_wait<0>();
+    __syncwarp();  // the ring is reused by the next group (or the fused P2G)
+}
+
 template <bool PB, bool STD = false>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(const __grid_constant__ Params P) {
     pdl_enter();
@@ -752,81 +854,34 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(cons
     const int lane = threadIdx.x & 31;
     const uint32_t n_groups = *P.n_groups;
     const uint32_t wpb = blockDim.x >> 5;
-    constexpr int NS = kG2PStages;
-    Stager<NP, NS, MPMB_G2P_CG != 0> st;
-    st.buf = smem + (threadIdx.x >> 5) * (NS * NP * 32);
-    st.lane = lane;
+    float4* ring = smem + (threadIdx.x >> 5) * (kG2PStages * NP * 32);
+    for (uint32_t g = blockIdx.x * wpb + (threadIdx.x >> 5); g < n_groups; g += gridDim.x * wpb)
+        g2p_group<PB, STD>(P, g, ring, lane);
+}
+
+// Fused G2P of substep s + P2G of substep s+1 (MLS / standard MPM inside a frame), one warp
+// per group: the reference runs push-out, free-body integration and deactivation between
+// them (scene.hpp:209-235), and only deactivation and push-out touch particles; both are
+// fused into the G2P phase, free bodies only need the contact sums of substep s.  The G2P
+// phase writes the group in its new order to the other buffer; the P2G phase of the same
+// warp re-sorts and stages it from there while the lines are still in L2, so the state
+// crosses HBM once per substep (read x, F, flags; write everything) and the P2G load
+// latency is an L2 latency.  Grid pools: G2P reads grid_vel (substep s), P2G accumulates
+// into grid_acc (zeroed by the grid update of substep s), so the phases never alias.
+template <bool STD>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_g2p2g(const __grid_constant__ Params P) {
+    pdl_enter();
+    extern __shared__ float4 smem[];
+    const int lane = threadIdx.x & 31;
+    const uint32_t n_groups = *P.n_groups;
+    const uint32_t wpb = blockDim.x >> 5;
+    constexpr int kRing = kStages * kPlanes > kG2PStages * 7 ? kStages * kPlanes : kG2PStages * 7;
+    float4* ring = smem + (threadIdx.x >> 5) * (kRing * 32);
     for (uint32_t g = blockIdx.x * wpb + (threadIdx.x >> 5); g < n_groups; g += gridDim.x * wpb) {
-        // replay the order P2G sorted this group into (positions are unchanged since);
-        // lane L takes positions g2p_pos(L, k): the warp's 32 lanes gather around a few
-        // neighbouring stencils at every iteration.  Every position is written to the other
-        // buffer at slot group_phys(pos): the state leaves G2P in the new order.
-        const uint32_t n_act = P.group_nact[g];
-        st.cnt = 0;
-        {
-            const uint8_t* ob = P.order + static_cast<uint64_t>(g) * kGroup;
-            uint64_t o = 0;
-#pragma unroll
-            for (int k = 0; k < kPer; ++k) {
-                o |= static_cast<uint64_t>(ob[g2p_pos(lane, k)]) << (8 * k);
-                st.cnt += g2p_pos(lane, k) < n_act ? 1 : 0;
-            }
-            st.order = o;
-        }
-        st.slot0 = g * kGroup;
-        const int kmax = __reduce_max_sync(0xffffffffu, st.cnt);
-        for (int k = 0; k < NS - 1; ++k) st.issue(P, k);
-        G2PLane L;
-        for (int k = 0; k < kmax; ++k) {
-            st.issue(P, k + NS - 1);
-            cp_wait<(NS > 3 ? NS - 2 : NS - 1)>();  // particles k (and k+1) have landed
-            if (k >= st.cnt) continue;
-            if (NS > 3 && k + 1 < st.cnt) {  // warm L1 with the next particle's stencil rows
-                const float4 xn = st.buf[((k + 1) % NS) * NP * 32 + lane];
-                int bn[3];
-                float fn[3];
-                const float xq[3] = {xn.x, xn.y, xn.z};
-                local_base(P.geo, xq, bn, fn);
-                const uint32_t sn = (__float_as_uint(st.buf[((k + 1) % NS) * NP * 32 + (NP - 1) * 32 + lane].z) >>
-                                     kSceneShift) & kSceneMask;
-                uint32_t base, px, pxy;
-                stencil_rows(P.geo, bn, base, px, pxy);
-                prefetch_stencil_l1(P.grid_vel + sn * P.geo.nodes_per_scene + base, px, pxy);
-            }
-            const uint32_t so = st.slot0 + group_phys(g2p_pos(lane, k));
-            const float4* src = st.buf + (k % NS) * NP * 32 + lane;
-            float4 r = src[(NP - 1) * 32];
-            Part p;
-            {
-                const float4 q0 = src[0];
-                p.x[0] = q0.x; p.x[1] = q0.y; p.x[2] = q0.z;
-                if (PB || STD) {
-                    const float4 q1 = src[32], q2 = src[64], q3 = src[96], q4 = src[128], q5 = src[160];
-                    p.C[0] = q1.z; p.C[1] = q1.w; p.C[2] = q2.x; p.C[3] = q2.y; p.C[4] = q2.z;
-                    p.C[5] = q2.w; p.C[6] = q3.x; p.C[7] = q3.y; p.C[8] = q3.z;
-                    p.F[0] = q3.w; p.F[1] = q4.x; p.F[2] = q4.y; p.F[3] = q4.z; p.F[4] = q4.w;
-                    p.F[5] = q5.x; p.F[6] = q5.y; p.F[7] = q5.z; p.F[8] = q5.w;
-                } else {
-                    const float4 q3 = src[32], q4 = src[64], q5 = src[96];
-                    p.F[0] = q3.w; p.F[1] = q4.x; p.F[2] = q4.y; p.F[3] = q4.z; p.F[4] = q4.w;
-                    p.F[5] = q5.x; p.F[6] = q5.y; p.F[7] = q5.z; p.F[8] = q5.w;
-                }
-            }
-            g2p_particle<PB, STD>(P, p, r, L);
-            store_part_out(P, so, p, r);
-        }
-        // inactive particles and holes of the group move to their new slots unchanged
-        for (int k = st.cnt; k < kPer; ++k) {
-            const uint32_t si = st.slot(k), so = st.slot0 + group_phys(g2p_pos(lane, k));
-#pragma unroll
-            for (int q = 0; q < kPlanes; ++q) P.pl_out[q][so] = P.pl[q][si];
-        }
-        add_scene_counter(P.counters, L.my_scene, 0, L.n_inv);
-        add_scene_counter(P.counters, L.my_scene, 1, L.n_fail);
-        add_scene_counter(P.counters, L.my_scene, 2, L.n_push);
-        add_scene_counter(P.counters, L.my_scene, 3, L.n_deact);
+        g2p_group<false, STD>(P, g, ring, lane);
+        __syncwarp();  // orders this warp's stores of the group before the P2G loads
+        p2g_group<true, STD, true>(P, g, ring, lane);
     }
-    cp_wait<0>();
 }
 
 // Wide G2P for small problems, where one warp per group would leave most SMs idle: one
@@ -972,6 +1027,21 @@ void launch_g2p(const Params& P, bool pb, int64_t max_groups, cudaStream_t st, b
     if (standard) launch_chain(k_g2p<false, true>, blocks, threads, smem7, st, P);
     else if (pb) launch_chain(k_g2p<true>, blocks, threads, smem7, st, P);
     else launch_chain(k_g2p<false>, blocks, threads, smem5, st, P);
+}
+
+void launch_g2p2g(const Params& P, int64_t max_groups, cudaStream_t st, bool standard) {
+    const int threads = kWarpsPerBlock * 32;
+    const int blocks = grid_for(max_groups * 32, threads, 148 * 16);
+    constexpr int kRing = kStages * kPlanes > kG2PStages * 7 ? kStages * kPlanes : kG2PStages * 7;
+    const int smem = kWarpsPerBlock * kRing * 32 * static_cast<int>(sizeof(float4));
+    static bool attr = false;
+    if (!attr) {
+        opt_in_smem(k_g2p2g<false>, smem);
+        opt_in_smem(k_g2p2g<true>, smem);
+        attr = true;
+    }
+    if (standard) launch_chain(k_g2p2g<true>, blocks, threads, smem, st, P);
+    else launch_chain(k_g2p2g<false>, blocks, threads, smem, st, P);
 }
 
 void launch_pushout(const Params& P, cudaStream_t st) {

@@ -88,6 +88,7 @@ struct Params {
     int exact;  // exact mode: frame accumulators merge in float (scene.hpp:228-231)
     uint32_t epoch;
     float dt;
+    float zero;  // always 0: a multiplier the compiler cannot fold (P2G accumulator reset)
     float g[3];
     int sub;
     int gravity;

@@ -208,3 +208,38 @@ def test_rotating_needle_within_reference_envelope(name, spec_fn, frames):
     assert err <= max(1e-3 * dx, 10 * env), f"{name}: {err / dx:.2e} dx vs envelope {env / dx:.2e} dx"
     p_scale = ro["total_mass"] * max(np.abs(ro["velocities"]).max(), 1e-3)
     assert imp_err <= 10 * imp_env + 1e-6 * p_scale
+
+
+# Substep fusion (k_g2p2g: G2P of substep s + P2G of s+1 in one kernel).  At these sizes the
+# engine would run the thread-per-slot G2P without fusion, so mode 2 forces it; the same
+# horizon bounds as the unfused scenes apply (the change is float atomic order only).
+@pytest.mark.parametrize("name,spec_fn,frames", [
+    ("cube_drop", scenes.cube_drop, 5),
+    ("cube_drop_standard", lambda: scenes.cube_drop(solver="standard"), 5),
+    ("cutting", scenes.cutting, 5),
+    ("mesh_slicer", scenes.mesh_slicer_scene, 4),
+    ("rigid_coupling", scenes.rigid_coupling, 4),
+])
+def test_fused_substeps_vs_oracle(name, spec_fn, frames):
+    spec = spec_fn()
+    o, g = _scene_pair(spec)
+    assert g.lib.mpmb_set_fusion(g.h, 2) == capi.OK
+    assert g.lib.mpmb_set_fusion(g.h, 3) != capi.OK
+    dx = spec["grid"]["dx"]
+    g.set_profiling(True)
+    for _ in range(frames):
+        o.advance(spec["dt_frame"])
+        g.advance(spec["dt_frame"])
+        ro, rg = o.fetch_results(), g.fetch_results()
+    assert g.profile()["ms_fused"] > 0.0  # the fused kernel ran
+    assert np.array_equal(ro["active"], rg["active"])
+    assert ro["deactivated"] == rg["deactivated"] and ro["inverted_f"] == rg["inverted_f"]
+    err = np.abs(ro["positions"] - rg["positions"]).max()
+    assert err <= 1e-3 * dx, f"{name}: max|dx| {err / dx:.2e} dx"
+    vmax = np.abs(ro["velocities"]).max()
+    assert np.abs(ro["velocities"] - rg["velocities"]).max() <= 1e-3 * vmax + 1e-6
+    assert abs(ro["total_mass"] - rg["total_mass"]) <= 1e-9 * ro["total_mass"]
+    if ro["n_shapes"]:
+        s = np.abs(ro["shape_impulses"]).max()
+        p_scale = ro["total_mass"] * max(vmax, 1e-3)
+        assert np.abs(ro["shape_impulses"] - rg["shape_impulses"]).max() <= 2e-3 * s + 1e-6 * p_scale

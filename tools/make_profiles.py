@@ -17,7 +17,7 @@ from collections import defaultdict
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
-CLASSES = [("p2g", r"k_p2g"), ("g2p", r"k_g2p"), ("grid", r"k_grid_update|k_collect_bricks"),
+CLASSES = [("fused", r"k_g2p2g"), ("p2g", r"k_p2g"), ("g2p", r"k_g2p"), ("grid", r"k_grid_update|k_collect_bricks"),
            ("sort", r"k_bin_|k_scan_")]
 
 
