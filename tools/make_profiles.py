@@ -76,13 +76,24 @@ def main():
     lines += ["", "| class | share |", "|---|---|"]
     lines += [f"| {c} | {100 * us / tot:.1f}% |" for c, us in sorted(cls.items(), key=lambda kv: -kv[1])]
     (prof / f"{tag}_launches.md").write_text("\n".join(lines) + "\n")
-    summ = subprocess.run([sys.executable, str(ROOT / "tools" / "ncu_summary.py"), rep], capture_output=True,
-                          text=True).stdout
+    reps = rep.split(",")  # several captures (e.g. the fused kernel and the rest)
+    summ = "".join(subprocess.run([sys.executable, str(ROOT / "tools" / "ncu_summary.py"), r],
+                                  capture_output=True, text=True).stdout for r in reps)
     (prof / f"{tag}_full.txt").write_text(summ)
-    tr = full(rep)
+    tr = defaultdict(list)
+    for r in reps:
+        for k, v in full(r).items():
+            tr[k] += v
     bpp = {c: sum(v) / len(v) / n for c, v in tr.items() if v}
-    js = {"source": f"{tag}: ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum per launch / particles",
-          "particles": int(n), "bytes_per_particle": bpp}
+    old = prof / "ncu_summary.json"
+    src = f"{tag}: ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum per launch / particles"
+    if old.exists():  # classes this round did not capture keep the earlier figure, labelled
+        prev = json.loads(old.read_text())
+        for k, v in prev.get("bytes_per_particle", {}).items():
+            if k not in bpp and prev.get("particles") == int(n):
+                bpp[k] = v
+                src += f"; {k} from {prev.get('source', '?').split(':')[0]}"
+    js = {"source": src, "particles": int(n), "bytes_per_particle": bpp}
     (prof / "ncu_summary.json").write_text(json.dumps(js, indent=1) + "\n")
     print(json.dumps(js, indent=1))
     print("\n".join(lines[-len(cls) - 2:]))
