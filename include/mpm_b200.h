@@ -281,6 +281,14 @@ mpmb_status mpmb_dd_pack_vel(mpmb_state st);
 mpmb_status mpmb_dd_unpack_vel(mpmb_state st);
 mpmb_status mpmb_dd_g2p(mpmb_state st, float dt, int32_t pushout, int32_t deactivate);
 /* Migration: synchronous counts; buffers hold `capacity` particles of 112 bytes. */
+/* Free bodies under DD (scene.hpp:220-232 split over slabs).  Each slab sums contact over the
+ * nodes it owns; the per-substep sums live in device memory (impulse + torque impulse:
+ * double[6 * n_shapes], node counts: int32[n_shapes]).  The caller all-reduces them (sum)
+ * across slabs after mpmb_dd_grid, then calls mpmb_dd_free_bodies after mpmb_dd_g2p:
+ * integrate_free_body (rigid_dynamics.hpp:82-103) on every slab with the same sums (so every
+ * slab holds the same pose), then the sums merge into the frame sums and clear. */
+mpmb_status mpmb_dd_contact_sums(mpmb_state st, void** sums, void** counts, int32_t* n_shapes);
+mpmb_status mpmb_dd_free_bodies(mpmb_state st, float dt, const float gravity[3]);
 mpmb_status mpmb_dd_migrate_pack(mpmb_state st, int64_t* n_to_lo, int64_t* n_to_hi);
 mpmb_status mpmb_dd_migrate_buffers(mpmb_state st, void** send_lo, void** send_hi, void** recv_lo, void** recv_hi,
                                     int64_t* capacity);

@@ -360,6 +360,22 @@ extern "C" mpmb_status mpmb_dd_g2p(mpmb_state st, float dt, int32_t pushout, int
         return MPMB_OK;
     });
 }
+extern "C" mpmb_status mpmb_dd_contact_sums(mpmb_state st, void** sums, void** counts, int32_t* n_shapes) {
+    return guarded([&] {
+        if (!sums || !counts || !n_shapes) fail(MPMB_INVALID_ARGUMENT, "null argument");
+        int n = 0;
+        S(st)->eng->contact_sub_buffers(sums, counts, &n);
+        *n_shapes = n;
+        return MPMB_OK;
+    });
+}
+extern "C" mpmb_status mpmb_dd_free_bodies(mpmb_state st, float dt, const float g[3]) {
+    return guarded([&] {
+        if (dt <= 0 || !g) fail(MPMB_INVALID_ARGUMENT, "free bodies: dt must be positive");
+        S(st)->eng->free_bodies(0, dt, g, true, true);
+        return MPMB_OK;
+    });
+}
 extern "C" mpmb_status mpmb_dd_migrate_pack(mpmb_state st, int64_t* n_lo, int64_t* n_hi) {
     return guarded([&] {
         if (!n_lo || !n_hi) fail(MPMB_INVALID_ARGUMENT, "null argument");

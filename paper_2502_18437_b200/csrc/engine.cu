@@ -803,6 +803,13 @@ void Engine::g2p2g(int sub, float dt, bool standard) {
 }
 
 void Engine::set_fusion(int mode) { impl_->fusion = mode; }
+
+void Engine::contact_sub_buffers(void** sums, void** counts, int* n_shapes) {
+    Impl& I = *impl_;
+    if (sums) *sums = I.acc_sub.p;
+    if (counts) *counts = I.cnt_sub.p;
+    if (n_shapes) *n_shapes = I.n_shapes;
+}
 bool Engine::fuse_ok() const {
     const Impl& I = *impl_;
     return !I.exact && I.n_cap > 0 && (I.fusion == 2 || (I.fusion == 1 && !I.wide));

@@ -102,6 +102,8 @@ class Engine {
     void g2p2g(int sub, float dt, bool standard);
     // fusion policy: 0 off, 1 when G2P runs one warp per group (default), 2 always
     void set_fusion(int mode);
+    // per-substep contact sums (device): double[6 * n_shapes], int32[n_shapes]
+    void contact_sub_buffers(void** sums, void** counts, int* n_shapes);
     bool fuse_ok() const;
     // exact mode (k_exact.cu): MLS substeps in the reference's float order and arithmetic,
     // bit-identical to the reference and run to run; much slower than the default fast mode

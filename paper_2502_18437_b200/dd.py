@@ -9,7 +9,8 @@ the single-domain run up to float summation order at the cut planes.
 Per substep (library phases, include/mpm_b200.h):
 
     p2g -> pack_acc -> EXCHANGE(acc) -> unpack_acc -> grid -> pack_vel -> EXCHANGE(vel) ->
-    unpack_vel -> g2p                       [+ every `margin` substeps: migrate]
+    unpack_vel -> g2p -> [free bodies: ALLREDUCE(contact sums) -> free_bodies]
+                                            [+ every `margin` substeps: migrate]
 
 EXCHANGE: each rank sends `send_lo` to its lower neighbour (into that rank's `recv_hi`) and
 `send_hi` to its upper neighbour (into `recv_lo`); grid-sum phase: `margin` planes go down
@@ -81,6 +82,11 @@ class SlabDomain:
         arr = (capi.ShapeDesc * len(keep))(*[d for d, _ in keep])
         api.check(self.lib.mpmb_state_set_shapes(self.h, arr, len(keep)), self.lib, "shapes")
 
+    def shape_poses(self, n: int):
+        arr = (capi.Pose * max(1, n))()
+        api.check(self.lib.mpmb_state_get_shape_poses(self.h, arr, n), self.lib, "poses")
+        return [api.pose_dict(arr[i]) for i in range(n)]
+
     def set_particles(self, p: dict, ids: np.ndarray):
         n = len(ids)
         c = {k: np.ascontiguousarray(p[k]) for k in ("x", "v", "mass", "volume0", "F", "C")}
@@ -142,6 +148,21 @@ class SlabDomain:
 
     def g2p(self, dt, pushout=False, deactivate=False):
         api.check(self.lib.mpmb_dd_g2p(self.h, float(F32(dt)), int(pushout), int(deactivate)), self.lib, "dd_g2p")
+
+    def contact_sums(self):
+        """Device views of the per-substep contact sums: (float64[6 n], int32[n]) or None."""
+        s, k, n = C.c_void_p(), C.c_void_p(), C.c_int32()
+        api.check(self.lib.mpmb_dd_contact_sums(self.h, C.byref(s), C.byref(k), C.byref(n)), self.lib,
+                  "dd_contact_sums")
+        if n.value == 0:
+            return None
+        import torch
+        return (_dev_bytes(s.value, 48 * n.value).view(torch.float64),
+                _dev_bytes(k.value, 4 * n.value).view(torch.int32))
+
+    def free_bodies(self, dt, gravity):
+        api.check(self.lib.mpmb_dd_free_bodies(self.h, float(F32(dt)), api._fp(np.array(gravity, F32))), self.lib,
+                  "dd_free_bodies")
 
     def migrate_pack(self):
         a, b = C.c_int64(), C.c_int64()
@@ -214,6 +235,16 @@ class LocalTransport:
                 (_, _, rlo, _), _, _ = domains[r + 1].halo_buffers()
                 _dev_bytes(rlo, up).copy_(_dev_bytes(shi, up))  # same stream as the kernels
 
+    def reduce_contact(self, domains):
+        """Sum the slabs' per-substep contact sums and hand every slab the total."""
+        views = [d.contact_sums() for d in domains]
+        if views[0] is None:
+            return
+        tot = [sum(v[q] for v in views) for q in range(2)]
+        for v in views:
+            v[0].copy_(tot[0])
+            v[1].copy_(tot[1])
+
     def migrate(self, domains, counts):
         import torch
         rec = [[0, 0] for _ in domains]
@@ -259,6 +290,18 @@ class DistTransport:
             for w in dist.batch_isend_irecv(ops):
                 w.wait()
 
+    def allreduce_tensors(self, *tensors):
+        """Sum each tensor over all ranks in place (contact sums; also the CPU tests)."""
+        import torch.distributed as dist
+        for t in tensors:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+
+    def reduce_contact(self, domains):
+        (d,) = domains
+        v = d.contact_sums()
+        if v is not None:
+            self.allreduce_tensors(*v)
+
     def exchange_tensors(self, send_lo, send_hi, recv_lo, recv_hi):
         """The exchange rule on caller-provided tensors (also used by the CPU tests)."""
         self._p2p(send_lo, send_hi, recv_lo, recv_hi)
@@ -292,8 +335,10 @@ class DistTransport:
 
 
 def run_substeps(domains, transport, n_sub, dt, gravity, *, contact=True, boundary=0, pushout=False,
-                 deactivate=False, migrate_every=None):
-    """Advance every slab of this process `n_sub` substeps (MLS), exchanging halos."""
+                 deactivate=False, migrate_every=None, free_bodies=False):
+    """Advance every slab of this process `n_sub` substeps (MLS), exchanging halos.
+    free_bodies: all-reduce the per-shape contact sums every substep and integrate the free
+    bodies on every slab (scene.hpp:220-232)."""
     import torch
     cur = torch.cuda.current_stream()
     # library kernels and the transport's copies / NCCL calls must share ONE real stream
@@ -303,11 +348,11 @@ def run_substeps(domains, transport, n_sub, dt, gravity, *, contact=True, bounda
         for d in domains:
             d.set_stream(stream.cuda_stream)
         _run(domains, transport, n_sub, dt, gravity, contact, boundary, pushout, deactivate,
-             migrate_every or min(d.margin for d in domains))
+             migrate_every or min(d.margin for d in domains), free_bodies)
     stream.synchronize()
 
 
-def _run(domains, transport, n_sub, dt, gravity, contact, boundary, pushout, deactivate, every):
+def _run(domains, transport, n_sub, dt, gravity, contact, boundary, pushout, deactivate, every, free_bodies):
     for s in range(n_sub):
         for d in domains:
             d.p2g(dt)
@@ -321,6 +366,10 @@ def _run(domains, transport, n_sub, dt, gravity, contact, boundary, pushout, dea
         for d in domains:
             d.unpack("vel")
             d.g2p(dt, pushout, deactivate)
+        if free_bodies:
+            transport.reduce_contact(domains)
+            for d in domains:
+                d.free_bodies(dt, gravity)
         if (s + 1) % every == 0:
             counts = [d.migrate_pack() for d in domains]
             transport.migrate(domains, counts)

@@ -80,6 +80,88 @@ def test_slabs_match_single_domain(k):
     assert np.abs(v - want["v"]).max() <= 1e-3 * np.abs(want["v"]).max()
 
 
+def _free_sphere():
+    return scenes.shape_spec({"geometry": {"kind": "sphere", "radius": 0.08}, "mu_k": 0.2, "c_d": 1.0,
+                              "motion": {"kind": "free", "mass": 0.5, "inertia": [0.00128] * 3,
+                                         "position": [0.61, 0.37, 0.4], "velocity": [0.0, -1.0, 0.0]}}, DX)
+
+
+@pytest.mark.gpu
+def test_slabs_free_body_match_single_domain():
+    """A free sphere pressed into the tissue across the cut plane: every slab sums contact
+    over its owned nodes, the sums are all-reduced, and every slab integrates the same pose."""
+    p = _slab_particles()
+    p["v"][:] = 0.0
+    n, sub, dt = len(p["x"]), 24, 1e-3
+    shapes = [_floor(), _free_sphere()]
+    ref = api.SolverState(DIMS, DX, (0.0, 0.0, 0.0))
+    ref.set_materials(MATS)
+    ref.set_particles(p, with_stress=False)
+    ref.set_shapes(shapes)
+    for _ in range(sub):
+        ref.reset_contact()
+        ref.step_mls(dt, GRAV, contact=True)
+        ref.integrate_free_bodies(GRAV, dt)
+    want, want_pose = ref.get_particles(), ref.shape_poses()[1]
+
+    bx = dd.base_x(p["x"][:, 0], 0.0, DX)
+    bounds = dd.slab_bounds(DIMS[0], 2, np.bincount(np.clip(bx, 0, DIMS[0] - 1), minlength=DIMS[0]))
+    assert bounds[0][1] * DX > 0.53 and bounds[0][1] * DX < 0.69  # the sphere straddles the cut
+    own = dd.owner_of(bx, bounds)
+    doms = []
+    for r, (lo, hi) in enumerate(bounds):
+        d = dd.SlabDomain(DIMS, DX, (0.0, 0.0, 0.0), lo, hi, margin=2, capacity=n)
+        d.set_materials(MATS)
+        d.set_shapes(shapes)
+        sel = np.nonzero(own == r)[0]
+        d.set_particles({key: val[sel] for key, val in p.items()}, sel.astype(np.uint32))
+        doms.append(d)
+    dd.run_substeps(doms, dd.LocalTransport(), sub, dt, GRAV, contact=True, migrate_every=2, free_bodies=True)
+    poses = [d.shape_poses(2)[1] for d in doms]
+    for q in poses:  # every slab integrated the same body
+        assert np.array_equal(q["position"], poses[0]["position"])
+    moved = want_pose["position"] - np.array([0.61, 0.37, 0.4], F32)
+    assert np.abs(moved).max() > 0.01  # the sphere moved and was decelerated by the tissue
+    assert want_pose["linear_velocity"][1] > -1.0 - 9.81 * dt * sub + 0.05  # contact slowed it
+    assert np.abs(poses[0]["position"] - want_pose["position"]).max() <= 1e-3 * DX
+    assert np.abs(poses[0]["linear_velocity"] - want_pose["linear_velocity"]).max() <= \
+        1e-3 * np.abs(want_pose["linear_velocity"]).max()
+    got = [d.download() for d in doms]
+    x = np.zeros((n, 3), F32)
+    for g in got:
+        x[g["ids"]] = g["x"]
+    assert np.abs(x - want["x"]).max() <= 1e-3 * DX
+
+
+def _allreduce_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    t = dd.DistTransport(rank, world)
+    sums = torch.full((12,), 1.5 * (rank + 1), dtype=torch.float64)  # 2 shapes x 6
+    cnt = torch.tensor([rank + 1, 10 * (rank + 1)], dtype=torch.int32)
+    t.allreduce_tensors(sums, cnt)
+    q.put((rank, sums.tolist(), cnt.tolist()))
+    dist.destroy_process_group()
+
+
+def test_dist_transport_contact_allreduce_gloo():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_allreduce_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in ps:
+        pr.start()
+    res = [q.get(timeout=120) for _ in ps]
+    for pr in ps:
+        pr.join(timeout=60)
+    for _, sums, cnt in res:  # both ranks hold the total
+        assert sums == [4.5] * 12 and cnt == [3, 30]
+
+
 def test_slab_bounds_balance_and_min_width():
     w = np.zeros(64)
     w[10:30] = 100.0
