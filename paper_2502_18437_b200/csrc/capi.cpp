@@ -842,8 +842,11 @@ void run_frame(Batch& b, float dt) {
     const float dt_sub = dt / static_cast<float>(n_sub);
     const int ns = e.n_shapes();
     bool any_free = false;
-    // host: per-substep kinematic / target poses (bit-identical float math)
-    if (ns > 0) {
+    // host: per-substep kinematic / target poses (bit-identical float math).  Only the grid
+    // update and later kernels read the table, so it is built while the frame's binning
+    // and first P2G already run on the device.
+    auto build_pose_table = [&] {
+        if (ns <= 0) return;
         std::vector<DevPose> table(static_cast<size_t>(n_sub) * ns);
         std::vector<uint8_t> ovr(table.size(), 0);
         std::vector<DevPose> fp;
@@ -885,7 +888,7 @@ void run_frame(Batch& b, float dt) {
             }
         }
         e.set_pose_table(n_sub, table, ovr);
-    }
+    };
     e.reset_counters();
     e.reset_contact(true, true);
     // binning restores the spatial compactness of the 256-slot groups; drift inside a group
@@ -905,6 +908,7 @@ void run_frame(Batch& b, float dt) {
             }
             ++b.since_sort;
             if (!fused_in) e.p2g(true, dt_sub, true, standard);
+            if (sub == 0) build_pose_table();
             e.grid_update(sub, dt_sub, cfg.gravity, true, true, cfg.boundary);
             const bool fuse = can_fuse && sub + 1 < n_sub && b.since_sort < resort;
             if (fuse) e.g2p2g(sub, dt_sub, standard);
@@ -918,6 +922,7 @@ void run_frame(Batch& b, float dt) {
         for (int it = 0; it < cfg.iterations; ++it) {
             const bool last = it == cfg.iterations - 1;
             e.p2g(false, dt_sub);
+            if (it == 0) build_pose_table();
             e.grid_update(0, dt_sub, cfg.gravity, it == 0, true, cfg.boundary);
             e.g2p_pb(0, dt_sub, last, last, last);
         }

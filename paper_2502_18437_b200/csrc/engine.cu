@@ -973,9 +973,8 @@ void Engine::snapshot(float* x, float* v, uint8_t* active, std::vector<double>& 
         if (x) { I.io_x.alloc(12 * N); io.x = I.io_x.as<float>(); }
         if (v) { I.io_v.alloc(12 * N); io.v = I.io_v.as<float>(); }
         if (active) { I.io_a.alloc(N); io.active = I.io_a.as<uint8_t>(); }
-        launch_download(P, io, I.st);
-        launch_totals(P, I.io_tot.as<double>(), I.st);
-        I.counted(2);
+        launch_frame_result(P, io, I.io_tot.as<double>(), I.st);
+        I.counted(1);
     }
     // the small totals copy goes first: queued behind the arrays on the same copy engine it
     // would hold the host for the whole transfer

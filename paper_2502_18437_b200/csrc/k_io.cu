@@ -134,6 +134,69 @@ __global__ void __launch_bounds__(kTotThreads) k_totals(const Params P, double* 
     }
 }
 
+// FrameResult in one pass (scene.hpp:251-266): x, v, active into original-order staging and
+// the per-scene FP64 totals of k_totals, reading each slot's P0 / P1 / PR planes once.
+__global__ void __launch_bounds__(kTotThreads) k_frame_result(const Params P, IoArrays out, double* totals) {
+    __shared__ double red[5][kTotThreads];
+    __shared__ int scn[kTotThreads];
+    const int64_t span = static_cast<int64_t>(kTotThreads) * kTotPerThread;
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * span; base < P.n_total;
+         base += static_cast<int64_t>(gridDim.x) * span) {
+        double t[5] = {0, 0, 0, 0, 0};
+        int scene = -1;
+        for (int i = 0; i < kTotPerThread; ++i) {  // coalesced: stride blockDim per step
+            const int64_t s = base + static_cast<int64_t>(i) * kTotThreads + threadIdx.x;
+            if (s >= P.n_total) break;
+            const float4 r = P.pl[PR][s];
+            const uint32_t o32 = __float_as_uint(r.w);
+            if (o32 == kHoleOrig) continue;
+            const uint64_t o = o32;
+            const uint32_t flags = __float_as_uint(r.z);
+            const bool act = (flags & kActiveBit) != 0;
+            const float4 a = P.pl[0][s], b = P.pl[1][s];
+            if (out.x) { out.x[3 * o] = a.x; out.x[3 * o + 1] = a.y; out.x[3 * o + 2] = a.z; }
+            if (out.v) { out.v[3 * o] = a.w; out.v[3 * o + 1] = b.x; out.v[3 * o + 2] = b.y; }
+            if (out.active) out.active[o] = act ? 1 : 0;
+            if (!act) continue;
+            const int sc = static_cast<int>((flags >> kSceneShift) & kSceneMask);
+            if (sc != scene) {
+                if (scene >= 0)
+                    for (int q = 0; q < 5; ++q) atomicAdd(&totals[5 * scene + q], t[q]);
+                scene = sc;
+                for (int q = 0; q < 5; ++q) t[q] = 0.0;
+            }
+            const double m = r.x;
+            const float vx = a.w, vy = b.x, vz = b.y;
+            t[0] += m;
+            t[1] += m * vx;
+            t[2] += m * vy;
+            t[3] += m * vz;
+            t[4] += 0.5 * m * static_cast<double>(vx * vx + vy * vy + vz * vz);
+        }
+        scn[threadIdx.x] = scene;
+        for (int q = 0; q < 5; ++q) red[q][threadIdx.x] = t[q];
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int cur = -1;
+            double acc[5] = {0, 0, 0, 0, 0};
+            for (int k = 0; k < kTotThreads; ++k) {
+                const int sc = scn[k];
+                if (sc < 0) continue;
+                if (sc != cur) {
+                    if (cur >= 0)
+                        for (int q = 0; q < 5; ++q) atomicAdd(&totals[5 * cur + q], acc[q]);
+                    cur = sc;
+                    for (int q = 0; q < 5; ++q) acc[q] = 0.0;
+                }
+                for (int q = 0; q < 5; ++q) acc[q] += red[q][k];
+            }
+            if (cur >= 0)
+                for (int q = 0; q < 5; ++q) atomicAdd(&totals[5 * cur + q], acc[q]);
+        }
+        __syncthreads();
+    }
+}
+
 // sigma(F) into an original-order array (materialises the cached stress, solvers.hpp:69-74).
 __global__ void k_stress(const Params P, float* out) {
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -211,6 +274,10 @@ void launch_upload(const Params& P, const IoArrays& in, int64_t n, cudaStream_t 
 }
 void launch_download(const Params& P, const IoArrays& out, cudaStream_t st) {
     k_download<<<blocks_for(P.n_total, 256, 148 * 16), 256, 0, st>>>(P, out);
+}
+void launch_frame_result(const Params& P, const IoArrays& out, double* totals, cudaStream_t st) {
+    k_frame_result<<<blocks_for(P.n_total, kTotThreads * kTotPerThread, 148 * 8), kTotThreads, 0, st>>>(P, out,
+                                                                                                     totals);
 }
 void launch_totals(const Params& P, double* totals, cudaStream_t st) {
     k_totals<<<blocks_for(P.n_total, kTotThreads * kTotPerThread, 148 * 8), kTotThreads, 0, st>>>(P, totals);
