@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU-baseline sample length")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dd", action="store_true", help="c4 through slab DD even at N=1 (one slab)")
+    ap.add_argument("--fusion", type=int, default=1, choices=[0, 1, 2],
+                    help="substep fusion (mpmb_set_fusion): 0 off, 1 auto, 2 always")
     return ap.parse_args()
 
 
@@ -281,6 +283,7 @@ def run_ours(args, rank, world, local_rank):
     sub = substeps_of(specs[0])
     t0 = time.time()
     batch = build_batch(specs)
+    batch.set_fusion(args.fusion)
     # a real (non-legacy) stream shared by the library launches and the timing events
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
@@ -325,6 +328,7 @@ def run_ours(args, rank, world, local_rank):
     # frame, so later frames cost more): the two numbers differ only by the host path.
     batch.destroy()
     batch = build_batch(specs)
+    batch.set_fusion(args.fusion)
     batch.set_stream(stream.cuda_stream)
     batch.advance_frames(DT_FRAME, max(args.warmup, 1))
     batch.fetch_results()
