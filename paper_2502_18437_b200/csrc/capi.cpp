@@ -911,10 +911,13 @@ void run_frame(Batch& b, float dt) {
             if (sub == 0) build_pose_table();
             e.grid_update(sub, dt_sub, cfg.gravity, true, true, cfg.boundary);
             const bool fuse = can_fuse && sub + 1 < n_sub && b.since_sort < resort;
-            if (fuse) e.g2p2g(sub, dt_sub, standard);
-            else if (standard) e.g2p_standard(sub, dt_sub, true, true);
-            else e.g2p_mls(sub, dt_sub, true, true);
-            if (ns > 0) e.free_bodies(sub, dt_sub, cfg.gravity, any_free, true, sub + 1 < n_sub ? sub + 1 : -1);
+            if (fuse) {
+                e.g2p2g(sub, dt_sub, standard, cfg.gravity, any_free);  // + free bodies of sub
+            } else {
+                if (standard) e.g2p_standard(sub, dt_sub, true, true);
+                else e.g2p_mls(sub, dt_sub, true, true);
+                if (ns > 0) e.free_bodies(sub, dt_sub, cfg.gravity, any_free, true, sub + 1 < n_sub ? sub + 1 : -1);
+            }
             fused_in = fuse;
         }
     } else {

@@ -783,19 +783,25 @@ void Engine::g2p_mls(int sub, float dt, bool pushout, bool deactivate) {
 // G2P(sub) + P2G(sub+1) in one launch (k_g2p2g), then the brick collect of sub+1.  The
 // caller runs free_bodies(sub) after it (its shape cull for sub+1 would overwrite the
 // table the fused push-out of sub still reads).
-void Engine::g2p2g(int sub, float dt, bool standard) {
+void Engine::g2p2g(int sub, float dt, bool standard, const float g[3], bool integrate) {
     Impl& I = *impl_;
     if (I.n_cap == 0) return;
     auto ev = I.begin();
-    cudaMemsetAsync(I.misc.p, 0, sizeof(uint32_t), I.st);  // active brick count of sub+1
     Params P = I.params();
     P.sub = std::min(sub, I.table_subs - 1);
     P.dt = dt;
+    P.g[0] = g[0]; P.g[1] = g[1]; P.g[2] = g[2];
     P.pushout = 1;
     P.deactivate = 1;
     P.commit = 1;
-    launch_g2p2g(P, (I.n + kGroup - 1) / kGroup, I.st, standard);
-    launch_collect_bricks(P, I.total_bricks, I.st);
+    launch_g2p2g(P, (I.n + kGroup - 1) / kGroup, I.st, standard);  // zeroes the brick count
+    if (I.n_shapes > 0) {
+        const int next = std::min(sub + 1, I.table_subs - 1);
+        launch_collect_free(P, I.total_bricks, integrate, true, next, I.st);
+        I.cull_sub = next;
+    } else {
+        launch_collect_bricks(P, I.total_bricks, I.st);
+    }
     I.counted(2);
     I.flag_parity = 1 - I.flag_parity;
     I.cur = 1 - I.cur;  // the state of sub+1 is in the other buffer

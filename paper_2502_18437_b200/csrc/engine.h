@@ -99,7 +99,9 @@ class Engine {
     void g2p_standard(int sub, float dt, bool pushout, bool deactivate);  // K4, PIC (solvers.hpp:107-135)
     // K4 of substep `sub` fused with K2 of sub+1 (MLS or standard; push-out and deactivation
     // on), followed by the brick collect of sub+1: replaces g2p_* then p2g inside a frame
-    void g2p2g(int sub, float dt, bool standard);
+    // With shapes, the free bodies of `sub` (free_bodies(sub, dt, g, integrate, true, sub+1))
+    // run in the collect launch; the caller then skips free_bodies.
+    void g2p2g(int sub, float dt, bool standard, const float g[3], bool integrate);
     // fusion policy: 0 off, 1 when G2P runs one warp per group (default), 2 always
     void set_fusion(int mode);
     // per-substep contact sums (device): double[6 * n_shapes], int32[n_shapes]

@@ -207,8 +207,7 @@ __global__ void __launch_bounds__(256) k_grid_bc(const Params P) {
 // the substep accumulators into the frame accumulators (scene.hpp:220-232).
 // next_sub >= 0: also build the cull table of that substep (its poses are final once the free
 // bodies have moved), saving the next substep's k_shape_cull launch.
-__global__ void k_free_bodies(const Params P, int integrate, int merge, int next_sub) {
-    pdl_enter();
+__device__ __forceinline__ void free_bodies_body(const Params& P, int integrate, int merge, int next_sub) {
     for (int i = threadIdx.x; i < P.n_shapes; i += blockDim.x) {
         const DevShape& sh = P.shapes[i];
         if (integrate && sh.motion == MOTION_FREE) {
@@ -283,6 +282,21 @@ __global__ void k_free_bodies(const Params P, int integrate, int merge, int next
     }
 }
 
+__global__ void k_free_bodies(const Params P, int integrate, int merge, int next_sub) {
+    pdl_enter();
+    free_bodies_body(P, integrate, merge, next_sub);
+}
+
+// The two small passes between K8 and the next grid update in one launch: the last block
+// runs the free bodies (K7), the others collect the active bricks of the next substep.
+// Both only read what K8 and the grid update before it wrote.
+__global__ void __launch_bounds__(256) k_collect_free(const Params P, uint32_t n_bricks, int integrate, int merge,
+                                                      int next_sub) {
+    pdl_enter();
+    if (blockIdx.x == gridDim.x - 1) free_bodies_body(P, integrate, merge, next_sub);
+    else collect_bricks_body(P, n_bricks, blockIdx.x, gridDim.x - 1);
+}
+
 // ===================================================================  launchers
 static int grid_for(int64_t work, int threads, int max_blocks) {
     int64_t b = (work + threads - 1) / threads;
@@ -300,6 +314,15 @@ void launch_grid_update(const Params& P, int64_t max_bricks, cudaStream_t st) {
 
 
 
+
+void launch_collect_free(const Params& P, uint32_t n_bricks, bool integrate, bool merge, int next_sub,
+                         cudaStream_t st) {
+    int64_t blocks = (static_cast<int64_t>(n_bricks) + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks < 1) blocks = 1;
+    launch_chain(k_collect_free, static_cast<int>(blocks) + 1, 256, 0, st, P, n_bricks, integrate ? 1 : 0,
+                 merge ? 1 : 0, next_sub);
+}
 
 void launch_free_bodies(const Params& P, bool integrate, bool merge, cudaStream_t st, int next_sub) {
     launch_chain(k_free_bodies, 1, 128, 0, st, P, integrate ? 1 : 0, merge ? 1 : 0, next_sub);

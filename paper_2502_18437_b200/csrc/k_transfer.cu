@@ -245,38 +245,10 @@ __device__ __forceinline__ void bspline_dw(float fx, float inv_dx, float dw[3]) 
     dw[2] = (fx - 0.5f) * inv_dx;
 }
 
-// Active-brick list from the P2G marks (warp-aggregated append; order is irrelevant).
-// Brick X is active when some X - d, d in {0,1}^3 (same scene), is marked with every bit of
-// d set (mark_bricks).  The marks are read across neighbours, so they cannot be cleared
-// here: the flag arrays alternate per substep and this pass zeroes the OTHER one, which
-// the next P2G marks.
+// Active-brick list from the P2G marks (collect_bricks_body, kernels.cuh).
 __global__ void __launch_bounds__(256) k_collect_bricks(const Params P, uint32_t n_bricks) {
     pdl_enter();
-    const unsigned full = 0xffffffffu;
-    const uint32_t stride = gridDim.x * blockDim.x;
-    const uint32_t nb0 = P.geo.nb[0], nb1 = P.geo.nb[1], bps = P.geo.bricks_per_scene;
-    for (uint32_t base = blockIdx.x * blockDim.x; base < n_bricks; base += stride) {
-        const uint32_t b = base + threadIdx.x;
-        bool on = false;
-        if (b < n_bricks) {
-            P.brick_flag_next[b] = 0u;
-            const uint32_t local = b % bps;
-            const uint32_t bx = local % nb0, by = (local / nb0) % nb1, bz = local / (nb0 * nb1);
-#pragma unroll
-            for (int d = 0; d < 8; ++d) {
-                const uint32_t dx = d & 1, dy = (d >> 1) & 1, dz = d >> 2;
-                if (bx < dx || by < dy || bz < dz) continue;
-                const uint32_t f = P.brick_flag[b - dx - dy * nb0 - dz * nb0 * nb1];
-                on = on || ((f & 8u) && (f & static_cast<uint32_t>(d)) == static_cast<uint32_t>(d));
-            }
-        }
-        const unsigned m = __ballot_sync(full, on);
-        if (m == 0u) continue;
-        uint32_t start = 0;
-        if ((threadIdx.x & 31) == 0) start = atomicAdd(P.n_active_bricks, __popc(m));
-        start = __shfl_sync(full, start, 0);
-        if (on) P.active_bricks[start + __popc(m & lanemask_lt())] = b;
-    }
+    collect_bricks_body(P, n_bricks, blockIdx.x, gridDim.x);
 }
 
 void launch_collect_bricks(const Params& P, uint32_t n_bricks, cudaStream_t st) {
@@ -871,6 +843,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(cons
 template <bool STD>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_g2p2g(const __grid_constant__ Params P) {
     pdl_enter();
+    // the active-brick count of substep s+1 (read by the grid update of s, appended to by
+    // the collect after this kernel): zeroed here instead of by a memset node, which would
+    // break the programmatic-launch chain
+    if (blockIdx.x == 0 && threadIdx.x == 0) *P.n_active_bricks = 0u;
     extern __shared__ float4 smem[];
     const int lane = threadIdx.x & 31;
     const uint32_t n_groups = *P.n_groups;

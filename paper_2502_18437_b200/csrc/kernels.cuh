@@ -152,6 +152,40 @@ __device__ __forceinline__ unsigned lanemask_lt() {
     return m;
 }
 
+// Active-brick list from the P2G marks (warp-aggregated append; order is irrelevant).
+// Brick X is active when some X - d, d in {0,1}^3 (same scene), is marked with every bit of
+// d set (mark_bricks).  The marks are read across neighbours, so they cannot be cleared
+// here: the flag arrays alternate per substep and this pass zeroes the OTHER one, which
+// the next P2G marks.  Blocks [0, nblk) of 256 threads stride over the bricks.
+__device__ __forceinline__ void collect_bricks_body(const Params& P, uint32_t n_bricks, uint32_t blk,
+                                                    uint32_t nblk) {
+    const unsigned full = 0xffffffffu;
+    const uint32_t stride = nblk * blockDim.x;
+    const uint32_t nb0 = P.geo.nb[0], nb1 = P.geo.nb[1], bps = P.geo.bricks_per_scene;
+    for (uint32_t base = blk * blockDim.x; base < n_bricks; base += stride) {
+        const uint32_t b = base + threadIdx.x;
+        bool on = false;
+        if (b < n_bricks) {
+            P.brick_flag_next[b] = 0u;
+            const uint32_t local = b % bps;
+            const uint32_t bx = local % nb0, by = (local / nb0) % nb1, bz = local / (nb0 * nb1);
+#pragma unroll
+            for (int d = 0; d < 8; ++d) {
+                const uint32_t dx = d & 1, dy = (d >> 1) & 1, dz = d >> 2;
+                if (bx < dx || by < dy || bz < dz) continue;
+                const uint32_t f = P.brick_flag[b - dx - dy * nb0 - dz * nb0 * nb1];
+                on = on || ((f & 8u) && (f & static_cast<uint32_t>(d)) == static_cast<uint32_t>(d));
+            }
+        }
+        const unsigned m = __ballot_sync(full, on);
+        if (m == 0u) continue;
+        uint32_t start = 0;
+        if ((threadIdx.x & 31) == 0) start = atomicAdd(P.n_active_bricks, __popc(m));
+        start = __shfl_sync(full, start, 0);
+        if (on) P.active_bricks[start + __popc(m & lanemask_lt())] = b;
+    }
+}
+
 struct Part {
     float x[3], v[3], C[9], F[9];
 };

@@ -49,6 +49,9 @@ void launch_g2p2g(const Params& P, int64_t max_groups, cudaStream_t st, bool sta
 void launch_collect_bricks(const Params& P, uint32_t n_bricks, cudaStream_t st);
 void launch_pushout(const Params& P, cudaStream_t st);
 void launch_deactivate(const Params& P, cudaStream_t st);
+// k_collect_free: the brick collect of the next substep + the free bodies, one launch
+void launch_collect_free(const Params& P, uint32_t n_bricks, bool integrate, bool merge, int next_sub,
+                         cudaStream_t st);
 void launch_free_bodies(const Params& P, bool integrate, bool merge, cudaStream_t st, int next_sub = -1);
 void launch_grid_bc(const Params& P, int64_t max_bricks, cudaStream_t st);
 
