@@ -137,7 +137,7 @@ struct Engine::Impl {
     uint64_t total_nodes = 0;
     uint32_t total_bricks = 0;
     DevBuf dead_mom;  // grid readback only (enable_grid_readback)
-    DevBuf grid_acc, grid_vel, brick_flag, brick_stamp, active_bricks, brick_scene, misc;
+    DevBuf grid_acc, grid_vel, brick_flag, brick_stamp, active_bricks, active_info, brick_scene, misc;
     int flag_parity = 0;  // which half of brick_flag P2G marks (flips at every collect)
     bool exact = false;   // exact mode (k_exact.cu): the reference's arithmetic and order
     DevBuf ex_scratch, ex_bidx;
@@ -261,6 +261,7 @@ struct Engine::Impl {
         P.brick_flag_next = brick_flag.as<uint32_t>() + static_cast<size_t>(1 - flag_parity) * total_bricks;
         P.brick_stamp = brick_stamp.as<uint32_t>();
         P.active_bricks = active_bricks.as<uint32_t>();
+        P.active_info = active_info.as<uint2>();
         P.n_active_bricks = misc.as<uint32_t>();
         P.brick_scene = brick_scene.as<uint32_t>();
         P.order = order.as<uint8_t>();  // per-substep group order (k_transfer.cu)
@@ -315,6 +316,9 @@ Engine::Engine(const std::vector<SceneGrid>& scenes) : impl_(new Impl), scenes_(
         d.node_base = node_base;
         d.brick_base = brick_base;
         const uint64_t nb = static_cast<uint64_t>(d.nb[0]) * d.nb[1] * d.nb[2];
+        // the decoded active-brick list packs 10 bits per brick coordinate (active_info)
+        if (d.nb[0] >= 1024 || d.nb[1] >= 1024 || d.nb[2] >= 1024)
+            throw std::invalid_argument("engine: grid too large (4096 nodes per axis at most)");
         // brick ids are 32-bit; the brick flags/stamps are one word per brick
         if (brick_base + nb >= (1ull << 31)) throw std::invalid_argument("engine: too many grid bricks (>2^31)");
         node_base += nb * kBrickNodes;
@@ -370,6 +374,7 @@ Engine::Engine(const std::vector<SceneGrid>& scenes) : impl_(new Impl), scenes_(
     I.brick_flag.alloc(2 * sizeof(uint32_t) * I.total_bricks);  // alternating mark arrays
     I.brick_stamp.alloc(sizeof(uint32_t) * I.total_bricks);
     I.active_bricks.alloc(sizeof(uint32_t) * I.total_bricks);
+    I.active_info.alloc(sizeof(uint2) * I.total_bricks);
     check(cudaMemset(I.brick_flag.p, 0, 2 * sizeof(uint32_t) * I.total_bricks), "memset");
     check(cudaMemset(I.brick_stamp.p, 0xFF, sizeof(uint32_t) * I.total_bricks), "memset");
     std::vector<uint32_t> bs(I.total_bricks);

@@ -59,39 +59,62 @@ void launch_shape_cull(const Params& P, cudaStream_t st) { launch_chain(k_shape_
 // in order per node (last shape wins, contact.hpp:106-134); each warp reduces its
 // per-shape impulse/torque/count with shuffles and adds them in FP64.
 //
-// Latency: the per-brick chain (brick id -> accumulator -> shapes) is software-pipelined
-// over the grid-stride loop: brick ids are loaded two iterations ahead and accumulators
-// one ahead; the scene follows from the brick id arithmetically (uniform geometry).
+// Latency: the per-brick chain (brick -> accumulator -> shapes) is software-pipelined over
+// the grid-stride loop: the decoded brick (active_info, written by the collect) is loaded
+// two iterations ahead and the accumulator one ahead; the scene's shape range and first cull
+// box are cached per thread (consecutive bricks mostly belong to one scene).
 __global__ void __launch_bounds__(256) k_grid_update(const Params P) {
     pdl_enter();
     const uint32_t n_bricks = *P.n_active_bricks;
     const int l = threadIdx.x & 63;
+    const int li = l & 3, lj = (l >> 2) & 3, lk = l >> 4;
     const uint32_t per_block = blockDim.x >> 6;
     const int lane = threadIdx.x & 31;
     const uint32_t bstride = gridDim.x * per_block;
+    const uint64_t nps = P.geo.nodes_per_scene;
     uint32_t bi = blockIdx.x * per_block + (threadIdx.x >> 6);
-    uint32_t gb_next = bi < n_bricks ? P.active_bricks[bi] : 0u;
-    uint32_t gb_after = bi + bstride < n_bricks ? P.active_bricks[bi + bstride] : 0u;
+    uint2 in_next = bi < n_bricks ? P.active_info[bi] : make_uint2(0u, 0u);
+    uint2 in_after = bi + bstride < n_bricks ? P.active_info[bi + bstride] : make_uint2(0u, 0u);
+    // node of this thread in decoded brick `in`
+    auto node_of = [&](uint2 in, int& i, int& j, int& k) {
+        i = static_cast<int>(in.x & 1023u) * 4 + li;
+        j = static_cast<int>((in.x >> 10) & 1023u) * 4 + lj;
+        k = static_cast<int>(in.x >> 20) * 4 + lk;
+        return static_cast<uint64_t>(in.y) * nps + node_linear(P.geo, i, j, k);
+    };
+    int ni, nj, nk;
+    uint64_t idx_next = node_of(in_next, ni, nj, nk);
     float4 a_next = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (bi < n_bricks) a_next = P.grid_acc[brick_node(P, gb_next, l)];
+    if (bi < n_bricks) a_next = P.grid_acc[idx_next];
+    int cs_scene = -1, cs_begin = 0, cs_count = 0;
+    float4 cs_lo = make_float4(0.f, 0.f, 0.f, -1.f), cs_hi = cs_lo;
     for (; bi < n_bricks; bi += bstride) {
-        const uint32_t gb = gb_next;
+        const uint2 in = in_next;
         const float4 a = a_next;
-        if (bi + bstride < n_bricks) a_next = P.grid_acc[brick_node(P, gb_after, l)];
-        gb_next = gb_after;
-        if (bi + 2 * bstride < n_bricks) gb_after = P.active_bricks[bi + 2 * bstride];
-        const int scene = static_cast<int>(gb / P.geo.bricks_per_scene);
+        const uint64_t idx = idx_next;
+        int i, j, k;
+        node_of(in, i, j, k);
+        in_next = in_after;
+        if (bi + bstride < n_bricks) {
+            idx_next = node_of(in_next, ni, nj, nk);
+            a_next = P.grid_acc[idx_next];
+        }
+        if (bi + 2 * bstride < n_bricks) in_after = P.active_info[bi + 2 * bstride];
+        const int scene = static_cast<int>(in.y);
         const SceneView S = scene_view(P, scene);
-        const uint32_t local = gb - S.brick_base;
-        const int bx = static_cast<int>(local % S.nb[0]);
-        const int by = static_cast<int>((local / S.nb[0]) % S.nb[1]);
-        const int bz = static_cast<int>(local / (static_cast<uint32_t>(S.nb[0]) * S.nb[1]));
-        const int i = bx * 4 + (l & 3), j = by * 4 + ((l >> 2) & 3), k = bz * 4 + (l >> 4);
-        const uint64_t idx = S.node_base + node_linear(P.geo, i, j, k);
+        if (P.contact && scene != cs_scene) {  // per-thread cache of the scene's shape range
+            cs_scene = scene;
+            cs_begin = P.scenes[scene].shape_begin;
+            cs_count = P.scenes[scene].shape_count;
+            if (cs_count > 0) {
+                cs_lo = P.cull[2 * cs_begin];
+                cs_hi = P.cull[2 * cs_begin + 1];
+            }
+        }
         const bool own = i >= P.geo.own_lo && i < P.geo.own_hi;
         const int ig = i + P.geo.goff;  // global x index (BC, node position)
         P.grid_acc[idx] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (l == 0) P.brick_stamp[gb] = P.epoch;
+        if (l == 0) P.brick_stamp[P.active_bricks[bi]] = P.epoch;
         const float m = a.w;
         const bool live = m > kMassEps;
         V3 v = mk(0.f, 0.f, 0.f);
@@ -99,17 +122,19 @@ __global__ void __launch_bounds__(256) k_grid_update(const Params P) {
             v = vdiv(mk(a.x, a.y, a.z), m);
             if (P.gravity) v = v + mk(P.g[0], P.g[1], P.g[2]) * P.dt;
         }
-        if (P.contact && P.scenes[S.scene].shape_count > 0) {  // contact.hpp:97-136, shapes in order
+        if (P.contact && cs_count > 0) {  // contact.hpp:97-136, shapes in order
             const V3 xn = mk(FA(S.origin[0], FM(static_cast<float>(i + P.geo.goff), S.dx)),  // state.hpp:49-51
                              FA(S.origin[1], FM(static_cast<float>(j), S.dx)),
                              FA(S.origin[2], FM(static_cast<float>(k), S.dx)));
-            for (int si = P.scenes[S.scene].shape_begin; si < P.scenes[S.scene].shape_begin + P.scenes[S.scene].shape_count; ++si) {
+            for (int si = cs_begin; si < cs_begin + cs_count; ++si) {
                 const DevShape& sh = P.shapes[si];
                 V3 imp = mk(0.f, 0.f, 0.f), tq = mk(0.f, 0.f, 0.f);
                 int hit = 0;
                 // a slab domain sums contact only over the nodes it owns (ghosts are the
                 // neighbour's; their velocities are overwritten by the halo exchange)
-                if (live && own && cull_may_touch(P, si, xn.x, xn.y, xn.z)) {
+                const bool near = si == cs_begin ? aabb_may_touch(cs_lo, cs_hi, xn.x, xn.y, xn.z)
+                                                 : cull_may_touch(P, si, xn.x, xn.y, xn.z);
+                if (live && own && near) {
                     const DevPose& pose = pose_of(P, si);
                     const Sdf s = sdf_query(sh, pose, P.verts, P.ints, xn);
                     if (node_in_contact(s, sh.hw)) {

@@ -64,6 +64,7 @@ struct Params {
     uint32_t* brick_flag_next;  // the other array: zeroed by k_collect_bricks for the next P2G
     uint32_t* brick_stamp;
     uint32_t* active_bricks;
+    uint2* active_info;  // per active brick: {bx | by << 10 | bz << 20, scene} (collect)
     uint32_t* n_active_bricks;
     const uint32_t* brick_scene;
     uint8_t* order;        // per group: kGroup bytes, slot-in-group by current stencil base
@@ -182,7 +183,13 @@ __device__ __forceinline__ void collect_bricks_body(const Params& P, uint32_t n_
         uint32_t start = 0;
         if ((threadIdx.x & 31) == 0) start = atomicAdd(P.n_active_bricks, __popc(m));
         start = __shfl_sync(full, start, 0);
-        if (on) P.active_bricks[start + __popc(m & lanemask_lt())] = b;
+        if (on) {
+            const uint32_t w = start + __popc(m & lanemask_lt());
+            P.active_bricks[w] = b;
+            const uint32_t local = b % bps;
+            P.active_info[w] = make_uint2((local % nb0) | (((local / nb0) % nb1) << 10) | ((local / (nb0 * nb1)) << 20),
+                                          b / bps);
+        }
     }
 }
 
