@@ -273,6 +273,14 @@ mpmb_status mpmb_state_synchronize(mpmb_state st);
  * velocity phase the reverse. */
 mpmb_status mpmb_dd_halo_buffers(mpmb_state st, void** send_lo, void** send_hi, void** recv_lo, void** recv_hi,
                                  int64_t* bytes, int64_t* plane_bytes, int32_t* margin);
+/* Halo window: the exchanged x-planes carry only nodes y in [y0, y1), z in [z0, z1) (clamped
+ * to the slab's storage).  Every slab must use the same window; it must cover every node a
+ * particle stencil can reach until the next update (mpmb_dd_particle_window + the drift
+ * margin).  plane_bytes of mpmb_dd_halo_buffers follows the window.  Default: whole planes. */
+mpmb_status mpmb_dd_set_window(mpmb_state st, int32_t y0, int32_t y1, int32_t z0, int32_t z1);
+/* Stencil reach of this slab's active particles: {min y node, max y node, min z node,
+ * max z node} (INT_MAX / INT_MIN when there are none).  Synchronises the stream. */
+mpmb_status mpmb_dd_particle_window(mpmb_state st, int32_t* out);
 mpmb_status mpmb_dd_p2g(mpmb_state st, float dt);  /* bins if needed; MLS P2G */
 mpmb_status mpmb_dd_pack_acc(mpmb_state st);
 mpmb_status mpmb_dd_unpack_acc(mpmb_state st);

@@ -166,6 +166,8 @@ PRODUCT_API.update({
     "dd_g2p": (C.c_int, [P, C.c_float, C.c_int32, C.c_int32]),
     "dd_migrate_pack": (C.c_int, [P, I64P, I64P]),
     "dd_contact_sums": (C.c_int, [P, VPP, VPP, ip]),
+    "dd_set_window": (C.c_int, [P, C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
+    "dd_particle_window": (C.c_int, [P, ip]),
     "dd_free_bodies": (C.c_int, [P, C.c_float, fp]),
     "dd_migrate_buffers": (C.c_int, [P, VPP, VPP, VPP, VPP, I64P]),
     "dd_migrate_unpack": (C.c_int, [P, C.c_int64, C.c_int64]),

@@ -323,7 +323,26 @@ extern "C" mpmb_status mpmb_dd_halo_buffers(mpmb_state st, void** send_lo, void*
         Engine& e = *S(st)->eng;
         e.dd_halo_buffers(send_lo, send_hi, recv_lo, recv_hi, bytes);
         if (margin) *margin = st->grid.margin;
-        if (plane_bytes) *plane_bytes = *bytes / (2 + st->grid.margin);
+        int y0, ny, z0, nz;
+        e.dd_plane_window(&y0, &ny, &z0, &nz);
+        if (plane_bytes) *plane_bytes = static_cast<int64_t>(ny) * nz * 16;  // one windowed x-plane
+        return MPMB_OK;
+    });
+}
+
+extern "C" mpmb_status mpmb_dd_set_window(mpmb_state st, int32_t y0, int32_t y1, int32_t z0, int32_t z1) {
+    return guarded([&] {
+        S(st)->eng->dd_set_window(y0, y1, z0, z1);
+        return MPMB_OK;
+    });
+}
+
+extern "C" mpmb_status mpmb_dd_particle_window(mpmb_state st, int32_t* out) {
+    return guarded([&] {
+        if (!out) fail(MPMB_INVALID_ARGUMENT, "null argument");
+        int w[4];
+        S(st)->eng->particle_window(w);
+        for (int q = 0; q < 4; ++q) out[q] = w[q];
         return MPMB_OK;
     });
 }

@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cstdlib>
 #include <cfloat>
 #include <cmath>
@@ -155,10 +156,15 @@ struct Engine::Impl {
     int slab_lo = 0, slab_hi = 0, margin = 0;
     DevBuf halo[4];      // send_lo, send_hi, recv_lo, recv_hi
     int64_t halo_bytes = 0;
+    int win[4] = {0, 0, 0, 0};  // halo y/z window: y0, ny, z0, nz (ny = 0: whole extent)
     DevBuf mig[4];       // particles: send_lo, send_hi, recv_lo, recv_hi
     int64_t mig_cap = 0;
     DevBuf mig_counts;
     int64_t mig_sent = 0;
+    // DD arrivals appended as extra groups since the last binning (no re-sort):
+    // free_slot = first slot past the groups + inactive tail (-1: read from the bin counts)
+    int64_t free_slot = -1, n_at_bin = 0;
+    int appends = 0;
     DevBuf dl_ids, dl_x, dl_v, dl_a, dl_cnt;  // download_compact staging (persistent)
     DevBuf planes[2][kPlanes];
     int cur = 0;
@@ -672,6 +678,9 @@ void Engine::bin() {
     I.counted(k);
     I.cur = 1 - I.cur;
     I.binned = true;
+    I.free_slot = -1;
+    I.n_at_bin = I.n;
+    I.appends = 0;
     I.end(CAT_SORT, ev);
 }
 
@@ -1165,12 +1174,23 @@ void Engine::dd_halo_buffers(void** send_lo, void** send_hi, void** recv_lo, voi
     *bytes = b;
 }
 
+// the y/z window of the halo planes (whole storage extent unless dd_set_window narrowed it)
+static void halo_window(const Params& P, const int win[4], int& y0, int& ny, int& z0, int& nz) {
+    if (win[1] > 0) {
+        y0 = win[0]; ny = win[1]; z0 = win[2]; nz = win[3];
+    } else {
+        y0 = 0; ny = P.geo.nb[1] * 4; z0 = 0; nz = P.geo.nb[2] * 4;
+    }
+}
+
 void Engine::dd_pack_acc() {
     Impl& I = *impl_;
     ensure_halo();
     Params P = I.params();
-    launch_halo(P, 0, P.grid_acc, I.halo[0].as<float4>(), 0, I.margin, I.st);
-    launch_halo(P, 0, P.grid_acc, I.halo[1].as<float4>(), P.geo.own_hi, 2 + I.margin, I.st);
+    int y0, ny, z0, nz;
+    halo_window(P, I.win, y0, ny, z0, nz);
+    launch_halo(P, 0, P.grid_acc, I.halo[0].as<float4>(), 0, I.margin, y0, ny, z0, nz, I.st);
+    launch_halo(P, 0, P.grid_acc, I.halo[1].as<float4>(), P.geo.own_hi, 2 + I.margin, y0, ny, z0, nz, I.st);
     I.counted(2);
 }
 
@@ -1178,8 +1198,10 @@ void Engine::dd_unpack_acc() {
     Impl& I = *impl_;
     ensure_halo();
     Params P = I.params();
-    launch_halo(P, 1, P.grid_acc, I.halo[3].as<float4>(), P.geo.own_hi - I.margin, I.margin, I.st);
-    launch_halo(P, 1, P.grid_acc, I.halo[2].as<float4>(), P.geo.own_lo, 2 + I.margin, I.st);
+    int y0, ny, z0, nz;
+    halo_window(P, I.win, y0, ny, z0, nz);
+    launch_halo(P, 1, P.grid_acc, I.halo[3].as<float4>(), P.geo.own_hi - I.margin, I.margin, y0, ny, z0, nz, I.st);
+    launch_halo(P, 1, P.grid_acc, I.halo[2].as<float4>(), P.geo.own_lo, 2 + I.margin, y0, ny, z0, nz, I.st);
     I.counted(2);
 }
 
@@ -1187,8 +1209,10 @@ void Engine::dd_pack_vel() {
     Impl& I = *impl_;
     ensure_halo();
     Params P = I.params();
-    launch_halo(P, 0, P.grid_vel, I.halo[0].as<float4>(), P.geo.own_lo, 2 + I.margin, I.st);
-    launch_halo(P, 0, P.grid_vel, I.halo[1].as<float4>(), P.geo.own_hi - I.margin, I.margin, I.st);
+    int y0, ny, z0, nz;
+    halo_window(P, I.win, y0, ny, z0, nz);
+    launch_halo(P, 0, P.grid_vel, I.halo[0].as<float4>(), P.geo.own_lo, 2 + I.margin, y0, ny, z0, nz, I.st);
+    launch_halo(P, 0, P.grid_vel, I.halo[1].as<float4>(), P.geo.own_hi - I.margin, I.margin, y0, ny, z0, nz, I.st);
     I.counted(2);
 }
 
@@ -1196,9 +1220,45 @@ void Engine::dd_unpack_vel() {
     Impl& I = *impl_;
     ensure_halo();
     Params P = I.params();
-    launch_halo(P, 2, P.grid_vel, I.halo[2].as<float4>(), 0, I.margin, I.st);
-    launch_halo(P, 2, P.grid_vel, I.halo[3].as<float4>(), P.geo.own_hi, 2 + I.margin, I.st);
+    int y0, ny, z0, nz;
+    halo_window(P, I.win, y0, ny, z0, nz);
+    launch_halo(P, 2, P.grid_vel, I.halo[2].as<float4>(), 0, I.margin, y0, ny, z0, nz, I.st);
+    launch_halo(P, 2, P.grid_vel, I.halo[3].as<float4>(), P.geo.own_hi, 2 + I.margin, y0, ny, z0, nz, I.st);
     I.counted(2);
+}
+
+void Engine::dd_set_window(int y0, int y1, int z0, int z1) {
+    Impl& I = *impl_;
+    const int py = I.geo.nb[1] * 4, pz = I.geo.nb[2] * 4;
+    y0 = std::max(y0, 0); z0 = std::max(z0, 0);
+    y1 = std::min(y1, py); z1 = std::min(z1, pz);
+    if (y1 <= y0 || z1 <= z0) {  // empty: keep one node so the buffers stay well formed
+        y1 = y0 + 1; z1 = z0 + 1;
+    }
+    I.win[0] = y0; I.win[1] = y1 - y0; I.win[2] = z0; I.win[3] = z1 - z0;
+}
+
+void Engine::dd_plane_window(int* y0, int* ny, int* z0, int* nz) {
+    Impl& I = *impl_;
+    Params P = I.params();
+    int a, b, c2, d;
+    halo_window(P, I.win, a, b, c2, d);
+    *y0 = a; *ny = b; *z0 = c2; *nz = d;
+}
+
+void Engine::particle_window(int out[4]) {
+    Impl& I = *impl_;
+    DevBuf w;
+    w.alloc(4 * sizeof(int));
+    const int init[4] = {INT_MAX, INT_MIN, INT_MAX, INT_MIN};
+    check(cudaMemcpyAsync(w.p, init, sizeof(init), cudaMemcpyHostToDevice, I.st), "h2d");
+    if (I.n_cap > 0) {
+        Params P = I.params();
+        launch_particle_window(P, w.as<int>(), I.st);
+        I.counted(1);
+    }
+    check(cudaMemcpyAsync(out, w.p, sizeof(init), cudaMemcpyDeviceToHost, I.st), "d2h");
+    check(cudaStreamSynchronize(I.st), "window");
 }
 
 void Engine::collect_bricks() {
@@ -1246,22 +1306,54 @@ void Engine::dd_migrate_pack(int64_t* n_lo, int64_t* n_hi) {
 void Engine::dd_migrate_unpack(int64_t n_from_lo, int64_t n_from_hi) {
     Impl& I = *impl_;
     if (n_from_lo > I.mig_cap || n_from_hi > I.mig_cap) throw std::invalid_argument("engine: migration count");
+    const int64_t arrivals = n_from_lo + n_from_hi;
+    if (arrivals == 0 && I.binned) {
+        // departures only left holes inside their groups (never active): the binned layout
+        // stays valid, so no re-binning
+        I.n -= I.mig_sent;
+        n_total_ = I.n;
+        I.mig_sent = 0;
+        return;
+    }
     int64_t first = I.n;  // upload layout: particles then holes
     if (I.binned) {       // binned layout: groups, then the inactive tail, then holes
-        uint32_t c[4] = {0, 0, 0, 0};
-        check(cudaMemcpyAsync(c, I.b_counts.p, sizeof(c), cudaMemcpyDeviceToHost, I.st), "d2h");
-        check(cudaStreamSynchronize(I.st), "migrate");
-        first = static_cast<int64_t>(c[3]) + (I.n - static_cast<int64_t>(c[2]));
+        if (I.free_slot < 0) {
+            uint32_t c[4] = {0, 0, 0, 0};
+            check(cudaMemcpyAsync(c, I.b_counts.p, sizeof(c), cudaMemcpyDeviceToHost, I.st), "d2h");
+            check(cudaStreamSynchronize(I.st), "migrate");
+            I.free_slot = static_cast<int64_t>(c[3]) + (I.n_at_bin - static_cast<int64_t>(c[2]));
+        }
+        first = I.free_slot;
     }
-    if (first + n_from_lo + n_from_hi > I.n_cap) throw std::runtime_error("engine: slab capacity exceeded (set_capacity)");
+    if (first + arrivals > I.n_cap) throw std::runtime_error("engine: slab capacity exceeded (set_capacity)");
     Params P = I.params();
     launch_migrate_unpack(P, I.mig[2].as<float4>(), static_cast<uint32_t>(n_from_lo), static_cast<uint32_t>(first), I.st);
     launch_migrate_unpack(P, I.mig[3].as<float4>(), static_cast<uint32_t>(n_from_hi),
                           static_cast<uint32_t>(first + n_from_lo), I.st);
     I.counted(2);
-    I.n += n_from_lo + n_from_hi - I.mig_sent;
+    I.n += arrivals - I.mig_sent;
     n_total_ = I.n;
     I.mig_sent = 0;
+    // A few arrivals become extra groups over [old groups, first + arrivals): they take the
+    // inactive tail and some holes along (the transfers handle both), and P2G's per-substep
+    // warp sort orders them.  The other buffer gets the same slots (the transfers rewrite
+    // only grouped slots, which must start identical in both).  Many arrivals, or many
+    // appends since the last binning, re-bin instead (spatial compactness of the groups).
+    if (I.binned && arrivals * 64 <= I.n && I.appends < 16) {
+        const uint64_t end = static_cast<uint64_t>(first + arrivals);
+        const uint32_t groups = static_cast<uint32_t>((end + kGroup - 1) / kGroup);
+        const uint32_t tail = groups * static_cast<uint32_t>(kGroup);
+        for (int q = 0; q < kPlanes; ++q)
+            check(cudaMemcpyAsync(I.planes[1 - I.cur][q].as<float4>() + first, I.planes[I.cur][q].as<float4>() + first,
+                                  sizeof(float4) * arrivals, cudaMemcpyDeviceToDevice, I.st), "copy");
+        uint32_t c2[2] = {groups, tail};
+        check(cudaMemcpyAsync(static_cast<uint32_t*>(I.b_counts.p) + 1, &c2[0], 4, cudaMemcpyHostToDevice, I.st), "h2d");
+        check(cudaMemcpyAsync(static_cast<uint32_t*>(I.b_counts.p) + 3, &c2[1], 4, cudaMemcpyHostToDevice, I.st), "h2d");
+        check(cudaStreamSynchronize(I.st), "groups");  // c2 is on the host stack
+        I.free_slot = static_cast<int64_t>(end);
+        ++I.appends;
+        return;
+    }
     I.binned = false;
     bin();
 }

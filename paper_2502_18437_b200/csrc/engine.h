@@ -166,6 +166,11 @@ class Engine {
     void dd_unpack_vel();   // recv_lo -> low ghosts (M planes), recv_hi -> high ghosts (2+M)
     int dd_halo_planes(int side_send_hi, bool acc) const;
     void ensure_halo();
+    // halo planes restricted to nodes y in [y0, y1), z in [z0, z1) (clamped to the storage)
+    void dd_set_window(int y0, int y1, int z0, int z1);
+    void dd_plane_window(int* y0, int* ny, int* z0, int* nz);
+    // {min, max} stencil node reach of the active particles in y and z (synchronises)
+    void particle_window(int out[4]);
     // Migration (synchronous): particles whose base left the slab are packed for the
     // neighbours; returns their counts.  Buffers hold `cap` particles of 7 float4 each.
     void dd_migrate_pack(int64_t* n_lo, int64_t* n_hi);

@@ -8,9 +8,11 @@
 //                ghosts, [own_hi - M, own_hi) -> upper neighbour's low ghosts
 //   at binning   particles whose global base x left [lo, hi) move to the neighbour
 //
-// Halo buffers are dense x-planes over the storage's y/z extent: element
-// ((xr * PZ) + z) * PY + y, xr = plane within the halo.
+// Halo buffers hold x-planes restricted to a y/z window (default: the whole storage
+// extent; dd_set_window narrows it to the particles' reach).
 #include <cuda_runtime.h>
+
+#include <climits>
 
 #include "launch.h"
 
@@ -24,16 +26,16 @@ static int dd_blocks(int64_t n, int threads) {
 }
 
 // mode 0: copy pool -> buf; 1: add buf into pool (and mark the brick of every node with
-// mass); 2: copy buf -> pool
+// mass); 2: copy buf -> pool.  Only the y/z window [y0, y0 + ny) x [z0, z0 + nz) of each
+// x-plane travels (Engine::dd_set_window): buf element ((xr * nz) + z - z0) * ny + y - y0.
 template <int MODE>
-__global__ void k_halo(const Params P, float4* pool, float4* buf, int x0, int w) {
-    const int py = P.geo.nb[1] * 4, pz = P.geo.nb[2] * 4;
-    const int64_t n = static_cast<int64_t>(w) * py * pz;
+__global__ void k_halo(const Params P, float4* pool, float4* buf, int x0, int w, int y0, int ny, int z0, int nz) {
+    const int64_t n = static_cast<int64_t>(w) * ny * nz;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += stride) {
-        const int y = static_cast<int>(e % py);
-        const int z = static_cast<int>((e / py) % pz);
-        const int xr = static_cast<int>(e / (static_cast<int64_t>(py) * pz));
+        const int y = y0 + static_cast<int>(e % ny);
+        const int z = z0 + static_cast<int>((e / ny) % nz);
+        const int xr = static_cast<int>(e / (static_cast<int64_t>(ny) * nz));
         const int x = x0 + xr;
         const uint64_t idx = node_linear(P.geo, x, y, z);
         if (MODE == 0) {
@@ -58,13 +60,47 @@ int64_t dd_plane_nodes(const Params& P) {
     return static_cast<int64_t>(P.geo.nb[1]) * 4 * P.geo.nb[2] * 4;
 }
 
-void launch_halo(const Params& P, int mode, float4* pool, float4* buf, int x0, int w, cudaStream_t st) {
-    const int64_t n = dd_plane_nodes(P) * w;
+void launch_halo(const Params& P, int mode, float4* pool, float4* buf, int x0, int w, int y0, int ny, int z0, int nz,
+                 cudaStream_t st) {
+    const int64_t n = static_cast<int64_t>(ny) * nz * w;
     if (n <= 0) return;
     const int blocks = dd_blocks(n, 256);
-    if (mode == 0) k_halo<0><<<blocks, 256, 0, st>>>(P, pool, buf, x0, w);
-    else if (mode == 1) k_halo<1><<<blocks, 256, 0, st>>>(P, pool, buf, x0, w);
-    else k_halo<2><<<blocks, 256, 0, st>>>(P, pool, buf, x0, w);
+    if (mode == 0) k_halo<0><<<blocks, 256, 0, st>>>(P, pool, buf, x0, w, y0, ny, z0, nz);
+    else if (mode == 1) k_halo<1><<<blocks, 256, 0, st>>>(P, pool, buf, x0, w, y0, ny, z0, nz);
+    else k_halo<2><<<blocks, 256, 0, st>>>(P, pool, buf, x0, w, y0, ny, z0, nz);
+}
+
+// Node window of the active particles' stencils in y and z: out = {min base y, max base
+// y + 2, min base z, max base z + 2} (atomicMin / atomicMax; initialised by the host).
+__global__ void k_particle_window(const Params P, int* out) {
+    int ylo = INT_MAX, yhi = INT_MIN, zlo = INT_MAX, zhi = INT_MIN;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < P.n_total; s += stride) {
+        const float4 r = P.pl[PR][s];
+        if (__float_as_uint(r.w) == kHoleOrig || !(__float_as_uint(r.z) & kActiveBit)) continue;
+        const float4 a = P.pl[0][s];
+        float f;
+        const int by = stencil_base(a.y, P.geo.origin[1], P.geo.inv_dx, f);
+        const int bz = stencil_base(a.z, P.geo.origin[2], P.geo.inv_dx, f);
+        ylo = min(ylo, by); yhi = max(yhi, by + 2);
+        zlo = min(zlo, bz); zhi = max(zhi, bz + 2);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        ylo = min(ylo, __shfl_xor_sync(0xffffffffu, ylo, o));
+        yhi = max(yhi, __shfl_xor_sync(0xffffffffu, yhi, o));
+        zlo = min(zlo, __shfl_xor_sync(0xffffffffu, zlo, o));
+        zhi = max(zhi, __shfl_xor_sync(0xffffffffu, zhi, o));
+    }
+    if ((threadIdx.x & 31) == 0 && ylo <= yhi) {
+        atomicMin(&out[0], ylo);
+        atomicMax(&out[1], yhi);
+        atomicMin(&out[2], zlo);
+        atomicMax(&out[3], zhi);
+    }
+}
+
+void launch_particle_window(const Params& P, int* out, cudaStream_t st) {
+    k_particle_window<<<dd_blocks(P.n_total, 256), 256, 0, st>>>(P, out);
 }
 
 // Particles whose global stencil base x left [lo, hi): packed (7 float4 each) into the

@@ -57,7 +57,9 @@ void launch_grid_bc(const Params& P, int64_t max_bricks, cudaStream_t st);
 
 // ---- slab domain decomposition (k_dd.cu) ----
 int64_t dd_plane_nodes(const Params& P);
-void launch_halo(const Params& P, int mode, float4* pool, float4* buf, int x0, int w, cudaStream_t st);
+void launch_halo(const Params& P, int mode, float4* pool, float4* buf, int x0, int w, int y0, int ny, int z0, int nz,
+                 cudaStream_t st);
+void launch_particle_window(const Params& P, int* out /*{ylo, yhi, zlo, zhi}*/, cudaStream_t st);
 void launch_migrate_pack(const Params& P, int lo, int hi, float4* out_lo, float4* out_hi, uint32_t cap,
                          uint32_t* counts, cudaStream_t st);
 void launch_migrate_unpack(const Params& P, const float4* in, uint32_t n, uint32_t first, cudaStream_t st);

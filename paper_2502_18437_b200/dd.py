@@ -12,7 +12,8 @@ Per substep (library phases, include/mpm_b200.h):
     unpack_vel -> g2p -> [free bodies: ALLREDUCE(contact sums) -> free_bodies]
                                             [+ every `margin` substeps: migrate]
 
-EXCHANGE: each rank sends `send_lo` to its lower neighbour (into that rank's `recv_hi`) and
+Halos carry only the y/z window the particles' stencils can reach (set at every migration),
+not whole x-planes.  EXCHANGE: each rank sends `send_lo` to its lower neighbour (into that rank's `recv_hi`) and
 `send_hi` to its upper neighbour (into `recv_lo`); grid-sum phase: `margin` planes go down
 and `2 + margin` up, the velocity phase the reverse.  Two transports share that rule:
 
@@ -114,6 +115,18 @@ class SlabDomain:
                                                     C.byref(m)), self.lib, "halo_buffers")
             self.halo = ([q.value for q in p], b.value, pb.value)
         return self.halo
+
+    def set_window(self, y0, y1, z0, z1):
+        """Exchange only nodes y in [y0, y1), z in [z0, z1) of each halo x-plane."""
+        api.check(self.lib.mpmb_dd_set_window(self.h, int(y0), int(y1), int(z0), int(z1)), self.lib, "dd_set_window")
+        self.halo = None  # plane bytes changed
+
+    def particle_window(self):
+        """(min y node, max y node, min z node, max z node) the active particles' stencils reach."""
+        out = np.zeros(4, np.int32)
+        api.check(self.lib.mpmb_dd_particle_window(self.h, out.ctypes.data_as(capi.ip)), self.lib,
+                  "dd_particle_window")
+        return [int(v) for v in out]
 
     def halo_sizes(self, phase: str):
         """Bytes sent down / up in a phase ('acc': M planes down, 2+M up; 'vel': reverse)."""
@@ -245,6 +258,10 @@ class LocalTransport:
             v[0].copy_(tot[0])
             v[1].copy_(tot[1])
 
+    def union_window(self, domains):
+        w = [d.particle_window() for d in domains]
+        return [min(v[0] for v in w), max(v[1] for v in w), min(v[2] for v in w), max(v[3] for v in w)]
+
     def migrate(self, domains, counts):
         import torch
         rec = [[0, 0] for _ in domains]
@@ -296,6 +313,21 @@ class DistTransport:
         for t in tensors:
             dist.all_reduce(t, op=dist.ReduceOp.SUM)
 
+    def union_window(self, domains):
+        """The stencil-reach window of every rank's particles (all-reduce of min / max)."""
+        import torch
+        import torch.distributed as dist
+        (d,) = domains
+        w = d.particle_window()
+        if self.world == 1:
+            return w
+        big = 1 << 30  # an empty slab reports INT_MAX / INT_MIN: neutral after clamping
+        t = torch.tensor([-min(w[0], big), max(w[1], -big), -min(w[2], big), max(w[3], -big)], dtype=torch.int64,
+                         device="cuda" if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t = t.tolist()
+        return [-t[0], t[1], -t[2], t[3]]
+
     def reduce_contact(self, domains):
         (d,) = domains
         v = d.contact_sums()
@@ -335,10 +367,13 @@ class DistTransport:
 
 
 def run_substeps(domains, transport, n_sub, dt, gravity, *, contact=True, boundary=0, pushout=False,
-                 deactivate=False, migrate_every=None, free_bodies=False):
+                 deactivate=False, migrate_every=None, free_bodies=False, window=True):
     """Advance every slab of this process `n_sub` substeps (MLS), exchanging halos.
     free_bodies: all-reduce the per-shape contact sums every substep and integrate the free
-    bodies on every slab (scene.hpp:220-232)."""
+    bodies on every slab (scene.hpp:220-232).
+    window: exchange only the y/z window the particles' stencils can reach until the next
+    migration (their current reach, widened by one cell per substep: CFL), instead of
+    whole x-planes; recomputed at every migration."""
     import torch
     cur = torch.cuda.current_stream()
     # library kernels and the transport's copies / NCCL calls must share ONE real stream
@@ -348,11 +383,23 @@ def run_substeps(domains, transport, n_sub, dt, gravity, *, contact=True, bounda
         for d in domains:
             d.set_stream(stream.cuda_stream)
         _run(domains, transport, n_sub, dt, gravity, contact, boundary, pushout, deactivate,
-             migrate_every or min(d.margin for d in domains), free_bodies)
+             migrate_every or min(d.margin for d in domains), free_bodies, window)
     stream.synchronize()
 
 
-def _run(domains, transport, n_sub, dt, gravity, contact, boundary, pushout, deactivate, every, free_bodies):
+def _set_window(domains, transport, every):
+    w = transport.union_window(domains)
+    if w[0] > w[1]:  # no active particle anywhere: keep a minimal window
+        w = [0, 0, 0, 0]
+    pad = every + 1
+    for d in domains:
+        d.set_window(w[0] - pad, w[1] + 1 + pad, w[2] - pad, w[3] + 1 + pad)
+
+
+def _run(domains, transport, n_sub, dt, gravity, contact, boundary, pushout, deactivate, every, free_bodies,
+         window):
+    if window:
+        _set_window(domains, transport, every)
     for s in range(n_sub):
         for d in domains:
             d.p2g(dt)
@@ -373,3 +420,5 @@ def _run(domains, transport, n_sub, dt, gravity, contact, boundary, pushout, dea
         if (s + 1) % every == 0:
             counts = [d.migrate_pack() for d in domains]
             transport.migrate(domains, counts)
+            if window:
+                _set_window(domains, transport, every)

@@ -42,8 +42,8 @@ def _floor():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("k", [2, 3])
-def test_slabs_match_single_domain(k):
+@pytest.mark.parametrize("k,window", [(2, True), (3, True), (2, False)])
+def test_slabs_match_single_domain(k, window):
     p = _slab_particles()
     n, sub, dt = len(p["x"]), 24, 1e-3
     ref = api.SolverState(DIMS, DX, (0.0, 0.0, 0.0))
@@ -65,7 +65,10 @@ def test_slabs_match_single_domain(k):
         sel = np.nonzero(own == r)[0]
         d.set_particles({key: val[sel] for key, val in p.items()}, sel.astype(np.uint32))
         doms.append(d)
-    dd.run_substeps(doms, dd.LocalTransport(), sub, dt, GRAV, contact=True, migrate_every=2)
+    dd.run_substeps(doms, dd.LocalTransport(), sub, dt, GRAV, contact=True, migrate_every=2, window=window)
+    _, _, plane = doms[0].halo_buffers()
+    full = (DIMS[1] + (-DIMS[1]) % 4) * (DIMS[2] + (-DIMS[2]) % 4) * 16
+    assert (plane < full) if window else (plane == full)  # the window narrows the planes
     got = [d.download() for d in doms]
     ids = np.concatenate([g["ids"] for g in got])
     assert len(ids) == n and np.array_equal(np.sort(ids), np.arange(n))
