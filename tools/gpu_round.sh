@@ -10,5 +10,5 @@ if [ "${NCU:-1}" = "1" ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
   $CMD > gpurun_out/plain2.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_g2p2g" -s 2 -c 1 -o gpurun_out/${PROF:-prof}_fused -f $CMD > gpurun_out/ncu_full.log 2>&1; echo "ncu full (fused) rc=$?"
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_p2g|k_g2p[^2]|k_g2p$|k_grid_update" -s 3 -c 3 -o gpurun_out/${PROF:-prof} -f $CMD >> gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_p2g|k_grid_update" -s 0 -c 2 -o gpurun_out/${PROF:-prof} -f $CMD >> gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
 fi
