@@ -146,6 +146,7 @@ struct Engine::Impl {
     DevBuf ex_ckey, ex_crec, ex_cn, ex_cscratch;
     bool wide = false;  // thread-per-slot G2P (small problems, launch_g2p)
     int fusion = 1;     // k_g2p2g inside frames: 0 off, 1 unless wide, 2 always
+    int sps = 0;        // shapes per scene when uniform (Params::shapes_per_scene)
     int cull_sub = -1;  // the substep whose shape cull table is current (-1: none)  // exact contact records (k_exact.cu)
     PinnedBuf ex_cn_host;
     // misc u32 slots: [0] n_active_bricks
@@ -259,6 +260,7 @@ struct Engine::Impl {
         P.free_pose = free_pose.as<DevPose>();
         P.cull = cull.as<float4>();
         P.n_shapes = n_shapes;
+        P.shapes_per_scene = sps;
         P.mats = mats.as<float4>();
         P.grid_acc = grid_acc.as<float4>();
         P.grid_vel = grid_vel.as<float4>();
@@ -591,6 +593,9 @@ void Engine::set_shapes(const std::vector<std::vector<EngineShape>>& per_scene) 
     }
     I.n_shapes = static_cast<int>(ds.size());
     n_shapes_ = I.n_shapes;
+    I.sps = per_scene.empty() ? 0 : static_cast<int>(per_scene[0].size());
+    for (size_t s = 0; s < per_scene.size(); ++s)
+        if (static_cast<int>(per_scene[s].size()) != I.sps) I.sps = 0;
     check(cudaMemcpy(I.d_scenes.p, I.hs.data(), sizeof(DevScene) * I.hs.size(), cudaMemcpyHostToDevice), "scenes");
     const size_t ns = std::max<size_t>(1, ds.size());
     I.shapes.alloc(sizeof(DevShape) * ns);

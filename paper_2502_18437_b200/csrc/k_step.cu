@@ -60,9 +60,10 @@ void launch_shape_cull(const Params& P, cudaStream_t st) { launch_chain(k_shape_
 // per-shape impulse/torque/count with shuffles and adds them in FP64.
 //
 // Latency: the per-brick chain (brick -> accumulator -> shapes) is software-pipelined over
-// the grid-stride loop: the decoded brick (active_info, written by the collect) is loaded
-// two iterations ahead and the accumulator one ahead; the scene's shape range and first cull
-// box are cached per thread (consecutive bricks mostly belong to one scene).
+// the grid-stride loop (a stride spreads the costly contact bricks over all workers): the
+// decoded brick (active_info, written by the collect) is loaded two iterations ahead, its
+// accumulator and -- when every scene has the same shape count -- the first shape's cull box
+// one ahead.
 __global__ void __launch_bounds__(256) k_grid_update(const Params P) {
     pdl_enter();
     const uint32_t n_bricks = *P.n_active_bricks;
@@ -72,6 +73,8 @@ __global__ void __launch_bounds__(256) k_grid_update(const Params P) {
     const int lane = threadIdx.x & 31;
     const uint32_t bstride = gridDim.x * per_block;
     const uint64_t nps = P.geo.nodes_per_scene;
+    const uint32_t nb0 = static_cast<uint32_t>(P.geo.nb[0]), nb1 = static_cast<uint32_t>(P.geo.nb[1]);
+    const int sps = P.contact ? P.shapes_per_scene : 0;  // > 0: uniform shape ranges
     uint32_t bi = blockIdx.x * per_block + (threadIdx.x >> 6);
     uint2 in_next = bi < n_bricks ? P.active_info[bi] : make_uint2(0u, 0u);
     uint2 in_after = bi + bstride < n_bricks ? P.active_info[bi + bstride] : make_uint2(0u, 0u);
@@ -85,25 +88,39 @@ __global__ void __launch_bounds__(256) k_grid_update(const Params P) {
     int ni, nj, nk;
     uint64_t idx_next = node_of(in_next, ni, nj, nk);
     float4 a_next = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (bi < n_bricks) a_next = P.grid_acc[idx_next];
-    int cs_scene = -1, cs_begin = 0, cs_count = 0;
-    float4 cs_lo = make_float4(0.f, 0.f, 0.f, -1.f), cs_hi = cs_lo;
+    float4 lo_next = make_float4(0.f, 0.f, 0.f, -1.f), hi_next = lo_next;
+    if (bi < n_bricks) {
+        a_next = P.grid_acc[idx_next];
+        if (sps > 0) {
+            lo_next = P.cull[2 * in_next.y * sps];
+            hi_next = P.cull[2 * in_next.y * sps + 1];
+        }
+    }
     for (; bi < n_bricks; bi += bstride) {
         const uint2 in = in_next;
         const float4 a = a_next;
         const uint64_t idx = idx_next;
+        const float4 lo0 = lo_next, hi0 = hi_next;
         int i, j, k;
         node_of(in, i, j, k);
         in_next = in_after;
         if (bi + bstride < n_bricks) {
             idx_next = node_of(in_next, ni, nj, nk);
             a_next = P.grid_acc[idx_next];
+            if (sps > 0) {
+                lo_next = P.cull[2 * in_next.y * sps];
+                hi_next = P.cull[2 * in_next.y * sps + 1];
+            }
         }
         if (bi + 2 * bstride < n_bricks) in_after = P.active_info[bi + 2 * bstride];
         const int scene = static_cast<int>(in.y);
         const SceneView S = scene_view(P, scene);
-        if (P.contact && scene != cs_scene) {  // per-thread cache of the scene's shape range
-            cs_scene = scene;
+        int cs_begin = 0, cs_count = 0;
+        float4 cs_lo = lo0, cs_hi = hi0;
+        if (sps > 0) {
+            cs_begin = scene * sps;
+            cs_count = sps;
+        } else if (P.contact) {
             cs_begin = P.scenes[scene].shape_begin;
             cs_count = P.scenes[scene].shape_count;
             if (cs_count > 0) {
@@ -114,7 +131,9 @@ __global__ void __launch_bounds__(256) k_grid_update(const Params P) {
         const bool own = i >= P.geo.own_lo && i < P.geo.own_hi;
         const int ig = i + P.geo.goff;  // global x index (BC, node position)
         P.grid_acc[idx] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (l == 0) P.brick_stamp[P.active_bricks[bi]] = P.epoch;
+        if (l == 0)  // the brick id, rebuilt from the decoded coordinates
+            P.brick_stamp[S.brick_base + ((in.x >> 20) * nb1 + ((in.x >> 10) & 1023u)) * nb0 + (in.x & 1023u)] =
+                P.epoch;
         const float m = a.w;
         const bool live = m > kMassEps;
         V3 v = mk(0.f, 0.f, 0.f);

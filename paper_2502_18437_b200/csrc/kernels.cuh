@@ -56,6 +56,7 @@ struct Params {
     DevPose* free_pose;
     float4* cull;   // per shape, this substep: world AABB {min, bounded}, {max, 0} (k_shape_cull)
     int n_shapes;
+    int shapes_per_scene;  // > 0: scene s owns shapes [s k, s k + k) (batches of replicas); else 0
     const float4* mats;  // {kind, mu, lambda, beta}
     float4* grid_acc;
     float4* grid_vel;   // {v, m}; v = 0 at nodes of mass <= kMassEps
