@@ -356,9 +356,9 @@ mpmb_status mpmb_set_profiling(mpmb_handle h, int32_t on);
  * times slower than the default fast mode (float atomics). */
 mpmb_status mpmb_set_exact(mpmb_handle h, int32_t on);
 /* Substep fusion inside run_frame (Scene::run_frame, scene.hpp:199-235, MLS / standard):
- * G2P of substep s and P2G of s+1 run as one kernel.  0 off, 1 (default) when the engine
- * runs one warp per particle group, 2 always.  Results are the same up to float atomic
- * order either way. */
+ * G2P of substep s and P2G of s+1 run as one kernel.  0 off; 1 (default) and 2 on (2 was
+ * "always" when 1 excluded small problems).  Results are the same up to float atomic order
+ * either way. */
 mpmb_status mpmb_set_fusion(mpmb_handle h, int32_t mode);
 mpmb_status mpmb_get_profile(mpmb_handle h, mpmb_profile* out);
 /* Blocks until every frame enqueued on h has finished. */

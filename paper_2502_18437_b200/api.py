@@ -326,7 +326,7 @@ class Scene:
         check(self.lib.mpmb_advance(self.h, float(F32(dt))), self.lib, "advance")
 
     def set_fusion(self, mode: int):
-        """0 off, 1 (default) when G2P runs one warp per group, 2 always (mpmb_set_fusion)."""
+        """Substep fusion (mpmb_set_fusion): 0 off, 1 (default) / 2 on."""
         check(self.lib.mpmb_set_fusion(self.h, mode), self.lib, "fusion")
 
     def set_profiling(self, on: bool):
@@ -408,7 +408,7 @@ class SceneBatch:
         check(self.lib.mpmb_set_stream(self.h, C.c_void_p(stream_ptr)), self.lib, "set_stream")
 
     def set_fusion(self, mode: int):
-        """0 off, 1 (default) when G2P runs one warp per group, 2 always (mpmb_set_fusion)."""
+        """Substep fusion (mpmb_set_fusion): 0 off, 1 (default) / 2 on."""
         check(self.lib.mpmb_set_fusion(self.h, mode), self.lib, "fusion")
 
     def set_resort_interval(self, k: int):

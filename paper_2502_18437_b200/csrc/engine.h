@@ -102,7 +102,7 @@ class Engine {
     // With shapes, the free bodies of `sub` (free_bodies(sub, dt, g, integrate, true, sub+1))
     // run in the collect launch; the caller then skips free_bodies.
     void g2p2g(int sub, float dt, bool standard, const float g[3], bool integrate);
-    // fusion policy: 0 off, 1 when G2P runs one warp per group (default), 2 always
+    // fusion policy: 0 off, 1 (default) or 2 on
     void set_fusion(int mode);
     // per-substep contact sums (device): double[6 * n_shapes], int32[n_shapes]
     void contact_sub_buffers(void** sums, void** counts, int* n_shapes);

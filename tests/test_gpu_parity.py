@@ -157,6 +157,7 @@ def _scene_pair(spec):
 def test_scene_frames_vs_oracle(name, spec_fn, frames):
     spec = spec_fn()
     o, g = _scene_pair(spec)
+    g.set_profiling(True)
     dx = spec["grid"]["dx"]
     for _ in range(frames):
         o.advance(spec["dt_frame"])
@@ -165,6 +166,7 @@ def test_scene_frames_vs_oracle(name, spec_fn, frames):
     assert ro["n_particles"] == rg["n_particles"]
     assert np.array_equal(ro["active"], rg["active"])
     assert ro["deactivated"] == rg["deactivated"] and ro["inverted_f"] == rg["inverted_f"]
+    assert (g.profile()["ms_fused"] > 0.0) == (spec["solver"] != "pbmpm")  # MLS / standard run fused
     err = np.abs(ro["positions"] - rg["positions"]).max()
     assert err <= 1e-3 * dx, f"{name}: max|dx| {err / dx:.2e} dx"
     vmax = np.abs(ro["velocities"]).max()
@@ -210,9 +212,9 @@ def test_rotating_needle_within_reference_envelope(name, spec_fn, frames):
     assert imp_err <= 10 * imp_env + 1e-6 * p_scale
 
 
-# Substep fusion (k_g2p2g: G2P of substep s + P2G of s+1 in one kernel).  At these sizes the
-# engine would run the thread-per-slot G2P without fusion, so mode 2 forces it; the same
-# horizon bounds as the unfused scenes apply (the change is float atomic order only).
+# Substep fusion (k_g2p2g: G2P of substep s + P2G of s+1 in one kernel) is the default, so
+# the scene tests above run fused; this one runs the same scenes UNFUSED (mode 0: separate
+# P2G / thread-per-slot G2P launches) at the same horizon bounds.
 @pytest.mark.parametrize("name,spec_fn,frames", [
     ("cube_drop", scenes.cube_drop, 5),
     ("cube_drop_standard", lambda: scenes.cube_drop(solver="standard"), 5),
@@ -220,18 +222,18 @@ def test_rotating_needle_within_reference_envelope(name, spec_fn, frames):
     ("mesh_slicer", scenes.mesh_slicer_scene, 4),
     ("rigid_coupling", scenes.rigid_coupling, 4),
 ])
-def test_fused_substeps_vs_oracle(name, spec_fn, frames):
+def test_unfused_substeps_vs_oracle(name, spec_fn, frames):
     spec = spec_fn()
     o, g = _scene_pair(spec)
-    assert g.lib.mpmb_set_fusion(g.h, 2) == capi.OK
     assert g.lib.mpmb_set_fusion(g.h, 3) != capi.OK
+    assert g.lib.mpmb_set_fusion(g.h, 0) == capi.OK
     dx = spec["grid"]["dx"]
     g.set_profiling(True)
     for _ in range(frames):
         o.advance(spec["dt_frame"])
         g.advance(spec["dt_frame"])
         ro, rg = o.fetch_results(), g.fetch_results()
-    assert g.profile()["ms_fused"] > 0.0  # the fused kernel ran
+    assert g.profile()["ms_fused"] == 0.0  # the fused kernel did not run
     assert np.array_equal(ro["active"], rg["active"])
     assert ro["deactivated"] == rg["deactivated"] and ro["inverted_f"] == rg["inverted_f"]
     err = np.abs(ro["positions"] - rg["positions"]).max()
