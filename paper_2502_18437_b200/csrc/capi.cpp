@@ -941,12 +941,16 @@ void run_frame(Batch& b, float dt) {
         }
     } else {
         e.bin();
+        const bool can_fuse = e.fuse_ok();
+        bool fused_in = false;  // P2G of this iteration already ran inside the previous kernel
         for (int it = 0; it < cfg.iterations; ++it) {
             const bool last = it == cfg.iterations - 1;
-            e.p2g(false, dt_sub);
+            if (!fused_in) e.p2g(false, dt_sub);
             if (it == 0) build_pose_table();
             e.grid_update(0, dt_sub, cfg.gravity, it == 0, true, cfg.boundary);
-            e.g2p_pb(0, dt_sub, last, last, last);
+            fused_in = can_fuse && !last;  // the final G2P commits (solvers.hpp:269-277)
+            if (fused_in) e.g2p2g_pb(dt_sub);
+            else e.g2p_pb(0, dt_sub, last, last, last);
         }
         if (ns > 0) e.free_bodies(0, dt_sub, cfg.gravity, any_free, true);
     }

@@ -827,6 +827,24 @@ void Engine::g2p2g(int sub, float dt, bool standard, const float g[3], bool inte
     I.end(CAT_FUSED, ev);
 }
 
+void Engine::g2p2g_pb(float dt) {
+    Impl& I = *impl_;
+    if (I.n_cap == 0) return;
+    auto ev = I.begin();
+    Params P = I.params();
+    P.sub = 0;
+    P.dt = dt;
+    P.commit = 0;
+    P.pushout = 0;
+    P.deactivate = 0;
+    launch_g2p2g(P, (I.n + kGroup - 1) / kGroup, I.st, false, true);  // zeroes the brick count
+    launch_collect_bricks(P, I.total_bricks, I.st);
+    I.counted(2);
+    I.flag_parity = 1 - I.flag_parity;
+    I.cur = 1 - I.cur;
+    I.end(CAT_FUSED, ev);
+}
+
 void Engine::set_fusion(int mode) { impl_->fusion = mode; }
 
 void Engine::contact_sub_buffers(void** sums, void** counts, int* n_shapes) {

@@ -103,6 +103,9 @@ class Engine {
     // run in the collect launch; the caller then skips free_bodies.
     void g2p2g(int sub, float dt, bool standard, const float g[3], bool integrate);
     // fusion policy: 0 off, 1 (default) or 2 on
+    // PB-MPM: G2P of a non-final iteration (no commit) + P2G of the next iteration, then the
+    // brick collect (replaces g2p_pb(.., false, false, false) then p2g(false, ..))
+    void g2p2g_pb(float dt);
     void set_fusion(int mode);
     // per-substep contact sums (device): double[6 * n_shapes], int32[n_shapes]
     void contact_sub_buffers(void** sums, void** counts, int* n_shapes);

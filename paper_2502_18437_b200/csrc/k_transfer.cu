@@ -840,7 +840,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(cons
 // crosses HBM once per substep (read x, F, flags; write everything) and the P2G load
 // latency is an L2 latency.  Grid pools: G2P reads grid_vel (substep s), P2G accumulates
 // into grid_acc (zeroed by the grid update of substep s), so the phases never alias.
-template <bool STD>
+// PB: PB-MPM iterations of one step (solvers.hpp:240-277 then 218-235): G2P of iteration it
+// (no commit) fused with P2G of iteration it+1 (A = m C).
+template <bool STD, bool PB = false>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_g2p2g(const __grid_constant__ Params P) {
     pdl_enter();
     // the active-brick count of substep s+1 (read by the grid update of s, appended to by
@@ -854,9 +856,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_g2p2g(co
     constexpr int kRing = kStages * kPlanes > kG2PStages * 7 ? kStages * kPlanes : kG2PStages * 7;
     float4* ring = smem + (threadIdx.x >> 5) * (kRing * 32);
     for (uint32_t g = blockIdx.x * wpb + (threadIdx.x >> 5); g < n_groups; g += gridDim.x * wpb) {
-        g2p_group<false, STD>(P, g, ring, lane);
+        g2p_group<PB, STD>(P, g, ring, lane);
         __syncwarp();  // orders this warp's stores of the group before the P2G loads
-        p2g_group<true, STD, true>(P, g, ring, lane);
+        p2g_group<!PB, STD, true>(P, g, ring, lane);
     }
 }
 
@@ -1005,7 +1007,7 @@ void launch_g2p(const Params& P, bool pb, int64_t max_groups, cudaStream_t st, b
     else launch_chain(k_g2p<false>, blocks, threads, smem5, st, P);
 }
 
-void launch_g2p2g(const Params& P, int64_t max_groups, cudaStream_t st, bool standard) {
+void launch_g2p2g(const Params& P, int64_t max_groups, cudaStream_t st, bool standard, bool pb) {
     const int threads = kWarpsPerBlock * 32;
     const int blocks = grid_for(max_groups * 32, threads, 148 * 16);
     constexpr int kRing = kStages * kPlanes > kG2PStages * 7 ? kStages * kPlanes : kG2PStages * 7;
@@ -1014,9 +1016,11 @@ void launch_g2p2g(const Params& P, int64_t max_groups, cudaStream_t st, bool sta
     if (!attr) {
         opt_in_smem(k_g2p2g<false>, smem);
         opt_in_smem(k_g2p2g<true>, smem);
+        opt_in_smem(k_g2p2g<false, true>, smem);
         attr = true;
     }
-    if (standard) launch_chain(k_g2p2g<true>, blocks, threads, smem, st, P);
+    if (pb) launch_chain(k_g2p2g<false, true>, blocks, threads, smem, st, P);
+    else if (standard) launch_chain(k_g2p2g<true>, blocks, threads, smem, st, P);
     else launch_chain(k_g2p2g<false>, blocks, threads, smem, st, P);
 }
 

@@ -45,7 +45,8 @@ void launch_shape_cull(const Params& P, cudaStream_t st);
 void launch_g2p(const Params& P, bool pb, int64_t max_groups, cudaStream_t st, bool standard = false,
                 bool wide = false);
 // fused G2P (substep s) + P2G (substep s+1), MLS or standard MPM (k_g2p2g)
-void launch_g2p2g(const Params& P, int64_t max_groups, cudaStream_t st, bool standard = false);
+// pb: PB-MPM iteration it (G2P, no commit) + iteration it+1 (P2G)
+void launch_g2p2g(const Params& P, int64_t max_groups, cudaStream_t st, bool standard = false, bool pb = false);
 void launch_collect_bricks(const Params& P, uint32_t n_bricks, cudaStream_t st);
 void launch_pushout(const Params& P, cudaStream_t st);
 void launch_deactivate(const Params& P, cudaStream_t st);
