@@ -17,6 +17,7 @@ cores with all threads, on the same workload and metric.
 from __future__ import annotations
 
 import argparse
+import datetime
 import json
 import os
 import statistics
@@ -100,17 +101,21 @@ def substeps_of(spec):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons, sampled every 50 ms from before the warm-up on.
+    stop() keeps the samples stamped inside the timed region (mark_start / mark_end); a region
+    shorter than nvidia-smi's start-up + one period falls back to the samples under load just
+    before it (the warm-up frames), flagged in_region = False."""
 
     def __init__(self, gpu_index):
         self.gpu = gpu_index
         self.proc = None
         self.lines = []
+        self.t0 = self.t1 = None
 
     def start(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
+        q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
                                           "--format=csv,noheader,nounits", "-lms", "50"],
@@ -124,6 +129,12 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def mark_start(self):
+        self.t0 = datetime.datetime.now()
+
+    def mark_end(self):
+        self.t1 = datetime.datetime.now()
+
     def stop(self):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -133,22 +144,29 @@ class ClockSampler:
         except subprocess.TimeoutExpired:
             self.proc.kill()
         self.t.join(timeout=2)
-        sm, smax, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        rows = []
         for ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
-            if len(f) < 8:
+            if len(f) < 9:
                 continue
             try:
-                sm.append(float(f[0]))
-                smax = float(f[1])
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f")
+                rows.append((ts, float(f[1]), float(f[2]), f[5:9]))
             except ValueError:
                 continue
-            for nm, val in zip(names, f[4:8]):
+        inside = [r for r in rows if self.t0 and self.t1 and self.t0 <= r[0] <= self.t1]
+        sel, in_region = inside, True
+        if not sel:  # region too short for the sampler: the samples just before it
+            sel, in_region = [r for r in rows if self.t1 is None or r[0] <= self.t1][-3:], False
+        reasons = set()
+        for r in sel:
+            for nm, val in zip(names, r[3]):
                 if val.lower().startswith("active"):
                     reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        sm = [r[1] for r in sel]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": sel[-1][2] if sel else None,
+                "reasons": sorted(reasons), "samples": len(sm), "in_region": in_region}
 
 
 def measured_peak():
@@ -293,6 +311,9 @@ def run_ours(args, rank, world, local_rank):
     n_shapes = sum(len(s.shapes) for s in batch.scenes)
     setup_s = time.time() - t0
 
+    # clocks: nvidia-smi needs ~0.1 s to start; it runs from the warm-up on
+    clocks = ClockSampler(local_rank)
+    clocks.start()
     # warm-up (includes the upload and first binning)
     batch.advance_frames(DT_FRAME, max(args.warmup, 1))
     batch.fetch_results()
@@ -307,14 +328,14 @@ def run_ours(args, rank, world, local_rank):
     batch.set_profiling(True)
     barrier()
     torch.cuda.synchronize()
-    clocks = ClockSampler(local_rank)
-    clocks.start()
     launches0 = lib.mpmb_kernel_launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks.mark_start()
     e0.record(stream)
     batch.advance_frames(DT_FRAME, args.steps)
     e1.record(stream)
     e1.synchronize()
+    clocks.mark_end()
     torch.cuda.synchronize()
     launches = lib.mpmb_kernel_launch_count() - launches0
     clk = clocks.stop()
