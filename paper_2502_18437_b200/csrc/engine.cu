@@ -171,7 +171,7 @@ struct Engine::Impl {
     int cur = 0;
     bool binned = false;
     DevBuf b_count, b_off, b_key, b_rank, b_cell, b_orig, e_orig, e_cell, e_src, b_tmp, g_orig,
-        g_src, g_cell, s_src, s_orig, b_counts, scan_tmp, key_by_orig, order, group_nact;
+        g_src, g_cell, s_src, s_orig, b_counts, scan_tmp, key_by_orig, order, group_nact, group_box;
     BinBuffers bb{};
     DevBuf mats;
     DevBuf shapes, verts, ints, free_pose, pose_table, pose_override, cull;
@@ -274,6 +274,7 @@ struct Engine::Impl {
         P.brick_scene = brick_scene.as<uint32_t>();
         P.order = order.as<uint8_t>();  // per-substep group order (k_transfer.cu)
         P.group_nact = group_nact.as<uint32_t>();
+        P.group_box = group_box.as<int4>();
         P.n_groups = b_counts.as<uint32_t>() + 1;
         P.n_active = b_counts.as<uint32_t>() + 2;
         P.n_total = n_cap;
@@ -474,7 +475,7 @@ void Engine::upload_particles(int64_t n, const float* x, const float* v, const f
     I.g_orig.alloc(4 * N); I.g_src.alloc(4 * N); I.g_cell.alloc(N); I.s_src.alloc(4 * N);
     I.s_orig.alloc(4 * N);
     const size_t n_groups = (N + kGroup - 1) / kGroup;
-    I.order.alloc(kGroup * n_groups); I.group_nact.alloc(4 * n_groups);
+    I.order.alloc(kGroup * n_groups); I.group_nact.alloc(4 * n_groups); I.group_box.alloc(16 * n_groups);
     const size_t nbk = static_cast<size_t>(I.total_bricks) + 2;  // + inactive, holes
     I.b_count.alloc(4 * nbk);
     I.b_off.alloc(4 * (nbk + 1));

@@ -37,6 +37,19 @@ constexpr int kG2PStages = MPMB_G2P_STAGES;  // G2P: one more, so particle k+1 h
 #endif
 constexpr int kWarpsPerBlock = MPMB_WPB;
 constexpr int kPer = kGroup / 32;  // sorted positions per lane
+// G2P gathers from a per-warp shared-memory copy of the group's node box (the stencil-base
+// box the P2G sort recorded, + 2 nodes per axis) when it has at most kBoxCap nodes
+#ifndef MPMB_G2P_BOX
+#define MPMB_G2P_BOX 1
+#endif
+#ifndef MPMB_BOX_CAP
+#define MPMB_BOX_CAP 256
+#endif
+constexpr int kBoxCap = MPMB_G2P_BOX ? MPMB_BOX_CAP : 0;
+// The box pays off while a launch has few groups per warp slot (latency-bound tail: the
+// 874k-particle scene +4%); at C5 sizes its shared memory costs more than it saves (-1.3%,
+// DESIGN.md §7), so launches with more groups than this use the plain gather.
+constexpr int64_t kBoxMaxGroups = 4 * 148 * 3 * kWarpsPerBlock;
 constexpr int kBins = 512;         // sort bins: ((global brick & 7) << 6) | cell
 constexpr int kBinWords = kBins + kBins / 32;  // one pad word per 32 bins (conflict-free scan)
 static_assert(kPer == 8, "order bytes are read as one u64 per lane");
@@ -266,7 +279,7 @@ __device__ __forceinline__ uint32_t bin_word(uint32_t b) { return b + (b >> 5); 
 // smem atomics).  Active particles come first in bin order, then inactive ones and holes
 // in previous order.  Writes all kGroup order bytes (slot-in-group of each position) to
 // order_s and returns the lane's 8 P2G positions [8L, 8L+8); `bins` is kBinWords words.
-template <bool OUT>
+template <bool OUT, bool BOX>
 __device__ __forceinline__ uint64_t group_sort(const Params& P, uint32_t g, uint32_t* bins, uint8_t* order_s,
                                                uint32_t& n_act) {
     const unsigned full = 0xffffffffu;
@@ -274,6 +287,8 @@ __device__ __forceinline__ uint64_t group_sort(const Params& P, uint32_t g, uint
     const unsigned lt = lanemask_lt();
     const uint32_t slot0 = g * kGroup;
     uint32_t bin[kPer];
+    int lo[3] = {INT_MAX, INT_MAX, INT_MAX}, hi[3] = {INT_MIN, INT_MIN, INT_MIN};
+    int sc_lo = INT_MAX, sc_hi = INT_MIN;
     // all 16 loads first: one memory latency per group
     float4 xa4[kPer];
     uint32_t fl[kPer];
@@ -304,7 +319,27 @@ __device__ __forceinline__ uint64_t group_sort(const Params& P, uint32_t g, uint
                                     static_cast<uint32_t>(b[1] >> 2)) * P.geo.nb[0] +
                                    static_cast<uint32_t>(b[0] >> 2);
             bin[i] = ((brick & 7u) << 6) | static_cast<uint32_t>(((b[2] & 3) << 4) | ((b[1] & 3) << 2) | (b[0] & 3));
+            if (BOX) {
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    lo[a] = min(lo[a], b[a]);
+                    hi[a] = max(hi[a], b[a]);
+                }
+                sc_lo = min(sc_lo, scene);
+                sc_hi = max(sc_hi, scene);
+            }
         }
+    }
+    if (BOX) {  // the group's stencil-base box for the G2P of this substep (same x, same bases)
+        int4 bx;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const int l = __reduce_min_sync(full, lo[a]), h = __reduce_max_sync(full, hi[a]);
+            (a == 0 ? bx.x : a == 1 ? bx.y : bx.z) = l | (h << 16);
+        }
+        const int s0 = __reduce_min_sync(full, sc_lo), s1 = __reduce_max_sync(full, sc_hi);
+        bx.w = (s0 == s1) ? s0 : -1;  // empty or several scenes: no box
+        if (lane == 0) P.group_box[g] = bx;
     }
     for (int w = lane; w < kBinWords; w += 32) bins[w] = 0u;
     __syncwarp();
@@ -418,7 +453,7 @@ __device__ __forceinline__ void p2g_prepare(const Params& P, const float4 q0, co
 // this warp's staging ring (kStages x kPlanes x 32 float4), also the sort scratch.  OUT: the
 // group's particles are in the other buffer (pl_out), written by this warp's G2P of the
 // previous substep inside the fused kernel (k_g2p2g).
-template <bool MLS, bool STD, bool OUT>
+template <bool MLS, bool STD, bool OUT, bool BOX>
 __device__ __forceinline__ void p2g_group(const Params& P, uint32_t g, float4* ring, int lane) {
     constexpr int NP = kPlanes;
     Stager<NP, kStages, OUT || MPMB_P2G_CG != 0, OUT> st;
@@ -427,7 +462,7 @@ __device__ __forceinline__ void p2g_group(const Params& P, uint32_t g, float4* r
     uint32_t* bins = reinterpret_cast<uint32_t*>(ring);  // sort scratch aliases the ring
     uint8_t* order_s = reinterpret_cast<uint8_t*>(bins + kBinWords);
     uint32_t n_act;
-    st.order = group_sort<OUT>(P, g, bins, order_s, n_act);
+    st.order = group_sort<OUT, BOX>(P, g, bins, order_s, n_act);
     st.slot0 = g * kGroup;
     st.cnt = min(max(static_cast<int>(n_act) - kPer * lane, 0), kPer);
     reinterpret_cast<uint64_t*>(P.order)[static_cast<uint64_t>(g) * 32 + lane] = st.order;
@@ -465,7 +500,8 @@ __device__ __forceinline__ void p2g_group(const Params& P, uint32_t g, float4* r
     __syncwarp();  // the ring is the next group's sort scratch
 }
 
-template <bool MLS, bool STD = false>
+// BOX: record each group's stencil-base box for the (box-gathering) G2P that follows
+template <bool MLS, bool STD = false, bool BOX = false>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_p2g(const __grid_constant__ Params P) {
     pdl_enter();
     extern __shared__ float4 smem[];
@@ -474,7 +510,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_p2g(cons
     const uint32_t wpb = blockDim.x >> 5;
     float4* ring = smem + (threadIdx.x >> 5) * (kStages * kPlanes * 32);
     for (uint32_t g = blockIdx.x * wpb + (threadIdx.x >> 5); g < n_groups; g += gridDim.x * wpb)
-        p2g_group<MLS, STD, false>(P, g, ring, lane);
+        p2g_group<MLS, STD, false, BOX>(P, g, ring, lane);
 }
 
 // ================================================================  G2P
@@ -485,6 +521,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_p2g(cons
 // (dk, dj) over di with the x-weights, then scaled by w_y w_z.  The 27 nodes are read
 // straight from L1: the warp's 32 lanes hold 32 consecutive sorted particles (a few
 // stencil bases), so each load instruction touches only a handful of lines.
+// GENERIC: plain (generic-address) loads, the node box may be in shared memory; else
+// read-only global loads
+template <bool GENERIC>
 __device__ __forceinline__ void g2p_gather(const float4* g, uint32_t px, uint32_t pxy, const float w[3][3],
                                            const float rel[3][3], float vn[3], float B[9]) {
     float wr0[3];
@@ -498,9 +537,11 @@ __device__ __forceinline__ void g2p_gather(const float4* g, uint32_t px, uint32_
     for (int dk = 0; dk < 3; ++dk) {
         float4 q[9];
 #pragma unroll
-        for (int n = 0; n < 9; ++n)
-            q[n] = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const char*>(g) +
-                                                         (dk * pxy + (n / 3) * px) * 16u) + (n % 3));
+        for (int n = 0; n < 9; ++n) {
+            const float4* a = reinterpret_cast<const float4*>(reinterpret_cast<const char*>(g) +
+                                                              (dk * pxy + (n / 3) * px) * 16u) + (n % 3);
+            q[n] = GENERIC ? *a : __ldg(a);
+        }
 #pragma unroll
         for (int dj = 0; dj < 3; ++dj) {
             float2 a01 = f2(0.f, 0.f), b01 = f2(0.f, 0.f);
@@ -536,6 +577,7 @@ __device__ __forceinline__ void g2p_gather(const float4* g, uint32_t px, uint32_
 // Standard MPM gather (solvers.hpp:112-128): v = sum w v_I, L = sum v_I (x) grad w, the
 // same separable row sums as g2p_gather with dw_x in place of w_x r_x and the row factors
 // (w_y w_z, dw_y w_z, w_y dw_z) for the three gradient columns.
+template <bool GENERIC>
 __device__ __forceinline__ void g2p_gather_std(const float4* g, uint32_t px, uint32_t pxy, const float w[3][3],
                                                const float dw[3][3], float vn[3], float L[9]) {
     float2 v01 = f2(0.f, 0.f);
@@ -546,9 +588,11 @@ __device__ __forceinline__ void g2p_gather_std(const float4* g, uint32_t px, uin
     for (int dk = 0; dk < 3; ++dk) {
         float4 q[9];
 #pragma unroll
-        for (int n = 0; n < 9; ++n)
-            q[n] = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const char*>(g) +
-                                                         (dk * pxy + (n / 3) * px) * 16u) + (n % 3));
+        for (int n = 0; n < 9; ++n) {
+            const float4* a = reinterpret_cast<const float4*>(reinterpret_cast<const char*>(g) +
+                                                              (dk * pxy + (n / 3) * px) * 16u) + (n % 3);
+            q[n] = GENERIC ? *a : __ldg(a);
+        }
 #pragma unroll
         for (int dj = 0; dj < 3; ++dj) {
             float2 a01 = f2(0.f, 0.f), d01 = f2(0.f, 0.f);
@@ -662,8 +706,18 @@ struct G2PLane {
 
 // One particle's G2P (MLS solvers.hpp:173-196; PB :240-277; STD :107-135) with the F update,
 // push-out and deactivation; p holds x, F (PB/STD: C) on entry, the new state on exit.
-template <bool PB, bool STD>
-__device__ __forceinline__ void g2p_particle(const Params& P, Part& p, float4& r, G2PLane& L) {
+// The group's node box in shared memory (g2p_group): nodes [o, o + n) per axis, row-major x,
+// packed o | n << 16 per axis (few registers: they stay live across the particle loop).
+struct NodeBox {
+    const float4* s;  // nullptr: gather from global memory
+    int a[3];
+    __device__ __forceinline__ int o(int d) const { return a[d] & 0xFFFF; }
+    __device__ __forceinline__ int n(int d) const { return a[d] >> 16; }
+};
+
+template <bool PB, bool STD, bool BOX = false>
+__device__ __forceinline__ void g2p_particle(const Params& P, Part& p, float4& r, G2PLane& L,
+                                             const NodeBox& box = NodeBox{nullptr, {0, 0, 0}}) {
     uint32_t flags = __float_as_uint(r.z);
     const int scene = static_cast<int>((flags >> kSceneShift) & kSceneMask);
     L.my_scene = scene;
@@ -685,10 +739,20 @@ __device__ __forceinline__ void g2p_particle(const Params& P, Part& p, float4& r
     }
     float B[9];  // STD: the velocity gradient L
     {
+        // one gather: from the shared-memory node box when the stencil lies in it (generic
+        // loads), else from the global pool
         uint32_t base, px, pxy;
         stencil_rows(P.geo, b, base, px, pxy);
-        if (STD) g2p_gather_std(P.grid_vel + S.node_base + base, px, pxy, w, rel, p.v, B);
-        else g2p_gather(P.grid_vel + S.node_base + base, px, pxy, w, rel, p.v, B);
+        const float4* gp = P.grid_vel + S.node_base + base;
+        const int r0 = b[0] - box.o(0), r1 = b[1] - box.o(1), r2 = b[2] - box.o(2);
+        if (BOX && box.s && r0 >= 0 && r0 + 3 <= box.n(0) && r1 >= 0 && r1 + 3 <= box.n(1) && r2 >= 0 &&
+            r2 + 3 <= box.n(2)) {
+            px = static_cast<uint32_t>(box.n(0));
+            pxy = px * static_cast<uint32_t>(box.n(1));
+            gp = box.s + (r2 * box.n(1) + r1) * box.n(0) + r0;
+        }
+        if (STD) g2p_gather_std<BOX>(gp, px, pxy, w, rel, p.v, B);
+        else g2p_gather<BOX>(gp, px, pxy, w, rel, p.v, B);
     }
     bool do_commit;
     if (STD) {  // solvers.hpp:130-134: x += v dt, F = (I + L dt) F; C unchanged
@@ -743,8 +807,9 @@ __device__ __forceinline__ void g2p_particle(const Params& P, Part& p, float4& r
 // positions g2p_pos(L, k): the warp's 32 lanes gather around a few neighbouring stencils at
 // every iteration.  Every position is written to the other buffer at slot
 // group_phys(pos): the state leaves G2P in the new order.  `ring`: this warp's staging ring.
-template <bool PB, bool STD>
-__device__ __forceinline__ void g2p_group(const Params& P, uint32_t g, float4* ring, int lane) {
+template <bool PB, bool STD, bool BOX>
+__device__ __forceinline__ void g2p_group(const Params& P, uint32_t g, float4* ring, int lane,
+                                          float4* box_s = nullptr) {
     constexpr int NP = (PB || STD) ? 7 : 5;
     constexpr int NS = kG2PStages;
     Stager<NP, NS, MPMB_G2P_CG != 0> st;
@@ -765,6 +830,41 @@ __device__ __forceinline__ void g2p_group(const Params& P, uint32_t g, float4* r
     st.slot0 = g * kGroup;
     const int kmax = __reduce_max_sync(0xffffffffu, st.cnt);
     for (int k = 0; k < NS - 1; ++k) st.issue(P, k);
+    NodeBox box{nullptr, {0, 0, 0}};
+#ifdef MPMB_BOX_UNUSED  // A/B: the shared memory is reserved but never used
+    if (false) {
+#else
+    if (BOX && box_s) {
+#endif
+        const int4 gb = P.group_box[g];
+        if (gb.w >= 0) {
+            const int ox = gb.x & 0xFFFF, oy = gb.y & 0xFFFF, oz = gb.z & 0xFFFF;
+            const int nx = (gb.x >> 16) - ox + 3, ny = (gb.y >> 16) - oy + 3, nz = (gb.z >> 16) - oz + 3;
+            const int rows = ny * nz;
+            if (nx <= 32 && rows * nx <= kBoxCap) {
+                // lanes cover rpi rows of nx nodes per step: coalesced row segments
+                const int rpi = 32 / nx;
+                const int lx = lane % nx, lr = lane / nx;
+                if (lr < rpi) {
+                    const float4* gv = P.grid_vel + static_cast<uint64_t>(gb.w) * P.geo.nodes_per_scene;
+                    int j = lr % ny, k = lr / ny;
+                    for (int r = lr; r < rows; r += rpi) {
+                        box_s[r * nx + lx] = __ldg(gv + node_linear(P.geo, ox + lx, oy + j, oz + k));
+                        j += rpi;
+                        while (j >= ny) {
+                            j -= ny;
+                            ++k;
+                        }
+                    }
+                }
+                box.s = box_s;
+                box.a[0] = ox | (nx << 16);
+                box.a[1] = oy | (ny << 16);
+                box.a[2] = oz | (nz << 16);
+            }
+        }
+        __syncwarp();
+    }
     G2PLane L;
     for (int k = 0; k < kmax; ++k) {
         st.issue(P, k + NS - 1);
@@ -801,7 +901,7 @@ __device__ __forceinline__ void g2p_group(const Params& P, uint32_t g, float4* r
                 p.F[5] = q5.x; p.F[6] = q5.y; p.F[7] = q5.z; p.F[8] = q5.w;
             }
         }
-        g2p_particle<PB, STD>(P, p, r, L);
+        g2p_particle<PB, STD, BOX>(P, p, r, L, box);
         store_part_out(P, so, p, r);
     }
     // inactive particles and holes of the group move to their new slots unchanged
@@ -818,7 +918,7 @@ __device__ __forceinline__ void g2p_group(const Params& P, uint32_t g, float4* r
     __syncwarp();  // the ring is reused by the next group (or the fused P2G)
 }
 
-template <bool PB, bool STD = false>
+template <bool PB, bool STD = false, bool BOX = false>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(const __grid_constant__ Params P) {
     pdl_enter();
     extern __shared__ float4 smem[];
@@ -827,8 +927,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(cons
     const uint32_t n_groups = *P.n_groups;
     const uint32_t wpb = blockDim.x >> 5;
     float4* ring = smem + (threadIdx.x >> 5) * (kG2PStages * NP * 32);
+    float4* box = BOX ? smem + wpb * (kG2PStages * NP * 32) + (threadIdx.x >> 5) * kBoxCap : nullptr;
     for (uint32_t g = blockIdx.x * wpb + (threadIdx.x >> 5); g < n_groups; g += gridDim.x * wpb)
-        g2p_group<PB, STD>(P, g, ring, lane);
+        g2p_group<PB, STD, BOX>(P, g, ring, lane, box);
 }
 
 // Fused G2P of substep s + P2G of substep s+1 (MLS / standard MPM inside a frame), one warp
@@ -842,7 +943,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(cons
 // into grid_acc (zeroed by the grid update of substep s), so the phases never alias.
 // PB: PB-MPM iterations of one step (solvers.hpp:240-277 then 218-235): G2P of iteration it
 // (no commit) fused with P2G of iteration it+1 (A = m C).
-template <bool STD, bool PB = false>
+template <bool STD, bool PB = false, bool BOX = false>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_g2p2g(const __grid_constant__ Params P) {
     pdl_enter();
     // the active-brick count of substep s+1 (read by the grid update of s, appended to by
@@ -855,10 +956,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_g2p2g(co
     const uint32_t wpb = blockDim.x >> 5;
     constexpr int kRing = kStages * kPlanes > kG2PStages * 7 ? kStages * kPlanes : kG2PStages * 7;
     float4* ring = smem + (threadIdx.x >> 5) * (kRing * 32);
+    float4* box = BOX ? smem + wpb * (kRing * 32) + (threadIdx.x >> 5) * kBoxCap : nullptr;
     for (uint32_t g = blockIdx.x * wpb + (threadIdx.x >> 5); g < n_groups; g += gridDim.x * wpb) {
-        g2p_group<PB, STD>(P, g, ring, lane);
+        g2p_group<PB, STD, BOX>(P, g, ring, lane, box);
         __syncwarp();  // orders this warp's stores of the group before the P2G loads
-        p2g_group<!PB, STD, true>(P, g, ring, lane);
+        p2g_group<!PB, STD, true, BOX>(P, g, ring, lane);
     }
 }
 
@@ -976,7 +1078,16 @@ void launch_p2g(const Params& P, bool mls, int64_t max_groups, cudaStream_t st, 
         opt_in_smem(k_p2g<true>, smem);
         opt_in_smem(k_p2g<false>, smem);
         opt_in_smem(k_p2g<true, true>, smem);
+        opt_in_smem(k_p2g<true, false, true>, smem);
+        opt_in_smem(k_p2g<false, false, true>, smem);
+        opt_in_smem(k_p2g<true, true, true>, smem);
         attr = true;
+    }
+    if (kBoxCap > 0 && max_groups <= kBoxMaxGroups) {  // the G2P after it gathers from boxes
+        if (standard) launch_chain(k_p2g<true, true, true>, blocks, threads, smem, st, P);
+        else if (mls) launch_chain(k_p2g<true, false, true>, blocks, threads, smem, st, P);
+        else launch_chain(k_p2g<false, false, true>, blocks, threads, smem, st, P);
+        return;
     }
     if (standard) launch_chain(k_p2g<true, true>, blocks, threads, smem, st, P);
     else if (mls) launch_chain(k_p2g<true>, blocks, threads, smem, st, P);
@@ -993,6 +1104,8 @@ void launch_g2p(const Params& P, bool pb, int64_t max_groups, cudaStream_t st, b
     }
     const int threads = kWarpsPerBlock * 32;
     const int blocks = grid_for(max_groups * 32, threads, 148 * 16);
+    const bool box = kBoxCap > 0 && max_groups <= kBoxMaxGroups;
+    const int boxb = kWarpsPerBlock * kBoxCap * static_cast<int>(sizeof(float4));
     const int smem7 = kWarpsPerBlock * kG2PStages * 7 * 32 * static_cast<int>(sizeof(float4));
     const int smem5 = kWarpsPerBlock * kG2PStages * 5 * 32 * static_cast<int>(sizeof(float4));
     static bool attr = false;
@@ -1000,7 +1113,16 @@ void launch_g2p(const Params& P, bool pb, int64_t max_groups, cudaStream_t st, b
         opt_in_smem(k_g2p<true>, smem7);
         opt_in_smem(k_g2p<false, true>, smem7);
         opt_in_smem(k_g2p<false>, smem5);
+        opt_in_smem(k_g2p<true, false, true>, smem7 + boxb);
+        opt_in_smem(k_g2p<false, true, true>, smem7 + boxb);
+        opt_in_smem(k_g2p<false, false, true>, smem5 + boxb);
         attr = true;
+    }
+    if (box) {
+        if (standard) launch_chain(k_g2p<false, true, true>, blocks, threads, smem7 + boxb, st, P);
+        else if (pb) launch_chain(k_g2p<true, false, true>, blocks, threads, smem7 + boxb, st, P);
+        else launch_chain(k_g2p<false, false, true>, blocks, threads, smem5 + boxb, st, P);
+        return;
     }
     if (standard) launch_chain(k_g2p<false, true>, blocks, threads, smem7, st, P);
     else if (pb) launch_chain(k_g2p<true>, blocks, threads, smem7, st, P);
@@ -1011,13 +1133,24 @@ void launch_g2p2g(const Params& P, int64_t max_groups, cudaStream_t st, bool sta
     const int threads = kWarpsPerBlock * 32;
     const int blocks = grid_for(max_groups * 32, threads, 148 * 16);
     constexpr int kRing = kStages * kPlanes > kG2PStages * 7 ? kStages * kPlanes : kG2PStages * 7;
+    const bool box = kBoxCap > 0 && max_groups <= kBoxMaxGroups;
     const int smem = kWarpsPerBlock * kRing * 32 * static_cast<int>(sizeof(float4));
+    const int smem_box = smem + kWarpsPerBlock * kBoxCap * static_cast<int>(sizeof(float4));
     static bool attr = false;
     if (!attr) {
         opt_in_smem(k_g2p2g<false>, smem);
         opt_in_smem(k_g2p2g<true>, smem);
         opt_in_smem(k_g2p2g<false, true>, smem);
+        opt_in_smem(k_g2p2g<false, false, true>, smem_box);
+        opt_in_smem(k_g2p2g<true, false, true>, smem_box);
+        opt_in_smem(k_g2p2g<false, true, true>, smem_box);
         attr = true;
+    }
+    if (box) {
+        if (pb) launch_chain(k_g2p2g<false, true, true>, blocks, threads, smem_box, st, P);
+        else if (standard) launch_chain(k_g2p2g<true, false, true>, blocks, threads, smem_box, st, P);
+        else launch_chain(k_g2p2g<false, false, true>, blocks, threads, smem_box, st, P);
+        return;
     }
     if (pb) launch_chain(k_g2p2g<false, true>, blocks, threads, smem, st, P);
     else if (standard) launch_chain(k_g2p2g<true>, blocks, threads, smem, st, P);

@@ -70,6 +70,7 @@ struct Params {
     const uint32_t* brick_scene;
     uint8_t* order;        // per group: kGroup bytes, slot-in-group by current stencil base
     uint32_t* group_nact;  // per group: active particles (written by P2G, replayed by G2P)
+    int4* group_box;       // per group: stencil-base box {x0 | x1 << 16, y.., z.., scene or -1} (P2G sort)
     const uint32_t* n_groups;
     const uint32_t* n_active;
     int64_t n_total;          // slots (particles + holes), a fixed bound
