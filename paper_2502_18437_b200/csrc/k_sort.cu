@@ -179,49 +179,114 @@ __global__ void __launch_bounds__(256) k_bin_rest(BinBuffers B) {
     }
 }
 
+// Buckets of at most kLocalCap entries sort in shared memory: counting sort by cell (atomic
+// ranks), then each entry's rank inside its cell by original index (cells hold ~8 entries).
+// Larger buckets take the same steps through global scratch.
+constexpr int kLocalCap = 2048;
+constexpr int kLocalPer = kLocalCap / 256;
 __global__ void __launch_bounds__(256) k_bin_local(BinBuffers B) {
     __shared__ uint32_t hist[64];
     __shared__ uint32_t cstart[64];
+    __shared__ uint32_t s_orig[kLocalCap];
+    __shared__ uint32_t s_src[kLocalCap];
+    __shared__ uint8_t s_cell[kLocalCap];
+    __shared__ uint32_t s_list[256];
+    __shared__ uint32_t s_n;
     const uint32_t inactive = B.n_buckets - 2;  // the inactive and hole buckets: k_bin_rest
-    for (uint32_t b = blockIdx.x; b < inactive; b += gridDim.x) {
-        const uint32_t beg = B.bucket_off[b], end = B.bucket_off[b + 1];
-        if (beg == end) continue;
-        if (threadIdx.x < 64) hist[threadIdx.x] = 0u;
+    // most bricks are empty: each block scans 256 buckets at a time (coalesced offsets), lists
+    // the non-empty ones, then sorts them one by one
+    for (uint32_t base = blockIdx.x * 256u; base < inactive; base += gridDim.x * 256u) {
+        if (threadIdx.x == 0) s_n = 0u;
         __syncthreads();
-        for (uint32_t q = beg + threadIdx.x; q < end; q += blockDim.x)
-            B.tmp[q] = atomicAdd(&hist[B.e_cell[q]], 1u);
+        {
+            const uint32_t b = base + threadIdx.x;
+            const bool ne = b < inactive && B.bucket_off[b + 1] > B.bucket_off[b];
+            const unsigned m = __ballot_sync(0xffffffffu, ne);
+            uint32_t w0 = 0;
+            if ((threadIdx.x & 31) == 0 && m) w0 = atomicAdd(&s_n, static_cast<uint32_t>(__popc(m)));
+            w0 = __shfl_sync(0xffffffffu, w0, 0);
+            if (ne) s_list[w0 + __popc(m & ((1u << (threadIdx.x & 31)) - 1u))] = b;
+        }
         __syncthreads();
-        if (threadIdx.x < 32) {  // exclusive scan of 64 bins by one warp
-            const uint32_t a = hist[2 * threadIdx.x], c = hist[2 * threadIdx.x + 1];
-            uint32_t inc = a + c;
+        const uint32_t n_list = s_n;
+        for (uint32_t li = 0; li < n_list; ++li) {
+            const uint32_t b = s_list[li];
+            const uint32_t beg = B.bucket_off[b], end = B.bucket_off[b + 1];
+            const bool local = end - beg <= static_cast<uint32_t>(kLocalCap);
+            if (threadIdx.x < 64) hist[threadIdx.x] = 0u;
+            __syncthreads();
+            uint32_t cr[kLocalPer];  // shared-memory path: cell << 16 | rank of this thread's entries
+            if (local) {
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
-                if (threadIdx.x >= o) inc += t;
+                for (int i = 0; i < kLocalPer; ++i) {
+                    const uint32_t q = beg + threadIdx.x + 256u * i;
+                    cr[i] = 0xFFFFFFFFu;
+                    if (q < end) {
+                        const uint32_t cl = B.e_cell[q];
+                        cr[i] = (cl << 16) | atomicAdd(&hist[cl], 1u);
+                    }
+                }
+            } else {
+                for (uint32_t q = beg + threadIdx.x; q < end; q += blockDim.x)
+                    B.tmp[q] = atomicAdd(&hist[B.e_cell[q]], 1u);
             }
-            const uint32_t ex = inc - a - c;
-            cstart[2 * threadIdx.x] = ex;
-            cstart[2 * threadIdx.x + 1] = ex + a;
+            __syncthreads();
+            if (threadIdx.x < 32) {  // exclusive scan of 64 bins by one warp
+                const uint32_t a = hist[2 * threadIdx.x], cc = hist[2 * threadIdx.x + 1];
+                uint32_t inc = a + cc;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (threadIdx.x >= o) inc += t;
+                }
+                const uint32_t ex = inc - a - cc;
+                cstart[2 * threadIdx.x] = ex;
+                cstart[2 * threadIdx.x + 1] = ex + a;
+            }
+            __syncthreads();
+            if (local) {
+#pragma unroll
+                for (int i = 0; i < kLocalPer; ++i) {
+                    if (cr[i] == 0xFFFFFFFFu) continue;
+                    const uint32_t q = beg + threadIdx.x + 256u * i;
+                    const uint32_t cl = cr[i] >> 16;
+                    const uint32_t d = cstart[cl] + (cr[i] & 0xFFFFu);
+                    s_orig[d] = B.e_orig[q];
+                    s_src[d] = B.e_src[q];
+                    s_cell[d] = static_cast<uint8_t>(cl);
+                }
+                __syncthreads();
+                for (uint32_t d = threadIdx.x; d < end - beg; d += blockDim.x) {
+                    const uint32_t cl = s_cell[d];
+                    const uint32_t o = s_orig[d];
+                    const uint32_t lo = cstart[cl], hi = lo + hist[cl];
+                    uint32_t rk = 0;
+                    for (uint32_t f = lo; f < hi; ++f) rk += s_orig[f] < o ? 1u : 0u;
+                    B.sorted_src[beg + lo + rk] = s_src[d];
+                    B.sorted_orig[beg + lo + rk] = o;
+                }
+            } else {
+                for (uint32_t q = beg + threadIdx.x; q < end; q += blockDim.x) {
+                    const uint32_t cl = B.e_cell[q];
+                    const uint32_t d = beg + cstart[cl] + B.tmp[q];
+                    B.g_orig[d] = B.e_orig[q];
+                    B.g_src[d] = B.e_src[q];
+                    B.g_cell[d] = static_cast<uint8_t>(cl);
+                }
+                __syncthreads();
+                for (uint32_t q = beg + threadIdx.x; q < end; q += blockDim.x) {
+                    const uint32_t cl = B.g_cell[q];
+                    const uint32_t o = B.g_orig[q];
+                    const uint32_t lo = beg + cstart[cl], hi = lo + hist[cl];
+                    uint32_t rk = 0;
+                    for (uint32_t f = lo; f < hi; ++f) rk += B.g_orig[f] < o ? 1u : 0u;
+                    B.sorted_src[lo + rk] = B.g_src[q];
+                    B.sorted_orig[lo + rk] = o;
+                }
+            }
+            __syncthreads();
         }
-        __syncthreads();
-        for (uint32_t q = beg + threadIdx.x; q < end; q += blockDim.x) {
-            const uint32_t c = B.e_cell[q];
-            const uint32_t d = beg + cstart[c] + B.tmp[q];
-            B.g_orig[d] = B.e_orig[q];
-            B.g_src[d] = B.e_src[q];
-            B.g_cell[d] = static_cast<uint8_t>(c);
-        }
-        __syncthreads();
-        for (uint32_t q = beg + threadIdx.x; q < end; q += blockDim.x) {
-            const uint32_t c = B.g_cell[q];
-            const uint32_t o = B.g_orig[q];
-            const uint32_t lo = beg + cstart[c], hi = lo + hist[c];
-            uint32_t rk = 0;
-            for (uint32_t f = lo; f < hi; ++f) rk += B.g_orig[f] < o ? 1u : 0u;
-            B.sorted_src[lo + rk] = B.g_src[q];
-            B.sorted_orig[lo + rk] = o;
-        }
-        __syncthreads();
+        __syncthreads();  // s_list / s_n are rewritten for the next range
     }
 }
 
@@ -291,7 +356,7 @@ void launch_bin(const Params& P, const BinBuffers& B, float4* const new_planes[k
     k_bin_keys<<<blocks_for(n_total, 256, cap), 256, 0, st>>>(P, B);
     launch_exclusive_scan(B.bucket_count, B.bucket_off, B.n_buckets, B.scan_tmp, st, launches);
     k_bin_scatter<<<blocks_for(n_total, 256, cap), 256, 0, st>>>(B, n_total);
-    k_bin_local<<<blocks_for(static_cast<int64_t>(B.n_buckets) * 256, 256, 148 * 8), 256, 0, st>>>(B);
+    k_bin_local<<<blocks_for(static_cast<int64_t>(B.n_buckets), 256, 148 * 8), 256, 0, st>>>(B);
     k_bin_rest<<<blocks_for(n_total, 256, cap), 256, 0, st>>>(B);
     k_bin_gather<<<blocks_for(n_total, 256, cap), 256, 0, st>>>(
         P, B, n_total, new_planes[0], new_planes[1], new_planes[2], new_planes[3],
