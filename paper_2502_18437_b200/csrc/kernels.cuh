@@ -170,14 +170,27 @@ __device__ __forceinline__ void collect_bricks_body(const Params& P, uint32_t n_
         bool on = false;
         if (b < n_bricks) {
             P.brick_flag_next[b] = 0u;
-            const uint32_t local = b % bps;
-            const uint32_t bx = local % nb0, by = (local / nb0) % nb1, bz = local / (nb0 * nb1);
+            // fast path: most bricks have no mark around them (raw neighbour loads, indices
+            // clamped; a nonzero word only means "decode exactly")
+            uint32_t fr[8];
 #pragma unroll
             for (int d = 0; d < 8; ++d) {
-                const uint32_t dx = d & 1, dy = (d >> 1) & 1, dz = d >> 2;
-                if (bx < dx || by < dy || bz < dz) continue;
-                const uint32_t f = P.brick_flag[b - dx - dy * nb0 - dz * nb0 * nb1];
-                on = on || ((f & 8u) && (f & static_cast<uint32_t>(d)) == static_cast<uint32_t>(d));
+                const uint32_t off = (d & 1) + ((d >> 1) & 1) * nb0 + (d >> 2) * nb0 * nb1;
+                fr[d] = P.brick_flag[b >= off ? b - off : 0u];
+            }
+            uint32_t any = 0;
+#pragma unroll
+            for (int d = 0; d < 8; ++d) any |= fr[d];
+            if (any) {
+                const uint32_t local = b % bps;
+                const uint32_t bx = local % nb0, by = (local / nb0) % nb1, bz = local / (nb0 * nb1);
+#pragma unroll
+                for (int d = 0; d < 8; ++d) {
+                    const uint32_t dx = d & 1, dy = (d >> 1) & 1, dz = d >> 2;
+                    if (bx < dx || by < dy || bz < dz) continue;
+                    const uint32_t f = fr[d];
+                    on = on || ((f & 8u) && (f & static_cast<uint32_t>(d)) == static_cast<uint32_t>(d));
+                }
             }
         }
         const unsigned m = __ballot_sync(full, on);
@@ -188,7 +201,7 @@ __device__ __forceinline__ void collect_bricks_body(const Params& P, uint32_t n_
         if (on) {
             const uint32_t w = start + __popc(m & lanemask_lt());
             P.active_bricks[w] = b;
-            const uint32_t local = b % bps;
+            const uint32_t local = b % bps;  // (only for the ~3% active bricks)
             P.active_info[w] = make_uint2((local % nb0) | (((local / nb0) % nb1) << 10) | ((local / (nb0 * nb1)) << 20),
                                           b / bps);
         }
