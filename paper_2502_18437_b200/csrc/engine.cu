@@ -187,7 +187,7 @@ struct Engine::Impl {
     DevBuf stress_in;
     bool use_stress_in = false;
     uint32_t epoch = 0;
-    DevBuf io_x, io_v, io_a, io_tot;
+    DevBuf io_x, io_v, io_a, io_tot, io_inv;
     PinnedBuf io_tot_h;
     PinnedBuf pin_io;
     // profiling
@@ -1019,8 +1019,9 @@ void Engine::snapshot(float* x, float* v, uint8_t* active, std::vector<double>& 
         if (x) { I.io_x.alloc(12 * N); io.x = I.io_x.as<float>(); }
         if (v) { I.io_v.alloc(12 * N); io.v = I.io_v.as<float>(); }
         if (active) { I.io_a.alloc(N); io.active = I.io_a.as<uint8_t>(); }
-        launch_frame_result(P, io, I.io_tot.as<double>(), I.st);
-        I.counted(1);
+        I.io_inv.alloc(4 * N);
+        launch_frame_result_orig(P, I.io_inv.as<uint32_t>(), I.n, io, I.io_tot.as<double>(), I.st);
+        I.counted(2);
     }
     // the small totals copy goes first: queued behind the arrays on the same copy engine it
     // would hold the host for the whole transfer

@@ -90,8 +90,9 @@ struct IoArrays {  // original-order device staging arrays (any may be null)
 void launch_upload(const Params& P, const IoArrays& in, int64_t n, cudaStream_t st);
 void launch_download(const Params& P, const IoArrays& out, cudaStream_t st);
 void launch_totals(const Params& P, double* totals /*5 per scene*/, cudaStream_t st);
-// x / v / active (original order) + the totals in one pass over the slots
-void launch_frame_result(const Params& P, const IoArrays& out, double* totals, cudaStream_t st);
+// x / v / active (original order) + the totals through the inverse permutation (inv: n words)
+void launch_frame_result_orig(const Params& P, uint32_t* inv, int64_t n, const IoArrays& out, double* totals,
+                              cudaStream_t st);
 void launch_stress(const Params& P, float* stress_orig, cudaStream_t st);
 void launch_grid_download(const Params& P, int scene, const DevScene& S, float* mass, float* mom,
                           float* vel, cudaStream_t st);
