@@ -296,3 +296,39 @@ def test_c3_full_size_within_reference_envelope():
     imp_err = np.abs(rg["shape_impulses"] - ro["shape_impulses"]).max()
     p_scale = ro["total_mass"] * max(np.abs(ro["velocities"]).max(), 1e-3)
     assert imp_err <= 10 * imp_env + 1e-6 * p_scale
+
+
+def _cutting_engaged():
+    """cutting.json with the blade starting INSIDE the tissue (the bundled keyframes keep it
+    above the block until ~0.7 s), so the two-sided slicer band, push-out and the blade's
+    impulse sums act from the first substep."""
+    spec = scenes.cutting()
+    spec["shapes"][0]["motion"]["keyframes"] = [
+        {"time": 0.0, "position": [0.6875, 0.50, 0.6875], "orientation": [0, 0, 0, 1]},
+        {"time": 1.0, "position": [0.6875, 0.35, 0.6875], "orientation": [0, 0, 0, 1]}]
+    return spec
+
+
+def test_blade_in_tissue_within_reference_envelope():
+    spec = _cutting_engaged()
+    o = backends.make_scene("oracle", spec)
+    f = backends.make_scene("oracle_fma", spec)
+    g = backends.make_scene("gpu", spec)
+    dx = spec["grid"]["dx"]
+    env = err = imp_env = imp_err = 0.0
+    pushed = 0
+    for _ in range(8):
+        for s in (o, f, g):
+            s.advance(spec["dt_frame"])
+        ro, rf, rg = o.fetch_results(), f.fetch_results(), g.fetch_results()
+        env = max(env, np.abs(rf["positions"] - ro["positions"]).max())
+        err = max(err, np.abs(rg["positions"] - ro["positions"]).max())
+        imp_env = max(imp_env, np.abs(rf["shape_impulses"] - ro["shape_impulses"]).max())
+        imp_err = max(imp_err, np.abs(rg["shape_impulses"] - ro["shape_impulses"]).max())
+        pushed += ro["pushed_out"]
+        assert abs(ro["total_mass"] - rg["total_mass"]) <= 1e-9 * ro["total_mass"]
+        assert np.array_equal(ro["active"], rg["active"])
+    assert pushed > 0 and np.abs(ro["shape_impulses"]).max() > 0.0  # the blade engaged the tissue
+    assert err <= max(1e-3 * dx, 10 * env), f"{err / dx:.2e} dx vs envelope {env / dx:.2e} dx"
+    p_scale = ro["total_mass"] * max(np.abs(ro["velocities"]).max(), 1e-3)
+    assert imp_err <= max(10 * imp_env, 2e-3 * np.abs(ro["shape_impulses"]).max()) + 1e-6 * p_scale
