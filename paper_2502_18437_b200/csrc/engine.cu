@@ -180,8 +180,16 @@ struct Engine::Impl {
     PinnedBuf pin_table[2];
     cudaEvent_t pin_done[2] = {nullptr, nullptr};
     cudaStream_t copy_st = nullptr;  // snapshot D2H (Engine::snapshot async)
-    cudaEvent_t ev_dl = nullptr, ev_copy = nullptr;
+    cudaEvent_t ev_dl = nullptr, ev_copy = nullptr, ev_gather = nullptr;
     bool copy_pending = false;
+    // the FrameResult gather (K9) runs on copy_st while the next frame's first P2G and grid
+    // update read the same particle planes; anything that WRITES planes waits for it first
+    bool gather_pending = false;
+    void planes_barrier() {
+        if (!gather_pending) return;
+        check(cudaStreamWaitEvent(st, ev_gather, 0), "wait gather");
+        gather_pending = false;
+    }
     int pin_slot = 0;
     DevBuf acc_sub, cnt_sub, acc_frame, cnt_frame, counters;
     DevBuf stress_in;
@@ -241,7 +249,10 @@ struct Engine::Impl {
         if (profiling) times.launches += k;
     }
 
-    Params params() {
+    // planes_read_only: the launch only reads the particle planes (P2G, grid update), so it
+    // may overlap a pending FrameResult gather; every other launch waits for it
+    Params params(bool planes_read_only = false) {
+        if (!planes_read_only) planes_barrier();
         Params P{};
         for (int q = 0; q < kPlanes; ++q) {
             P.pl[q] = planes[cur][q].as<float4>();
@@ -414,6 +425,7 @@ Engine::~Engine() {
         cudaStreamDestroy(I.copy_st);
         cudaEventDestroy(I.ev_dl);
         cudaEventDestroy(I.ev_copy);
+        cudaEventDestroy(I.ev_gather);
     }
     for (auto& e : I.events) {
         cudaEventDestroy(e.second.first);
@@ -696,7 +708,7 @@ void Engine::p2g(bool mls, float dt, bool collect, bool standard) {
     if (!I.binned) bin();
     auto ev = I.begin();
     cudaMemsetAsync(I.misc.p, 0, sizeof(uint32_t), I.st);  // active brick count
-    Params P = I.params();
+    Params P = I.params(!I.exact);
     P.dt = dt;
     if (I.exact) {
         if (standard || !mls) throw std::invalid_argument("engine: exact mode covers the MLS solver");
@@ -730,7 +742,7 @@ void Engine::grid_update(int sub, float dt, const float g[3], bool gravity, bool
     auto ev = I.begin();
     ++I.epoch;
     if (I.epoch == 0xFFFFFFFFu) I.epoch = 1;
-    Params P = I.params();
+    Params P = I.params(true);
     P.sub = std::min(sub, I.table_subs - 1);
     P.dt = dt;
     P.g[0] = g[0]; P.g[1] = g[1]; P.g[2] = g[2];
@@ -1009,19 +1021,25 @@ void Engine::snapshot(float* x, float* v, uint8_t* active, std::vector<double>& 
         check(cudaStreamCreateWithFlags(&I.copy_st, cudaStreamNonBlocking), "cudaStreamCreate");
         check(cudaEventCreateWithFlags(&I.ev_dl, cudaEventDisableTiming), "event");
         check(cudaEventCreateWithFlags(&I.ev_copy, cudaEventDisableTiming), "event");
+        check(cudaEventCreateWithFlags(&I.ev_gather, cudaEventDisableTiming), "event");
     }
     cudaStream_t cs = async ? I.copy_st : I.st;
     I.io_tot.alloc(sizeof(double) * 5 * std::max<size_t>(S, 1));
     check(cudaMemsetAsync(I.io_tot.p, 0, I.io_tot.bytes, I.st), "memset");
     Params P = I.params();
+    IoArrays io{};
     if (I.n > 0) {
-        IoArrays io{};
         if (x) { I.io_x.alloc(12 * N); io.x = I.io_x.as<float>(); }
         if (v) { I.io_v.alloc(12 * N); io.v = I.io_v.as<float>(); }
         if (active) { I.io_a.alloc(N); io.active = I.io_a.as<uint8_t>(); }
         I.io_inv.alloc(4 * N);
-        launch_frame_result_orig(P, I.io_inv.as<uint32_t>(), I.n, io, I.io_tot.as<double>(), I.st);
-        I.counted(2);
+        if (async) {  // totals now (the caller waits for them), the arrays on the copy stream
+            launch_totals(P, I.io_tot.as<double>(), I.st);
+            I.counted(1);
+        } else {
+            launch_frame_result_orig(P, I.io_inv.as<uint32_t>(), I.n, io, I.io_tot.as<double>(), I.st);
+            I.counted(2);
+        }
     }
     // the small totals copy goes first: queued behind the arrays on the same copy engine it
     // would hold the host for the whole transfer
@@ -1029,8 +1047,14 @@ void Engine::snapshot(float* x, float* v, uint8_t* active, std::vector<double>& 
     check(cudaMemcpyAsync(I.io_tot_h.p, I.io_tot.p, sizeof(double) * 5 * S, cudaMemcpyDeviceToHost, I.st), "d2h");
     if (I.n > 0) {
         if (async) {
+            // K9 on the copy stream: it reads the planes of this frame while the next frame's
+            // P2G and grid update (read-only) run; plane writers wait for ev_gather
             check(cudaEventRecord(I.ev_dl, I.st), "event");
             check(cudaStreamWaitEvent(cs, I.ev_dl, 0), "wait download");
+            launch_frame_result_orig(P, I.io_inv.as<uint32_t>(), I.n, io, nullptr, cs);
+            I.counted(2);
+            check(cudaEventRecord(I.ev_gather, cs), "event");
+            I.gather_pending = true;
         }
         if (x) check(cudaMemcpyAsync(x, I.io_x.p, 12 * I.n, cudaMemcpyDeviceToHost, cs), "d2h");
         if (v) check(cudaMemcpyAsync(v, I.io_v.p, 12 * I.n, cudaMemcpyDeviceToHost, cs), "d2h");

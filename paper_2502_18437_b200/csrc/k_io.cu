@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(kTotThreads) k_frame_result_orig(const Params 
             if (out.x) { out.x[3 * o] = a.x; out.x[3 * o + 1] = a.y; out.x[3 * o + 2] = a.z; }
             if (out.v) { out.v[3 * o] = a.w; out.v[3 * o + 1] = b.x; out.v[3 * o + 2] = b.y; }
             if (out.active) out.active[o] = act ? 1 : 0;
-            if (!act) continue;
+            if (!act || !totals) continue;
             const int sc = static_cast<int>((flags >> kSceneShift) & kSceneMask);
             if (sc != scene) {
                 if (scene >= 0)
@@ -181,6 +181,7 @@ __global__ void __launch_bounds__(kTotThreads) k_frame_result_orig(const Params 
             t[3] += m * vz;
             t[4] += 0.5 * m * static_cast<double>(vx * vx + vy * vy + vz * vz);
         }
+        if (!totals) continue;  // arrays only (block-uniform)
         scn[threadIdx.x] = scene;
         for (int q = 0; q < 5; ++q) red[q][threadIdx.x] = t[q];
         __syncthreads();
