@@ -831,11 +831,7 @@ __device__ __forceinline__ void g2p_group(const Params& P, uint32_t g, float4* r
     const int kmax = __reduce_max_sync(0xffffffffu, st.cnt);
     for (int k = 0; k < NS - 1; ++k) st.issue(P, k);
     NodeBox box{nullptr, {0, 0, 0}};
-#ifdef MPMB_BOX_UNUSED  // A/B: the shared memory is reserved but never used
-    if (false) {
-#else
     if (BOX && box_s) {
-#endif
         const int4 gb = P.group_box[g];
         if (gb.w >= 0) {
             const int ox = gb.x & 0xFFFF, oy = gb.y & 0xFFFF, oz = gb.z & 0xFFFF;
