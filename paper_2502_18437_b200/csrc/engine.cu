@@ -174,7 +174,7 @@ struct Engine::Impl {
         g_src, g_cell, s_src, s_orig, b_counts, scan_tmp, key_by_orig, order, group_nact, group_box;
     BinBuffers bb{};
     DevBuf mats;
-    DevBuf shapes, verts, ints, free_pose, pose_table, pose_override, cull;
+    DevBuf shapes, verts, ints, free_pose, pose_table, pose_override, cull, pose_eff;
     int n_shapes = 0;
     int table_subs = 1;
     PinnedBuf pin_table[2];
@@ -270,6 +270,7 @@ struct Engine::Impl {
         P.pose_override = pose_override.as<uint8_t>();
         P.free_pose = free_pose.as<DevPose>();
         P.cull = cull.as<float4>();
+        P.pose_eff = pose_eff.as<DevPose>();
         P.n_shapes = n_shapes;
         P.shapes_per_scene = sps;
         P.mats = mats.as<float4>();
@@ -616,6 +617,7 @@ void Engine::set_shapes(const std::vector<std::vector<EngineShape>>& per_scene) 
     I.ints.alloc(sizeof(int) * std::max<size_t>(1, ints.size()));
     I.free_pose.alloc(sizeof(DevPose) * ns);
     I.cull.alloc(2 * sizeof(float4) * ns);
+    I.pose_eff.alloc(sizeof(DevPose) * ns);
     I.acc_sub.alloc(sizeof(double) * 6 * ns);
     I.acc_frame.alloc(sizeof(double) * 6 * ns);
     I.cnt_sub.alloc(sizeof(int) * ns);

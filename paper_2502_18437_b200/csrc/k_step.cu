@@ -22,6 +22,7 @@ __device__ __forceinline__ uint64_t brick_node(const Params& P, uint32_t gb, int
 // (DevShape::lbox) under this substep's pose (kinematic table or integrated free pose):
 // cull[2i] = {min, bounded ? 1 : -1}, cull[2i+1] = {max, 0}.
 __device__ __forceinline__ void cull_shape(const Params& P, int i, int sub) {
+    P.pose_eff[i] = pose_of_sub(P, i, sub);  // the contact pass and push-out of `sub` read it
     {
         const DevShape& sh = P.shapes[i];
         if (sh.lbox_h[0] < 0.f) {
@@ -154,7 +155,7 @@ __global__ void __launch_bounds__(256) k_grid_update(const Params P) {
                 const bool near = si == cs_begin ? aabb_may_touch(cs_lo, cs_hi, xn.x, xn.y, xn.z)
                                                  : cull_may_touch(P, si, xn.x, xn.y, xn.z);
                 if (live && own && near) {
-                    const DevPose& pose = pose_of(P, si);
+                    const DevPose& pose = P.pose_eff[si];  // this substep's (cull pass)
                     const Sdf s = sdf_query(sh, pose, P.verts, P.ints, xn);
                     if (node_in_contact(s, sh.hw)) {
                         V3 delta;

@@ -641,7 +641,7 @@ __device__ __forceinline__ int pushout_particle(const Params& P, const SceneView
             if (!near) continue;
         }
         const DevShape& sh = P.shapes[si];
-        const DevPose& pose = pose_of(P, si);
+        const DevPose& pose = kCull ? P.pose_eff[si] : pose_of(P, si);  // kCull: the cull pass's copy
         if (!kCull && !shape_may_touch(sh, pose, mk(x[0], x[1], x[2]))) continue;
         const Sdf s = sdf_query(sh, pose, P.verts, P.ints, mk(x[0], x[1], x[2]));
         float move = 0.f;

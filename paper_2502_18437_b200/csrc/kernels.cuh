@@ -55,6 +55,7 @@ struct Params {
     const uint8_t* pose_override;
     DevPose* free_pose;
     float4* cull;   // per shape, this substep: world AABB {min, bounded}, {max, 0} (k_shape_cull)
+    DevPose* pose_eff;  // per shape, this substep: pose_of_sub() copied by the cull pass (one load)
     int n_shapes;
     int shapes_per_scene;  // > 0: scene s owns shapes [s k, s k + k) (batches of replicas); else 0
     const float4* mats;  // {kind, mu, lambda, beta}
