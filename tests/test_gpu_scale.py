@@ -267,3 +267,27 @@ def test_c5_replicas_long_horizon_through_the_cut():
         assert r["inverted_f"] == 0
     assert (pushed > 0).all() and (imp > 0).all()
     assert b.profile()["ms_fused"] > 0.0
+
+
+def test_frame_result_arrays_survive_the_next_advance():
+    """fetch_results returns after the totals; the original-order arrays are gathered on the
+    copy stream while the next frame's P2G / grid update already run.  A frame's arrays read
+    AFTER the next advance was enqueued must equal the ones read right away."""
+    R = 16  # 1.04M particles: grouped (non-wide) transfers, K8 fused
+    specs = [scenes.c5_cutting_replica(r) for r in range(R)]
+    a, b = _batch(specs), _batch(specs)
+    dt = specs[0]["dt_frame"]
+    for _ in range(2):
+        a.advance(dt)
+        ra = a.fetch_results(arrays=True)  # copied right away
+        b.advance(dt)
+        b.fetch_results()                  # arrays still in flight ...
+        b.advance(dt)                      # ... while the next frame starts
+        rb = [s._result(dict(n_particles=s.particle_count(), n_shapes=len(ra[i]["shape_ids"])))
+              for i, s in enumerate(b.scenes)]
+        b.fetch_results()
+        a.advance(dt)
+        a.fetch_results()
+        for x, y in zip(ra, rb):
+            np.testing.assert_array_equal(x["active"], y["active"])
+            assert np.abs(x["positions"] - y["positions"]).max() <= 1e-3 * specs[0]["grid"]["dx"]
