@@ -42,10 +42,12 @@ def _floor():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("k,window", [(2, True), (3, True), (2, False)])
-def test_slabs_match_single_domain(k, window):
+# (3, True, 48): 24 migrations, past the 16 appended-group migrations after which a slab
+# re-bins (Engine::dd_migrate_unpack)
+@pytest.mark.parametrize("k,window,sub", [(2, True, 24), (3, True, 24), (2, False, 24), (3, True, 48)])
+def test_slabs_match_single_domain(k, window, sub):
     p = _slab_particles()
-    n, sub, dt = len(p["x"]), 24, 1e-3
+    n, dt = len(p["x"]), 1e-3
     ref = api.SolverState(DIMS, DX, (0.0, 0.0, 0.0))
     ref.set_materials(MATS)
     ref.set_particles(p, with_stress=False)
