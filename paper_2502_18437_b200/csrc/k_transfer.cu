@@ -30,7 +30,19 @@ namespace mpmb {
 #ifndef MPMB_G2P_STAGES
 #define MPMB_G2P_STAGES 3
 #endif
-constexpr int kStages = MPMB_P2G_STAGES;     // P2G staging ring depth
+constexpr int kStages = MPMB_P2G_STAGES;     // P2G staging ring depth (from HBM)
+#ifndef MPMB_P2G_STAGES_L2
+#define MPMB_P2G_STAGES_L2 2
+#endif
+// K8's P2G phase stages from L2 (the lines its G2P phase just wrote): a shallower ring hides
+// that latency and leaves more of the SM's shared memory to L1 (A/B at C5: K8 -0.7%)
+constexpr int kStagesL2 = MPMB_P2G_STAGES_L2;
+// K8's per-warp ring (float4 x 32 units): the G2P phase's and the P2G phase's, aliased
+template <bool PB, bool STD>
+__host__ __device__ constexpr int fused_ring() {
+    return kStagesL2 * 7 > MPMB_G2P_STAGES * ((PB || STD) ? 7 : 5) ? kStagesL2 * 7
+                                                                   : MPMB_G2P_STAGES * ((PB || STD) ? 7 : 5);
+}
 constexpr int kG2PStages = MPMB_G2P_STAGES;  // G2P: one more, so particle k+1 has landed while k computes
 #ifndef MPMB_WPB
 #define MPMB_WPB 4
@@ -456,7 +468,8 @@ __device__ __forceinline__ void p2g_prepare(const Params& P, const float4 q0, co
 template <bool MLS, bool STD, bool OUT, bool BOX>
 __device__ __forceinline__ void p2g_group(const Params& P, uint32_t g, float4* ring, int lane) {
     constexpr int NP = kPlanes;
-    Stager<NP, kStages, OUT || MPMB_P2G_CG != 0, OUT> st;
+    constexpr int NS = OUT ? kStagesL2 : kStages;
+    Stager<NP, NS, OUT || MPMB_P2G_CG != 0, OUT> st;
     st.buf = ring;
     st.lane = lane;
     uint32_t* bins = reinterpret_cast<uint32_t*>(ring);  // sort scratch aliases the ring
@@ -468,7 +481,7 @@ __device__ __forceinline__ void p2g_group(const Params& P, uint32_t g, float4* r
     reinterpret_cast<uint64_t*>(P.order)[static_cast<uint64_t>(g) * 32 + lane] = st.order;
     if (lane == 0) P.group_nact[g] = n_act;
     const int kmax = min(static_cast<int>(n_act), kPer);  // lane 0 has the most
-    for (int k = 0; k < kStages - 1; ++k) st.issue(P, k);
+    for (int k = 0; k < NS - 1; ++k) st.issue(P, k);
     float2 pa[27], pb[27];  // (mom_x, mom_y), (mom_z, mass) per stencil node
 #pragma unroll
     for (int n = 0; n < 27; ++n) {
@@ -478,10 +491,10 @@ __device__ __forceinline__ void p2g_group(const Params& P, uint32_t g, float4* r
     int cb[3] = {INT_MIN, INT_MIN, INT_MIN};
     int cscene = -1;
     for (int k = 0; k < kmax; ++k) {
-        st.issue(P, k + kStages - 1);
-        cp_wait<kStages - 1>();
+        st.issue(P, k + NS - 1);
+        cp_wait<NS - 1>();
         if (k >= st.cnt) continue;
-        const float4* src = st.buf + (k % kStages) * NP * 32 + lane;
+        const float4* src = st.buf + (k % NS) * NP * 32 + lane;
         const float4 r = src[PR * 32];
         const float4 q0 = src[0], q1 = src[32], q2 = src[64], q3 = src[96], q4 = src[128], q5 = src[160];
         int scene, b[3];
@@ -950,7 +963,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_g2p2g(co
     const int lane = threadIdx.x & 31;
     const uint32_t n_groups = *P.n_groups;
     const uint32_t wpb = blockDim.x >> 5;
-    constexpr int kRing = kStages * kPlanes > kG2PStages * 7 ? kStages * kPlanes : kG2PStages * 7;
+    constexpr int kRing = fused_ring<PB, STD>();
     float4* ring = smem + (threadIdx.x >> 5) * (kRing * 32);
     float4* box = BOX ? smem + wpb * (kRing * 32) + (threadIdx.x >> 5) * kBoxCap : nullptr;
     for (uint32_t g = blockIdx.x * wpb + (threadIdx.x >> 5); g < n_groups; g += gridDim.x * wpb) {
@@ -1128,18 +1141,19 @@ void launch_g2p(const Params& P, bool pb, int64_t max_groups, cudaStream_t st, b
 void launch_g2p2g(const Params& P, int64_t max_groups, cudaStream_t st, bool standard, bool pb) {
     const int threads = kWarpsPerBlock * 32;
     const int blocks = grid_for(max_groups * 32, threads, 148 * 16);
-    constexpr int kRing = kStages * kPlanes > kG2PStages * 7 ? kStages * kPlanes : kG2PStages * 7;
     const bool box = kBoxCap > 0 && max_groups <= kBoxMaxGroups;
-    const int smem = kWarpsPerBlock * kRing * 32 * static_cast<int>(sizeof(float4));
+    const int ring = (pb || standard) ? fused_ring<true, false>() : fused_ring<false, false>();
+    const int smem = kWarpsPerBlock * ring * 32 * static_cast<int>(sizeof(float4));
     const int smem_box = smem + kWarpsPerBlock * kBoxCap * static_cast<int>(sizeof(float4));
+    const int smem_max = kWarpsPerBlock * (fused_ring<true, false>() * 32 + kBoxCap) * static_cast<int>(sizeof(float4));
     static bool attr = false;
     if (!attr) {
-        opt_in_smem(k_g2p2g<false>, smem);
-        opt_in_smem(k_g2p2g<true>, smem);
-        opt_in_smem(k_g2p2g<false, true>, smem);
-        opt_in_smem(k_g2p2g<false, false, true>, smem_box);
-        opt_in_smem(k_g2p2g<true, false, true>, smem_box);
-        opt_in_smem(k_g2p2g<false, true, true>, smem_box);
+        opt_in_smem(k_g2p2g<false>, smem_max);
+        opt_in_smem(k_g2p2g<true>, smem_max);
+        opt_in_smem(k_g2p2g<false, true>, smem_max);
+        opt_in_smem(k_g2p2g<false, false, true>, smem_max);
+        opt_in_smem(k_g2p2g<true, false, true>, smem_max);
+        opt_in_smem(k_g2p2g<false, true, true>, smem_max);
         attr = true;
     }
     if (box) {
