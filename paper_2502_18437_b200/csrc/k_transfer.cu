@@ -61,7 +61,10 @@ constexpr int kBoxCap = MPMB_G2P_BOX ? MPMB_BOX_CAP : 0;
 // The box pays off while a launch has few groups per warp slot (latency-bound tail: the
 // 874k-particle scene +4%); at C5 sizes its shared memory costs more than it saves (-1.3%,
 // DESIGN.md §7), so launches with more groups than this use the plain gather.
-constexpr int64_t kBoxMaxGroups = 4 * 148 * 3 * kWarpsPerBlock;
+#ifndef MPMB_BOX_MAX_GROUPS
+#define MPMB_BOX_MAX_GROUPS (4 * 148 * 3 * kWarpsPerBlock)
+#endif
+constexpr int64_t kBoxMaxGroups = MPMB_BOX_MAX_GROUPS;
 constexpr int kBins = 512;         // sort bins: ((global brick & 7) << 6) | cell
 constexpr int kBinWords = kBins + kBins / 32;  // one pad word per 32 bins (conflict-free scan)
 static_assert(kPer == 8, "order bytes are read as one u64 per lane");
