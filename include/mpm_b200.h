@@ -330,10 +330,14 @@ mpmb_status mpmb_advance(mpmb_handle h, float dt);
  * frames are enqueued back to back; the last one is left pending for mpmb_fetch_results.
  * (Extension; the reference's advance is synchronous, scene.hpp:117-123.) */
 mpmb_status mpmb_advance_frames(mpmb_handle h, float dt, int32_t n_frames);
-/* Waits for the pending frame and snapshots FrameResult. For a batch, out has n entries. */
+/* Waits for the pending frame and snapshots FrameResult. For a batch, out has n entries.
+ * Returns once the scalar part (FP64 totals, counters, contact sums) is on the host; the
+ * original-order arrays are gathered and copied asynchronously (they stay valid while the
+ * next frame is enqueued). */
 mpmb_status mpmb_fetch_results(mpmb_handle h, mpmb_frame_summary* out);
 /* Arrays of the last fetched FrameResult of one scene (any pointer may be NULL):
- * positions/velocities 3n floats, active n bytes, shape ids/impulses/torques per shape. */
+ * positions/velocities 3n floats, active n bytes, shape ids/impulses/torques per shape.
+ * Waits for the asynchronous array copy of mpmb_fetch_results. */
 mpmb_status mpmb_result_copy(mpmb_handle scene, float* positions, float* velocities,
                              uint8_t* active, int32_t* shape_ids, float* shape_impulses,
                              float* shape_torque_impulses);
