@@ -24,6 +24,13 @@
 
 namespace mpmb {
 
+// resident blocks per SM the register allocation targets (A/B-tuned, DESIGN.md §7)
+#ifndef MPMB_P2G_MINB
+#define MPMB_P2G_MINB 3
+#endif
+#ifndef MPMB_G2P_MINB
+#define MPMB_G2P_MINB 3
+#endif
 #ifndef MPMB_P2G_STAGES
 #define MPMB_P2G_STAGES 3
 #endif
@@ -45,7 +52,7 @@ __host__ __device__ constexpr int fused_ring() {
 }
 constexpr int kG2PStages = MPMB_G2P_STAGES;  // G2P: one more, so particle k+1 has landed while k computes
 #ifndef MPMB_WPB
-#define MPMB_WPB 4
+#define MPMB_WPB 4  // A/B: 3 warps x 4 blocks per SM: C5 +0.5%, C1 +3%, but C2 -7%, C3 -3%
 #endif
 constexpr int kWarpsPerBlock = MPMB_WPB;
 constexpr int kPer = kGroup / 32;  // sorted positions per lane
@@ -62,20 +69,12 @@ constexpr int kBoxCap = MPMB_G2P_BOX ? MPMB_BOX_CAP : 0;
 // 874k-particle scene +4%); at C5 sizes its shared memory costs more than it saves (-1.3%,
 // DESIGN.md §7), so launches with more groups than this use the plain gather.
 #ifndef MPMB_BOX_MAX_GROUPS
-#define MPMB_BOX_MAX_GROUPS (4 * 148 * 3 * kWarpsPerBlock)
+#define MPMB_BOX_MAX_GROUPS (4 * 148 * MPMB_P2G_MINB * kWarpsPerBlock)
 #endif
 constexpr int64_t kBoxMaxGroups = MPMB_BOX_MAX_GROUPS;
 constexpr int kBins = 512;         // sort bins: ((global brick & 7) << 6) | cell
 constexpr int kBinWords = kBins + kBins / 32;  // one pad word per 32 bins (conflict-free scan)
 static_assert(kPer == 8, "order bytes are read as one u64 per lane");
-// resident blocks per SM the register allocation targets (A/B-tuned, DESIGN.md §5)
-#ifndef MPMB_P2G_MINB
-#define MPMB_P2G_MINB 3
-#endif
-#ifndef MPMB_G2P_MINB
-#define MPMB_G2P_MINB 3
-#endif
-
 // G2P position of lane L at iteration k.  LDGSTS costs one L1 wavefront per (8-lane phase,
 // source line): lanes 8j..8j+7 take positions 64 b + 8 c + a (c = L & 7) that group_phys
 // maps to ONE 128-byte line (8 (4a + b) + c), and the warp's 32 positions lie in a
