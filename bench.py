@@ -36,11 +36,25 @@ import numpy as np  # noqa: E402
 METRIC = "particle-substeps/sec"
 UNIT = "particle-substeps/s"
 DT_FRAME = 0.02
-# algorithmic bytes per particle per launch
-# per particle per launch.  fused = k_g2p2g (G2P of substep s + P2G of s+1):
-# one substep of compulsory state turnover, the §8d per-substep figure.
-ALG_BYTES = {"p2g": 108.0, "g2p": 148.0, "grid": 0.0, "sort": 224.0, "fused": 204.0}
+# Algorithmic (compulsory) bytes per particle per launch:
+#   p2g   108 = read x, v, C, F, mass, volume0, flags
+#   g2p   148 = read x, F, flags (52) + write x, v, C, F (96)
+#   fused k_g2p2g (G2P of substep s + P2G of s+1): v and C need not persist between the two
+#         phases, so the compulsory state traffic is read x, F, mass, volume0, flags (60) +
+#         write x, F (48) = 108 B, plus the grid: the G2P phase reads and the P2G phase
+#         accumulates ~0.2 active nodes per particle (SURVEY.md §8 probe) x 16 B each = 6.4 B.
+#         §8d: "report it with its own denominator (108 + grid); do not divide by 204".
+#   PB-MPM (c3) per particle-iteration: 168 B (P2G reads x, v, C, mass, flags = 68; G2P reads
+#         x, F, flags = 52 and writes v, C = 48); the fused PB kernel moves one iteration.
+GRID_BYTES = 0.2 * 2 * 16.0
+ALG_BYTES = {"p2g": 108.0, "g2p": 148.0, "grid": 0.0, "sort": 224.0, "fused": 108.0 + GRID_BYTES}
+ALG_BYTES_PB = {"p2g": 68.0, "g2p": 100.0, "grid": 0.0, "sort": 224.0, "fused": 168.0}
 SUBSTEP_BYTES = 204.0
+SUBSTEP_BYTES_PB = 172.8
+# Untimed pre-roll frames before the warm-up: the cutting workloads' blade reaches the tissue
+# only after it has fallen and bounced (oracle probe, C5 replica 0: first blade impulse and
+# push-out at frame 53, t = 1.08 s), so the timed frames start inside the cut.
+PREROLL = {"c5": 55, "c2": 55, "m1": 65}
 
 
 def parse():
@@ -49,7 +63,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c5", choices=["c5", "c1", "c2", "c3", "c4"])
+    ap.add_argument("--workload", default="c5", choices=["c5", "c1", "c2", "c3", "c4", "m1"])
+    ap.add_argument("--preroll", type=int, default=None,
+                    help="untimed frames before the warm-up (default: PREROLL[workload], 0 for others)")
     ap.add_argument("--replicas", type=int, default=512, help="C5 replicas per GPU")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU-baseline sample length")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -70,7 +86,11 @@ def workload_specs(name, rank, replicas):
     if name == "c5":
         return [scenes.c5_cutting_replica(r) for r in shard_replicas(rank, replicas)]
     return [{"c1": scenes.c1_cube_drop, "c2": scenes.c2_cutting, "c3": scenes.c3_suture,
-             "c4": scenes.c4_slab}[name]()]
+             "c4": scenes.c4_slab, "m1": scenes.m1_cutting}[name]()]
+
+
+def preroll_of(args):
+    return PREROLL.get(args.workload, 0) if args.preroll is None else args.preroll
 
 
 def reduce_over_ranks(ms, ms_e2e, n_particles, world, device):
@@ -91,6 +111,8 @@ def workload_desc(name, replicas, n_per_gpu):
         return (f"C5 shard: {replicas} independent cutting replicas x 64,800 p per GPU, 84^3 grid each, "
                 f"MLS 10 substeps/frame, quad-slicer blade (BASELINE.json configs[4])")
     return {"c1": "C1 cube drop, MLS, 32,768 p, 64^3", "c2": "C2 cutting, MLS, 262,144 p, 128^3",
+            "m1": "M1 north-star scene: one 1,049,600-particle MLS tissue block cut by the quad-slicer blade "
+                  "(cutting.json rescaled to 128^3, dx 1.4/128)",
             "c4": "C4 tissue slab on a floor, MLS 20 substeps/frame, 8,388,608 p, 512^3 (slab DD over NCCL "
                   "when N > 1)",
             "c3": "C3 suture, PB-MPM K=10, 262,144 p, 128^3, arc needle + 16 free thread capsules"}[name]
@@ -198,24 +220,32 @@ def reference_scenes(specs):
     return out
 
 
-def time_reference(specs_fn, threads, frames, warmup=0):
-    """Advance `threads` independent reference scenes `frames` frames on `threads` host
-    threads (oracle/_ref/libmpmref.so, unmodified reference code).  Returns
-    (particle-substeps/s, wall seconds, total particles, substeps/frame)."""
-    import ctypes as C
-    import backends
-    lib = backends.reference()
-    specs = specs_fn(threads)
-    scs = reference_scenes(specs)
-    hs = (C.c_uint64 * len(scs))(*[s.h for s, _ in scs])
-    if warmup:
-        lib.mpmref_advance_many(hs, len(scs), DT_FRAME, warmup, threads)
-    wall = lib.mpmref_advance_many(hs, len(scs), DT_FRAME, frames, threads)
-    n = sum(s.particle_count() for s, _ in scs)
-    sub = substeps_of(specs[0])
-    for s, _ in scs:
-        s.destroy()
-    return n * sub * frames / wall, wall, n, sub
+class RefSet:
+    """`threads` independent reference scenes (oracle/_ref/libmpmref.so: the UNMODIFIED
+    reference code), advanced together on `threads` host threads, one scene per thread."""
+
+    def __init__(self, specs, threads, preroll=0):
+        import ctypes as C
+        import backends
+        self.lib = backends.reference()
+        self.scs = reference_scenes(specs)
+        self.hs = (C.c_uint64 * len(self.scs))(*[sc.h for sc, _ in self.scs])
+        self.threads = threads
+        self.n = sum(sc.particle_count() for sc, _ in self.scs)
+        self.sub = substeps_of(specs[0])
+        if preroll:
+            self.advance(preroll)
+
+    def advance(self, frames):
+        """Wall seconds of `frames` frames of every scene (advance + fetch_results)."""
+        return self.lib.mpmref_advance_many(self.hs, len(self.scs), DT_FRAME, frames, self.threads)
+
+    def rate(self, frames, wall):
+        return self.n * self.sub * frames / wall
+
+    def destroy(self):
+        for sc, _ in self.scs:
+            sc.destroy()
 
 
 def cpu_specs_fn(workload):
@@ -256,21 +286,23 @@ def run_reference(args, rank):
                                  "sample": f"{k} step_mls substeps per step on all {n} particles"},
                 "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     threads = cpu_threads() if args.workload == "c5" else 1
-    fn = cpu_specs_fn(args.workload)
-    # size one step to ~cpu_seconds/steps: probe one frame first
-    rate1, wall1, n, sub = time_reference(fn, threads, 1)
+    pre = preroll_of(args) if args.workload != "m1" else 0
+    rs = RefSet(cpu_specs_fn(args.workload)(threads), threads, pre)
+    # size one step to ~cpu_seconds/steps: probe one frame first (it is part of the pre-roll)
+    wall1 = rs.advance(1)
     frames = max(1, int(round(args.cpu_seconds / max(wall1, 1e-3) / max(args.steps, 1))))
-    vals = []
     for _ in range(args.warmup):
-        time_reference(fn, threads, frames)
-    t_total = 0.0
+        rs.advance(frames)
+    vals, t_total = [], 0.0
     for _ in range(args.steps):
-        r, w, _, _ = time_reference(fn, threads, frames)
-        vals.append(r)
+        w = rs.advance(frames)
+        vals.append(rs.rate(frames, w))
         t_total += w
+    n, sub = rs.n, rs.sub
+    rs.destroy()
     value = statistics.median(vals)
     sample = (f"{threads} concurrent reference scenes ({'C5 replicas' if args.workload == 'c5' else args.workload}), "
-              f"{frames} frame(s) x {sub} substeps per step, {n} particles total")
+              f"{frames} frame(s) x {sub} substeps per step, {n} particles total, after {pre + 1} untimed frames")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * t_total / max(args.steps, 1),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
@@ -314,7 +346,11 @@ def run_ours(args, rank, world, local_rank):
     # clocks: nvidia-smi needs ~0.1 s to start; it runs from the warm-up on
     clocks = ClockSampler(local_rank)
     clocks.start()
-    # warm-up (includes the upload and first binning)
+    pre = preroll_of(args)
+    # untimed pre-roll (cutting workloads: until the blade is in the tissue), then the warm-up
+    if pre:
+        batch.advance_frames(DT_FRAME, pre)
+        batch.fetch_results()
     batch.advance_frames(DT_FRAME, max(args.warmup, 1))
     batch.fetch_results()
     torch.cuda.synchronize()
@@ -331,6 +367,9 @@ def run_ours(args, rank, world, local_rank):
         b = build_batch(specs)
         b.set_fusion(args.fusion)
         b.set_stream(stream.cuda_stream)
+        if pre:
+            b.advance_frames(DT_FRAME, pre)
+            b.fetch_results()
         b.advance_frames(DT_FRAME, max(args.warmup, 1))
         b.fetch_results()
         barrier()
@@ -370,19 +409,28 @@ def run_ours(args, rank, world, local_rank):
     batch.fetch_results()
 
     # ---- e2e: public facade, host buffers every frame, on the same frames again: the two
-    # numbers differ only by the host path
+    # numbers differ only by the host path.  The caller's FrameResult arrays (one x / v /
+    # active array over every scene, allocated once like a data-generation consumer would)
+    # are bound with mpmb_bind_results, so each frame's D2H lands in them directly; the
+    # frame's arrays are complete (mpmb_result_wait) before the next frame's copy is issued,
+    # and the last frame's copy is inside the timed region.
     batch = fresh_batch(batch)
+    hx = np.empty((n_particles, 3), np.float32)
+    hv = np.empty((n_particles, 3), np.float32)
+    ha = np.empty(n_particles, np.uint8)
+    batch.bind_results(hx, hv, ha)
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record(stream)
-    for _ in range(args.steps):
-        batch.advance(DT_FRAME)
+    batch.advance(DT_FRAME)
+    for k in range(args.steps):
         batch.fetch_results()
-    # each frame's x / v / active D2H overlaps the next frame (copy stream); the last one
-    # lands inside the timed region
-    batch.synchronize()
+        if k + 1 < args.steps:
+            batch.advance(DT_FRAME)  # frame k+1 runs on the device while frame k's arrays land
+        batch.wait_results()  # frame k's x / v / active are in hx / hv / ha
     f1.record(stream)
     f1.synchronize()
     ms_e2e = f0.elapsed_time(f1)
+    batch.bind_results()
 
     ms, ms_e2e, n_total = reduce_over_ranks(ms, ms_e2e, n_particles, world, "cuda")
 
@@ -401,7 +449,9 @@ def run_ours(args, rank, world, local_rank):
               "fused": prof["ms_fused"]}
     dom = max(cls_ms, key=lambda k: cls_ms[k])
     per_launch_ms = cls_ms[dom] / max(launches_per_class[dom], 1)
-    alg = ALG_BYTES[dom] * n_particles
+    pb = specs[0]["solver"] == "pbmpm"
+    alg_table = ALG_BYTES_PB if pb else ALG_BYTES
+    alg = alg_table[dom] * n_particles
     achieved = alg / (per_launch_ms / 1e3) / 1e9 if per_launch_ms > 0 else 0.0
     tr = ncu_traffic()
     traffic = None
@@ -413,7 +463,9 @@ def run_ours(args, rank, world, local_rank):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": workload_desc(args.workload, args.replicas, n_particles),
+        "config": {"workload": workload_desc(args.workload, args.replicas, n_particles) +
+                   (f"; timed frames {pre + max(args.warmup, 1)}..{pre + max(args.warmup, 1) + args.steps - 1} "
+                    f"after {pre} untimed pre-roll frames (blade in the tissue)" if pre else ""),
                    "particles_per_gpu": n_particles, "scenes_per_gpu": len(batch.scenes),
                    "substeps_per_step": sub, "parallelism": f"scene replicas x{world} (no collective)",
                    "l2": "inputs larger than L2 (%.1f GB particle state per GPU)" % (n_particles * 112 / 1e9)},
@@ -421,11 +473,12 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "alg_bytes_per_particle": ALG_BYTES[dom], "per_launch_ms": per_launch_ms,
+                     "alg_bytes_per_particle": alg_table[dom], "per_launch_ms": per_launch_ms,
                      "timing": "per-kernel-class CUDA events on the library stream, profiled replay of the "
                                "timed frames (%.2f ms/step with the events vs %.2f without)"
                                % (ms_profiled / args.steps, ms / args.steps),
-                     "substep_frac": value * SUBSTEP_BYTES / 1e9 / peak},
+                     "substep_frac": value * (SUBSTEP_BYTES_PB if pb else SUBSTEP_BYTES) / 1e9 / peak,
+                     "substep_bytes_per_particle": SUBSTEP_BYTES_PB if pb else SUBSTEP_BYTES},
         "kernel_ms": {k: v / max(launches_per_class[k], 1) for k, v in cls_ms.items()},
         "clocks": clk,
         "setup_s": setup_s,
@@ -557,13 +610,16 @@ def cpu_baseline(args):
                 "sample": f"C4 (1 core): {k} step_mls substeps with the contact hook on all {n} particles, "
                           f"{wall:.1f} s wall"}
     threads = cpu_threads() if args.workload == "c5" else 1
-    fn = cpu_specs_fn(args.workload)
-    rate1, wall1, n, sub = time_reference(fn, threads, 1)
+    pre = preroll_of(args) if args.workload != "m1" else 0
+    rs = RefSet(cpu_specs_fn(args.workload)(threads), threads, pre)
+    wall1 = rs.advance(1)
     frames = max(1, int(round(args.cpu_seconds / max(wall1, 1e-3))))
-    rate, wall, n, sub = time_reference(fn, threads, frames)
+    wall = rs.advance(frames)
+    rate, n, sub = rs.rate(frames, wall), rs.n, rs.sub
+    rs.destroy()
     return {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
             "sample": f"{threads} concurrent reference scenes ({args.workload}), {frames} frames x {sub} substeps, "
-                      f"{n} particles, {wall:.1f} s wall"}
+                      f"{n} particles, {wall:.1f} s wall, after {pre + 1} untimed frames"}
 
 
 def main():

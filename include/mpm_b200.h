@@ -179,6 +179,10 @@ int32_t mpmb_device_available(void);
 const char* mpmb_last_error(void);
 /* Total kernels this process launched through the library. */
 int64_t mpmb_kernel_launch_count(void);
+/* The device's P2G stress function on n row-major F matrices (known-answer tests): the
+ * cancellation-free FP32 form of neo_hookean_cauchy_stress (materials.hpp:35-54) that P2G
+ * evaluates; sigma 9n floats, J (may be NULL) n floats. */
+mpmb_status mpmb_eval_stress_f32(const float* F, int64_t n, float mu, float lambda, float* sigma, float* J);
 
 /* ------------------------------------------------------------ solver layer */
 typedef struct mpmb_state_s* mpmb_state;
@@ -341,6 +345,18 @@ mpmb_status mpmb_fetch_results(mpmb_handle h, mpmb_frame_summary* out);
 mpmb_status mpmb_result_copy(mpmb_handle scene, float* positions, float* velocities,
                              uint8_t* active, int32_t* shape_ids, float* shape_impulses,
                              float* shape_torque_impulses);
+/* Zero-copy FrameResult arrays (extension): the caller's own arrays become the destination of
+ * every later fetch_results' device->host copy (page-locked in place with cudaHostRegister, so
+ * the DMA lands in them directly; no staging buffer, no host memcpy).  h = scene or batch
+ * handle; for a batch the arrays cover every scene in batch order (positions/velocities 3n
+ * floats, active n bytes, n = total particle count).  A fetch overwrites them; they hold the
+ * newest fetched frame once mpmb_result_wait (or mpmb_result_copy) returns.  All-NULL unbinds
+ * (also done by mpmb_destroy).  The reference's FrameResult owns its vectors
+ * (scene.hpp:251-258); a caller that keeps one FrameResult object per scene binds its vectors. */
+mpmb_status mpmb_bind_results(mpmb_handle h, float* positions, float* velocities, uint8_t* active,
+                              int64_t n);
+/* Waits for the array copy of the last mpmb_fetch_results (bound or internal buffer). */
+mpmb_status mpmb_result_wait(mpmb_handle h);
 int32_t mpmb_particle_count(mpmb_handle scene);
 mpmb_status mpmb_copy_positions(mpmb_handle scene, float* out, size_t capacity_floats,
                                 size_t* written_floats);

@@ -355,6 +355,13 @@ class Scene:
     def particle_count(self) -> int:
         return self.lib.mpmb_particle_count(self.h)
 
+    def bind_results(self, x=None, v=None, active=None):
+        """Zero-copy FrameResult arrays of this scene (see SceneBatch.bind_results)."""
+        SceneBatch.bind_results(self, x, v, active)
+
+    def wait_results(self):
+        check(self.lib.mpmb_result_wait(self.h), self.lib, "result_wait")
+
     def particles(self) -> dict:
         n = self.particle_count()
         x, v = np.zeros((n, 3), F32), np.zeros((n, 3), F32)
@@ -403,6 +410,24 @@ class SceneBatch:
         if arrays:
             res = [s._result(r) for s, r in zip(self.scenes, res)]
         return res
+
+    def bind_results(self, x: np.ndarray = None, v: np.ndarray = None, active: np.ndarray = None):
+        """Zero-copy FrameResult arrays (mpmb_bind_results): every later fetch_results DMAs the
+        positions / velocities / active flags of all scenes (batch order) straight into these
+        arrays, valid after wait_results().  No arguments: unbind."""
+        if x is None:
+            check(self.lib.mpmb_bind_results(self.h, None, None, None, 0), self.lib, "bind_results")
+            self._bound = None
+            return
+        n = len(active)
+        assert x.dtype == F32 and v.dtype == F32 and active.dtype == np.uint8
+        assert x.flags.c_contiguous and v.flags.c_contiguous and x.size == v.size == 3 * n
+        check(self.lib.mpmb_bind_results(self.h, _fp(x), _fp(v), active.ctypes.data_as(capi.u8p), n),
+              self.lib, "bind_results")
+        self._bound = (x, v, active)  # keep them alive while bound
+
+    def wait_results(self):
+        check(self.lib.mpmb_result_wait(self.h), self.lib, "result_wait")
 
     def set_stream(self, stream_ptr: int):
         check(self.lib.mpmb_set_stream(self.h, C.c_void_p(stream_ptr)), self.lib, "set_stream")

@@ -134,6 +134,9 @@ PRODUCT_API.update({
     "advance_frames": (C.c_int, [u64, C.c_float, C.c_int32]),
     "fetch_results": (C.c_int, [u64, C.POINTER(FrameSummary)]),
     "result_copy": (C.c_int, [u64, fp, fp, u8p, ip, fp, fp]),
+    "bind_results": (C.c_int, [u64, fp, fp, u8p, C.c_int64]),
+    "eval_stress_f32": (C.c_int, [fp, C.c_int64, C.c_float, C.c_float, fp, fp]),
+    "result_wait": (C.c_int, [u64]),
     "particle_count": (C.c_int32, [u64]),
     "copy_positions": (C.c_int, [u64, fp, C.c_size_t, C.POINTER(C.c_size_t)]),
     "shape_impulse": (C.c_int, [u64, u64, fp]),

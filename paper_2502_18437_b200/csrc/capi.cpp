@@ -168,6 +168,16 @@ extern "C" int32_t mpmb_device_available(void) { return device_available() ? 1 :
 extern "C" const char* mpmb_last_error(void) { return g_error.c_str(); }
 extern "C" int64_t mpmb_kernel_launch_count(void) { return global_launch_count(); }
 
+extern "C" mpmb_status mpmb_eval_stress_f32(const float* F, int64_t n, float mu, float lambda, float* sigma,
+                                            float* J) {
+    return guarded([&] {
+        if (!F || !sigma || n < 0) fail(MPMB_INVALID_ARGUMENT, "eval_stress_f32: null argument");
+        require_device();
+        Engine::eval_stress_f32(F, n, mu, lambda, sigma, J);
+        return MPMB_OK;
+    });
+}
+
 // ============================================================== solver layer
 struct mpmb_state_s {
     std::unique_ptr<Engine> eng;
@@ -674,9 +684,25 @@ struct Batch {
     std::vector<Scene*> scenes;
     std::unique_ptr<Engine> eng;
     std::shared_ptr<void> frame;  // pinned FrameResult buffer (x, v, active of all scenes)
+    // caller arrays bound by mpmb_bind_results (page-locked in place): the FrameResult
+    // destination instead of `frame`
+    float* bound_x = nullptr;
+    float* bound_v = nullptr;
+    uint8_t* bound_a = nullptr;
+    int64_t bound_n = 0;
+    void unbind() {
+        if (eng) eng->wait_results();  // no copy may still target the arrays
+        Engine::host_unregister(bound_x);
+        Engine::host_unregister(bound_v);
+        Engine::host_unregister(bound_a);
+        bound_x = bound_v = nullptr;
+        bound_a = nullptr;
+        bound_n = 0;
+    }
     ~Batch() {  // the frame buffer goes before the engine: finish its copy first
         try {
             if (eng) eng->wait_results();
+            if (bound_n) unbind();
         } catch (...) {  // at process exit the driver may already be gone
         }
     }
@@ -976,14 +1002,15 @@ void fetch(Batch& b) {
     size_t total = 0;
     for (Scene* s : b.scenes) total += s->count();
     const size_t bytes = 24 * total + total + 16;
-    if (!b.frame || b.frame_bytes < bytes) {
+    const bool bound = b.bound_n > 0 && static_cast<size_t>(b.bound_n) == total;
+    if (!bound && (!b.frame || b.frame_bytes < bytes)) {
         e.wait_results();  // the previous frame's copy may still target the old buffer
         b.frame = Engine::pinned_host(bytes);
         b.frame_bytes = bytes;
     }
-    float* x = static_cast<float*>(b.frame.get());
-    float* v = x + 3 * total;
-    uint8_t* a = reinterpret_cast<uint8_t*>(v + 3 * total);
+    float* x = bound ? b.bound_x : static_cast<float*>(b.frame.get());
+    float* v = bound ? b.bound_v : x + 3 * total;
+    uint8_t* a = bound ? b.bound_a : reinterpret_cast<uint8_t*>(v + 3 * total);
     // counters and contact first: a device->host copy issued after the arrays' would queue
     // behind them on the copy engine
     std::vector<SceneCounters> cnt = e.read_counters();
@@ -1016,7 +1043,7 @@ void fetch(Batch& b) {
     for (size_t si = 0; si < b.scenes.size(); ++si) {
         Scene* s = b.scenes[si];
         const size_t o = b.offsets[si], n = s->count();
-        s->frame = b.frame;
+        s->frame = bound ? nullptr : b.frame;
         s->rx = x + 3 * o;
         s->rv = v + 3 * o;
         s->ra = a + o;
@@ -1343,12 +1370,49 @@ extern "C" mpmb_status mpmb_result_copy(mpmb_handle sh, float* pos, float* vel, 
         Scene* s = reg().scene(sh);
         if (!s) return MPMB_BAD_HANDLE;
         if ((pos || vel || active) && s->rn && s->batch && s->batch->eng) s->batch->eng->wait_results();
-        if (pos && s->rn) std::copy(s->rx, s->rx + 3 * s->rn, pos);
-        if (vel && s->rn) std::copy(s->rv, s->rv + 3 * s->rn, vel);
-        if (active && s->rn) std::copy(s->ra, s->ra + s->rn, active);
+        // a bound destination already holds the arrays (mpmb_bind_results)
+        if (pos && s->rn && pos != s->rx) std::copy(s->rx, s->rx + 3 * s->rn, pos);
+        if (vel && s->rn && vel != s->rv) std::copy(s->rv, s->rv + 3 * s->rn, vel);
+        if (active && s->rn && active != s->ra) std::copy(s->ra, s->ra + s->rn, active);
         if (ids) std::copy(s->rid.begin(), s->rid.end(), ids);
         if (imp) std::copy(s->rimp.begin(), s->rimp.end(), imp);
         if (tq) std::copy(s->rtq.begin(), s->rtq.end(), tq);
+        return MPMB_OK;
+    });
+}
+
+extern "C" mpmb_status mpmb_bind_results(mpmb_handle h, float* pos, float* vel, uint8_t* active, int64_t n) {
+    std::lock_guard<std::mutex> lk(reg().mu);
+    return guarded([&]() -> mpmb_status {
+        bool is_batch = false;
+        Batch* b = batch_of_handle(reg(), h, is_batch);
+        if (!b) return MPMB_BAD_HANDLE;
+        if (!is_batch && b->scenes.size() != 1)
+            fail(MPMB_INVALID_ARGUMENT, "bind_results: a batch member binds through its batch handle");
+        if (b->bound_n) b->unbind();
+        if (!pos && !vel && !active) return MPMB_OK;
+        if (!pos || !vel || !active || n <= 0) fail(MPMB_INVALID_ARGUMENT, "bind_results: three arrays and n > 0");
+        int64_t total = 0;
+        for (Scene* s : b->scenes) total += static_cast<int64_t>(s->count());
+        if (n != total) fail(MPMB_INVALID_ARGUMENT, "bind_results: n must equal the particle count");
+        Engine::host_register(pos, 12 * static_cast<size_t>(n));
+        Engine::host_register(vel, 12 * static_cast<size_t>(n));
+        Engine::host_register(active, static_cast<size_t>(n));
+        b->bound_x = pos;
+        b->bound_v = vel;
+        b->bound_a = active;
+        b->bound_n = n;
+        return MPMB_OK;
+    });
+}
+
+extern "C" mpmb_status mpmb_result_wait(mpmb_handle h) {
+    std::lock_guard<std::mutex> lk(reg().mu);
+    return guarded([&]() -> mpmb_status {
+        bool is_batch = false;
+        Batch* b = batch_of_handle(reg(), h, is_batch);
+        if (!b) return MPMB_BAD_HANDLE;
+        if (b->eng) b->eng->wait_results();
         return MPMB_OK;
     });
 }

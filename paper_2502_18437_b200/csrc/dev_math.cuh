@@ -158,8 +158,9 @@ __device__ __forceinline__ void neo_hookean(const float F[9], float mu, float la
 //   F F^T - I = H + H^T + H H^T   and   J - 1 = tr H + (principal 2x2 minors of H) + det H
 // with H = F - I (exact for F near I), ln J = log1p(J - 1).  The reference evaluates in
 // FP64 because the float difference F F^T - I cancels (materials.hpp:29-34); this form
-// has no such difference, and agrees with the FP64 value to a few float ulps.  J is
-// clamped at 1e-6 exactly as the reference (materials.hpp:42).
+// has no such difference, and agrees with the FP64 value to a few float ulps.  Away from
+// F = I (|J - 1| >= 0.5) J is the cofactor determinant of F, clamped at 1e-6 exactly as the
+// reference (materials.hpp:42); tests/test_gpu_stress_kat.py pins both branches.
 __device__ __forceinline__ float neo_hookean_f32(const float F[9], float mu, float lambda, float s[9]) {
     const float h0 = F[0] - 1.f, h1 = F[1], h2 = F[2];
     const float h3 = F[3], h4 = F[4] - 1.f, h5 = F[5];
@@ -167,14 +168,20 @@ __device__ __forceinline__ float neo_hookean_f32(const float F[9], float mu, flo
     const float m2 = fmaf(h0, h4, -h1 * h3) + fmaf(h0, h8, -h2 * h6) + fmaf(h4, h8, -h5 * h7);
     const float dh = h0 * fmaf(h4, h8, -h5 * h7) + h1 * fmaf(h5, h6, -h3 * h8) + h2 * fmaf(h3, h7, -h4 * h6);
     const float j1 = (h0 + h4 + h8) + m2 + dh;
-    const float J = 1.f + j1;
-    float lnJ, invJ;
-    if (J < 1e-6f) {
-        lnJ = -13.815510558f;  // log(1e-6)
-        invJ = 1e6f;
-    } else {
+    float J, lnJ, invJ;
+    if (fabsf(j1) < 0.5f) {  // near F = I: J - 1 without cancellation, ln J = log1p(J - 1)
+        J = 1.f + j1;
         lnJ = log1pf(j1);
         invJ = 1.f / J;
+    } else {
+        // far from I the H-expansion sums O(1) terms of opposite sign (F = 0.01 I: tr H +
+        // minors + det H = -2.97 + 2.94 - 0.97), which loses J near the 1e-6 clamp; the
+        // cofactor determinant of F itself is exact there (products of the small entries)
+        J = fmaf(F[0], fmaf(F[4], F[8], -F[5] * F[7]),
+                 fmaf(-F[1], fmaf(F[3], F[8], -F[5] * F[6]), F[2] * fmaf(F[3], F[7], -F[4] * F[6])));
+        const float Jc = J < 1e-6f ? 1e-6f : J;  // materials.hpp:42
+        lnJ = logf(Jc);
+        invJ = 1.f / Jc;
     }
     const float d = lambda * lnJ;
     // (b - I)_ij = h_ij + h_ji + sum_k h_ik h_jk

@@ -1077,6 +1077,18 @@ std::shared_ptr<void> Engine::pinned_host(size_t bytes) {
     return std::shared_ptr<void>(p, [](void* q) { cudaFreeHost(q); });
 }
 
+void Engine::host_register(void* p, size_t bytes) {
+    if (p && bytes) check(cudaHostRegister(p, bytes, cudaHostRegisterPortable), "cudaHostRegister");
+}
+
+void Engine::eval_stress_f32(const float* F, int64_t n, float mu, float lambda, float* sigma, float* J) {
+    mpmb::eval_stress_f32(F, n, mu, lambda, sigma, J);
+}
+
+void Engine::host_unregister(void* p) {
+    if (p) check(cudaHostUnregister(p), "cudaHostUnregister");
+}
+
 void Engine::enable_grid_readback() {
     Impl& I = *impl_;
     if (I.dead_mom.p) return;

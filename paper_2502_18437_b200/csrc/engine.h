@@ -141,6 +141,11 @@ class Engine {
     // page-locked host memory (cudaMallocHost) freed with the last reference: D2H of a
     // FrameResult straight into it runs at link speed, with no staging copies
     static std::shared_ptr<void> pinned_host(size_t bytes);
+    // page-lock caller memory in place (cudaHostRegister) / release it
+    static void host_register(void* p, size_t bytes);
+    static void host_unregister(void* p);
+    // the P2G stress function (neo_hookean_f32) on n host matrices, synchronously (KATs)
+    static void eval_stress_f32(const float* F, int64_t n, float mu, float lambda, float* sigma, float* J);
     // dense grid of one scene (node-major i + nx*(j + ny*k)); for tests and the hook adapter
     void download_grid(int scene, float* mass, float* momentum, float* velocity);
     // keep the momentum of nodes below kMassEps for download_grid (one more float4 per node;

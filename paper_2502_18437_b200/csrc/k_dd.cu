@@ -68,6 +68,7 @@ void launch_halo(const Params& P, int mode, float4* pool, float4* buf, int x0, i
     if (mode == 0) k_halo<0><<<blocks, 256, 0, st>>>(P, pool, buf, x0, w, y0, ny, z0, nz);
     else if (mode == 1) k_halo<1><<<blocks, 256, 0, st>>>(P, pool, buf, x0, w, y0, ny, z0, nz);
     else k_halo<2><<<blocks, 256, 0, st>>>(P, pool, buf, x0, w, y0, ny, z0, nz);
+    MPMB_LAUNCHED("k_halo");
 }
 
 // Node window of the active particles' stencils in y and z: out = {min base y, max base
@@ -101,6 +102,7 @@ __global__ void k_particle_window(const Params P, int* out) {
 
 void launch_particle_window(const Params& P, int* out, cudaStream_t st) {
     k_particle_window<<<dd_blocks(P.n_total, 256), 256, 0, st>>>(P, out);
+    MPMB_LAUNCHED("k_particle_window");
 }
 
 // Particles whose global stencil base x left [lo, hi): packed (7 float4 each) into the
@@ -131,6 +133,7 @@ __global__ void k_migrate_pack(const Params P, int lo, int hi, float4* out_lo, f
 void launch_migrate_pack(const Params& P, int lo, int hi, float4* out_lo, float4* out_hi, uint32_t cap,
                          uint32_t* counts, cudaStream_t st) {
     k_migrate_pack<<<dd_blocks(P.n_total, 256), 256, 0, st>>>(P, lo, hi, out_lo, out_hi, cap, counts);
+    MPMB_LAUNCHED("k_migrate_pack");
 }
 
 // Received particles into the holes past the last occupied slot (slots [first, first + n)).
@@ -146,6 +149,7 @@ __global__ void k_migrate_unpack(const Params P, const float4* in, uint32_t n, u
 void launch_migrate_unpack(const Params& P, const float4* in, uint32_t n, uint32_t first, cudaStream_t st) {
     if (n == 0) return;
     k_migrate_unpack<<<dd_blocks(n, 256), 256, 0, st>>>(P, in, n, first);
+    MPMB_LAUNCHED("k_migrate_unpack");
 }
 
 // The slab's particles compacted (warp-aggregated append, any order): original index, x,
@@ -177,6 +181,7 @@ __global__ void k_download_slots(const Params P, uint32_t* ids, float* x, float*
 void launch_download_slots(const Params& P, uint32_t* ids, float* x, float* v, uint8_t* active, uint32_t* count,
                            cudaStream_t st) {
     k_download_slots<<<dd_blocks(P.n_total, 256), 256, 0, st>>>(P, ids, x, v, active, count);
+    MPMB_LAUNCHED("k_download_slots");
 }
 
 }  // namespace mpmb

@@ -343,8 +343,10 @@ void launch_exact_contact(const Params& P, uint32_t n, void* scratch, cudaStream
     cub::DeviceRadixSort::SortPairs(nullptr, temp, P.ex_ckey, skey, val, sval, static_cast<int>(n));
     void* tmp = take(temp);
     k_ex_iota<<<blocks_of(n, 256), 256, 0, st>>>(val, n);
+    MPMB_LAUNCHED("k_ex_iota");
     cub::DeviceRadixSort::SortPairs(tmp, temp, P.ex_ckey, skey, val, sval, static_cast<int>(n), 0, 64, st);
     k_ex_contact_sum<<<1, 128, 0, st>>>(P, skey, sval, n);
+    MPMB_LAUNCHED("k_ex_contact_sum");
 }
 
 size_t exact_scratch_bytes(int64_t n, int64_t n_bricks) {
@@ -376,16 +378,21 @@ void launch_exact_p2g(const Params& P, bool mls, void* scratch, uint2* brick_idx
     cub::DeviceRadixSort::SortPairs(nullptr, temp, key, skey, val, sval, static_cast<int>(n));
     void* tmp = take(temp);
     k_ex_prep<<<blocks_of(n, 256), 256, 0, st>>>(P, mls ? 1 : 0, key, val, prep);
+    MPMB_LAUNCHED("k_ex_prep");
     cub::DeviceRadixSort::SortPairs(tmp, temp, key, skey, val, sval, static_cast<int>(n), 0, 64, st);
     launch_collect_bricks(P, static_cast<uint32_t>(n_bricks), st);
     k_ex_index<<<blocks_of(n_bricks, 256), 256, 0, st>>>(P, bidx, epoch);
+    MPMB_LAUNCHED("k_ex_index");
     cudaMemsetAsync(range, 0, 8 * 64 * n_bricks, st);
     k_ex_ranges<<<blocks_of(n, 256), 256, 0, st>>>(P, skey, bidx, epoch, range);
+    MPMB_LAUNCHED("k_ex_ranges");
     k_ex_gather<<<blocks_of(n_bricks * 64, 64), 64, 0, st>>>(P, skey, sval, prep, bidx, epoch, range);
+    MPMB_LAUNCHED("k_ex_gather");
 }
 
 void launch_exact_g2p(const Params& P, cudaStream_t st) {
     k_ex_g2p<<<blocks_of(P.n_total, 128), 128, 0, st>>>(P);
+    MPMB_LAUNCHED("k_ex_g2p");
 }
 
 }  // namespace mpmb

@@ -280,31 +280,69 @@ __global__ void k_grid_upload(const Params P, DevScene S, int64_t n_nodes, const
 
 void launch_upload(const Params& P, const IoArrays& in, int64_t n, cudaStream_t st) {
     k_upload<<<blocks_for(n, 256, 148 * 16), 256, 0, st>>>(P, in, n);
+    MPMB_LAUNCHED("k_upload");
 }
 void launch_download(const Params& P, const IoArrays& out, cudaStream_t st) {
     k_download<<<blocks_for(P.n_total, 256, 148 * 16), 256, 0, st>>>(P, out);
+    MPMB_LAUNCHED("k_download");
 }
 void launch_frame_result_orig(const Params& P, uint32_t* inv, int64_t n, const IoArrays& out, double* totals,
                               cudaStream_t st) {
     k_inv_perm<<<blocks_for(P.n_total, 256, 148 * 16), 256, 0, st>>>(P, inv, n);
+    MPMB_LAUNCHED("k_inv_perm");
     k_frame_result_orig<<<blocks_for(n, kTotThreads * kTotPerThread, 148 * 8), kTotThreads, 0, st>>>(P, inv, n, out,
                                                                                                    totals);
+    MPMB_LAUNCHED("k_frame_result_orig");
 }
 void launch_totals(const Params& P, double* totals, cudaStream_t st) {
     k_totals<<<blocks_for(P.n_total, kTotThreads * kTotPerThread, 148 * 8), kTotThreads, 0, st>>>(P, totals);
+    MPMB_LAUNCHED("k_totals");
 }
 void launch_stress(const Params& P, float* stress_orig, cudaStream_t st) {
     k_stress<<<blocks_for(P.n_total, 256, 148 * 16), 256, 0, st>>>(P, stress_orig);
+    MPMB_LAUNCHED("k_stress");
 }
 void launch_grid_download(const Params& P, int, const DevScene& S, float* mass, float* mom,
                           float* vel, cudaStream_t st) {
     const int64_t n = static_cast<int64_t>(S.dims[0]) * S.dims[1] * S.dims[2];
     k_grid_download<<<blocks_for(n, 256, 148 * 16), 256, 0, st>>>(P, S, n, mass, mom, vel);
+    MPMB_LAUNCHED("k_grid_download");
 }
 void launch_grid_upload(const Params& P, int, const DevScene& S, const float* mass,
                         const float* mom, const float* vel, cudaStream_t st) {
     const int64_t n = static_cast<int64_t>(S.dims[0]) * S.dims[1] * S.dims[2];
     k_grid_upload<<<blocks_for(n, 256, 148 * 16), 256, 0, st>>>(P, S, n, mass, mom, vel);
+    MPMB_LAUNCHED("k_grid_upload");
+}
+
+// ---- device evaluation of the P2G stress (known-answer tests of neo_hookean_f32) ----
+__global__ void k_eval_stress_f32(const float* F, int64_t n, float mu, float lambda, float* s, float* J) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float f[9], o[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) f[k] = F[9 * i + k];
+    const float j = neo_hookean_f32(f, mu, lambda, o);
+#pragma unroll
+    for (int k = 0; k < 9; ++k) s[9 * i + k] = o[k];
+    if (J) J[i] = j;
+}
+
+void eval_stress_f32(const float* F, int64_t n, float mu, float lambda, float* s, float* J) {
+    if (n <= 0) return;
+    float *dF = nullptr, *ds = nullptr, *dJ = nullptr;
+    auto ck = [](cudaError_t e, const char* w) { launch_check(e, w); };
+    ck(cudaMalloc(&dF, 36 * n), "cudaMalloc");
+    ck(cudaMalloc(&ds, 36 * n), "cudaMalloc");
+    ck(cudaMalloc(&dJ, 4 * n), "cudaMalloc");
+    ck(cudaMemcpy(dF, F, 36 * n, cudaMemcpyHostToDevice), "h2d");
+    k_eval_stress_f32<<<static_cast<unsigned>((n + 255) / 256), 256>>>(dF, n, mu, lambda, ds, dJ);
+    MPMB_LAUNCHED("k_eval_stress_f32");
+    ck(cudaMemcpy(s, ds, 36 * n, cudaMemcpyDeviceToHost), "d2h");
+    if (J) ck(cudaMemcpy(J, dJ, 4 * n, cudaMemcpyDeviceToHost), "d2h");
+    cudaFree(dF);
+    cudaFree(ds);
+    cudaFree(dJ);
 }
 
 }  // namespace mpmb

@@ -229,16 +229,22 @@ void launch_scenario(const Params& P, int mode, const float* cell, void* scratch
     cudaMemsetAsync(S.n_act, 0, 4 * static_cast<size_t>(n_scenes), st);
     cudaMemsetAsync(S.size, 0, 4 * n, st);
     k_cc_keys<<<blocks(n), 256, 0, st>>>(P, cell, S.hkey, S.ckey, S.val, S.parent, S.n_act);
+    MPMB_LAUNCHED("k_cc_keys");
     cub::DeviceRadixSort::SortPairs(S.temp, S.temp_bytes, S.hkey, S.skey, S.val, S.sval, static_cast<int>(n), 0, 64,
                                     st);
     if (mode == 0) {
         k_cc_probe<0><<<blocks(n), 256, 0, st>>>(P, cell, S.skey, S.sval, S.ckey, S.parent, nullptr);
+        MPMB_LAUNCHED("k_cc_probe");
         k_cc_sizes<<<blocks(n), 256, 0, st>>>(P, S.parent, S.size);
+        MPMB_LAUNCHED("k_cc_sizes");
         cudaMemsetAsync(count, 0, 4 * static_cast<size_t>(n_scenes), st);
         k_cc_count<<<blocks(n), 256, 0, st>>>(P, S.parent, S.size, S.n_act, count);
+        MPMB_LAUNCHED("k_cc_count");
     } else {
         k_cc_probe<1><<<blocks(n), 256, 0, st>>>(P, cell, S.skey, S.sval, S.ckey, S.parent, best2);
+        MPMB_LAUNCHED("k_cc_probe");
         k_cc_orig<<<blocks(n), 256, 0, st>>>(P, orig);
+        MPMB_LAUNCHED("k_cc_orig");
     }
 }
 

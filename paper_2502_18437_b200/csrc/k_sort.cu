@@ -103,8 +103,11 @@ void launch_exclusive_scan(const uint32_t* in, uint32_t* out, int64_t n, uint32_
     const int tiles = static_cast<int>((n + kScanTile - 1) / kScanTile);
     const int t = tiles > 0 ? tiles : 1;
     k_scan_reduce<<<t, kScanThreads, 0, st>>>(in, n, tmp);
+    MPMB_LAUNCHED("k_scan_reduce");
     k_scan_sums<<<1, kScanThreads, 0, st>>>(tmp, t);
+    MPMB_LAUNCHED("k_scan_sums");
     k_scan_down<<<t, kScanThreads, 0, st>>>(in, n, tmp, out, t);
+    MPMB_LAUNCHED("k_scan_down");
     *launches += 3;
 }
 
@@ -354,19 +357,25 @@ void launch_bin(const Params& P, const BinBuffers& B, float4* const new_planes[k
     cudaMemsetAsync(B.bucket_count, 0, sizeof(uint32_t) * B.n_buckets, st);
     const int cap = 148 * 16;
     k_bin_keys<<<blocks_for(n_total, 256, cap), 256, 0, st>>>(P, B);
+    MPMB_LAUNCHED("k_bin_keys");
     launch_exclusive_scan(B.bucket_count, B.bucket_off, B.n_buckets, B.scan_tmp, st, launches);
     k_bin_scatter<<<blocks_for(n_total, 256, cap), 256, 0, st>>>(B, n_total);
+    MPMB_LAUNCHED("k_bin_scatter");
     k_bin_local<<<blocks_for(static_cast<int64_t>(B.n_buckets), 256, 148 * 8), 256, 0, st>>>(B);
+    MPMB_LAUNCHED("k_bin_local");
     k_bin_rest<<<blocks_for(n_total, 256, cap), 256, 0, st>>>(B);
+    MPMB_LAUNCHED("k_bin_rest");
     k_bin_gather<<<blocks_for(n_total, 256, cap), 256, 0, st>>>(
         P, B, n_total, new_planes[0], new_planes[1], new_planes[2], new_planes[3],
         new_planes[4], new_planes[5], new_planes[6]);
+    MPMB_LAUNCHED("k_bin_gather");
     Params Q = P;
     for (int q = 0; q < kPlanes; ++q) {
         Q.pl_out[q] = P.pl[q];
         Q.pl[q] = new_planes[q];
     }
     k_bin_tail<<<blocks_for(n_total / 8, 256, cap), 256, 0, st>>>(Q, B, n_total);
+    MPMB_LAUNCHED("k_bin_tail");
     *launches += 6;
 }
 

@@ -376,6 +376,7 @@ void launch_free_bodies(const Params& P, bool integrate, bool merge, cudaStream_
 void launch_grid_bc(const Params& P, int64_t max_bricks, cudaStream_t st) {
     const int threads = 256;
     k_grid_bc<<<grid_for(max_bricks * 64, threads, 148 * 8), threads, 0, st>>>(P);
+    MPMB_LAUNCHED("k_grid_bc");
 }
 
 }  // namespace mpmb

@@ -1074,26 +1074,21 @@ static int grid_for(int64_t work, int threads, int max_blocks) {
 }
 
 // dynamic shared memory per block: warps x stages x planes x 32 lanes x 16 B; kernels above
-// 48 KB opt in once
-template <class K>
-static void opt_in_smem(K kernel, int bytes) {
-    if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-}
+// 48 KB opt in once per device (opt_in_smem, kernels.cuh)
 
 void launch_p2g(const Params& P, bool mls, int64_t max_groups, cudaStream_t st, bool standard) {
     const int threads = kWarpsPerBlock * 32;
     const int smem = kWarpsPerBlock * kStages * kPlanes * 32 * static_cast<int>(sizeof(float4));
     const int blocks = grid_for(max_groups * 32, threads, 148 * 16);
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<uint64_t> attr{0};
+    smem_opt_in_once(attr, [&] {
         opt_in_smem(k_p2g<true>, smem);
         opt_in_smem(k_p2g<false>, smem);
         opt_in_smem(k_p2g<true, true>, smem);
         opt_in_smem(k_p2g<true, false, true>, smem);
         opt_in_smem(k_p2g<false, false, true>, smem);
         opt_in_smem(k_p2g<true, true, true>, smem);
-        attr = true;
-    }
+    });
     if (kBoxCap > 0 && max_groups <= kBoxMaxGroups) {  // the G2P after it gathers from boxes
         if (standard) launch_chain(k_p2g<true, true, true>, blocks, threads, smem, st, P);
         else if (mls) launch_chain(k_p2g<true, false, true>, blocks, threads, smem, st, P);
@@ -1119,16 +1114,15 @@ void launch_g2p(const Params& P, bool pb, int64_t max_groups, cudaStream_t st, b
     const int boxb = kWarpsPerBlock * kBoxCap * static_cast<int>(sizeof(float4));
     const int smem7 = kWarpsPerBlock * kG2PStages * 7 * 32 * static_cast<int>(sizeof(float4));
     const int smem5 = kWarpsPerBlock * kG2PStages * 5 * 32 * static_cast<int>(sizeof(float4));
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<uint64_t> attr{0};
+    smem_opt_in_once(attr, [&] {
         opt_in_smem(k_g2p<true>, smem7);
         opt_in_smem(k_g2p<false, true>, smem7);
         opt_in_smem(k_g2p<false>, smem5);
         opt_in_smem(k_g2p<true, false, true>, smem7 + boxb);
         opt_in_smem(k_g2p<false, true, true>, smem7 + boxb);
         opt_in_smem(k_g2p<false, false, true>, smem5 + boxb);
-        attr = true;
-    }
+    });
     if (box) {
         if (standard) launch_chain(k_g2p<false, true, true>, blocks, threads, smem7 + boxb, st, P);
         else if (pb) launch_chain(k_g2p<true, false, true>, blocks, threads, smem7 + boxb, st, P);
@@ -1148,16 +1142,15 @@ void launch_g2p2g(const Params& P, int64_t max_groups, cudaStream_t st, bool sta
     const int smem = kWarpsPerBlock * ring * 32 * static_cast<int>(sizeof(float4));
     const int smem_box = smem + kWarpsPerBlock * kBoxCap * static_cast<int>(sizeof(float4));
     const int smem_max = kWarpsPerBlock * (fused_ring<true, false>() * 32 + kBoxCap) * static_cast<int>(sizeof(float4));
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<uint64_t> attr{0};
+    smem_opt_in_once(attr, [&] {
         opt_in_smem(k_g2p2g<false>, smem_max);
         opt_in_smem(k_g2p2g<true>, smem_max);
         opt_in_smem(k_g2p2g<false, true>, smem_max);
         opt_in_smem(k_g2p2g<false, false, true>, smem_max);
         opt_in_smem(k_g2p2g<true, false, true>, smem_max);
         opt_in_smem(k_g2p2g<false, true, true>, smem_max);
-        attr = true;
-    }
+    });
     if (box) {
         if (pb) launch_chain(k_g2p2g<false, true, true>, blocks, threads, smem_box, st, P);
         else if (standard) launch_chain(k_g2p2g<true, false, true>, blocks, threads, smem_box, st, P);
@@ -1171,10 +1164,12 @@ void launch_g2p2g(const Params& P, int64_t max_groups, cudaStream_t st, bool sta
 
 void launch_pushout(const Params& P, cudaStream_t st) {
     k_pushout<<<grid_for(P.n_total, 256, 148 * 8), 256, 0, st>>>(P);
+    MPMB_LAUNCHED("k_pushout");
 }
 
 void launch_deactivate(const Params& P, cudaStream_t st) {
     k_deactivate<<<grid_for(P.n_total, 256, 148 * 8), 256, 0, st>>>(P);
+    MPMB_LAUNCHED("k_deactivate");
 }
 
 }  // namespace mpmb

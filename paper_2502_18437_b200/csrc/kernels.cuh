@@ -14,9 +14,12 @@
 //   K7 k_free_bodies   free-body integration + accumulator merge (rigid_dynamics.hpp:82-103,
 //                      scene.hpp:220-232)
 #pragma once
+#include <atomic>
 #include <climits>
 #include <cstdint>
 #include <cstdlib>
+#include <stdexcept>
+#include <string>
 #include <utility>
 
 #include "dev_math.cuh"
@@ -285,6 +288,37 @@ __device__ __forceinline__ void add_scene_counter(int* counters, int scene, int 
     }
 }
 
+// ---- launch errors ----------------------------------------------------------------------
+// A launch-configuration error (grid / block / shared-memory size, a missing opt-in) does not
+// stick: the next stream synchronise still succeeds and the kernel silently never ran.  Every
+// launch is therefore checked at once (no sync), and the error travels to the C-ABI status.
+inline void launch_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        cudaGetLastError();  // consume it: the error is reported by the exception
+        throw std::runtime_error(std::string("kernel launch failed (") + what + "): " + cudaGetErrorString(e));
+    }
+}
+#define MPMB_LAUNCHED(what) ::mpmb::launch_check(cudaGetLastError(), what)
+
+// >48 KB dynamic shared memory is an opt-in per kernel AND per device; it is cheap, so the
+// launchers keep one bit per device (64 devices) instead of a process-wide flag.
+// The bit is set only after every opt-in succeeded; a racing thread repeats them (harmless).
+template <class F>
+inline void smem_opt_in_once(std::atomic<uint64_t>& done, F&& opt_in) {
+    int dev = 0;
+    launch_check(cudaGetDevice(&dev), "cudaGetDevice");
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return;
+    opt_in();
+    done.fetch_or(bit, std::memory_order_release);
+}
+template <class K>
+inline void opt_in_smem(K kernel, int bytes) {
+    if (bytes > 48 * 1024)
+        launch_check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+                     "cudaFuncSetAttribute(MaxDynamicSharedMemorySize)");
+}
+
 // ---- programmatic dependent launch (PDL) for the per-substep kernel chain -------------
 // A chain kernel is launched with programmatic stream serialisation: its grid may start while
 // the previous kernel's last blocks drain, and waits at entry (griddepcontrol.wait) until that
@@ -315,7 +349,7 @@ inline void launch_chain(void (*kernel)(Exp...), dim3 grid, dim3 block, size_t s
     at[0].val.programmaticStreamSerializationAllowed = 1;
     c.attrs = at;
     c.numAttrs = pdl_enabled() ? 1 : 0;
-    cudaLaunchKernelEx(&c, kernel, std::forward<Act>(args)...);
+    launch_check(cudaLaunchKernelEx(&c, kernel, std::forward<Act>(args)...), "cudaLaunchKernelEx");
 }
 
 }  // namespace mpmb

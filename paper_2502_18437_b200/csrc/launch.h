@@ -94,6 +94,8 @@ void launch_totals(const Params& P, double* totals /*5 per scene*/, cudaStream_t
 void launch_frame_result_orig(const Params& P, uint32_t* inv, int64_t n, const IoArrays& out, double* totals,
                               cudaStream_t st);
 void launch_stress(const Params& P, float* stress_orig, cudaStream_t st);
+// synchronous: the P2G stress function (neo_hookean_f32) on n host matrices, for KATs
+void eval_stress_f32(const float* F, int64_t n, float mu, float lambda, float* sigma, float* J);
 void launch_grid_download(const Params& P, int scene, const DevScene& S, float* mass, float* mom,
                           float* vel, cudaStream_t st);
 void launch_grid_upload(const Params& P, int scene, const DevScene& S, const float* mass,

@@ -11,6 +11,7 @@ Workloads of BASELINE.json:
   C3  suture: arc needle + 16 free thread capsules, PB-MPM, 262,144 p, 128^3 -> ``c3_suture()``
   C4  large tissue slab, MLS, 8,388,608 p, 512^3           -> ``c4_slab()``
   C5  replica r of 4096 cutting scenes, 64,800 p, 84^3     -> ``c5_cutting_replica(r)``
+  M1  north-star 1M-particle cutting scene, MLS, 1,049,600 p, 128^3 -> ``m1_cutting()``
 """
 from __future__ import annotations
 
@@ -157,6 +158,18 @@ def cutting(dims=(56, 56, 56), dx=0.025, box=((0.4375, 0.075, 0.5375), (0.9375, 
 
 def c2_cutting():
     return cutting(dims=(128, 128, 128), dx=1.4 / 128, box=((0.35, 0.075, 0.525), (1.05, 0.25, 0.875)),
+                   hw=0.0375 * 56 / 128, seed=4242)
+
+
+def m1_cutting():
+    """North-star scene (BASELINE.json north_star: "1M-particle MLS-MPM tissue scene"): one
+    cutting.json block rescaled to 160 x 40 x 164 particles (8 ppc, 80 x 20 x 82 cells) on the
+    C2 grid (128^3, dx 1.4/128), centred under the unchanged quad-slicer blade -- the way
+    run_benchmark rescales its template's first object (scenario.hpp:328-336)."""
+    dx = 1.4 / 128
+    c = (0.6875, 0.6875)
+    hx, hz = 40 * dx, 41 * dx
+    return cutting(dims=(128, 128, 128), dx=dx, box=((c[0] - hx, 0.075, c[1] - hz), (c[0] + hx, 0.075 + 20 * dx, c[1] + hz)),
                    hw=0.0375 * 56 / 128, seed=4242)
 
 
