@@ -13,6 +13,7 @@
 
 #include "mpm/facade.hpp"  // reference value types + Status (header-only, unchanged)
 #include "mpm_b200.h"
+#include "mpm_b200_types.hpp"
 
 namespace mpm_b200::facade {
 
@@ -21,6 +22,11 @@ inline constexpr Handle kInvalidHandle = MPMB_INVALID_HANDLE;
 using Status = mpm::facade::Status;  // facade.hpp:18-24 (plus device errors -> invalid_argument)
 
 namespace detail {
+using ::mpm_b200::detail::material;
+using ::mpm_b200::detail::put3;
+using ::mpm_b200::detail::put4;
+using ::mpm_b200::detail::shape;
+using ::mpm_b200::detail::ShapeStore;
 inline Status status(mpmb_status s) {
     switch (s) {
         case MPMB_OK: return Status::ok;
@@ -30,8 +36,6 @@ inline Status status(mpmb_status s) {
         default: return Status::invalid_argument;
     }
 }
-inline void put3(float* o, const mpm::Vec3& v) { o[0] = v.x; o[1] = v.y; o[2] = v.z; }
-inline void put4(float* o, const mpm::Quat& q) { o[0] = q.x; o[1] = q.y; o[2] = q.z; o[3] = q.w; }
 }  // namespace detail
 
 inline Handle create_scene(const mpm::SceneConfig& c) {
@@ -50,9 +54,7 @@ inline Handle create_scene(const mpm::SceneConfig& c) {
 inline Status destroy(Handle h) { return detail::status(mpmb_destroy(h)); }
 
 inline Handle create_material(Handle scene, const mpm::Material& m) {
-    mpmb_material k{m.kind == mpm::MaterialKind::corotational_pb ? MPMB_MAT_COROTATIONAL_PB
-                                                                 : MPMB_MAT_NEO_HOOKEAN,
-                    m.mu, m.lambda, m.beta};
+    const mpmb_material k = detail::material(m);
     return mpmb_create_material(scene, &k);
 }
 
@@ -66,66 +68,8 @@ inline Handle create_particle_object(Handle scene, Handle material, const mpm::V
 }
 
 inline Handle create_shape(Handle scene, const mpm::Shape& s) {
-    mpmb_shape_desc d{};
-    std::vector<float> verts;
-    std::visit(
-        [&](const auto& g) {
-            using T = std::decay_t<decltype(g)>;
-            if constexpr (std::is_same_v<T, mpm::PlaneGeom>) {
-                d.geometry = MPMB_GEOM_PLANE;
-            } else if constexpr (std::is_same_v<T, mpm::SphereGeom>) {
-                d.geometry = MPMB_GEOM_SPHERE;
-                d.gparam[0] = g.radius;
-            } else if constexpr (std::is_same_v<T, mpm::BoxGeom>) {
-                d.geometry = MPMB_GEOM_BOX;
-                detail::put3(d.gparam, g.half_extents);
-            } else if constexpr (std::is_same_v<T, mpm::QuadSlicerGeom>) {
-                d.geometry = MPMB_GEOM_QUAD_SLICER;
-                d.gparam[0] = g.half_length;
-                d.gparam[1] = g.half_height;
-                d.gparam[2] = g.spine_radius;
-            } else if constexpr (std::is_same_v<T, mpm::TriangleMeshSlicerGeom>) {
-                d.geometry = MPMB_GEOM_TRI_MESH_SLICER;
-                d.gparam[0] = g.spine_radius;
-                for (const auto& v : g.vertices) verts.insert(verts.end(), {v.x, v.y, v.z});
-                d.indices = g.indices.data();
-                d.n_indices = static_cast<int32_t>(g.indices.size());
-                d.spine_edges = g.spine_edges.data();
-                d.n_spine_edges = static_cast<int32_t>(g.spine_edges.size());
-            } else if constexpr (std::is_same_v<T, mpm::ArcGeom>) {
-                d.geometry = MPMB_GEOM_ARC;
-                d.gparam[0] = g.radius;
-                d.gparam[1] = g.angle;
-            } else {
-                d.geometry = MPMB_GEOM_POLYLINE;
-                for (const auto& v : g.vertices) verts.insert(verts.end(), {v.x, v.y, v.z});
-            }
-        },
-        s.geometry);
-    d.vertices = verts.empty() ? nullptr : verts.data();
-    d.n_vertices = static_cast<int32_t>(verts.size() / 3);
-    detail::put3(d.pose.position, s.pose.position);
-    detail::put4(d.pose.orientation, s.pose.orientation);
-    detail::put3(d.pose.linear_velocity, s.pose.linear_velocity);
-    detail::put3(d.pose.angular_velocity, s.pose.angular_velocity);
-    d.mu_k = s.mu_k;
-    d.c_d = s.c_d;
-    d.collision_halfwidth = s.collision_halfwidth;
-    d.motion = s.motion == mpm::MotionKind::kinematic   ? MPMB_MOTION_KINEMATIC
-               : s.motion == mpm::MotionKind::free_body ? MPMB_MOTION_FREE_BODY
-                                                        : MPMB_MOTION_FIXED;
-    std::vector<mpmb_keyframe> kf;
-    for (const auto& k : s.trajectory.keyframes) {
-        mpmb_keyframe e{};
-        e.time = k.time;
-        detail::put3(e.position, k.position);
-        detail::put4(e.orientation, k.orientation);
-        kf.push_back(e);
-    }
-    d.keyframes = kf.empty() ? nullptr : kf.data();
-    d.n_keyframes = static_cast<int32_t>(kf.size());
-    d.body_mass = s.body.mass;
-    detail::put3(d.inertia, s.body.inertia_diag);
+    detail::ShapeStore store;
+    const mpmb_shape_desc d = detail::shape(s, store);
     return mpmb_create_shape(scene, &d);
 }
 

