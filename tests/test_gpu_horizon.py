@@ -8,7 +8,7 @@ rounding.  Gates (v_max = the largest particle speed of the run 
        at every frame, 99.99th percentile            <= 1e-4 * v_max
        at every frame, max                           <= 1e-3 * v_max
   shape impulses, every frame                        <= 1e-4 * max |impulse| of the run, or
-                                                        10x the reversed-order envelope
+                                                        10x the order / FMA envelope
 The per-frame MAXIMUM velocity gate is 10x looser because a floor or blade contact is a
 discrete decision per node (v_n < 0, contact.hpp:49/67; the friction clamp, :33-38): at
 contact onset a node whose approach speed is ~0 flips under a 1-ulp change of its momentum,
@@ -16,7 +16,8 @@ and the few particles it feeds jump by up to ~1e-3 v_max for one frame (measured
 substeps, worst frame 1.9e-4 v_max on 1 of 32,768 particles, 0 frames above 1e-4 at the
 99.99th percentile).  The reference itself shows the same jumps when only its float
 evaluation changes: every test also runs the oracle with its P2G in reversed particle order
-(mpmor_set_order_perturbation(1)) and prints that envelope next to the device's deviation.
+(mpmor_set_order_perturbation(1)) and the oracle built with FMA contraction
+(libmpmoracle_fma.so), and prints that envelope next to the device's deviation.
 Mass is exact to 1e-9 and active sets are identical at every frame.
 """
 import contextlib
@@ -48,6 +49,7 @@ class Trio:
         self.spec = spec
         self.o = backends.make_scene("oracle", spec)
         self.b = backends.make_scene("oracle", spec)
+        self.f = backends.make_scene("oracle_fma", spec)
         self.g = backends.make_scene("gpu", spec) if device else None
         self.w = {"x": 0.0, "v_max": 0.0, "v_p9999": 0.0, "v_end": 0.0, "env_x": 0.0, "env_v": 0.0,
                   "imp": 0.0, "env_imp": 0.0, "imp_scale": 0.0}
@@ -58,16 +60,27 @@ class Trio:
         dt = self.spec["dt_frame"]
         if hook:
             hook(self)
-        self.o.advance(dt)
-        with reversed_p2g():
-            self.b.advance(dt)
         self.g.advance(dt)
-        ro = self.o.fetch_results()
-        with reversed_p2g():
-            rb = self.b.fetch_results()
+        ro, rb = self.oracles(dt)
         rg = self.g.fetch_results()
         self.check(ro, rb, rg)
         return ro, rb, rg
+
+    def oracles(self, dt):
+        """Advance the three oracles one frame; the FMA build's deviation joins the envelope."""
+        self.o.advance(dt)
+        with reversed_p2g():
+            self.b.advance(dt)
+        self.f.advance(dt)
+        ro = self.o.fetch_results()
+        with reversed_p2g():
+            rb = self.b.fetch_results()
+        rf = self.f.fetch_results()
+        w = self.w
+        if ro["n_shapes"]:
+            w["env_imp"] = max(w["env_imp"], np.abs(rf["shape_impulses"] - ro["shape_impulses"]).max())
+        w["env_x"] = max(w["env_x"], np.abs(rf["positions"] - ro["positions"]).max())
+        return ro, rb
 
     def check(self, ro, rb, rg):
         assert ro["n_particles"] == rg["n_particles"]
@@ -91,7 +104,7 @@ class Trio:
 
     def verdict(self, name, dx):
         w = self.w
-        print(f"\n{name} ({self.frames} frames): max|dx| {w['x'] / dx:.2e} dx (reversed-order envelope "
+        print(f"\n{name} ({self.frames} frames): max|dx| {w["x"] / dx:.2e} dx (order / FMA envelope "
               f"{w['env_x'] / dx:.2e}); |dv|/v_max end {w['v_end']:.2e}, worst-frame p99.99 {w['v_p9999']:.2e}, "
               f"worst-frame max {w['v_max']:.2e} (envelope {w['env_v']:.2e}); impulse |d| {w['imp']:.2e} of "
               f"{w['imp_scale']:.2e} (envelope {w['env_imp']:.2e})")
@@ -154,6 +167,7 @@ def test_sticky_boundary_single_step_grid():
         s.step_mls(0.002, (0.0, -9.81, 0.0), bc=capi.BC_STICKY)
     mo, _, vo = o.grid()
     mg, _, vg = g.grid()
+    mo, vo, vg = mo.reshape(24, 24, 24), vo.reshape(24, 24, 24, 3), vg.reshape(24, 24, 24, 3)  # [k][j][i]
     live = mo > 1e-9
     band = np.zeros(mo.shape, bool)
     band[:2], band[-2:], band[:, :2], band[:, -2:], band[:, :, :2], band[:, :, -2:] = (True,) * 6
@@ -231,12 +245,7 @@ def test_c5_engaged_replicas_vs_oracle():
         batch.advance(0.02)
         rgs = batch.fetch_results(arrays=True)
         for t, rg in zip(trios, rgs):
-            t.o.advance(0.02)
-            with reversed_p2g():
-                t.b.advance(0.02)
-            ro = t.o.fetch_results()
-            with reversed_p2g():
-                rb = t.b.fetch_results()
+            ro, rb = t.oracles(0.02)
             t.check(ro, rb, rg)
             pushed += ro["pushed_out"]
             assert rg["pushed_out"] > 0 or ro["pushed_out"] == 0

@@ -28,6 +28,7 @@ for c in cfgs:
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st); b.advance_frames(0.02, F); e1.record(st); e1.synchronize()
+    b.fetch_results()
     ms = e0.elapsed_time(e1)
     b.set_profiling(True)
     b.advance_frames(0.02, F); b.synchronize()
@@ -36,5 +37,4 @@ for c in cfgs:
     print(f"{wl} R={R} fusion={fu} resort={rs}: {ms / F:.2f} ms/frame -> {n * sub / (ms / 1e3):.4g} p-substeps/s | "
           f"per frame ms: fused {p['ms_fused'] / F:.2f} p2g {p['ms_p2g'] / F:.2f} g2p {p['ms_g2p'] / F:.2f} "
           f"grid {p['ms_grid'] / F:.2f} sort {p['ms_sort'] / F:.2f} other {p['ms_other'] / F:.2f}", flush=True)
-    b.fetch_results()
     b.destroy()
