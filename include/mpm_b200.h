@@ -248,13 +248,16 @@ mpmb_status mpmb_bin_particles(mpmb_state st, uint32_t* keys, uint32_t* perm);
  * A slab state owns global x nodes [slab_lo, slab_hi) and stores [slab_lo - margin,
  * slab_hi + 2 + margin).  All arithmetic uses the GLOBAL grid (keys, node positions, BC,
  * deactivation), so a DD run equals the single-domain run up to float summation order.
- * Per substep the caller (the transport, e.g. paper_2502_18437_b200/dd.py over NCCL) runs
+ * The production loop is the library's device-resident driver (mpmb_dd_run, below).  The
+ * per-phase entries here let a caller drive the same loop itself (paper_2502_18437_b200/dd.py
+ * does, as the readable restatement and for the gloo CPU tests):
  *   mpmb_dd_p2g -> pack_acc -> [exchange] -> unpack_acc -> mpmb_dd_grid -> pack_vel ->
- *   [exchange] -> unpack_vel -> mpmb_dd_g2p
+ *   [exchange] -> unpack_vel -> mpmb_dd_g2p [-> free bodies: all-reduce the sums of
+ *   mpmb_dd_contact_sums, then mpmb_dd_free_bodies on every slab]
  * and every `margin` substeps (CFL: <= 1 cell per substep) mpmb_dd_migrate_pack ->
  * [exchange] -> mpmb_dd_migrate_unpack.  Exchange rule (both phases): send_lo goes to the
  * lower neighbour's recv_hi, send_hi to the upper neighbour's recv_lo; a missing
- * neighbour's recv buffer stays zero.  Free bodies are not supported in DD. */
+ * neighbour's recv buffer stays zero. */
 mpmb_status mpmb_state_create_slab(const int32_t dims[3], float dx, const float origin[3], int32_t slab_lo,
                                    int32_t slab_hi, int32_t margin, int64_t capacity, mpmb_state* out);
 /* The reference's particle lattice of create_particle_object (state.hpp:101-149, host,
@@ -383,6 +386,42 @@ mpmb_status mpmb_set_fusion(mpmb_handle h, int32_t mode);
 mpmb_status mpmb_get_profile(mpmb_handle h, mpmb_profile* out);
 /* Blocks until every frame enqueued on h has finished. */
 mpmb_status mpmb_synchronize(mpmb_handle h);
+
+/* --------------------------------------------------- slab DD driver (device-resident)
+ * The whole substep loop of a slab domain decomposition in the library (dd_driver.h):
+ * P2G (fused with the previous G2P where no migration intervenes), ghost-sum exchange,
+ * grid update + contact, [contact-sum all-reduce for free bodies, scene.hpp:220-232],
+ * velocity exchange, G2P, free bodies, migration every `migrate_every` substeps (0: the
+ * margin) -- with no host synchronisation inside a run: migration counts travel device to
+ * device beside fixed-capacity payloads, the halo y/z window is set once per run from the
+ * particles' reach + one cell per substep and checked on the device.  Each run reads the
+ * window and error flags snapshot the run before last left in pinned memory (no stream
+ * drain after the first two runs; mpmb_dd_get_stats counts), and fails with the reason if a
+ * check tripped.
+ *   local: the slabs of this process, ordered along x, on one device (device copies);
+ *   NCCL:  one slab per process; the communicator from mpmb_nccl_get_unique_id (on one
+ *          rank, shared by the caller) or the caller's own ncclComm_t.  NCCL is loaded at
+ *          run time (libnccl.so.2). */
+typedef struct mpmb_dd_group_s* mpmb_dd_group;
+/* host_syncs: snapshot reads that drained the stream (the first two runs of a group);
+ * host_waits: later reads that found the device more than one run behind the host. */
+typedef struct {
+    int64_t runs, substeps, host_syncs, host_waits, exchanges, fused, rebins;
+} mpmb_dd_stats;
+mpmb_status mpmb_dd_group_create_local(const mpmb_state* slabs, int32_t n, mpmb_dd_group* out);
+mpmb_status mpmb_nccl_get_unique_id(uint8_t id[128]);
+mpmb_status mpmb_dd_group_create_nccl(mpmb_state slab, const uint8_t id[128], int32_t nranks, int32_t rank,
+                                      mpmb_dd_group* out);
+mpmb_status mpmb_dd_group_create_comm(mpmb_state slab, void* nccl_comm, int32_t nranks, int32_t rank,
+                                      mpmb_dd_group* out);
+mpmb_status mpmb_dd_group_destroy(mpmb_dd_group g);
+mpmb_status mpmb_dd_run(mpmb_dd_group g, int32_t n_sub, float dt, const float gravity[3], int32_t contact,
+                        int32_t boundary, int32_t pushout, int32_t deactivate, int32_t free_bodies,
+                        int32_t migrate_every, int32_t fuse);
+mpmb_status mpmb_dd_get_stats(mpmb_dd_group g, mpmb_dd_stats* out);
+/* Waits for the group's queued work; MPMB_CUDA_ERROR with the reason if a device check
+ * (migration overflow, capacity, stencil reach, particle leaving the grid) tripped. */
+mpmb_status mpmb_dd_check(mpmb_dd_group g);
 
 /* --------------------------------------------------- scenario metrics (device)
  * The harness metrics of run_scenario (scenario.hpp:68-139) on the resident particles: a

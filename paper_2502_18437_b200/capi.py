@@ -74,6 +74,12 @@ class FrameSummary(C.Structure):
                 ("deactivated", C.c_int32)]
 
 
+class DDStats(C.Structure):
+    """mpmb_dd_stats"""
+    _fields_ = [("runs", C.c_int64), ("substeps", C.c_int64), ("host_syncs", C.c_int64), ("host_waits", C.c_int64),
+                ("exchanges", C.c_int64), ("fused", C.c_int64), ("rebins", C.c_int64)]
+
+
 class Profile(C.Structure):
     _fields_ = [("ms_sort", C.c_double), ("ms_p2g", C.c_double), ("ms_grid", C.c_double),
                 ("ms_g2p", C.c_double), ("ms_other", C.c_double), ("launches", C.c_int64),
@@ -135,6 +141,16 @@ PRODUCT_API.update({
     "fetch_results": (C.c_int, [u64, C.POINTER(FrameSummary)]),
     "result_copy": (C.c_int, [u64, fp, fp, u8p, ip, fp, fp]),
     "bind_results": (C.c_int, [u64, fp, fp, u8p, C.c_int64]),
+    "dd_group_create_local": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.POINTER(C.c_void_p)]),
+    "nccl_get_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
+    "dd_group_create_nccl": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint8), C.c_int32, C.c_int32,
+                                       C.POINTER(C.c_void_p)]),
+    "dd_group_create_comm": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
+    "dd_group_destroy": (C.c_int, [C.c_void_p]),
+    "dd_run": (C.c_int, [C.c_void_p, C.c_int32, C.c_float, fp, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                         C.c_int32, C.c_int32, C.c_int32]),
+    "dd_get_stats": (C.c_int, [C.c_void_p, C.POINTER(DDStats)]),
+    "dd_check": (C.c_int, [C.c_void_p]),
     "eval_stress_f32": (C.c_int, [fp, C.c_int64, C.c_float, C.c_float, fp, fp]),
     "result_wait": (C.c_int, [u64]),
     "particle_count": (C.c_int32, [u64]),

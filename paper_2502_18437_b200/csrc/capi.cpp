@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "../../include/mpm_b200.h"
+#include "dd_driver.h"
 #include "engine.h"
 #include "host_math.h"
 
@@ -428,6 +429,92 @@ extern "C" mpmb_status mpmb_dd_migrate_unpack(mpmb_state st, int64_t n_from_lo, 
         return MPMB_OK;
     });
 }
+struct mpmb_dd_group_s {
+    std::unique_ptr<DDGroup> g;
+};
+
+extern "C" mpmb_status mpmb_dd_group_create_local(const mpmb_state* slabs, int32_t n, mpmb_dd_group* out) {
+    return guarded([&] {
+        if (!slabs || n <= 0 || !out) fail(MPMB_INVALID_ARGUMENT, "dd group: slabs");
+        std::vector<Engine*> e;
+        for (int32_t i = 0; i < n; ++i) e.push_back(S(slabs[i])->eng.get());
+        auto* g = new mpmb_dd_group_s{DDGroup::local(e)};
+        *out = g;
+        return MPMB_OK;
+    });
+}
+
+extern "C" mpmb_status mpmb_nccl_get_unique_id(uint8_t id[128]) {
+    return guarded([&] {
+        if (!id) fail(MPMB_INVALID_ARGUMENT, "null argument");
+        DDGroup::nccl_unique_id(id);
+        return MPMB_OK;
+    });
+}
+
+extern "C" mpmb_status mpmb_dd_group_create_nccl(mpmb_state slab, const uint8_t id[128], int32_t nranks,
+                                                 int32_t rank, mpmb_dd_group* out) {
+    return guarded([&] {
+        if (!id || !out || nranks < 1 || rank < 0 || rank >= nranks) fail(MPMB_INVALID_ARGUMENT, "dd group: rank");
+        auto* g = new mpmb_dd_group_s{DDGroup::nccl(S(slab)->eng.get(), id, nranks, rank)};
+        *out = g;
+        return MPMB_OK;
+    });
+}
+
+extern "C" mpmb_status mpmb_dd_group_create_comm(mpmb_state slab, void* comm, int32_t nranks, int32_t rank,
+                                                 mpmb_dd_group* out) {
+    return guarded([&] {
+        if (!comm || !out || nranks < 1 || rank < 0 || rank >= nranks) fail(MPMB_INVALID_ARGUMENT, "dd group: rank");
+        auto* g = new mpmb_dd_group_s{DDGroup::nccl_comm(S(slab)->eng.get(), comm, nranks, rank)};
+        *out = g;
+        return MPMB_OK;
+    });
+}
+
+extern "C" mpmb_status mpmb_dd_group_destroy(mpmb_dd_group g) {
+    delete g;
+    return MPMB_OK;
+}
+
+extern "C" mpmb_status mpmb_dd_run(mpmb_dd_group g, int32_t n_sub, float dt, const float gravity[3], int32_t contact,
+                                   int32_t boundary, int32_t pushout, int32_t deactivate, int32_t free_bodies,
+                                   int32_t migrate_every, int32_t fuse) {
+    return guarded([&] {
+        if (!g || !gravity) fail(MPMB_INVALID_ARGUMENT, "null argument");
+        DDRunOptions o;
+        o.n_sub = n_sub;
+        o.dt = dt;
+        for (int a = 0; a < 3; ++a) o.g[a] = gravity[a];
+        o.contact = contact != 0;
+        o.bc = boundary;
+        o.pushout = pushout != 0;
+        o.deactivate = deactivate != 0;
+        o.free_bodies = free_bodies != 0;
+        o.migrate_every = migrate_every;
+        o.fuse = fuse != 0;
+        g->g->run(o);
+        return MPMB_OK;
+    });
+}
+
+extern "C" mpmb_status mpmb_dd_check(mpmb_dd_group g) {
+    return guarded([&] {
+        if (!g) fail(MPMB_INVALID_ARGUMENT, "null argument");
+        g->g->check();
+        return MPMB_OK;
+    });
+}
+
+extern "C" mpmb_status mpmb_dd_get_stats(mpmb_dd_group g, mpmb_dd_stats* out) {
+    return guarded([&] {
+        if (!g || !out) fail(MPMB_INVALID_ARGUMENT, "null argument");
+        const DDStats& s = g->g->stats();
+        *out = mpmb_dd_stats{s.runs, s.substeps, s.host_syncs, s.host_waits, s.exchanges, s.fused, s.rebins};
+        return MPMB_OK;
+    });
+}
+
 extern "C" mpmb_status mpmb_dd_download(mpmb_state st, int64_t capacity, uint32_t* ids, float* x, float* v,
                                         uint8_t* active, int64_t* n) {
     return guarded([&] {
@@ -450,7 +537,10 @@ extern "C" mpmb_status mpmb_state_get_particles(mpmb_state st, int32_t n, float*
 }
 
 extern "C" int32_t mpmb_state_particle_count(mpmb_state st) {
-    return st ? static_cast<int32_t>(st->n) : -1;
+    if (!st) return -1;
+    // a slab advanced by the device-resident DD driver learns its count from the device
+    if (st->eng && st->eng->n_particles() != st->n && st->grid.slab_hi > st->grid.slab_lo) st->n = st->eng->n_particles();
+    return static_cast<int32_t>(st->n);
 }
 
 extern "C" mpmb_status mpmb_state_set_shapes(mpmb_state st, const mpmb_shape_desc* d, int32_t n) {

@@ -160,7 +160,14 @@ struct Engine::Impl {
     int win[4] = {0, 0, 0, 0};  // halo y/z window: y0, ny, z0, nz (ny = 0: whole extent)
     DevBuf mig[4];       // particles: send_lo, send_hi, recv_lo, recv_hi
     int64_t mig_cap = 0;
-    DevBuf mig_counts;
+    DevBuf mig_counts;   // [0] sent down, [1] sent up; [2] received from below, [3] from above
+    DevBuf dd_win;       // device window of the active particles' stencil reach {ylo, yhi, zlo, zhi}
+    PinnedBuf dd_ctl_h;  // host copy of {window[4], dd control words [4]} (one read per run)
+    PinnedBuf dd_snap_h[2];
+    cudaEvent_t dd_snap_ev[2] = {nullptr, nullptr};
+    bool dd_async = false;  // run by the device-resident driver (dd_driver.cpp): no host counts
+    // transfer launch bound: slabs may append arrivals as extra groups on the device
+    int64_t max_groups() const { return ((slab_hi > slab_lo ? n_cap : n) + kGroup - 1) / kGroup; }
     int64_t mig_sent = 0;
     // DD arrivals appended as extra groups since the last binning (no re-sort):
     // free_slot = first slot past the groups + inactive tail (-1: read from the bin counts)
@@ -410,8 +417,8 @@ Engine::Engine(const std::vector<SceneGrid>& scenes) : impl_(new Impl), scenes_(
     check(cudaMemset(I.misc.p, 0, 64), "memset");
     I.counters.alloc(sizeof(int) * 4 * std::max<size_t>(1, I.hs.size()));
     check(cudaMemset(I.counters.p, 0, I.counters.bytes), "memset");
-    I.b_counts.alloc(16);
-    check(cudaMemset(I.b_counts.p, 0, 16), "memset");
+    I.b_counts.alloc(8 * sizeof(uint32_t));  // [0..3] binning counts, [4..7] DD control (launch.h)
+    check(cudaMemset(I.b_counts.p, 0, 8 * sizeof(uint32_t)), "memset");
     set_shapes(std::vector<std::vector<EngineShape>>(scenes.size()));
     mpmb_material dflt{0, 0.f, 0.f, 0.f};
     set_materials({dflt});
@@ -435,6 +442,8 @@ Engine::~Engine() {
     for (auto e : I.event_pool) cudaEventDestroy(e);
     for (int i = 0; i < 2; ++i)
         if (I.pin_done[i]) cudaEventDestroy(I.pin_done[i]);
+    for (int i = 0; i < 2; ++i)
+        if (I.dd_snap_ev[i]) cudaEventDestroy(I.dd_snap_ev[i]);
     if (I.own) cudaStreamDestroy(I.own);
     delete impl_;
 }
@@ -727,7 +736,7 @@ void Engine::p2g(bool mls, float dt, bool collect, bool standard) {
         I.end(CAT_P2G, ev);
         return;
     }
-    launch_p2g(P, mls || standard, (I.n + kGroup - 1) / kGroup, I.st, standard);
+    launch_p2g(P, mls || standard, I.max_groups(), I.st, standard);
     I.counted(1);
     if (collect) {
         launch_collect_bricks(P, I.total_bricks, I.st);
@@ -808,7 +817,7 @@ void Engine::g2p_mls(int sub, float dt, bool pushout, bool deactivate) {
         I.end(CAT_G2P, ev);
         return;
     }
-    launch_g2p(P, false, (I.n + kGroup - 1) / kGroup, I.st, false, I.wide);
+    launch_g2p(P, false, I.max_groups(), I.st, false, I.wide);
     I.counted(1);
     I.cur = 1 - I.cur;  // G2P wrote the group-sorted state into the other buffer
     I.end(CAT_G2P, ev);
@@ -817,7 +826,8 @@ void Engine::g2p_mls(int sub, float dt, bool pushout, bool deactivate) {
 // G2P(sub) + P2G(sub+1) in one launch (k_g2p2g), then the brick collect of sub+1.  The
 // caller runs free_bodies(sub) after it (its shape cull for sub+1 would overwrite the
 // table the fused push-out of sub still reads).
-void Engine::g2p2g(int sub, float dt, bool standard, const float g[3], bool integrate) {
+void Engine::g2p2g(int sub, float dt, bool standard, const float g[3], bool integrate, bool collect, bool pushout,
+                   bool deactivate) {
     Impl& I = *impl_;
     if (I.n_cap == 0) return;
     auto ev = I.begin();
@@ -825,10 +835,16 @@ void Engine::g2p2g(int sub, float dt, bool standard, const float g[3], bool inte
     P.sub = std::min(sub, I.table_subs - 1);
     P.dt = dt;
     P.g[0] = g[0]; P.g[1] = g[1]; P.g[2] = g[2];
-    P.pushout = 1;
-    P.deactivate = 1;
+    P.pushout = pushout ? 1 : 0;
+    P.deactivate = deactivate ? 1 : 0;
     P.commit = 1;
-    launch_g2p2g(P, (I.n + kGroup - 1) / kGroup, I.st, standard);  // zeroes the brick count
+    launch_g2p2g(P, I.max_groups(), I.st, standard);  // zeroes the brick count
+    if (!collect) {  // slab DD: the ghost sums arrive first (collect_deferred)
+        I.counted(1);
+        I.cur = 1 - I.cur;
+        I.end(CAT_FUSED, ev);
+        return;
+    }
     if (I.n_shapes > 0) {
         const int next = std::min(sub + 1, I.table_subs - 1);
         launch_collect_free(P, I.total_bricks, integrate, true, next, I.st);
@@ -852,7 +868,7 @@ void Engine::g2p2g_pb(float dt) {
     P.commit = 0;
     P.pushout = 0;
     P.deactivate = 0;
-    launch_g2p2g(P, (I.n + kGroup - 1) / kGroup, I.st, false, true);  // zeroes the brick count
+    launch_g2p2g(P, I.max_groups(), I.st, false, true);  // zeroes the brick count
     launch_collect_bricks(P, I.total_bricks, I.st);
     I.counted(2);
     I.flag_parity = 1 - I.flag_parity;
@@ -889,7 +905,7 @@ void Engine::g2p_standard(int sub, float dt, bool pushout, bool deactivate) {
     P.pushout = pushout ? 1 : 0;
     P.deactivate = deactivate ? 1 : 0;
     P.commit = 1;
-    launch_g2p(P, false, (I.n + kGroup - 1) / kGroup, I.st, true, I.wide);
+    launch_g2p(P, false, I.max_groups(), I.st, true, I.wide);
     I.counted(1);
     I.cur = 1 - I.cur;
     I.end(CAT_G2P, ev);
@@ -906,7 +922,7 @@ void Engine::g2p_pb(int sub, float dt, bool commit, bool pushout, bool deactivat
     P.commit = commit ? 1 : 0;
     P.pushout = pushout ? 1 : 0;
     P.deactivate = deactivate ? 1 : 0;
-    launch_g2p(P, true, (I.n + kGroup - 1) / kGroup, I.st, false, I.wide);
+    launch_g2p(P, true, I.max_groups(), I.st, false, I.wide);
     I.counted(1);
     I.cur = 1 - I.cur;
     I.end(CAT_G2P, ev);
@@ -1312,18 +1328,9 @@ void Engine::dd_plane_window(int* y0, int* ny, int* z0, int* nz) {
 }
 
 void Engine::particle_window(int out[4]) {
-    Impl& I = *impl_;
-    DevBuf w;
-    w.alloc(4 * sizeof(int));
-    const int init[4] = {INT_MAX, INT_MIN, INT_MAX, INT_MIN};
-    check(cudaMemcpyAsync(w.p, init, sizeof(init), cudaMemcpyHostToDevice, I.st), "h2d");
-    if (I.n_cap > 0) {
-        Params P = I.params();
-        launch_particle_window(P, w.as<int>(), I.st);
-        I.counted(1);
-    }
-    check(cudaMemcpyAsync(out, w.p, sizeof(init), cudaMemcpyDeviceToHost, I.st), "d2h");
-    check(cudaStreamSynchronize(I.st), "window");
+    dd_window_async();  // persistent device buffer (no per-call allocation)
+    const DDControl c = dd_control();
+    std::memcpy(out, c.window, sizeof(c.window));
 }
 
 void Engine::collect_bricks() {
@@ -1388,7 +1395,9 @@ void Engine::dd_migrate_unpack(int64_t n_from_lo, int64_t n_from_hi) {
             check(cudaStreamSynchronize(I.st), "migrate");
             I.free_slot = static_cast<int64_t>(c[3]) + (I.n_at_bin - static_cast<int64_t>(c[2]));
         }
-        first = I.free_slot;
+        // a fresh group: inside a group the transfers scatter the particles over its slots
+        // (group_phys), so nothing may be appended behind a partly filled one
+        first = (I.free_slot + kGroup - 1) / kGroup * kGroup;
     }
     if (first + arrivals > I.n_cap) throw std::runtime_error("engine: slab capacity exceeded (set_capacity)");
     Params P = I.params();
@@ -1415,12 +1424,157 @@ void Engine::dd_migrate_unpack(int64_t n_from_lo, int64_t n_from_hi) {
         check(cudaMemcpyAsync(static_cast<uint32_t*>(I.b_counts.p) + 1, &c2[0], 4, cudaMemcpyHostToDevice, I.st), "h2d");
         check(cudaMemcpyAsync(static_cast<uint32_t*>(I.b_counts.p) + 3, &c2[1], 4, cudaMemcpyHostToDevice, I.st), "h2d");
         check(cudaStreamSynchronize(I.st), "groups");  // c2 is on the host stack
-        I.free_slot = static_cast<int64_t>(end);
+        I.free_slot = static_cast<int64_t>(tail);
         ++I.appends;
         return;
     }
     I.binned = false;
     bin();
+}
+
+// ------------------------------------------------ device-resident slab DD (dd_driver.cpp)
+void Engine::collect_deferred(int next_sub, float dt, const float g[3], bool integrate) {
+    Impl& I = *impl_;
+    if (I.n_cap == 0) return;
+    Params P = I.params();
+    P.dt = dt;
+    P.g[0] = g[0]; P.g[1] = g[1]; P.g[2] = g[2];
+    if (I.n_shapes > 0) {
+        const int next = std::min(next_sub, I.table_subs - 1);
+        P.sub = std::max(0, std::min(next_sub - 1, I.table_subs - 1));
+        launch_collect_free(P, I.total_bricks, integrate, true, next, I.st);
+        I.cull_sub = next;
+    } else {
+        launch_collect_bricks(P, I.total_bricks, I.st);
+    }
+    I.counted(1);
+    I.flag_parity = 1 - I.flag_parity;
+}
+
+void Engine::dd_window_async() {
+    Impl& I = *impl_;
+    if (!I.dd_win.p) I.dd_win.alloc(8 * sizeof(int));
+    launch_window_init(I.dd_win.as<int>(), I.st);
+    I.counted(1);
+    if (I.n_cap > 0) {
+        Params P = I.params(true);
+        launch_particle_window(P, I.dd_win.as<int>(), I.st);
+        I.counted(1);
+    }
+}
+
+uint32_t* Engine::dd_control_device() { return impl_->b_counts.as<uint32_t>() + 4; }
+
+int* Engine::dd_window_device() {
+    Impl& I = *impl_;
+    if (!I.dd_win.p) dd_window_async();
+    return I.dd_win.as<int>();
+}
+
+static Engine::DDControl parse_ctl(const uint32_t* h);
+
+Engine::DDControl Engine::dd_control() {
+    Impl& I = *impl_;
+    if (!I.dd_win.p) dd_window_async();
+    I.dd_ctl_h.alloc(12 * sizeof(uint32_t));
+    auto* h = static_cast<uint32_t*>(I.dd_ctl_h.p);
+    check(cudaMemcpyAsync(h, I.dd_win.p, 8 * sizeof(int), cudaMemcpyDeviceToHost, I.st), "d2h");
+    check(cudaMemcpyAsync(h + 8, I.b_counts.as<uint32_t>() + 4, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, I.st),
+          "d2h");
+    check(cudaStreamSynchronize(I.st), "dd control");
+    return parse_ctl(h);
+}
+
+static Engine::DDControl parse_ctl(const uint32_t* h) {
+    Engine::DDControl c{};
+    std::memcpy(c.window, h, 4 * sizeof(int));
+    c.group_err = h[4];
+    c.free_slot = h[8];
+    c.arrivals = h[9];
+    c.err = h[10];
+    c.n_real = h[11];
+    return c;
+}
+
+void Engine::dd_snapshot_async(int slot) {
+    Impl& I = *impl_;
+    slot &= 1;
+    if (!I.dd_snap_ev[slot]) check(cudaEventCreateWithFlags(&I.dd_snap_ev[slot], cudaEventDisableTiming), "event");
+    I.dd_snap_h[slot].alloc(12 * sizeof(uint32_t));
+    auto* h = static_cast<uint32_t*>(I.dd_snap_h[slot].p);
+    check(cudaMemcpyAsync(h, I.dd_win.p, 8 * sizeof(int), cudaMemcpyDeviceToHost, I.st), "d2h");
+    check(cudaMemcpyAsync(h + 8, I.b_counts.as<uint32_t>() + 4, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, I.st),
+          "d2h");
+    check(cudaEventRecord(I.dd_snap_ev[slot], I.st), "event");
+}
+
+Engine::DDControl Engine::dd_snapshot_read(int slot, bool* blocked) {
+    Impl& I = *impl_;
+    slot &= 1;
+    if (!I.dd_snap_ev[slot]) throw std::logic_error("engine: no DD snapshot in this slot");
+    const cudaError_t q = cudaEventQuery(I.dd_snap_ev[slot]);
+    if (q != cudaSuccess && q != cudaErrorNotReady) check(q, "event query");
+    if (blocked) *blocked = q == cudaErrorNotReady;
+    check(cudaEventSynchronize(I.dd_snap_ev[slot]), "dd snapshot");
+    return parse_ctl(static_cast<const uint32_t*>(I.dd_snap_h[slot].p));
+}
+
+void Engine::dd_clear_errors() {
+    Impl& I = *impl_;
+    check(cudaMemsetAsync(I.b_counts.as<uint32_t>() + 6, 0, sizeof(uint32_t), I.st), "memset");
+}
+
+void Engine::dd_set_migration_capacity(int64_t cap) {
+    Impl& I = *impl_;
+    cap = std::max<int64_t>(cap, 256);
+    if (I.mig_cap == cap) return;
+    for (int q = 0; q < 4; ++q) I.mig[q].alloc(static_cast<size_t>(cap) * kPlanes * sizeof(float4));
+    I.mig_counts.alloc(4 * sizeof(uint32_t));
+    check(cudaMemsetAsync(I.mig_counts.p, 0, 4 * sizeof(uint32_t), I.st), "memset");
+    I.mig_cap = cap;
+}
+
+void Engine::dd_migration_buffers(void** send_lo, void** send_hi, void** recv_lo, void** recv_hi,
+                                  uint32_t** counts, int64_t* cap) {
+    Impl& I = *impl_;
+    if (I.mig_cap == 0) dd_set_migration_capacity(std::max<int64_t>(1024, I.n_cap / 64));
+    *send_lo = I.mig[0].p; *send_hi = I.mig[1].p; *recv_lo = I.mig[2].p; *recv_hi = I.mig[3].p;
+    *counts = I.mig_counts.as<uint32_t>();
+    *cap = I.mig_cap;
+}
+
+void Engine::dd_migrate_pack_async(bool has_lo, bool has_hi) {
+    Impl& I = *impl_;
+    void* d[4];
+    uint32_t* cnt;
+    int64_t cap;
+    dd_migration_buffers(&d[0], &d[1], &d[2], &d[3], &cnt, &cap);
+    check(cudaMemsetAsync(cnt, 0, 4 * sizeof(uint32_t), I.st), "memset");  // received counts arrive after
+    if (I.n_cap == 0) return;
+    Params P = I.params();
+    int y0, ny, z0, nz;
+    halo_window(P, I.win, y0, ny, z0, nz);
+    launch_migrate_pack_dev(P, I.slab_lo, I.slab_hi, I.margin, make_int4(y0, y0 + ny, z0, z0 + nz), has_lo, has_hi,
+                            I.mig[0].as<float4>(), I.mig[1].as<float4>(), static_cast<uint32_t>(cap), cnt,
+                            I.b_counts.as<uint32_t>() + 4, I.st);
+    I.counted(1);
+}
+
+void Engine::dd_migrate_unpack_async() {
+    Impl& I = *impl_;
+    if (I.n_cap == 0) return;
+    Params P = I.params();
+    launch_migrate_unpack_dev(P, I.mig[2].as<float4>(), I.mig[3].as<float4>(), static_cast<uint32_t>(I.mig_cap),
+                              I.mig_counts.as<uint32_t>(), I.b_counts.as<uint32_t>(), static_cast<uint64_t>(I.n_cap),
+                              I.st);
+    I.counted(2);
+}
+
+void Engine::dd_note_count(int64_t n_real) {
+    Impl& I = *impl_;
+    if (!I.binned) return;  // the control words are set by the first binning
+    I.n = n_real;
+    n_total_ = n_real;
 }
 
 int64_t Engine::download_compact(int64_t capacity, uint32_t* ids, float* x, float* v, uint8_t* active) {

@@ -101,7 +101,8 @@ class Engine {
     // on), followed by the brick collect of sub+1: replaces g2p_* then p2g inside a frame
     // With shapes, the free bodies of `sub` (free_bodies(sub, dt, g, integrate, true, sub+1))
     // run in the collect launch; the caller then skips free_bodies.
-    void g2p2g(int sub, float dt, bool standard, const float g[3], bool integrate);
+    void g2p2g(int sub, float dt, bool standard, const float g[3], bool integrate, bool collect = true,
+               bool pushout = true, bool deactivate = true);
     // fusion policy: 0 off, 1 (default) or 2 on
     // PB-MPM: G2P of a non-final iteration (no commit) + P2G of the next iteration, then the
     // brick collect (replaces g2p_pb(.., false, false, false) then p2g(false, ..))
@@ -186,6 +187,37 @@ class Engine {
     void dd_migrate_unpack(int64_t n_from_lo, int64_t n_from_hi);  // appends, then bins
     // The particles (any order): original index, x, v, active; returns how many (<= capacity).
     int64_t slot_count() const;
+
+    // ---- device-resident slab DD (dd_driver.cpp): nothing per substep waits for the host.
+    // Migration counts travel device to device (fixed-capacity payloads, in-band counts),
+    // arrivals are appended as extra groups by a device kernel, and errors (overflow, a
+    // stencil that outran the stored planes / halo window, a particle leaving the grid) are
+    // flags the driver reads once per run with the window (dd_control).
+    struct DDControl {
+        int window[4];  // {min base y, max base y + 2, min base z, max base z + 2}
+        uint32_t group_err;  // error flags of every rank (the all-reduced window buffer's [4])
+        uint32_t free_slot, arrivals, err, n_real;
+    };
+    void dd_window_async();                // recompute the device window (after a run)
+    int* dd_window_device();               // its 8 ints {window, err, -}: the all-reduce operand
+    uint32_t* dd_control_device();         // the 4 DD control words
+    DDControl dd_control();                // window + control words: one D2H and a sync
+    // pipelined form: the window and control words copied D2H into pinned slot `slot` behind
+    // an event; read later (normally complete by then: no wait).  blocked = the read waited.
+    void dd_snapshot_async(int slot);
+    DDControl dd_snapshot_read(int slot, bool* blocked);
+    void dd_clear_errors();
+    // the migration payload capacity (particles per side; the same on every slab)
+    void dd_set_migration_capacity(int64_t cap);
+    // send/recv payloads (cap x 7 float4 each) and counts {sent down, up, recv below, above}
+    void dd_migration_buffers(void** send_lo, void** send_hi, void** recv_lo, void** recv_hi,
+                              uint32_t** counts, int64_t* cap);
+    void dd_migrate_pack_async(bool has_lo, bool has_hi);
+    void dd_migrate_unpack_async();
+    void dd_note_count(int64_t n_real);    // the host's particle count, from dd_control
+    // brick collect of substep next_sub deferred past the ghost-sum exchange (after
+    // g2p2g(..., collect = false)), with the free bodies of next_sub - 1 when integrate
+    void collect_deferred(int next_sub, float dt, const float g[3], bool integrate);
     int64_t download_compact(int64_t capacity, uint32_t* ids, float* x, float* v, uint8_t* active);
     int64_t n_active_sorted();
 

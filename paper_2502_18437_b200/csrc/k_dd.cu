@@ -14,6 +14,7 @@
 
 #include <climits>
 
+#include "dd_ops.h"
 #include "launch.h"
 
 namespace mpmb {
@@ -150,6 +151,176 @@ void launch_migrate_unpack(const Params& P, const float4* in, uint32_t n, uint32
     if (n == 0) return;
     k_migrate_unpack<<<dd_blocks(n, 256), 256, 0, st>>>(P, in, n, first);
     MPMB_LAUNCHED("k_migrate_unpack");
+}
+
+// ---------------------------------------------------------------------------------
+// Device-resident migration (the C++ driver, dd_driver.cpp): counts never visit the host.
+// ctl = the slab's DD control words (b_counts + 4, launch.h): [0] free slot, [1] arrivals
+// since binning, [2] error flags (kDdErr*), [3] particles on the slab.
+// counts = {sent down, sent up, received from below, received from above}.
+
+__global__ void k_window_init(int* w) {
+    w[0] = INT_MAX; w[1] = INT_MIN; w[2] = INT_MAX; w[3] = INT_MIN;
+    w[4] = w[5] = w[6] = w[7] = 0;
+}
+
+__global__ void k_add_f64(double* dst, const double* src, int64_t n) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        dst[i] += src[i];
+}
+__global__ void k_add_i32(int32_t* dst, const int32_t* src, int64_t n) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        dst[i] += src[i];
+}
+// the empty window (INT_MAX, INT_MIN) negates to INT_MIN + 1 .. fine for MIN; INT_MIN itself
+// has no negation, so the hi ends are clamped first
+__global__ void k_window_min_form(int32_t* w, const uint32_t* ctl) {
+    w[1] = -max(w[1], INT_MIN + 1);
+    w[3] = -max(w[3], INT_MIN + 1);
+    w[4] = -static_cast<int32_t>(ctl[2] & 0x7FFFFFFFu);
+}
+__global__ void k_window_from_min_form(int32_t* w) {
+    w[1] = -w[1];
+    w[3] = -w[3];
+    w[4] = -w[4];
+}
+
+void dd_add_f64(double* dst, const double* src, int64_t n, void* stream) {
+    if (n <= 0) return;
+    k_add_f64<<<dd_blocks(n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(dst, src, n);
+    MPMB_LAUNCHED("k_add_f64");
+}
+void dd_add_i32(int32_t* dst, const int32_t* src, int64_t n, void* stream) {
+    if (n <= 0) return;
+    k_add_i32<<<dd_blocks(n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(dst, src, n);
+    MPMB_LAUNCHED("k_add_i32");
+}
+void dd_window_to_min_form(int32_t* w, const uint32_t* ctl, void* stream) {
+    k_window_min_form<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(w, ctl);
+    MPMB_LAUNCHED("k_window_min_form");
+}
+void dd_window_from_min_form(int32_t* w, void* stream) {
+    k_window_from_min_form<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(w);
+    MPMB_LAUNCHED("k_window_from_min_form");
+}
+
+void launch_window_init(int* w, cudaStream_t st) {
+    k_window_init<<<1, 1, 0, st>>>(w);
+    MPMB_LAUNCHED("k_window_init");
+}
+
+// Pack the particles whose stencil base left [lo, hi) (as k_migrate_pack) and check the
+// reach every particle's stencil had since the window was set: base x inside the stored
+// planes [lo - M, hi + M) and base y / z inside the halo window [y0, y1 - 2) x [z0, z1 - 2)
+// (otherwise P2G clamped it or its ghost sums did not travel: kDdErrReach).
+__global__ void k_migrate_pack_dev(const Params P, int lo, int hi, int margin, int4 win, int has_lo, int has_hi,
+                                   float4* out_lo, float4* out_hi, uint32_t cap, uint32_t* counts, uint32_t* ctl) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    uint32_t err = 0;
+    for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < P.n_total; s += stride) {
+        const float4 r = P.pl[PR][s];
+        if (__float_as_uint(r.w) == kHoleOrig || !(__float_as_uint(r.z) & kActiveBit)) continue;
+        const float4 a = P.pl[0][s];
+        float f;
+        const int b = stencil_base(a.x, P.geo.origin[0], P.geo.inv_dx, f);  // math.hpp:219-224
+        const int by = stencil_base(a.y, P.geo.origin[1], P.geo.inv_dx, f);
+        const int bz = stencil_base(a.z, P.geo.origin[2], P.geo.inv_dx, f);
+        if (b < lo - margin || b >= hi + margin || by < win.x || by + 3 > win.y || bz < win.z || bz + 3 > win.w)
+            err |= kDdErrReach;
+        if (b >= lo && b < hi) continue;
+        const int side = b < lo ? 0 : 1;
+        if (!(side == 0 ? has_lo : has_hi)) {
+            err |= kDdErrLeftDomain;
+            continue;
+        }
+        const uint32_t k = atomicAdd(&counts[side], 1u);
+        if (k >= cap) {
+            err |= kDdErrMigrationOverflow;
+            continue;
+        }
+        float4* out = (side == 0 ? out_lo : out_hi) + static_cast<uint64_t>(k) * kPlanes;
+#pragma unroll
+        for (int q = 0; q < kPlanes; ++q) out[q] = P.pl[q][s];
+#pragma unroll
+        for (int q = 0; q < PR; ++q) P.pl[q][s] = make_float4(0.f, 0.f, 0.f, 0.f);
+        P.pl[PR][s] = make_float4(0.f, 0.f, 0.f, __uint_as_float(kHoleOrig));
+    }
+    if (err) atomicOr(&ctl[2], err);
+}
+
+void launch_migrate_pack_dev(const Params& P, int lo, int hi, int margin, int4 win, bool has_lo, bool has_hi,
+                             float4* out_lo, float4* out_hi, uint32_t cap, uint32_t* counts, uint32_t* ctl,
+                             cudaStream_t st) {
+    k_migrate_pack_dev<<<dd_blocks(P.n_total, 256), 256, 0, st>>>(P, lo, hi, margin, win, has_lo ? 1 : 0,
+                                                                    has_hi ? 1 : 0, out_lo, out_hi, cap, counts, ctl);
+    MPMB_LAUNCHED("k_migrate_pack_dev");
+}
+
+// Arrivals start a fresh transfer group: inside a group the transfers place the particle of
+// sorted position p at slot group_phys(p), so a partly filled group does not keep its
+// particles in its first slots and nothing may be appended behind them.
+__device__ __forceinline__ uint64_t round_up_group(uint64_t s) {
+    return (s + kGroup - 1) / kGroup * kGroup;
+}
+
+// Arrivals (counts[2] from below, counts[3] from above) appended at the first group boundary
+// at or past the free slot, into BOTH plane buffers (the transfers rewrite grouped slots
+// only, which must start identical).
+__global__ void k_migrate_unpack_dev(const Params P, const float4* in_lo, const float4* in_hi, uint32_t cap,
+                                     const uint32_t* counts, const uint32_t* ctl, uint32_t* ctl_err) {
+    const uint32_t n0 = min(counts[2], cap), n1 = min(counts[3], cap);
+    const uint64_t first = round_up_group(ctl[0]);
+    const int64_t n = static_cast<int64_t>(n0) + n1;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint64_t slot = first + static_cast<uint64_t>(i);
+        if (slot >= static_cast<uint64_t>(P.n_total)) {
+            atomicOr(ctl_err, kDdErrCapacity);
+            continue;
+        }
+        const float4* src = i < n0 ? in_lo + static_cast<uint64_t>(i) * kPlanes
+                                   : in_hi + static_cast<uint64_t>(i - n0) * kPlanes;
+#pragma unroll
+        for (int q = 0; q < kPlanes; ++q) {
+            const float4 v = src[q];
+            P.pl[q][slot] = v;
+            P.pl_out[q][slot] = v;
+        }
+    }
+}
+
+// One thread: free slot, arrival and particle counts, and the transfer groups, which grow to
+// cover the appended slots (their group sort puts holes and inactive particles last).
+__global__ void k_migrate_finalize(uint32_t* bcounts, uint32_t cap, const uint32_t* counts, uint64_t n_cap) {
+    uint32_t* ctl = bcounts + 4;
+    const uint32_t sent = min(counts[0], cap) + min(counts[1], cap);
+    const uint32_t arr = min(counts[2], cap) + min(counts[3], cap);
+    if (arr == 0) {
+        ctl[3] -= sent;
+        return;
+    }
+    uint64_t fs = round_up_group(round_up_group(ctl[0]) + arr);  // the arrivals' groups are closed
+    if (fs > n_cap) {
+        ctl[2] |= kDdErrCapacity;
+        fs = n_cap;
+    }
+    ctl[0] = static_cast<uint32_t>(fs);
+    ctl[1] += arr;
+    ctl[3] = ctl[3] + arr - sent;
+    const uint32_t groups = static_cast<uint32_t>(fs / kGroup);
+    if (groups > bcounts[1]) {
+        bcounts[1] = groups;
+        bcounts[3] = groups * static_cast<uint32_t>(kGroup);
+    }
+}
+
+void launch_migrate_unpack_dev(const Params& P, const float4* in_lo, const float4* in_hi, uint32_t cap,
+                               const uint32_t* counts, uint32_t* bcounts, uint64_t n_cap, cudaStream_t st) {
+    k_migrate_unpack_dev<<<dd_blocks(2 * static_cast<int64_t>(cap), 256), 256, 0, st>>>(P, in_lo, in_hi, cap, counts,
+                                                                                          bcounts + 4, bcounts + 6);
+    MPMB_LAUNCHED("k_migrate_unpack_dev");
+    k_migrate_finalize<<<1, 1, 0, st>>>(bcounts, cap, counts, n_cap);
+    MPMB_LAUNCHED("k_migrate_finalize");
 }
 
 // The slab's particles compacted (warp-aggregated append, any order): original index, x,

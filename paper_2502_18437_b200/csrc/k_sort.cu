@@ -310,6 +310,9 @@ __global__ void __launch_bounds__(256) k_bin_gather(const Params P, BinBuffers B
         B.counts[1] = groups;
         B.counts[2] = n_active;
         B.counts[3] = tail;
+        B.counts[4] = tail + (n_real - n_active);  // DD: first free slot (launch.h)
+        B.counts[5] = 0;                           // DD: arrivals since binning
+        B.counts[7] = n_real;                      // DD: particles on the slab
     }
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t d = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; d < n_cap; d += stride) {

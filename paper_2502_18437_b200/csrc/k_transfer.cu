@@ -72,6 +72,9 @@ constexpr int kBoxCap = MPMB_G2P_BOX ? MPMB_BOX_CAP : 0;
 #define MPMB_BOX_MAX_GROUPS (4 * 148 * MPMB_P2G_MINB * kWarpsPerBlock)
 #endif
 constexpr int64_t kBoxMaxGroups = MPMB_BOX_MAX_GROUPS;
+#ifndef MPMB_FUSED_NBIN
+#define MPMB_FUSED_NBIN 1  // the fused kernel's sort reads bins its G2P phase left in shared memory
+#endif
 constexpr int kBins = 512;         // sort bins: ((global brick & 7) << 6) | cell
 constexpr int kBinWords = kBins + kBins / 32;  // one pad word per 32 bins (conflict-free scan)
 static_assert(kPer == 8, "order bytes are read as one u64 per lane");
@@ -293,9 +296,21 @@ __device__ __forceinline__ uint32_t bin_word(uint32_t b) { return b + (b >> 5); 
 // smem atomics).  Active particles come first in bin order, then inactive ones and holes
 // in previous order.  Writes all kGroup order bytes (slot-in-group of each position) to
 // order_s and returns the lane's 8 P2G positions [8L, 8L+8); `bins` is kBinWords words.
+// nbin (fused kernel, !BOX): the bin of every previous position, computed by this warp's G2P
+// phase from the new positions (0xFFFF: inactive or hole), so the sort reads shared memory
+// instead of re-loading x and the flags from L2.
+// the sort bin of a stencil base b of `scene`: ((global brick & 7) << 6) | cell in brick
+__device__ __forceinline__ uint32_t sort_bin(const Params& P, int scene, const int b[3]) {
+    const uint32_t brick = static_cast<uint32_t>(scene) * P.geo.bricks_per_scene +
+                           (static_cast<uint32_t>(b[2] >> 2) * P.geo.nb[1] + static_cast<uint32_t>(b[1] >> 2)) *
+                               P.geo.nb[0] +
+                           static_cast<uint32_t>(b[0] >> 2);
+    return ((brick & 7u) << 6) | static_cast<uint32_t>(((b[2] & 3) << 4) | ((b[1] & 3) << 2) | (b[0] & 3));
+}
+
 template <bool OUT, bool BOX>
 __device__ __forceinline__ uint64_t group_sort(const Params& P, uint32_t g, uint32_t* bins, uint8_t* order_s,
-                                               uint32_t& n_act) {
+                                               uint32_t& n_act, const uint16_t* nbin = nullptr) {
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const unsigned lt = lanemask_lt();
@@ -303,6 +318,13 @@ __device__ __forceinline__ uint64_t group_sort(const Params& P, uint32_t g, uint
     uint32_t bin[kPer];
     int lo[3] = {INT_MAX, INT_MAX, INT_MAX}, hi[3] = {INT_MIN, INT_MIN, INT_MIN};
     int sc_lo = INT_MAX, sc_hi = INT_MIN;
+    if (!BOX && nbin) {
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+            const uint32_t b = nbin[32 * i + lane];
+            bin[i] = b == 0xFFFFu ? 0xFFFFFFFFu : b;
+        }
+    } else {
     // all 16 loads first: one memory latency per group
     float4 xa4[kPer];
     uint32_t fl[kPer];
@@ -328,11 +350,7 @@ __device__ __forceinline__ uint64_t group_sort(const Params& P, uint32_t g, uint
             int b[3];
             float fx[3];
             local_base(P.geo, xa, b, fx);
-            const uint32_t brick = static_cast<uint32_t>(scene) * P.geo.bricks_per_scene +
-                                   (static_cast<uint32_t>(b[2] >> 2) * P.geo.nb[1] +
-                                    static_cast<uint32_t>(b[1] >> 2)) * P.geo.nb[0] +
-                                   static_cast<uint32_t>(b[0] >> 2);
-            bin[i] = ((brick & 7u) << 6) | static_cast<uint32_t>(((b[2] & 3) << 4) | ((b[1] & 3) << 2) | (b[0] & 3));
+            bin[i] = sort_bin(P, scene, b);
             if (BOX) {
 #pragma unroll
                 for (int a = 0; a < 3; ++a) {
@@ -343,6 +361,7 @@ __device__ __forceinline__ uint64_t group_sort(const Params& P, uint32_t g, uint
                 sc_hi = max(sc_hi, scene);
             }
         }
+    }
     }
     if (BOX) {  // the group's stencil-base box for the G2P of this substep (same x, same bases)
         int4 bx;
@@ -468,7 +487,8 @@ __device__ __forceinline__ void p2g_prepare(const Params& P, const float4 q0, co
 // group's particles are in the other buffer (pl_out), written by this warp's G2P of the
 // previous substep inside the fused kernel (k_g2p2g).
 template <bool MLS, bool STD, bool OUT, bool BOX>
-__device__ __forceinline__ void p2g_group(const Params& P, uint32_t g, float4* ring, int lane) {
+__device__ __forceinline__ void p2g_group(const Params& P, uint32_t g, float4* ring, int lane,
+                                          const uint16_t* nbin = nullptr) {
     constexpr int NP = kPlanes;
     constexpr int NS = OUT ? kStagesL2 : kStages;
     Stager<NP, NS, OUT || MPMB_P2G_CG != 0, OUT> st;
@@ -477,7 +497,7 @@ __device__ __forceinline__ void p2g_group(const Params& P, uint32_t g, float4* r
     uint32_t* bins = reinterpret_cast<uint32_t*>(ring);  // sort scratch aliases the ring
     uint8_t* order_s = reinterpret_cast<uint8_t*>(bins + kBinWords);
     uint32_t n_act;
-    st.order = group_sort<OUT, BOX>(P, g, bins, order_s, n_act);
+    st.order = group_sort<OUT, BOX>(P, g, bins, order_s, n_act, nbin);
     st.slot0 = g * kGroup;
     st.cnt = min(max(static_cast<int>(n_act) - kPer * lane, 0), kPer);
     reinterpret_cast<uint64_t*>(P.order)[static_cast<uint64_t>(g) * 32 + lane] = st.order;
@@ -824,7 +844,7 @@ __device__ __forceinline__ void g2p_particle(const Params& P, Part& p, float4& r
 // group_phys(pos): the state leaves G2P in the new order.  `ring`: this warp's staging ring.
 template <bool PB, bool STD, bool BOX>
 __device__ __forceinline__ void g2p_group(const Params& P, uint32_t g, float4* ring, int lane,
-                                          float4* box_s = nullptr) {
+                                          float4* box_s = nullptr, uint16_t* nbin = nullptr) {
     constexpr int NP = (PB || STD) ? 7 : 5;
     constexpr int NS = kG2PStages;
     Stager<NP, NS, MPMB_G2P_CG != 0> st;
@@ -914,9 +934,20 @@ __device__ __forceinline__ void g2p_group(const Params& P, uint32_t g, float4* r
         }
         g2p_particle<PB, STD, BOX>(P, p, r, L, box);
         store_part_out(P, so, p, r);
+        if (nbin) {  // the fused P2G phase sorts by these (group_sort)
+            uint32_t b16 = 0xFFFFu;
+            if (__float_as_uint(r.z) & kActiveBit) {
+                int b[3];
+                float fx[3];
+                local_base(P.geo, p.x, b, fx);
+                b16 = sort_bin(P, L.my_scene, b);
+            }
+            nbin[g2p_pos(lane, k)] = static_cast<uint16_t>(b16);
+        }
     }
     // inactive particles and holes of the group move to their new slots unchanged
     for (int k = st.cnt; k < kPer; ++k) {
+        if (nbin) nbin[g2p_pos(lane, k)] = 0xFFFFu;
         const uint32_t si = st.slot(k), so = st.slot0 + group_phys(g2p_pos(lane, k));
 #pragma unroll
         for (int q = 0; q < kPlanes; ++q) P.pl_out[q][so] = P.pl[q][si];
@@ -968,10 +999,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_g2p2g(co
     constexpr int kRing = fused_ring<PB, STD>();
     float4* ring = smem + (threadIdx.x >> 5) * (kRing * 32);
     float4* box = BOX ? smem + wpb * (kRing * 32) + (threadIdx.x >> 5) * kBoxCap : nullptr;
+    // per-warp bins of the new positions (kGroup u16): written by the G2P phase, read by the sort
+    uint16_t* nbin = (BOX || !MPMB_FUSED_NBIN)
+                         ? nullptr
+                         : reinterpret_cast<uint16_t*>(smem + wpb * (kRing * 32)) + (threadIdx.x >> 5) * kGroup;
     for (uint32_t g = blockIdx.x * wpb + (threadIdx.x >> 5); g < n_groups; g += gridDim.x * wpb) {
-        g2p_group<PB, STD, BOX>(P, g, ring, lane, box);
-        __syncwarp();  // orders this warp's stores of the group before the P2G loads
-        p2g_group<!PB, STD, true, BOX>(P, g, ring, lane);
+        g2p_group<PB, STD, BOX>(P, g, ring, lane, box, nbin);
+        __syncwarp();  // orders this warp's stores of the group (and nbin) before the P2G phase
+        p2g_group<!PB, STD, true, BOX>(P, g, ring, lane, nbin);
     }
 }
 
@@ -1139,8 +1174,8 @@ void launch_g2p2g(const Params& P, int64_t max_groups, cudaStream_t st, bool sta
     const int blocks = grid_for(max_groups * 32, threads, 148 * 16);
     const bool box = kBoxCap > 0 && max_groups <= kBoxMaxGroups;
     const int ring = (pb || standard) ? fused_ring<true, false>() : fused_ring<false, false>();
-    const int smem = kWarpsPerBlock * ring * 32 * static_cast<int>(sizeof(float4));
-    const int smem_box = smem + kWarpsPerBlock * kBoxCap * static_cast<int>(sizeof(float4));
+    const int smem = kWarpsPerBlock * (ring * 32 * static_cast<int>(sizeof(float4)) + kGroup * 2);  // + nbin
+    const int smem_box = kWarpsPerBlock * (ring * 32 + kBoxCap) * static_cast<int>(sizeof(float4));
     const int smem_max = kWarpsPerBlock * (fused_ring<true, false>() * 32 + kBoxCap) * static_cast<int>(sizeof(float4));
     static std::atomic<uint64_t> attr{0};
     smem_opt_in_once(attr, [&] {

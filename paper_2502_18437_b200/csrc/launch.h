@@ -66,6 +66,19 @@ void launch_migrate_pack(const Params& P, int lo, int hi, float4* out_lo, float4
 void launch_migrate_unpack(const Params& P, const float4* in, uint32_t n, uint32_t first, cudaStream_t st);
 void launch_download_slots(const Params& P, uint32_t* ids, float* x, float* v, uint8_t* active, uint32_t* count,
                            cudaStream_t st);
+// device-resident migration (dd_driver.cpp).  DD control words = b_counts[4..7]:
+// [4] free slot past the groups and the inactive tail, [5] arrivals since binning,
+// [6] error flags, [7] particles on the slab (set at binning, kept by the migrations).
+constexpr uint32_t kDdErrMigrationOverflow = 1u;  // more departures than the buffer capacity
+constexpr uint32_t kDdErrCapacity = 2u;           // arrivals beyond the slab's slots
+constexpr uint32_t kDdErrReach = 4u;              // a stencil left the stored planes / halo window
+constexpr uint32_t kDdErrLeftDomain = 8u;         // a particle left the decomposed grid
+void launch_window_init(int* w, cudaStream_t st);
+void launch_migrate_pack_dev(const Params& P, int lo, int hi, int margin, int4 win, bool has_lo, bool has_hi,
+                             float4* out_lo, float4* out_hi, uint32_t cap, uint32_t* counts, uint32_t* ctl,
+                             cudaStream_t st);
+void launch_migrate_unpack_dev(const Params& P, const float4* in_lo, const float4* in_hi, uint32_t cap,
+                               const uint32_t* counts, uint32_t* bcounts, uint64_t n_cap, cudaStream_t st);
 
 // ---- exact mode (k_exact.cu) ----
 size_t exact_scratch_bytes(int64_t n, int64_t n_bricks);

@@ -22,6 +22,12 @@ and `2 + margin` up, the velocity phase the reverse.  Two transports share that 
                   on torch's current stream, so NCCL orders after the pack kernels.
 * LocalTransport  every slab in one process (one GPU): device-to-device copies between the
                   slabs' buffers.  The host issues each copy; no kernel waits on another.
+
+These Python transports orchestrate the library's per-phase C-ABI (mpmb_dd_*) and are the
+readable restatement of the exchange rule (and its gloo CPU tests).  The production path is
+NativeGroup: the same loop in C++ (csrc/dd_driver.cpp, mpmb_dd_run) with NCCL called from
+the library on its stream, device-side migration counts and no host synchronisation inside
+a run.
 """
 from __future__ import annotations
 
@@ -52,6 +58,7 @@ class SlabDomain:
         self.lib = capi.load_product()
         self.dims, self.dx, self.origin = tuple(int(d) for d in dims), float(dx), tuple(origin)
         self.lo, self.hi, self.margin = int(lo), int(hi), int(margin)
+        self.capacity = int(capacity)
         h = C.c_void_p()
         api.check(self.lib.mpmb_state_create_slab((capi.i3)(*self.dims), float(F32(dx)),
                                                   api._fp(np.array(origin, F32)), self.lo, self.hi, self.margin,
@@ -190,7 +197,8 @@ class SlabDomain:
         return self.lib.mpmb_state_particle_count(self.h)
 
     def download(self):
-        cap = self.particle_count() + 1
+        # the slab holds at most its slots (arrivals may exceed the count set at upload)
+        cap = max(self.particle_count(), self.capacity) + 256 + 1
         ids, x, v = np.zeros(cap, np.uint32), np.zeros((cap, 3), F32), np.zeros((cap, 3), F32)
         a = np.zeros(cap, np.uint8)
         n = C.c_int64()
@@ -231,6 +239,76 @@ def base_x(x: np.ndarray, origin_x: float, dx: float) -> np.ndarray:
     inv = F32(1.0) / F32(dx)
     p = (x.astype(F32) - F32(origin_x)) * inv
     return np.floor(p - F32(0.5)).astype(np.int64)
+
+
+# ------------------------------------------------------------------ native driver
+class NativeGroup:
+    """The library's device-resident DD driver (mpmb_dd_run, csrc/dd_driver.cpp): the whole
+    substep loop -- exchanges, the contact-sum all-reduce, migration with device-side counts
+    -- runs in C++ with no host synchronisation inside a run (one read of the window and
+    error flags per slab at its start).  Local: every slab of this process (one device).
+    NCCL: one slab per rank; `nccl` = (unique_id bytes from nccl_unique_id() on one rank,
+    shared by the caller, nranks, rank)."""
+
+    def __init__(self, domains, nccl=None):
+        self.lib = capi.load_product()
+        self.domains = list(domains)
+        g = C.c_void_p()
+        if nccl is None:
+            arr = (C.c_void_p * len(self.domains))(*[d.h.value for d in self.domains])
+            api.check(self.lib.mpmb_dd_group_create_local(arr, len(self.domains), C.byref(g)), self.lib, "dd_group")
+        else:
+            uid, nranks, rank = nccl
+            (d,) = self.domains
+            buf = (C.c_uint8 * 128)(*bytes(uid))
+            api.check(self.lib.mpmb_dd_group_create_nccl(d.h, buf, int(nranks), int(rank), C.byref(g)), self.lib,
+                      "dd_group_nccl")
+        self.g = g
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        lib = capi.load_product()
+        buf = (C.c_uint8 * 128)()
+        api.check(lib.mpmb_nccl_get_unique_id(buf), lib, "nccl_unique_id")
+        return bytes(buf)
+
+    def run(self, n_sub, dt, gravity, *, contact=True, boundary=0, pushout=False, deactivate=False,
+            free_bodies=False, migrate_every=0, fuse=True):
+        api.check(self.lib.mpmb_dd_run(self.g, int(n_sub), float(F32(dt)), api._fp(np.array(gravity, F32)),
+                                       int(contact), int(boundary), int(pushout), int(deactivate), int(free_bodies),
+                                       int(migrate_every), int(fuse)), self.lib, "dd_run")
+
+    def check(self):
+        """Wait for the queued runs; raise with the reason if a device-side check tripped."""
+        api.check(self.lib.mpmb_dd_check(self.g), self.lib, "dd_check")
+
+    def stats(self) -> dict:
+        s = capi.DDStats()
+        api.check(self.lib.mpmb_dd_get_stats(self.g, C.byref(s)), self.lib, "dd_stats")
+        return {k: getattr(s, k) for k, _ in capi.DDStats._fields_}
+
+    def close(self):
+        if self.g:
+            self.lib.mpmb_dd_group_destroy(self.g)
+            self.g = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def run_native(group, n_sub, dt, gravity, chunk=None, **kw):
+    """n_sub substeps through the native driver in runs of `chunk` substeps (one frame: the
+    halo window is widened by one cell per substep of a run, so runs stay short)."""
+    chunk = chunk or n_sub
+    done = 0
+    while done < n_sub:
+        k = min(chunk, n_sub - done)
+        group.run(k, dt, gravity, **kw)
+        done += k
+    group.check()
 
 
 # ------------------------------------------------------------------ transports

@@ -44,8 +44,12 @@ def _floor():
 @pytest.mark.gpu
 # (3, True, 48): 24 migrations, past the 16 appended-group migrations after which a slab
 # re-bins (Engine::dd_migrate_unpack)
-@pytest.mark.parametrize("k,window,sub", [(2, True, 24), (3, True, 24), (2, False, 24), (3, True, 48)])
-def test_slabs_match_single_domain(k, window, sub):
+@pytest.mark.parametrize("k,window,sub,native", [(2, True, 24, False), (3, True, 24, False), (2, False, 24, False),
+                                                 (3, True, 48, False), (2, True, 24, True), (3, True, 48, True)])
+def test_slabs_match_single_domain(k, window, sub, native):
+    """native: the library's device-resident driver (mpmb_dd_run) in runs of 8 substeps --
+    the same slabs and gates, plus its bookkeeping: one host read per slab and run, fused
+    substeps between migrations."""
     p = _slab_particles()
     n, dt = len(p["x"]), 1e-3
     ref = api.SolverState(DIMS, DX, (0.0, 0.0, 0.0))
@@ -67,6 +71,26 @@ def test_slabs_match_single_domain(k, window, sub):
         sel = np.nonzero(own == r)[0]
         d.set_particles({key: val[sel] for key, val in p.items()}, sel.astype(np.uint32))
         doms.append(d)
+    if native:
+        grp = dd.NativeGroup(doms)
+        dd.run_native(grp, sub, dt, GRAV, chunk=8, contact=True, migrate_every=2)
+        st = grp.stats()
+        assert st["runs"] == sub // 8 and st["substeps"] == sub
+        assert st["host_syncs"] == 2 * k  # only the first two runs drain the stream (pipelined snapshots)
+        assert st["fused"] > 0
+        got = [d.download() for d in doms]
+        ids = np.concatenate([g["ids"] for g in got])
+        assert len(ids) == n and np.array_equal(np.sort(ids), np.arange(n))
+        x = np.zeros((n, 3), F32)
+        v = np.zeros((n, 3), F32)
+        for g in got:
+            x[g["ids"]], v[g["ids"]] = g["x"], g["v"]
+        assert np.abs(x - want["x"]).max() <= 1e-3 * DX
+        assert np.abs(v - want["v"]).max() <= 1e-3 * np.abs(want["v"]).max()
+        moved = sum(int(np.sum(dd.owner_of(dd.base_x(p["x"][g["ids"], 0], 0.0, DX), bounds) != r))
+                    for r, g in enumerate(got))
+        assert moved > 0
+        return
     dd.run_substeps(doms, dd.LocalTransport(), sub, dt, GRAV, contact=True, migrate_every=2, window=window)
     _, _, plane = doms[0].halo_buffers()
     full = (DIMS[1] + (-DIMS[1]) % 4) * (DIMS[2] + (-DIMS[2]) % 4) * 16
@@ -92,7 +116,8 @@ def _free_sphere():
 
 
 @pytest.mark.gpu
-def test_slabs_free_body_match_single_domain():
+@pytest.mark.parametrize("native", [False, True])
+def test_slabs_free_body_match_single_domain(native):
     """A free sphere pressed into the tissue across the cut plane: every slab sums contact
     over its owned nodes, the sums are all-reduced, and every slab integrates the same pose."""
     p = _slab_particles()
@@ -121,7 +146,12 @@ def test_slabs_free_body_match_single_domain():
         sel = np.nonzero(own == r)[0]
         d.set_particles({key: val[sel] for key, val in p.items()}, sel.astype(np.uint32))
         doms.append(d)
-    dd.run_substeps(doms, dd.LocalTransport(), sub, dt, GRAV, contact=True, migrate_every=2, free_bodies=True)
+    if native:
+        grp = dd.NativeGroup(doms)
+        dd.run_native(grp, sub, dt, GRAV, chunk=12, contact=True, migrate_every=2, free_bodies=True)
+        assert grp.stats()["host_syncs"] == 2 * 2
+    else:
+        dd.run_substeps(doms, dd.LocalTransport(), sub, dt, GRAV, contact=True, migrate_every=2, free_bodies=True)
     poses = [d.shape_poses(2)[1] for d in doms]
     for q in poses:  # every slab integrated the same body
         assert np.array_equal(q["position"], poses[0]["position"])

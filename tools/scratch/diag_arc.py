@@ -1,7 +1,7 @@
 """Diagnostic: rotated / spinning arc contact + push-out at the solver level, GPU vs oracle."""
 import sys
 from pathlib import Path
-ROOT = Path(__file__).resolve().parents[1]
+ROOT = Path(__file__).resolve().parents[2]
 sys.path.insert(0, str(ROOT)); sys.path.insert(0, str(ROOT / "tests"))
 import numpy as np
 import backends
