@@ -268,6 +268,20 @@ __device__ __forceinline__ void p2g_nodes_std(const float w[3][3], const float d
         }
 }
 
+// node_position(base + o) - x (state.hpp:49-51) = (o - fx) dx along one axis, from the
+// fractional coordinate fx = (x - origin) / dx - base: three FMA-pipe ops per axis instead of
+// an int-to-float conversion, a multiply-add and a subtract per node.  It differs from the
+// reference's origin + i dx - x by the rounding of fx (a few ulps of dx), inside the
+// single-step gates (tests/test_gpu_parity.py).
+#ifndef MPMB_NODE_REL
+#define MPMB_NODE_REL 1
+#endif
+__device__ __forceinline__ void node_rel(float fx, float dx, float rel[3]) {
+    rel[0] = -fx * dx;
+    rel[1] = rel[0] + dx;
+    rel[2] = rel[1] + dx;
+}
+
 // quadratic B-spline weight derivatives (math.hpp:229-231)
 __device__ __forceinline__ void bspline_dw(float fx, float inv_dx, float dw[3]) {
     dw[0] = (fx - 1.5f) * inv_dx;
@@ -474,9 +488,12 @@ __device__ __forceinline__ void p2g_prepare(const Params& P, const float4 q0, co
         if (STD) {
             bspline_dw(fx[a], S.inv_dx, rel[a]);
         } else {
+            if (MPMB_NODE_REL) {
+                node_rel(fx[a], S.dx, rel[a]);
+            } else {
 #pragma unroll
-            for (int o = 0; o < 3; ++o)  // node_position - x (state.hpp:49-51)
-                rel[a][o] = node_coord(P.geo, a, b[a] + o) - x[a];
+                for (int o = 0; o < 3; ++o) rel[a][o] = node_coord(P.geo, a, b[a] + o) - x[a];
+            }
         }
     }
 }
@@ -766,10 +783,11 @@ __device__ __forceinline__ void g2p_particle(const Params& P, Part& p, float4& r
         bspline_w(fx[a], w[a]);
         if (STD) {
             bspline_dw(fx[a], S.inv_dx, rel[a]);
+        } else if (MPMB_NODE_REL) {
+            node_rel(fx[a], S.dx, rel[a]);
         } else {
 #pragma unroll
-            for (int o = 0; o < 3; ++o)
-                rel[a][o] = node_coord(P.geo, a, b[a] + o) - p.x[a];
+            for (int o = 0; o < 3; ++o) rel[a][o] = node_coord(P.geo, a, b[a] + o) - p.x[a];
         }
     }
     float B[9];  // STD: the velocity gradient L

@@ -261,3 +261,30 @@ def test_product_spawn_matches_oracle():
     for qa, qb in zip(a, b):
         assert np.array_equal(qa[:k], qb[:k])
     assert lib.mpmb_spawn_box(*args, 10, *[api._fp(q) for q in a], C.byref(n)) == capi.BUFFER_TOO_SMALL
+
+
+@pytest.mark.gpu
+def test_native_nccl_single_rank_matches_local():
+    """The NCCL transport of the native driver (libnccl.so.2 loaded at run time, communicator
+    from mpmb_nccl_get_unique_id, capacity agreed by ncclAllReduce) with one rank: the
+    whole-grid slab advances exactly like the same slab in a local group (no neighbours, so
+    both runs are the same kernels on the same data)."""
+    p = _slab_particles()
+    p["v"][:] = (0.3, 0.0, 0.1)
+    n = len(p["x"])
+    ids = np.arange(n, dtype=np.uint32)
+    res = []
+    for kind in ("local", "nccl"):
+        d = dd.SlabDomain(DIMS, DX, (0.0, 0.0, 0.0), 0, DIMS[0], margin=2, capacity=n)
+        d.set_materials(MATS)
+        d.set_shapes([_floor()])
+        d.set_particles(p, ids)
+        g = dd.NativeGroup([d]) if kind == "local" else dd.NativeGroup([d], nccl=(dd.NativeGroup.nccl_unique_id(), 1, 0))
+        dd.run_native(g, 12, 1e-3, GRAV, chunk=4, contact=True, pushout=True, deactivate=True)
+        r = d.download()
+        x = np.zeros((n, 3), F32)
+        x[r["ids"]] = r["x"]
+        res.append(x)
+        st = g.stats()
+        assert st["runs"] == 3 and st["host_syncs"] == 2
+    assert np.abs(res[0] - res[1]).max() <= 1e-4 * DX  # float atomics: order only
