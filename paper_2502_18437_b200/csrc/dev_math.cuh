@@ -161,6 +161,17 @@ __device__ __forceinline__ void neo_hookean(const float F[9], float mu, float la
 // has no such difference, and agrees with the FP64 value to a few float ulps.  Away from
 // F = I (|J - 1| >= 0.5) J is the cofactor determinant of F, clamped at 1e-6 exactly as the
 // reference (materials.hpp:42); tests/test_gpu_stress_kat.py pins both branches.
+// Far from F = I the H-expansion sums O(1) terms of opposite sign (F = 0.01 I: tr H + minors +
+// det H = -2.97 + 2.94 - 0.97), which loses J near the 1e-6 clamp; the cofactor determinant of
+// F itself is exact there (products of the small entries).
+// (by value both ways: the out-of-line call stays in registers)
+static __device__ __noinline__ float3 neo_hookean_far(float f0, float f1, float f2, float f3, float f4, float f5, float f6,
+                                               float f7, float f8) {
+    const float J = fmaf(f0, fmaf(f4, f8, -f5 * f7), fmaf(-f1, fmaf(f3, f8, -f5 * f6), f2 * fmaf(f3, f7, -f4 * f6)));
+    const float Jc = J < 1e-6f ? 1e-6f : J;  // materials.hpp:42
+    return make_float3(J, logf(Jc), 1.f / Jc);
+}
+
 __device__ __forceinline__ float neo_hookean_f32(const float F[9], float mu, float lambda, float s[9]) {
     const float h0 = F[0] - 1.f, h1 = F[1], h2 = F[2];
     const float h3 = F[3], h4 = F[4] - 1.f, h5 = F[5];
@@ -169,19 +180,27 @@ __device__ __forceinline__ float neo_hookean_f32(const float F[9], float mu, flo
     const float dh = h0 * fmaf(h4, h8, -h5 * h7) + h1 * fmaf(h5, h6, -h3 * h8) + h2 * fmaf(h3, h7, -h4 * h6);
     const float j1 = (h0 + h4 + h8) + m2 + dh;
     float J, lnJ, invJ;
-    if (fabsf(j1) < 0.5f) {  // near F = I: J - 1 without cancellation, ln J = log1p(J - 1)
+#ifndef MPMB_STRESS_FAR_OUTLINE
+#define MPMB_STRESS_FAR_OUTLINE 1
+#endif
+    if (__builtin_expect(fabsf(j1) < 0.5f, 1)) {  // near F = I: J - 1 without cancellation
         J = 1.f + j1;
         lnJ = log1pf(j1);
         invJ = 1.f / J;
     } else {
-        // far from I the H-expansion sums O(1) terms of opposite sign (F = 0.01 I: tr H +
-        // minors + det H = -2.97 + 2.94 - 0.97), which loses J near the 1e-6 clamp; the
-        // cofactor determinant of F itself is exact there (products of the small entries)
-        J = fmaf(F[0], fmaf(F[4], F[8], -F[5] * F[7]),
-                 fmaf(-F[1], fmaf(F[3], F[8], -F[5] * F[6]), F[2] * fmaf(F[3], F[7], -F[4] * F[6])));
-        const float Jc = J < 1e-6f ? 1e-6f : J;  // materials.hpp:42
-        lnJ = logf(Jc);
-        invJ = 1.f / Jc;
+        // out of line: the hot loop keeps one branch
+        float3 r;
+        if (MPMB_STRESS_FAR_OUTLINE) {
+            r = neo_hookean_far(F[0], F[1], F[2], F[3], F[4], F[5], F[6], F[7], F[8]);
+        } else {
+            const float Jd = fmaf(F[0], fmaf(F[4], F[8], -F[5] * F[7]),
+                                  fmaf(-F[1], fmaf(F[3], F[8], -F[5] * F[6]), F[2] * fmaf(F[3], F[7], -F[4] * F[6])));
+            const float Jc = Jd < 1e-6f ? 1e-6f : Jd;
+            r = make_float3(Jd, logf(Jc), 1.f / Jc);
+        }
+        J = r.x;
+        lnJ = r.y;
+        invJ = r.z;
     }
     const float d = lambda * lnJ;
     // (b - I)_ij = h_ij + h_ji + sum_k h_ik h_jk

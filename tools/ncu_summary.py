@@ -13,7 +13,15 @@ want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "l1tex__throughput.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
         "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
-        "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "lts__t_requests_op_red.sum"]
+        "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+        # SURVEY.md §8(d) evidence counters (atomics, FP64)
+        "lts__t_requests_op_red.sum", "lts__t_sectors_op_red.sum", "lts__t_requests_op_atom.sum",
+        "lts__t_sectors_op_atom.sum", "l1tex__t_requests_pipe_lsu_mem_global_op_red.sum",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum",
+        "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum", "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum",
+        "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum", "launch__grid_size", "launch__occupancy_limit_registers",
+        "launch__occupancy_limit_shared_mem", "l1tex__t_sector_pipe_lsu_mem_global_op_ld_hit_rate.pct",
+        "lts__t_sector_op_read_hit_rate.pct"]
 for r in rows[2:]:
     name = r[hdr.index("Kernel Name")]
     print("---", name)
