@@ -307,7 +307,9 @@ def run_reference(args, rank):
             "warmup": args.warmup, "ms_per_step": 1e3 * t_total / max(args.steps, 1),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": workload_desc(args.workload, args.replicas, None), "parallelism": "host threads"},
+            "config": {"workload": workload_desc(args.workload, args.replicas, None) +
+                       (f"; timed frames after {pre + 1} untimed pre-roll frames (blade in the tissue)" if pre else ""),
+                       "parallelism": "host threads"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     return line

@@ -204,7 +204,7 @@ __device__ __forceinline__ void p2g_flush(const Params& P, const SceneView& S, c
 // u and 0 through A.
 __device__ __forceinline__ void p2g_nodes(const float w[3][3], const float rel[3][3], const float A[9],
                                           float m, const float v[3], float2 (&pa)[27], float2 (&pb)[27]) {
-    const float2 A01_0 = f2(A[0], A[3]), A2m_0 = f2(A[6], 0.f);
+    const float2 A01_0 = f2(A[0], A[3]);
     const float2 A01_1 = f2(A[1], A[4]), A2m_1 = f2(A[7], 0.f);
     const float2 A01_2 = f2(A[2], A[5]), A2m_2 = f2(A[8], 0.f);
     const float2 mv01 = f2(v[0] * m, v[1] * m), mv2m = f2(v[2] * m, m);
@@ -223,7 +223,9 @@ __device__ __forceinline__ void p2g_nodes(const float w[3][3], const float rel[3
             const float2 U01 = __fmul2_rn(__ffma2_rn(A01_1, f2(ry, ry), uz01), f2(wyz, wyz));
             const float2 U2m = __fmul2_rn(__ffma2_rn(A2m_1, f2(ry, ry), uz2m), f2(wyz, wyz));
             const float2 G01 = __fmul2_rn(A01_0, f2(wyz, wyz));
-            const float2 G2m = __fmul2_rn(A2m_0, f2(wyz, wyz));
+            // the (A[6] wyz, 0) pair would cost two MOVs per row to assemble: its one live
+            // lane is a scalar FMA on mom_z instead
+            const float G2 = A[6] * wyz;
 #pragma unroll
             for (int di = 0; di < 3; ++di) {
                 const int n = (dk * 3 + dj) * 3 + di;
@@ -231,7 +233,7 @@ __device__ __forceinline__ void p2g_nodes(const float w[3][3], const float rel[3
                 pa[n] = __ffma2_rn(f2(wx, wx), U01, pa[n]);
                 pa[n] = __ffma2_rn(f2(wr, wr), G01, pa[n]);
                 pb[n] = __ffma2_rn(f2(wx, wx), U2m, pb[n]);  // .y: mass += w m
-                pb[n] = __ffma2_rn(f2(wr, wr), G2m, pb[n]);
+                pb[n].x = fmaf(wr, G2, pb[n].x);
             }
         }
     }
@@ -243,7 +245,7 @@ __device__ __forceinline__ void p2g_nodes(const float w[3][3], const float rel[3
 // G = M_col0 a; per node: w_x U + dw_x G -- the FFMA2 shape of p2g_nodes.
 __device__ __forceinline__ void p2g_nodes_std(const float w[3][3], const float dw[3][3], const float M[9], float m,
                                               const float v[3], float2 (&pa)[27], float2 (&pb)[27]) {
-    const float2 M0_01 = f2(M[0], M[3]), M0_2m = f2(M[6], 0.f);
+    const float2 M0_01 = f2(M[0], M[3]);
     const float2 M1_01 = f2(M[1], M[4]), M1_2m = f2(M[7], 0.f);
     const float2 M2_01 = f2(M[2], M[5]), M2_2m = f2(M[8], 0.f);
     const float2 mv01 = f2(v[0] * m, v[1] * m), mv2m = f2(v[2] * m, m);
@@ -255,7 +257,7 @@ __device__ __forceinline__ void p2g_nodes_std(const float w[3][3], const float d
             const float2 U01 = __ffma2_rn(M2_01, f2(c, c), __ffma2_rn(M1_01, f2(b, b), __fmul2_rn(mv01, f2(a, a))));
             const float2 U2m = __ffma2_rn(M2_2m, f2(c, c), __ffma2_rn(M1_2m, f2(b, b), __fmul2_rn(mv2m, f2(a, a))));
             const float2 G01 = __fmul2_rn(M0_01, f2(a, a));
-            const float2 G2m = __fmul2_rn(M0_2m, f2(a, a));
+            const float G2 = M[6] * a;  // scalar lane (see p2g_nodes)
 #pragma unroll
             for (int di = 0; di < 3; ++di) {
                 const int n = (dk * 3 + dj) * 3 + di;
@@ -263,7 +265,7 @@ __device__ __forceinline__ void p2g_nodes_std(const float w[3][3], const float d
                 pa[n] = __ffma2_rn(f2(wx, wx), U01, pa[n]);
                 pa[n] = __ffma2_rn(f2(dx, dx), G01, pa[n]);
                 pb[n] = __ffma2_rn(f2(wx, wx), U2m, pb[n]);  // .y: mass += w m
-                pb[n] = __ffma2_rn(f2(dx, dx), G2m, pb[n]);
+                pb[n].x = fmaf(dx, G2, pb[n].x);
             }
         }
 }
@@ -575,9 +577,53 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_p2g(cons
 // stencil bases), so each load instruction touches only a handful of lines.
 // GENERIC: plain (generic-address) loads, the node box may be in shared memory; else
 // read-only global loads
+#ifndef MPMB_G2P_PACK
+#define MPMB_G2P_PACK 0
+#endif
 template <bool GENERIC>
 __device__ __forceinline__ void g2p_gather(const float4* g, uint32_t px, uint32_t pxy, const float w[3][3],
                                            const float rel[3][3], float vn[3], float B[9]) {
+    if (MPMB_G2P_PACK) {  // z components in FFMA2 pairs as well: (a2, b2), (v2, c0_2), (c1_2, c2_2)
+        float2 wxr[3];
+#pragma unroll
+        for (int o = 0; o < 3; ++o) wxr[o] = f2(w[0][o], w[0][o] * rel[0][o]);
+        float2 v01 = f2(0.f, 0.f), vz_c0 = f2(0.f, 0.f), c12_2 = f2(0.f, 0.f);
+        float2 c0_01 = f2(0.f, 0.f), c1_01 = f2(0.f, 0.f), c2_01 = f2(0.f, 0.f);
+#pragma unroll
+        for (int dk = 0; dk < 3; ++dk) {
+            float4 q[9];
+#pragma unroll
+            for (int n = 0; n < 9; ++n) {
+                const float4* a = reinterpret_cast<const float4*>(reinterpret_cast<const char*>(g) +
+                                                                  (dk * pxy + (n / 3) * px) * 16u) + (n % 3);
+                q[n] = GENERIC ? *a : __ldg(a);
+            }
+#pragma unroll
+            for (int dj = 0; dj < 3; ++dj) {
+                float2 a01 = f2(0.f, 0.f), b01 = f2(0.f, 0.f), ab2 = f2(0.f, 0.f);  // ab2 = (a2, b2)
+#pragma unroll
+                for (int di = 0; di < 3; ++di) {
+                    const float4 nq = q[dj * 3 + di];
+                    a01 = __ffma2_rn(f2(wxr[di].x, wxr[di].x), f2(nq.x, nq.y), a01);
+                    b01 = __ffma2_rn(f2(wxr[di].y, wxr[di].y), f2(nq.x, nq.y), b01);
+                    ab2 = __ffma2_rn(wxr[di], f2(nq.z, nq.z), ab2);
+                }
+                const float wyz = w[1][dj] * w[2][dk];
+                const float2 wyz_r = __fmul2_rn(f2(wyz, wyz), f2(rel[1][dj], rel[2][dk]));  // (wy, wz)
+                v01 = __ffma2_rn(f2(wyz, wyz), a01, v01);
+                vz_c0 = __ffma2_rn(f2(wyz, wyz), ab2, vz_c0);
+                c0_01 = __ffma2_rn(f2(wyz, wyz), b01, c0_01);
+                c1_01 = __ffma2_rn(f2(wyz_r.x, wyz_r.x), a01, c1_01);
+                c2_01 = __ffma2_rn(f2(wyz_r.y, wyz_r.y), a01, c2_01);
+                c12_2 = __ffma2_rn(wyz_r, f2(ab2.x, ab2.x), c12_2);
+            }
+        }
+        vn[0] = v01.x; vn[1] = v01.y; vn[2] = vz_c0.x;
+        B[0] = c0_01.x; B[1] = c1_01.x; B[2] = c2_01.x;
+        B[3] = c0_01.y; B[4] = c1_01.y; B[5] = c2_01.y;
+        B[6] = vz_c0.y; B[7] = c12_2.x; B[8] = c12_2.y;
+        return;
+    }
     float wr0[3];
 #pragma unroll
     for (int o = 0; o < 3; ++o) wr0[o] = w[0][o] * rel[0][o];
