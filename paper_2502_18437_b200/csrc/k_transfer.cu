@@ -204,7 +204,7 @@ __device__ __forceinline__ void p2g_flush(const Params& P, const SceneView& S, c
 // u and 0 through A.
 __device__ __forceinline__ void p2g_nodes(const float w[3][3], const float rel[3][3], const float A[9],
                                           float m, const float v[3], float2 (&pa)[27], float2 (&pb)[27]) {
-    const float2 A01_0 = f2(A[0], A[3]);
+    const float2 A01_0 = f2(A[0], A[3]), A2m_0 = f2(A[6], 0.f);
     const float2 A01_1 = f2(A[1], A[4]), A2m_1 = f2(A[7], 0.f);
     const float2 A01_2 = f2(A[2], A[5]), A2m_2 = f2(A[8], 0.f);
     const float2 mv01 = f2(v[0] * m, v[1] * m), mv2m = f2(v[2] * m, m);
@@ -223,9 +223,7 @@ __device__ __forceinline__ void p2g_nodes(const float w[3][3], const float rel[3
             const float2 U01 = __fmul2_rn(__ffma2_rn(A01_1, f2(ry, ry), uz01), f2(wyz, wyz));
             const float2 U2m = __fmul2_rn(__ffma2_rn(A2m_1, f2(ry, ry), uz2m), f2(wyz, wyz));
             const float2 G01 = __fmul2_rn(A01_0, f2(wyz, wyz));
-            // the (A[6] wyz, 0) pair would cost two MOVs per row to assemble: its one live
-            // lane is a scalar FMA on mom_z instead
-            const float G2 = A[6] * wyz;
+            const float2 G2m = __fmul2_rn(A2m_0, f2(wyz, wyz));
 #pragma unroll
             for (int di = 0; di < 3; ++di) {
                 const int n = (dk * 3 + dj) * 3 + di;
@@ -233,7 +231,7 @@ __device__ __forceinline__ void p2g_nodes(const float w[3][3], const float rel[3
                 pa[n] = __ffma2_rn(f2(wx, wx), U01, pa[n]);
                 pa[n] = __ffma2_rn(f2(wr, wr), G01, pa[n]);
                 pb[n] = __ffma2_rn(f2(wx, wx), U2m, pb[n]);  // .y: mass += w m
-                pb[n].x = fmaf(wr, G2, pb[n].x);
+                pb[n] = __ffma2_rn(f2(wr, wr), G2m, pb[n]);
             }
         }
     }
@@ -245,7 +243,7 @@ __device__ __forceinline__ void p2g_nodes(const float w[3][3], const float rel[3
 // G = M_col0 a; per node: w_x U + dw_x G -- the FFMA2 shape of p2g_nodes.
 __device__ __forceinline__ void p2g_nodes_std(const float w[3][3], const float dw[3][3], const float M[9], float m,
                                               const float v[3], float2 (&pa)[27], float2 (&pb)[27]) {
-    const float2 M0_01 = f2(M[0], M[3]);
+    const float2 M0_01 = f2(M[0], M[3]), M0_2m = f2(M[6], 0.f);
     const float2 M1_01 = f2(M[1], M[4]), M1_2m = f2(M[7], 0.f);
     const float2 M2_01 = f2(M[2], M[5]), M2_2m = f2(M[8], 0.f);
     const float2 mv01 = f2(v[0] * m, v[1] * m), mv2m = f2(v[2] * m, m);
@@ -257,7 +255,7 @@ __device__ __forceinline__ void p2g_nodes_std(const float w[3][3], const float d
             const float2 U01 = __ffma2_rn(M2_01, f2(c, c), __ffma2_rn(M1_01, f2(b, b), __fmul2_rn(mv01, f2(a, a))));
             const float2 U2m = __ffma2_rn(M2_2m, f2(c, c), __ffma2_rn(M1_2m, f2(b, b), __fmul2_rn(mv2m, f2(a, a))));
             const float2 G01 = __fmul2_rn(M0_01, f2(a, a));
-            const float G2 = M[6] * a;  // scalar lane (see p2g_nodes)
+            const float2 G2m = __fmul2_rn(M0_2m, f2(a, a));
 #pragma unroll
             for (int di = 0; di < 3; ++di) {
                 const int n = (dk * 3 + dj) * 3 + di;
@@ -265,7 +263,7 @@ __device__ __forceinline__ void p2g_nodes_std(const float w[3][3], const float d
                 pa[n] = __ffma2_rn(f2(wx, wx), U01, pa[n]);
                 pa[n] = __ffma2_rn(f2(dx, dx), G01, pa[n]);
                 pb[n] = __ffma2_rn(f2(wx, wx), U2m, pb[n]);  // .y: mass += w m
-                pb[n].x = fmaf(dx, G2, pb[n].x);
+                pb[n] = __ffma2_rn(f2(dx, dx), G2m, pb[n]);
             }
         }
 }
