@@ -268,16 +268,18 @@ __device__ __forceinline__ void p2g_nodes_std(const float w[3][3], const float d
         }
 }
 
-// node_position(base + o) - x (state.hpp:49-51) = (o - fx) dx along one axis, from the
-// fractional coordinate fx = (x - origin) / dx - base: three FMA-pipe ops per axis instead of
-// an int-to-float conversion, a multiply-add and a subtract per node.  It differs from the
-// reference's origin + i dx - x by the rounding of fx (a few ulps of dx), inside the
-// single-step gates (tests/test_gpu_parity.py).
+// node_position(base + o) - x (state.hpp:49-51) along one axis: the first node exactly as the
+// reference computes it (origin + base dx - x), the next two by adding dx (one rounding of a
+// dx-sized number each) -- one int-to-float conversion per axis instead of one per node.
+// (Deriving all three from the fractional coordinate, (o - fx) dx, is cheaper still but
+// carries fx's rounding, ulp((x - origin) / dx) ~ 4e-6 of a cell at 40 cells: correlated
+// across neighbouring particles, it biased the affine transfer and took C1 to 1e-3 dx from
+// the oracle in 300 substeps, tests/test_gpu_horizon.py.)
 #ifndef MPMB_NODE_REL
 #define MPMB_NODE_REL 1
 #endif
-__device__ __forceinline__ void node_rel(float fx, float dx, float rel[3]) {
-    rel[0] = -fx * dx;
+__device__ __forceinline__ void node_rel(const Geo& G, int a, int b, float x, float dx, float rel[3]) {
+    rel[0] = node_coord(G, a, b) - x;
     rel[1] = rel[0] + dx;
     rel[2] = rel[1] + dx;
 }
@@ -322,29 +324,34 @@ __device__ __forceinline__ uint32_t sort_bin(const Params& P, int scene, const i
     return ((brick & 7u) << 6) | static_cast<uint32_t>(((b[2] & 3) << 4) | ((b[1] & 3) << 2) | (b[0] & 3));
 }
 
-template <bool OUT, bool BOX>
-__device__ __forceinline__ uint64_t group_sort(const Params& P, uint32_t g, uint32_t* bins, uint8_t* order_s,
-                                               uint32_t& n_act, const uint16_t* nbin = nullptr) {
+// KP = sorted positions per lane: 8 (the whole 256-slot group per warp) or 2 (one of its 4
+// 64-position units per warp, `unit` = s of 0..3; small problems: 4x the warps).  A unit's
+// positions [P0, P0 + 32 KP) map to a fixed quarter of the group's slots, so units never
+// exchange particles and their sorts are independent.
+template <bool OUT, bool BOX, int KP = kPer>
+__device__ __forceinline__ uint64_t group_sort(const Params& P, uint32_t g, uint32_t unit, uint32_t* bins,
+                                               uint8_t* order_s, uint32_t& n_act, const uint16_t* nbin = nullptr) {
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const unsigned lt = lanemask_lt();
     const uint32_t slot0 = g * kGroup;
-    uint32_t bin[kPer];
+    const uint32_t p0 = unit * 32u * KP;  // first position of the unit
+    uint32_t bin[KP];
     int lo[3] = {INT_MAX, INT_MAX, INT_MAX}, hi[3] = {INT_MIN, INT_MIN, INT_MIN};
     int sc_lo = INT_MAX, sc_hi = INT_MIN;
     if (!BOX && nbin) {
 #pragma unroll
-        for (int i = 0; i < kPer; ++i) {
+        for (int i = 0; i < KP; ++i) {
             const uint32_t b = nbin[32 * i + lane];
             bin[i] = b == 0xFFFFu ? 0xFFFFFFFFu : b;
         }
     } else {
     // all 16 loads first: one memory latency per group
-    float4 xa4[kPer];
-    uint32_t fl[kPer];
+    float4 xa4[KP];
+    uint32_t fl[KP];
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) {
-        const uint32_t s = slot0 + group_phys(32u * i + lane);
+    for (int i = 0; i < KP; ++i) {
+        const uint32_t s = slot0 + group_phys(p0 + 32u * i + lane);
         if (OUT) {  // written earlier in this kernel by the same warp: coherent L2 loads
             fl[i] = __float_as_uint(__ldcg(&P.pl_out[PR][s].z));
             xa4[i] = __ldcg(&P.pl_out[0][s]);
@@ -354,7 +361,7 @@ __device__ __forceinline__ uint64_t group_sort(const Params& P, uint32_t g, uint
         }
     }
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) {
+    for (int i = 0; i < KP; ++i) {
         bin[i] = 0xFFFFFFFFu;
         const uint32_t flags = fl[i];
         if (flags & kActiveBit) {
@@ -386,14 +393,14 @@ __device__ __forceinline__ uint64_t group_sort(const Params& P, uint32_t g, uint
         }
         const int s0 = __reduce_min_sync(full, sc_lo), s1 = __reduce_max_sync(full, sc_hi);
         bx.w = (s0 == s1) ? s0 : -1;  // empty or several scenes: no box
-        if (lane == 0) P.group_box[g] = bx;
+        if (lane == 0) P.group_box[g * (kPer / KP) + unit] = bx;
     }
     for (int w = lane; w < kBinWords; w += 32) bins[w] = 0u;
     __syncwarp();
-    uint32_t rank[kPer];
+    uint32_t rank[KP];
     uint32_t n_inact = 0;
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) {
+    for (int i = 0; i < KP; ++i) {
         const unsigned peers = __match_any_sync(full, bin[i]);
         const int lead = __ffs(peers) - 1;
         const unsigned inact = __ballot_sync(full, bin[i] == 0xFFFFFFFFu);
@@ -428,12 +435,15 @@ __device__ __forceinline__ uint64_t group_sort(const Params& P, uint32_t g, uint
     }
     __syncwarp();
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) {
+    for (int i = 0; i < KP; ++i) {
         const uint32_t pos = bin[i] != 0xFFFFFFFFu ? bins[bin_word(bin[i])] + rank[i] : n_act + rank[i];
-        order_s[pos] = static_cast<uint8_t>(group_phys(32u * i + lane));
+        order_s[pos] = static_cast<uint8_t>(group_phys(p0 + 32u * i + lane));
     }
     __syncwarp();
-    const uint64_t mine = reinterpret_cast<const uint64_t*>(order_s)[lane];
+    uint64_t mine;
+    if (KP == 8) mine = reinterpret_cast<const uint64_t*>(order_s)[lane];
+    else if (KP == 4) mine = reinterpret_cast<const uint32_t*>(order_s)[lane];
+    else mine = reinterpret_cast<const uint16_t*>(order_s)[lane];
     __syncwarp();  // the caller reuses this shared memory for staging
     return mine;
 }
@@ -489,7 +499,7 @@ __device__ __forceinline__ void p2g_prepare(const Params& P, const float4 q0, co
             bspline_dw(fx[a], S.inv_dx, rel[a]);
         } else {
             if (MPMB_NODE_REL) {
-                node_rel(fx[a], S.dx, rel[a]);
+                node_rel(P.geo, a, b[a], x[a], S.dx, rel[a]);
             } else {
 #pragma unroll
                 for (int o = 0; o < 3; ++o) rel[a][o] = node_coord(P.geo, a, b[a] + o) - x[a];
@@ -503,8 +513,8 @@ __device__ __forceinline__ void p2g_prepare(const Params& P, const float4 q0, co
 // this warp's staging ring (kStages x kPlanes x 32 float4), also the sort scratch.  OUT: the
 // group's particles are in the other buffer (pl_out), written by this warp's G2P of the
 // previous substep inside the fused kernel (k_g2p2g).
-template <bool MLS, bool STD, bool OUT, bool BOX>
-__device__ __forceinline__ void p2g_group(const Params& P, uint32_t g, float4* ring, int lane,
+template <bool MLS, bool STD, bool OUT, bool BOX, int KP = kPer>
+__device__ __forceinline__ void p2g_group(const Params& P, uint32_t g, uint32_t unit, float4* ring, int lane,
                                           const uint16_t* nbin = nullptr) {
     constexpr int NP = kPlanes;
     constexpr int NS = OUT ? kStagesL2 : kStages;
@@ -514,12 +524,19 @@ __device__ __forceinline__ void p2g_group(const Params& P, uint32_t g, float4* r
     uint32_t* bins = reinterpret_cast<uint32_t*>(ring);  // sort scratch aliases the ring
     uint8_t* order_s = reinterpret_cast<uint8_t*>(bins + kBinWords);
     uint32_t n_act;
-    st.order = group_sort<OUT, BOX>(P, g, bins, order_s, n_act, nbin);
+    st.order = group_sort<OUT, BOX, KP>(P, g, unit, bins, order_s, n_act, nbin);
     st.slot0 = g * kGroup;
-    st.cnt = min(max(static_cast<int>(n_act) - kPer * lane, 0), kPer);
-    reinterpret_cast<uint64_t*>(P.order)[static_cast<uint64_t>(g) * 32 + lane] = st.order;
-    if (lane == 0) P.group_nact[g] = n_act;
-    const int kmax = min(static_cast<int>(n_act), kPer);  // lane 0 has the most
+    st.cnt = min(max(static_cast<int>(n_act) - KP * lane, 0), KP);
+    if (KP == 8)
+        reinterpret_cast<uint64_t*>(P.order)[static_cast<uint64_t>(g) * 32 + lane] = st.order;
+    else if (KP == 4)  // the unit's 128 order bytes at [P0, P0 + 128) of the group's 256
+        reinterpret_cast<uint32_t*>(P.order)[static_cast<uint64_t>(g) * 64 + unit * 32 + lane] =
+            static_cast<uint32_t>(st.order);
+    else  // the unit's 64 order bytes at [P0, P0 + 64)
+        reinterpret_cast<uint16_t*>(P.order)[static_cast<uint64_t>(g) * 128 + unit * 32 + lane] =
+            static_cast<uint16_t>(st.order);
+    if (lane == 0) P.group_nact[g * (kPer / KP) + unit] = n_act;
+    const int kmax = min(static_cast<int>(n_act), KP);  // lane 0 has the most
     for (int k = 0; k < NS - 1; ++k) st.issue(P, k);
     float2 pa[27], pb[27];  // (mom_x, mom_y), (mom_z, mass) per stencil node
 #pragma unroll
@@ -553,16 +570,18 @@ __device__ __forceinline__ void p2g_group(const Params& P, uint32_t g, float4* r
 }
 
 // BOX: record each group's stencil-base box for the (box-gathering) G2P that follows
-template <bool MLS, bool STD = false, bool BOX = false>
+// KP: positions per lane (group_sort): one warp per group (8) or per 64-position unit (2)
+template <bool MLS, bool STD = false, bool BOX = false, int KP = kPer>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_p2g(const __grid_constant__ Params P) {
     pdl_enter();
     extern __shared__ float4 smem[];
     const int lane = threadIdx.x & 31;
-    const uint32_t n_groups = *P.n_groups;
+    constexpr uint32_t U = kPer / KP;  // units per group
+    const uint32_t n_units = *P.n_groups * U;
     const uint32_t wpb = blockDim.x >> 5;
     float4* ring = smem + (threadIdx.x >> 5) * (kStages * kPlanes * 32);
-    for (uint32_t g = blockIdx.x * wpb + (threadIdx.x >> 5); g < n_groups; g += gridDim.x * wpb)
-        p2g_group<MLS, STD, false, BOX>(P, g, ring, lane);
+    for (uint32_t u = blockIdx.x * wpb + (threadIdx.x >> 5); u < n_units; u += gridDim.x * wpb)
+        p2g_group<MLS, STD, false, BOX, KP>(P, u / U, u % U, ring, lane);
 }
 
 // ================================================================  G2P
@@ -828,7 +847,7 @@ __device__ __forceinline__ void g2p_particle(const Params& P, Part& p, float4& r
         if (STD) {
             bspline_dw(fx[a], S.inv_dx, rel[a]);
         } else if (MPMB_NODE_REL) {
-            node_rel(fx[a], S.dx, rel[a]);
+            node_rel(P.geo, a, b[a], p.x[a], S.dx, rel[a]);
         } else {
 #pragma unroll
             for (int o = 0; o < 3; ++o) rel[a][o] = node_coord(P.geo, a, b[a] + o) - p.x[a];
@@ -904,21 +923,22 @@ __device__ __forceinline__ void g2p_particle(const Params& P, Part& p, float4& r
 // positions g2p_pos(L, k): the warp's 32 lanes gather around a few neighbouring stencils at
 // every iteration.  Every position is written to the other buffer at slot
 // group_phys(pos): the state leaves G2P in the new order.  `ring`: this warp's staging ring.
-template <bool PB, bool STD, bool BOX>
-__device__ __forceinline__ void g2p_group(const Params& P, uint32_t g, float4* ring, int lane,
+template <bool PB, bool STD, bool BOX, int KP = kPer>
+__device__ __forceinline__ void g2p_group(const Params& P, uint32_t g, uint32_t unit, float4* ring, int lane,
                                           float4* box_s = nullptr, uint16_t* nbin = nullptr) {
     constexpr int NP = (PB || STD) ? 7 : 5;
     constexpr int NS = kG2PStages;
     Stager<NP, NS, MPMB_G2P_CG != 0> st;
     st.buf = ring;
     st.lane = lane;
-    const uint32_t n_act = P.group_nact[g];
+    const uint32_t p0 = unit * 32u * KP;  // the unit's first position (group_sort)
+    const uint32_t n_act = P.group_nact[g * (kPer / KP) + unit];
     st.cnt = 0;
     {
-        const uint8_t* ob = P.order + static_cast<uint64_t>(g) * kGroup;
+        const uint8_t* ob = P.order + static_cast<uint64_t>(g) * kGroup + p0;
         uint64_t o = 0;
 #pragma unroll
-        for (int k = 0; k < kPer; ++k) {
+        for (int k = 0; k < KP; ++k) {
             o |= static_cast<uint64_t>(ob[g2p_pos(lane, k)]) << (8 * k);
             st.cnt += g2p_pos(lane, k) < n_act ? 1 : 0;
         }
@@ -929,7 +949,7 @@ __device__ __forceinline__ void g2p_group(const Params& P, uint32_t g, float4* r
     for (int k = 0; k < NS - 1; ++k) st.issue(P, k);
     NodeBox box{nullptr, {0, 0, 0}};
     if (BOX && box_s) {
-        const int4 gb = P.group_box[g];
+        const int4 gb = P.group_box[g * (kPer / KP) + unit];
         if (gb.w >= 0) {
             const int ox = gb.x & 0xFFFF, oy = gb.y & 0xFFFF, oz = gb.z & 0xFFFF;
             const int nx = (gb.x >> 16) - ox + 3, ny = (gb.y >> 16) - oy + 3, nz = (gb.z >> 16) - oz + 3;
@@ -975,7 +995,7 @@ __device__ __forceinline__ void g2p_group(const Params& P, uint32_t g, float4* r
             stencil_rows(P.geo, bn, base, px, pxy);
             prefetch_stencil_l1(P.grid_vel + sn * P.geo.nodes_per_scene + base, px, pxy);
         }
-        const uint32_t so = st.slot0 + group_phys(g2p_pos(lane, k));
+        const uint32_t so = st.slot0 + group_phys(p0 + g2p_pos(lane, k));
         const float4* src = st.buf + (k % NS) * NP * 32 + lane;
         float4 r = src[(NP - 1) * 32];
         Part p;
@@ -1008,9 +1028,9 @@ __device__ __forceinline__ void g2p_group(const Params& P, uint32_t g, float4* r
         }
     }
     // inactive particles and holes of the group move to their new slots unchanged
-    for (int k = st.cnt; k < kPer; ++k) {
+    for (int k = st.cnt; k < KP; ++k) {
         if (nbin) nbin[g2p_pos(lane, k)] = 0xFFFFu;
-        const uint32_t si = st.slot(k), so = st.slot0 + group_phys(g2p_pos(lane, k));
+        const uint32_t si = st.slot(k), so = st.slot0 + group_phys(p0 + g2p_pos(lane, k));
 #pragma unroll
         for (int q = 0; q < kPlanes; ++q) P.pl_out[q][so] = P.pl[q][si];
     }
@@ -1022,18 +1042,19 @@ __device__ __forceinline__ void g2p_group(const Params& P, uint32_t g, float4* r
     __syncwarp();  // the ring is reused by the next group (or the fused P2G)
 }
 
-template <bool PB, bool STD = false, bool BOX = false>
+template <bool PB, bool STD = false, bool BOX = false, int KP = kPer>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(const __grid_constant__ Params P) {
     pdl_enter();
     extern __shared__ float4 smem[];
     constexpr int NP = (PB || STD) ? 7 : 5;
     const int lane = threadIdx.x & 31;
-    const uint32_t n_groups = *P.n_groups;
+    constexpr uint32_t U = kPer / KP;
+    const uint32_t n_units = *P.n_groups * U;
     const uint32_t wpb = blockDim.x >> 5;
     float4* ring = smem + (threadIdx.x >> 5) * (kG2PStages * NP * 32);
     float4* box = BOX ? smem + wpb * (kG2PStages * NP * 32) + (threadIdx.x >> 5) * kBoxCap : nullptr;
-    for (uint32_t g = blockIdx.x * wpb + (threadIdx.x >> 5); g < n_groups; g += gridDim.x * wpb)
-        g2p_group<PB, STD, BOX>(P, g, ring, lane, box);
+    for (uint32_t u = blockIdx.x * wpb + (threadIdx.x >> 5); u < n_units; u += gridDim.x * wpb)
+        g2p_group<PB, STD, BOX, KP>(P, u / U, u % U, ring, lane, box);
 }
 
 // Fused G2P of substep s + P2G of substep s+1 (MLS / standard MPM inside a frame), one warp
@@ -1047,7 +1068,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(cons
 // into grid_acc (zeroed by the grid update of substep s), so the phases never alias.
 // PB: PB-MPM iterations of one step (solvers.hpp:240-277 then 218-235): G2P of iteration it
 // (no commit) fused with P2G of iteration it+1 (A = m C).
-template <bool STD, bool PB = false, bool BOX = false>
+template <bool STD, bool PB = false, bool BOX = false, int KP = kPer>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_g2p2g(const __grid_constant__ Params P) {
     pdl_enter();
     // the active-brick count of substep s+1 (read by the grid update of s, appended to by
@@ -1056,7 +1077,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_g2p2g(co
     if (blockIdx.x == 0 && threadIdx.x == 0) *P.n_active_bricks = 0u;
     extern __shared__ float4 smem[];
     const int lane = threadIdx.x & 31;
-    const uint32_t n_groups = *P.n_groups;
+    constexpr uint32_t U = kPer / KP;
+    const uint32_t n_units = *P.n_groups * U;
     const uint32_t wpb = blockDim.x >> 5;
     constexpr int kRing = fused_ring<PB, STD>();
     float4* ring = smem + (threadIdx.x >> 5) * (kRing * 32);
@@ -1065,10 +1087,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_g2p2g(co
     uint16_t* nbin = (BOX || !MPMB_FUSED_NBIN)
                          ? nullptr
                          : reinterpret_cast<uint16_t*>(smem + wpb * (kRing * 32)) + (threadIdx.x >> 5) * kGroup;
-    for (uint32_t g = blockIdx.x * wpb + (threadIdx.x >> 5); g < n_groups; g += gridDim.x * wpb) {
-        g2p_group<PB, STD, BOX>(P, g, ring, lane, box, nbin);
+    for (uint32_t u = blockIdx.x * wpb + (threadIdx.x >> 5); u < n_units; u += gridDim.x * wpb) {
+        g2p_group<PB, STD, BOX, KP>(P, u / U, u % U, ring, lane, box, nbin);
         __syncwarp();  // orders this warp's stores of the group (and nbin) before the P2G phase
-        p2g_group<!PB, STD, true, BOX>(P, g, ring, lane, nbin);
+        p2g_group<!PB, STD, true, BOX, KP>(P, u / U, u % U, ring, lane, nbin);
     }
 }
 
@@ -1173,10 +1195,30 @@ static int grid_for(int64_t work, int threads, int max_blocks) {
 // dynamic shared memory per block: warps x stages x planes x 32 lanes x 16 B; kernels above
 // 48 KB opt in once per device (opt_in_smem, kernels.cuh)
 
+// Small problems (at most this many 256-slot groups) give every 64-position unit its own warp
+// (KP = 2: 4x the warps, shorter serial chains; the node box is always on there).  The
+// decision is a function of the engine's group bound, so P2G, G2P and the fused kernel of
+// one engine always agree.  MPMB_SPLIT_MAX_GROUPS (environment) overrides, for A/B.
+#ifndef MPMB_SPLIT_MAX_GROUPS
+#define MPMB_SPLIT_MAX_GROUPS 512  // A/B: C1 (129 groups) +45 %; C2 and C3 (1,024) -17 % / +5 %, M1 (4,101) -23 %
+#endif
+static bool split_units(int64_t max_groups) {
+    static const int64_t lim = [] {
+        const char* e = std::getenv("MPMB_SPLIT_MAX_GROUPS");
+        return e ? std::atoll(e) : static_cast<int64_t>(MPMB_SPLIT_MAX_GROUPS);
+    }();
+    return kBoxCap > 0 && max_groups <= std::min<int64_t>(lim, kBoxMaxGroups);
+}
+#ifndef MPMB_SPLIT_KP
+#define MPMB_SPLIT_KP 2
+#endif
+constexpr int kSplitKP = MPMB_SPLIT_KP;  // positions per lane when split (2 or 4)
+
 void launch_p2g(const Params& P, bool mls, int64_t max_groups, cudaStream_t st, bool standard) {
     const int threads = kWarpsPerBlock * 32;
     const int smem = kWarpsPerBlock * kStages * kPlanes * 32 * static_cast<int>(sizeof(float4));
-    const int blocks = grid_for(max_groups * 32, threads, 148 * 16);
+    const bool split = split_units(max_groups);
+    const int blocks = grid_for(max_groups * (split ? kPer / kSplitKP : 1) * 32, threads, 148 * 16);
     static std::atomic<uint64_t> attr{0};
     smem_opt_in_once(attr, [&] {
         opt_in_smem(k_p2g<true>, smem);
@@ -1185,7 +1227,16 @@ void launch_p2g(const Params& P, bool mls, int64_t max_groups, cudaStream_t st, 
         opt_in_smem(k_p2g<true, false, true>, smem);
         opt_in_smem(k_p2g<false, false, true>, smem);
         opt_in_smem(k_p2g<true, true, true>, smem);
+        opt_in_smem(k_p2g<true, false, true, kSplitKP>, smem);
+        opt_in_smem(k_p2g<false, false, true, kSplitKP>, smem);
+        opt_in_smem(k_p2g<true, true, true, kSplitKP>, smem);
     });
+    if (split) {
+        if (standard) launch_chain(k_p2g<true, true, true, kSplitKP>, blocks, threads, smem, st, P);
+        else if (mls) launch_chain(k_p2g<true, false, true, kSplitKP>, blocks, threads, smem, st, P);
+        else launch_chain(k_p2g<false, false, true, kSplitKP>, blocks, threads, smem, st, P);
+        return;
+    }
     if (kBoxCap > 0 && max_groups <= kBoxMaxGroups) {  // the G2P after it gathers from boxes
         if (standard) launch_chain(k_p2g<true, true, true>, blocks, threads, smem, st, P);
         else if (mls) launch_chain(k_p2g<true, false, true>, blocks, threads, smem, st, P);
@@ -1206,7 +1257,8 @@ void launch_g2p(const Params& P, bool pb, int64_t max_groups, cudaStream_t st, b
         return;
     }
     const int threads = kWarpsPerBlock * 32;
-    const int blocks = grid_for(max_groups * 32, threads, 148 * 16);
+    const bool split = split_units(max_groups);
+    const int blocks = grid_for(max_groups * (split ? kPer / kSplitKP : 1) * 32, threads, 148 * 16);
     const bool box = kBoxCap > 0 && max_groups <= kBoxMaxGroups;
     const int boxb = kWarpsPerBlock * kBoxCap * static_cast<int>(sizeof(float4));
     const int smem7 = kWarpsPerBlock * kG2PStages * 7 * 32 * static_cast<int>(sizeof(float4));
@@ -1219,7 +1271,16 @@ void launch_g2p(const Params& P, bool pb, int64_t max_groups, cudaStream_t st, b
         opt_in_smem(k_g2p<true, false, true>, smem7 + boxb);
         opt_in_smem(k_g2p<false, true, true>, smem7 + boxb);
         opt_in_smem(k_g2p<false, false, true>, smem5 + boxb);
+        opt_in_smem(k_g2p<true, false, true, kSplitKP>, smem7 + boxb);
+        opt_in_smem(k_g2p<false, true, true, kSplitKP>, smem7 + boxb);
+        opt_in_smem(k_g2p<false, false, true, kSplitKP>, smem5 + boxb);
     });
+    if (split) {
+        if (standard) launch_chain(k_g2p<false, true, true, kSplitKP>, blocks, threads, smem7 + boxb, st, P);
+        else if (pb) launch_chain(k_g2p<true, false, true, kSplitKP>, blocks, threads, smem7 + boxb, st, P);
+        else launch_chain(k_g2p<false, false, true, kSplitKP>, blocks, threads, smem5 + boxb, st, P);
+        return;
+    }
     if (box) {
         if (standard) launch_chain(k_g2p<false, true, true>, blocks, threads, smem7 + boxb, st, P);
         else if (pb) launch_chain(k_g2p<true, false, true>, blocks, threads, smem7 + boxb, st, P);
@@ -1233,7 +1294,8 @@ void launch_g2p(const Params& P, bool pb, int64_t max_groups, cudaStream_t st, b
 
 void launch_g2p2g(const Params& P, int64_t max_groups, cudaStream_t st, bool standard, bool pb) {
     const int threads = kWarpsPerBlock * 32;
-    const int blocks = grid_for(max_groups * 32, threads, 148 * 16);
+    const bool split = split_units(max_groups);
+    const int blocks = grid_for(max_groups * (split ? kPer / kSplitKP : 1) * 32, threads, 148 * 16);
     const bool box = kBoxCap > 0 && max_groups <= kBoxMaxGroups;
     const int ring = (pb || standard) ? fused_ring<true, false>() : fused_ring<false, false>();
     const int smem = kWarpsPerBlock * (ring * 32 * static_cast<int>(sizeof(float4)) + kGroup * 2);  // + nbin
@@ -1247,7 +1309,16 @@ void launch_g2p2g(const Params& P, int64_t max_groups, cudaStream_t st, bool sta
         opt_in_smem(k_g2p2g<false, false, true>, smem_max);
         opt_in_smem(k_g2p2g<true, false, true>, smem_max);
         opt_in_smem(k_g2p2g<false, true, true>, smem_max);
+        opt_in_smem(k_g2p2g<false, false, true, kSplitKP>, smem_max);
+        opt_in_smem(k_g2p2g<true, false, true, kSplitKP>, smem_max);
+        opt_in_smem(k_g2p2g<false, true, true, kSplitKP>, smem_max);
     });
+    if (split) {
+        if (pb) launch_chain(k_g2p2g<false, true, true, kSplitKP>, blocks, threads, smem_box, st, P);
+        else if (standard) launch_chain(k_g2p2g<true, false, true, kSplitKP>, blocks, threads, smem_box, st, P);
+        else launch_chain(k_g2p2g<false, false, true, kSplitKP>, blocks, threads, smem_box, st, P);
+        return;
+    }
     if (box) {
         if (pb) launch_chain(k_g2p2g<false, true, true>, blocks, threads, smem_box, st, P);
         else if (standard) launch_chain(k_g2p2g<true, false, true>, blocks, threads, smem_box, st, P);

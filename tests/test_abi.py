@@ -39,7 +39,7 @@ def test_struct_layout_matches_ctypes():
                                                                check=True).stdout.splitlines())
     m = {"mpmb_pose": capi.Pose, "mpmb_keyframe": capi.Keyframe, "mpmb_material": capi.Material,
          "mpmb_shape_desc": capi.ShapeDesc, "mpmb_step_stats": capi.StepStats, "mpmb_scene_config": capi.SceneConfig,
-         "mpmb_frame_summary": capi.FrameSummary, "mpmb_profile": capi.Profile}
+         "mpmb_frame_summary": capi.FrameSummary, "mpmb_profile": capi.Profile, "mpmb_dd_stats": capi.DDStats}
     for cname, ct in m.items():
         assert int(lines[cname]) == C.sizeof(ct), cname
     assert int(lines["mpmb_shape_desc.pose"]) == capi.ShapeDesc.pose.offset
@@ -48,6 +48,8 @@ def test_struct_layout_matches_ctypes():
     assert int(lines["mpmb_frame_summary.total_mass"]) == capi.FrameSummary.total_mass.offset
     assert int(lines["mpmb_frame_summary.deactivated"]) == capi.FrameSummary.deactivated.offset
     assert int(lines["mpmb_scene_config.boundary"]) == capi.SceneConfig.boundary.offset
+    assert int(lines["mpmb_dd_stats.host_waits"]) == capi.DDStats.host_waits.offset
+    assert int(lines["mpmb_dd_stats.rebins"]) == capi.DDStats.rebins.offset
 
 
 def test_checker_libraries_export_solver_layer():
