@@ -1056,7 +1056,14 @@ void run_frame(Batch& b, float dt) {
             fused_in = fuse;
         }
     } else {
-        e.bin();
+        // PB-MPM: one step per frame; positions move only at the commit, so the per-iteration
+        // group sort absorbs the drift and binning follows the same interval as MLS (every 4
+        // frames by default; it cost C3 a fifth of its frame when it ran every step)
+        if (b.since_sort >= resort) {
+            e.bin();
+            b.since_sort = 0;
+        }
+        ++b.since_sort;
         const bool can_fuse = e.fuse_ok();
         bool fused_in = false;  // P2G of this iteration already ran inside the previous kernel
         for (int it = 0; it < cfg.iterations; ++it) {

@@ -268,15 +268,17 @@ __device__ __forceinline__ void p2g_nodes_std(const float w[3][3], const float d
         }
 }
 
-// node_position(base + o) - x (state.hpp:49-51) along one axis: the first node exactly as the
-// reference computes it (origin + base dx - x), the next two by adding dx (one rounding of a
-// dx-sized number each) -- one int-to-float conversion per axis instead of one per node.
-// (Deriving all three from the fractional coordinate, (o - fx) dx, is cheaper still but
-// carries fx's rounding, ulp((x - origin) / dx) ~ 4e-6 of a cell at 40 cells: correlated
-// across neighbouring particles, it biased the affine transfer and took C1 to 1e-3 dx from
-// the oracle in 300 substeps, tests/test_gpu_horizon.py.)
+// node_position(base + o) - x (state.hpp:49-51) along one axis with one int-to-float
+// conversion per axis: the first node as the reference computes it, the next two by adding
+// dx.  NOT used (MPMB_NODE_REL 0, measured): every node must sit where the reference puts
+// it, origin + i dx rounded once per node.  origin + b dx + dx rounds differently (by
+// ~ulp(x)) and the difference is the same for every particle of a cell, so it biases the
+// affine transfer: the blade-engaged C5 replicas moved 3-8x farther from the oracle
+// (x 8.6e-5 vs 2.5e-5 dx, blade impulse 1.6e-5 vs 1.9e-6 in 100 substeps).  Deriving all
+// three from the fractional coordinate, (o - fx) dx, was worse still (C1: 1e-3 dx in 300
+// substeps).  Both were ~1.3 % faster at C5.
 #ifndef MPMB_NODE_REL
-#define MPMB_NODE_REL 1
+#define MPMB_NODE_REL 0
 #endif
 __device__ __forceinline__ void node_rel(const Geo& G, int a, int b, float x, float dx, float rel[3]) {
     rel[0] = node_coord(G, a, b) - x;
