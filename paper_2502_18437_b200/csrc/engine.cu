@@ -297,6 +297,7 @@ struct Engine::Impl {
         P.n_groups = b_counts.as<uint32_t>() + 1;
         P.n_active = b_counts.as<uint32_t>() + 2;
         P.n_total = n_cap;
+        P.total_nodes = total_nodes;
         P.stress_in = stress_in.as<float>();
         P.use_stress_in = use_stress_in ? 1 : 0;
         P.acc_sub = acc_sub.as<double>();

@@ -325,6 +325,7 @@ __global__ void __launch_bounds__(256) k_bin_gather(const Params P, BinBuffers B
             src = B.sorted_src[n_active + static_cast<uint32_t>(d - tail)];
         }
         if (src != kHoleOrig) {
+            MPMB_DCHECK(src < static_cast<uint64_t>(P.n_total));
 #pragma unroll
             for (int p = 0; p < kPlanes; ++p) np[p][d] = P.pl[p][src];
         } else {

@@ -129,6 +129,7 @@ __global__ void __launch_bounds__(256) k_grid_update(const Params P) {
                 cs_hi = P.cull[2 * cs_begin + 1];
             }
         }
+        MPMB_DCHECK(idx < P.total_nodes);
         const bool own = i >= P.geo.own_lo && i < P.geo.own_hi;
         const int ig = i + P.geo.goff;  // global x index (BC, node position)
         P.grid_acc[idx] = make_float4(0.f, 0.f, 0.f, 0.f);

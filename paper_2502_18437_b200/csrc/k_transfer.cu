@@ -144,6 +144,7 @@ struct Stager {
     __device__ __forceinline__ void issue(const Params& P, int k) {
         if (k < cnt) {
             const uint32_t s = slot(k);
+            MPMB_DCHECK(s < static_cast<uint64_t>(P.n_total));
             float4* dst = buf + (k % NS) * NP * 32 + lane;
 #pragma unroll
             for (int q = 0; q < NP; ++q)
@@ -177,6 +178,8 @@ __device__ __forceinline__ void p2g_flush(const Params& P, const SceneView& S, c
     stencil_rows(P.geo, cb, base, px, pxy);
     // one 64-bit stencil pointer; the 9 row offsets are warp-uniform byte counts (uniform
     // datapath), so each row costs one 64-bit add instead of an index-to-address chain
+    MPMB_DCHECK(S.node_base + base + 2ull * (pxy + px) + 2 < P.total_nodes);
+    MPMB_DCHECK(cb[0] >= 0 && cb[1] >= 0 && cb[2] >= 0);
     char* g = reinterpret_cast<char*>(P.grid_acc + S.node_base + base);
     const uint32_t pxb = px * 16u, pxyb = pxy * 16u;
     const float2 zero2 = f2(P.zero, P.zero);
@@ -354,6 +357,7 @@ __device__ __forceinline__ uint64_t group_sort(const Params& P, uint32_t g, uint
 #pragma unroll
     for (int i = 0; i < KP; ++i) {
         const uint32_t s = slot0 + group_phys(p0 + 32u * i + lane);
+        MPMB_DCHECK(s < static_cast<uint64_t>(P.n_total));
         if (OUT) {  // written earlier in this kernel by the same warp: coherent L2 loads
             fl[i] = __float_as_uint(__ldcg(&P.pl_out[PR][s].z));
             xa4[i] = __ldcg(&P.pl_out[0][s]);
@@ -439,6 +443,7 @@ __device__ __forceinline__ uint64_t group_sort(const Params& P, uint32_t g, uint
 #pragma unroll
     for (int i = 0; i < KP; ++i) {
         const uint32_t pos = bin[i] != 0xFFFFFFFFu ? bins[bin_word(bin[i])] + rank[i] : n_act + rank[i];
+        MPMB_DCHECK(pos < 32u * KP && (bin[i] == 0xFFFFFFFFu || bin[i] < static_cast<uint32_t>(kBins)));
         order_s[pos] = static_cast<uint8_t>(group_phys(p0 + 32u * i + lane));
     }
     __syncwarp();
@@ -861,6 +866,7 @@ __device__ __forceinline__ void g2p_particle(const Params& P, Part& p, float4& r
         // loads), else from the global pool
         uint32_t base, px, pxy;
         stencil_rows(P.geo, b, base, px, pxy);
+        MPMB_DCHECK(S.node_base + base + 2ull * (pxy + px) + 2 < P.total_nodes);
         const float4* gp = P.grid_vel + S.node_base + base;
         const int r0 = b[0] - box.o(0), r1 = b[1] - box.o(1), r2 = b[2] - box.o(2);
         if (BOX && box.s && r0 >= 0 && r0 + 3 <= box.n(0) && r1 >= 0 && r1 + 3 <= box.n(1) && r2 >= 0 &&
@@ -998,6 +1004,7 @@ __device__ __forceinline__ void g2p_group(const Params& P, uint32_t g, uint32_t 
             prefetch_stencil_l1(P.grid_vel + sn * P.geo.nodes_per_scene + base, px, pxy);
         }
         const uint32_t so = st.slot0 + group_phys(p0 + g2p_pos(lane, k));
+        MPMB_DCHECK(so < static_cast<uint64_t>(P.n_total) && g2p_pos(lane, k) < 32u * KP);
         const float4* src = st.buf + (k % NS) * NP * 32 + lane;
         float4 r = src[(NP - 1) * 32];
         Part p;
@@ -1033,6 +1040,7 @@ __device__ __forceinline__ void g2p_group(const Params& P, uint32_t g, uint32_t 
     for (int k = st.cnt; k < KP; ++k) {
         if (nbin) nbin[g2p_pos(lane, k)] = 0xFFFFu;
         const uint32_t si = st.slot(k), so = st.slot0 + group_phys(p0 + g2p_pos(lane, k));
+        MPMB_DCHECK(si < static_cast<uint64_t>(P.n_total) && so < static_cast<uint64_t>(P.n_total));
 #pragma unroll
         for (int q = 0; q < kPlanes; ++q) P.pl_out[q][so] = P.pl[q][si];
     }

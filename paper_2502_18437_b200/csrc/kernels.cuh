@@ -78,6 +78,7 @@ struct Params {
     const uint32_t* n_groups;
     const uint32_t* n_active;
     int64_t n_total;          // slots (particles + holes), a fixed bound
+    uint64_t total_nodes;     // grid pool length (bounds checks, MPMB_DEVICE_CHECKS)
     const float* stress_in;  // original-order uploaded sigma (first MLS P2G only)
     int use_stress_in;
     double* acc_sub;   // per shape: impulse[3], torque[3]
@@ -105,6 +106,28 @@ struct Params {
     int deactivate;
     int commit;
 };
+
+// Debug build (-DMPMB_DEVICE_CHECKS=1, tools/device_checks.sh): bounds of every computed slot,
+// node and shared-memory index on the hot path; a violation prints its site and traps, so the
+// launch fails loudly.  compute-sanitizer is not available on the GPU pool; this is the
+// substitute.  Compiled out otherwise.
+#ifndef MPMB_DEVICE_CHECKS
+#define MPMB_DEVICE_CHECKS 0
+#endif
+#if MPMB_DEVICE_CHECKS
+#define MPMB_DCHECK(cond)                                                                          \
+    do {                                                                                           \
+        if (!(cond)) {                                                                             \
+            printf("MPMB_DCHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__,       \
+                   __LINE__, blockIdx.x, threadIdx.x);                                             \
+            __trap();                                                                              \
+        }                                                                                          \
+    } while (0)
+#else
+#define MPMB_DCHECK(cond) \
+    do {                  \
+    } while (0)
+#endif
 
 // Per-scene view of the uniform geometry: scene-dependent offsets are scene x stride.
 struct SceneView {
