@@ -1223,6 +1223,10 @@ static bool split_units(int64_t max_groups) {
 #define MPMB_SPLIT_KP 2
 #endif
 constexpr int kSplitKP = MPMB_SPLIT_KP;  // positions per lane when split (2 or 4)
+// PB-MPM (no stress in P2G, FP64 polar in G2P): 128-position units pay off up to the node-box
+// bound (A/B, C3 at 1,024 groups: +8 %; MLS there: C2 -13 %, M1 -9 %)
+constexpr int kPbSplitKP = 4;
+static bool split_pb(int64_t max_groups) { return kBoxCap > 0 && max_groups <= kBoxMaxGroups; }
 
 void launch_p2g(const Params& P, bool mls, int64_t max_groups, cudaStream_t st, bool standard) {
     const int threads = kWarpsPerBlock * 32;
@@ -1240,7 +1244,13 @@ void launch_p2g(const Params& P, bool mls, int64_t max_groups, cudaStream_t st, 
         opt_in_smem(k_p2g<true, false, true, kSplitKP>, smem);
         opt_in_smem(k_p2g<false, false, true, kSplitKP>, smem);
         opt_in_smem(k_p2g<true, true, true, kSplitKP>, smem);
+        opt_in_smem(k_p2g<false, false, true, kPbSplitKP>, smem);
     });
+    if (!mls && !standard && split_pb(max_groups)) {
+        const int b4 = grid_for(max_groups * (kPer / kPbSplitKP) * 32, threads, 148 * 16);
+        launch_chain(k_p2g<false, false, true, kPbSplitKP>, b4, threads, smem, st, P);
+        return;
+    }
     if (split) {
         if (standard) launch_chain(k_p2g<true, true, true, kSplitKP>, blocks, threads, smem, st, P);
         else if (mls) launch_chain(k_p2g<true, false, true, kSplitKP>, blocks, threads, smem, st, P);
@@ -1284,7 +1294,13 @@ void launch_g2p(const Params& P, bool pb, int64_t max_groups, cudaStream_t st, b
         opt_in_smem(k_g2p<true, false, true, kSplitKP>, smem7 + boxb);
         opt_in_smem(k_g2p<false, true, true, kSplitKP>, smem7 + boxb);
         opt_in_smem(k_g2p<false, false, true, kSplitKP>, smem5 + boxb);
+        opt_in_smem(k_g2p<true, false, true, kPbSplitKP>, smem7 + boxb);
     });
+    if (pb && !standard && split_pb(max_groups)) {
+        const int b4 = grid_for(max_groups * (kPer / kPbSplitKP) * 32, threads, 148 * 16);
+        launch_chain(k_g2p<true, false, true, kPbSplitKP>, b4, threads, smem7 + boxb, st, P);
+        return;
+    }
     if (split) {
         if (standard) launch_chain(k_g2p<false, true, true, kSplitKP>, blocks, threads, smem7 + boxb, st, P);
         else if (pb) launch_chain(k_g2p<true, false, true, kSplitKP>, blocks, threads, smem7 + boxb, st, P);
@@ -1322,7 +1338,13 @@ void launch_g2p2g(const Params& P, int64_t max_groups, cudaStream_t st, bool sta
         opt_in_smem(k_g2p2g<false, false, true, kSplitKP>, smem_max);
         opt_in_smem(k_g2p2g<true, false, true, kSplitKP>, smem_max);
         opt_in_smem(k_g2p2g<false, true, true, kSplitKP>, smem_max);
+        opt_in_smem(k_g2p2g<false, true, true, kPbSplitKP>, smem_max);
     });
+    if (pb && split_pb(max_groups)) {
+        const int b4 = grid_for(max_groups * (kPer / kPbSplitKP) * 32, threads, 148 * 16);
+        launch_chain(k_g2p2g<false, true, true, kPbSplitKP>, b4, threads, smem_box, st, P);
+        return;
+    }
     if (split) {
         if (pb) launch_chain(k_g2p2g<false, true, true, kSplitKP>, blocks, threads, smem_box, st, P);
         else if (standard) launch_chain(k_g2p2g<true, false, true, kSplitKP>, blocks, threads, smem_box, st, P);
