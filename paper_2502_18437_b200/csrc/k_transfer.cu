@@ -71,7 +71,17 @@ constexpr int kBoxCap = MPMB_G2P_BOX ? MPMB_BOX_CAP : 0;
 #ifndef MPMB_BOX_MAX_GROUPS
 #define MPMB_BOX_MAX_GROUPS (4 * 148 * MPMB_P2G_MINB * kWarpsPerBlock)
 #endif
-constexpr int64_t kBoxMaxGroups = MPMB_BOX_MAX_GROUPS;
+constexpr int64_t kBoxMaxGroupsBuild = MPMB_BOX_MAX_GROUPS;
+// the launch-time bound (MPMB_BOX_MAX_GROUPS in the environment overrides it, for A/B; it
+// never exceeds the build's, which sized nothing but is the tuned default)
+static int64_t box_max_groups() {
+    static const int64_t v = [] {
+        const char* e = std::getenv("MPMB_BOX_MAX_GROUPS");
+        return e ? std::min<int64_t>(std::atoll(e), kBoxMaxGroupsBuild) : kBoxMaxGroupsBuild;
+    }();
+    return v;
+}
+#define kBoxMaxGroups box_max_groups()
 #ifndef MPMB_FUSED_NBIN
 #define MPMB_FUSED_NBIN 1  // the fused kernel's sort reads bins its G2P phase left in shared memory
 #endif
