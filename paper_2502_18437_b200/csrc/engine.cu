@@ -498,8 +498,8 @@ void Engine::upload_particles(int64_t n, const float* x, const float* v, const f
     I.g_orig.alloc(4 * N); I.g_src.alloc(4 * N); I.g_cell.alloc(N); I.s_src.alloc(4 * N);
     I.s_orig.alloc(4 * N);
     const size_t n_groups = (N + kGroup - 1) / kGroup;
-    // per group: 256 order bytes; n_act and the node box per 64-position unit (up to 4)
-    I.order.alloc(kGroup * n_groups); I.group_nact.alloc(4 * 4 * n_groups); I.group_box.alloc(16 * 4 * n_groups);
+    // per group: 256 order bytes; n_act and the node box per unit (up to 8 of 32 positions)
+    I.order.alloc(kGroup * n_groups); I.group_nact.alloc(4 * 8 * n_groups); I.group_box.alloc(16 * 8 * n_groups);
     const size_t nbk = static_cast<size_t>(I.total_bricks) + 2;  // + inactive, holes
     I.b_count.alloc(4 * nbk);
     I.b_off.alloc(4 * (nbk + 1));

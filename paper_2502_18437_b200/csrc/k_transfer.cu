@@ -92,7 +92,10 @@ static_assert(kPer == 8, "order bytes are read as one u64 per lane");
 // source line): lanes 8j..8j+7 take positions 64 b + 8 c + a (c = L & 7) that group_phys
 // maps to ONE 128-byte line (8 (4a + b) + c), and the warp's 32 positions lie in a
 // 64-position window of the sorted order (gather locality).  Increasing in k.
+// (KP = 1, 32-position units: position = lane.)
+template <int KP = 8>
 __device__ __forceinline__ uint32_t g2p_pos(int lane, int k) {
+    if (KP == 1) return static_cast<uint32_t>(lane);
     return 64u * (k >> 1) + 8u * (lane & 7) + 4u * (k & 1) + (lane >> 3);
 }
 
@@ -460,7 +463,8 @@ __device__ __forceinline__ uint64_t group_sort(const Params& P, uint32_t g, uint
     uint64_t mine;
     if (KP == 8) mine = reinterpret_cast<const uint64_t*>(order_s)[lane];
     else if (KP == 4) mine = reinterpret_cast<const uint32_t*>(order_s)[lane];
-    else mine = reinterpret_cast<const uint16_t*>(order_s)[lane];
+    else if (KP == 2) mine = reinterpret_cast<const uint16_t*>(order_s)[lane];
+    else mine = order_s[lane];
     __syncwarp();  // the caller reuses this shared memory for staging
     return mine;
 }
@@ -549,9 +553,11 @@ __device__ __forceinline__ void p2g_group(const Params& P, uint32_t g, uint32_t 
     else if (KP == 4)  // the unit's 128 order bytes at [P0, P0 + 128) of the group's 256
         reinterpret_cast<uint32_t*>(P.order)[static_cast<uint64_t>(g) * 64 + unit * 32 + lane] =
             static_cast<uint32_t>(st.order);
-    else  // the unit's 64 order bytes at [P0, P0 + 64)
+    else if (KP == 2)  // the unit's 64 order bytes at [P0, P0 + 64)
         reinterpret_cast<uint16_t*>(P.order)[static_cast<uint64_t>(g) * 128 + unit * 32 + lane] =
             static_cast<uint16_t>(st.order);
+    else  // KP = 1: the unit's 32 order bytes at [P0, P0 + 32)
+        P.order[static_cast<uint64_t>(g) * kGroup + unit * 32 + lane] = static_cast<uint8_t>(st.order);
     if (lane == 0) P.group_nact[g * (kPer / KP) + unit] = n_act;
     const int kmax = min(static_cast<int>(n_act), KP);  // lane 0 has the most
     for (int k = 0; k < NS - 1; ++k) st.issue(P, k);
@@ -957,8 +963,8 @@ __device__ __forceinline__ void g2p_group(const Params& P, uint32_t g, uint32_t 
         uint64_t o = 0;
 #pragma unroll
         for (int k = 0; k < KP; ++k) {
-            o |= static_cast<uint64_t>(ob[g2p_pos(lane, k)]) << (8 * k);
-            st.cnt += g2p_pos(lane, k) < n_act ? 1 : 0;
+            o |= static_cast<uint64_t>(ob[g2p_pos<KP>(lane, k)]) << (8 * k);
+            st.cnt += g2p_pos<KP>(lane, k) < n_act ? 1 : 0;
         }
         st.order = o;
     }
@@ -1013,8 +1019,8 @@ __device__ __forceinline__ void g2p_group(const Params& P, uint32_t g, uint32_t 
             stencil_rows(P.geo, bn, base, px, pxy);
             prefetch_stencil_l1(P.grid_vel + sn * P.geo.nodes_per_scene + base, px, pxy);
         }
-        const uint32_t so = st.slot0 + group_phys(p0 + g2p_pos(lane, k));
-        MPMB_DCHECK(so < static_cast<uint64_t>(P.n_total) && g2p_pos(lane, k) < 32u * KP);
+        const uint32_t so = st.slot0 + group_phys(p0 + g2p_pos<KP>(lane, k));
+        MPMB_DCHECK(so < static_cast<uint64_t>(P.n_total) && g2p_pos<KP>(lane, k) < 32u * KP);
         const float4* src = st.buf + (k % NS) * NP * 32 + lane;
         float4 r = src[(NP - 1) * 32];
         Part p;
@@ -1043,13 +1049,13 @@ __device__ __forceinline__ void g2p_group(const Params& P, uint32_t g, uint32_t 
                 local_base(P.geo, p.x, b, fx);
                 b16 = sort_bin(P, L.my_scene, b);
             }
-            nbin[g2p_pos(lane, k)] = static_cast<uint16_t>(b16);
+            nbin[g2p_pos<KP>(lane, k)] = static_cast<uint16_t>(b16);
         }
     }
     // inactive particles and holes of the group move to their new slots unchanged
     for (int k = st.cnt; k < KP; ++k) {
-        if (nbin) nbin[g2p_pos(lane, k)] = 0xFFFFu;
-        const uint32_t si = st.slot(k), so = st.slot0 + group_phys(p0 + g2p_pos(lane, k));
+        if (nbin) nbin[g2p_pos<KP>(lane, k)] = 0xFFFFu;
+        const uint32_t si = st.slot(k), so = st.slot0 + group_phys(p0 + g2p_pos<KP>(lane, k));
         MPMB_DCHECK(si < static_cast<uint64_t>(P.n_total) && so < static_cast<uint64_t>(P.n_total));
 #pragma unroll
         for (int q = 0; q < kPlanes; ++q) P.pl_out[q][so] = P.pl[q][si];
@@ -1222,6 +1228,19 @@ static int grid_for(int64_t work, int threads, int max_blocks) {
 #ifndef MPMB_SPLIT_MAX_GROUPS
 #define MPMB_SPLIT_MAX_GROUPS 512  // A/B: C1 (129 groups) +45 %; C2 and C3 (1,024) -17 % / +5 %, M1 (4,101) -23 %
 #endif
+// The smallest problems (at most this many groups) go one step further: 32-position units
+// (KP = 1, one particle per lane, 8x the warps).  MPMB_TINY_MAX_GROUPS (environment)
+// overrides, for A/B.
+#ifndef MPMB_TINY_MAX_GROUPS
+#define MPMB_TINY_MAX_GROUPS 0  // A/B at C1 (129 groups): 256 -> -12 % (K8 26.5 vs 23.3 us)
+#endif
+static bool tiny_units(int64_t max_groups) {
+    static const int64_t lim = [] {
+        const char* e = std::getenv("MPMB_TINY_MAX_GROUPS");
+        return e ? std::atoll(e) : static_cast<int64_t>(MPMB_TINY_MAX_GROUPS);
+    }();
+    return kBoxCap > 0 && max_groups <= std::min<int64_t>(lim, kBoxMaxGroups);
+}
 static bool split_units(int64_t max_groups) {
     static const int64_t lim = [] {
         const char* e = std::getenv("MPMB_SPLIT_MAX_GROUPS");
@@ -1255,10 +1274,18 @@ void launch_p2g(const Params& P, bool mls, int64_t max_groups, cudaStream_t st, 
         opt_in_smem(k_p2g<false, false, true, kSplitKP>, smem);
         opt_in_smem(k_p2g<true, true, true, kSplitKP>, smem);
         opt_in_smem(k_p2g<false, false, true, kPbSplitKP>, smem);
+        opt_in_smem(k_p2g<true, false, true, 1>, smem);
+        opt_in_smem(k_p2g<true, true, true, 1>, smem);
     });
     if (!mls && !standard && split_pb(max_groups)) {
         const int b4 = grid_for(max_groups * (kPer / kPbSplitKP) * 32, threads, 148 * 16);
         launch_chain(k_p2g<false, false, true, kPbSplitKP>, b4, threads, smem, st, P);
+        return;
+    }
+    if ((mls || standard) && tiny_units(max_groups)) {
+        const int b1 = grid_for(max_groups * kPer * 32, threads, 148 * 16);
+        if (standard) launch_chain(k_p2g<true, true, true, 1>, b1, threads, smem, st, P);
+        else launch_chain(k_p2g<true, false, true, 1>, b1, threads, smem, st, P);
         return;
     }
     if (split) {
@@ -1305,10 +1332,18 @@ void launch_g2p(const Params& P, bool pb, int64_t max_groups, cudaStream_t st, b
         opt_in_smem(k_g2p<false, true, true, kSplitKP>, smem7 + boxb);
         opt_in_smem(k_g2p<false, false, true, kSplitKP>, smem5 + boxb);
         opt_in_smem(k_g2p<true, false, true, kPbSplitKP>, smem7 + boxb);
+        opt_in_smem(k_g2p<false, true, true, 1>, smem7 + boxb);
+        opt_in_smem(k_g2p<false, false, true, 1>, smem5 + boxb);
     });
     if (pb && !standard && split_pb(max_groups)) {
         const int b4 = grid_for(max_groups * (kPer / kPbSplitKP) * 32, threads, 148 * 16);
         launch_chain(k_g2p<true, false, true, kPbSplitKP>, b4, threads, smem7 + boxb, st, P);
+        return;
+    }
+    if (!pb && tiny_units(max_groups)) {
+        const int b1 = grid_for(max_groups * kPer * 32, threads, 148 * 16);
+        if (standard) launch_chain(k_g2p<false, true, true, 1>, b1, threads, smem7 + boxb, st, P);
+        else launch_chain(k_g2p<false, false, true, 1>, b1, threads, smem5 + boxb, st, P);
         return;
     }
     if (split) {
@@ -1349,10 +1384,18 @@ void launch_g2p2g(const Params& P, int64_t max_groups, cudaStream_t st, bool sta
         opt_in_smem(k_g2p2g<true, false, true, kSplitKP>, smem_max);
         opt_in_smem(k_g2p2g<false, true, true, kSplitKP>, smem_max);
         opt_in_smem(k_g2p2g<false, true, true, kPbSplitKP>, smem_max);
+        opt_in_smem(k_g2p2g<false, false, true, 1>, smem_max);
+        opt_in_smem(k_g2p2g<true, false, true, 1>, smem_max);
     });
     if (pb && split_pb(max_groups)) {
         const int b4 = grid_for(max_groups * (kPer / kPbSplitKP) * 32, threads, 148 * 16);
         launch_chain(k_g2p2g<false, true, true, kPbSplitKP>, b4, threads, smem_box, st, P);
+        return;
+    }
+    if (!pb && tiny_units(max_groups)) {
+        const int b1 = grid_for(max_groups * kPer * 32, threads, 148 * 16);
+        if (standard) launch_chain(k_g2p2g<true, false, true, 1>, b1, threads, smem_box, st, P);
+        else launch_chain(k_g2p2g<false, false, true, 1>, b1, threads, smem_box, st, P);
         return;
     }
     if (split) {
