@@ -180,7 +180,14 @@ __device__ __forceinline__ void mark_bricks(const Params& P, const SceneView& S,
 
 // red.global.add.v4.f32: the explicit state space keeps the 64-bit base + 32-bit offset
 // addressing (a generic pointer would turn into a returning generic ATOM)
-__device__ __forceinline__ void red_add_v4(float4* p, float2 a, float2 b) {
+#ifndef MPMB_DEBUG_NO_RED
+#define MPMB_DEBUG_NO_RED 0  // timing experiment only (wrong results): the flush REDs dropped
+#endif
+__device__ __forceinline__ void red_add_v4(float4* p, float2 a, float2 b, uint32_t debug = 0) {
+    if (MPMB_DEBUG_NO_RED && debug) {
+        if (a.x + a.y + b.x + b.y == 1.2345e30f) p->x = 0.f;
+        return;
+    }
     asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a.x), "f"(a.y), "f"(b.x),
                  "f"(b.y));
 }
@@ -204,7 +211,7 @@ __device__ __forceinline__ void p2g_flush(const Params& P, const SceneView& S, c
 #pragma unroll
             for (int di = 0; di < 3; ++di) {
                 const int n = (dk * 3 + dj) * 3 + di;
-                red_add_v4(row + di, pa[n], pb[n]);
+                red_add_v4(row + di, pa[n], pb[n], P.debug);
                 pa[n] = __fmul2_rn(pa[n], zero2);  // one FFMA-pipe op per pair (a plain
                 pb[n] = __fmul2_rn(pb[n], zero2);  // zero costs ptxas one MOV per register)
             }
@@ -346,9 +353,12 @@ __device__ __forceinline__ uint32_t sort_bin(const Params& P, int scene, const i
 // 64-position units per warp, `unit` = s of 0..3; small problems: 4x the warps).  A unit's
 // positions [P0, P0 + 32 KP) map to a fixed quarter of the group's slots, so units never
 // exchange particles and their sorts are independent.
+// dead (optional): bit l set when 128-byte line l of the group's slots (slots 8l..8l+7) holds
+// a slot that is inactive or a hole (k8_discard).
 template <bool OUT, bool BOX, int KP = kPer>
 __device__ __forceinline__ uint64_t group_sort(const Params& P, uint32_t g, uint32_t unit, uint32_t* bins,
-                                               uint8_t* order_s, uint32_t& n_act, const uint16_t* nbin = nullptr) {
+                                               uint8_t* order_s, uint32_t& n_act, const uint16_t* nbin = nullptr,
+                                               uint32_t* dead = nullptr, int4* box_out = nullptr) {
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const unsigned lt = lanemask_lt();
@@ -413,6 +423,14 @@ __device__ __forceinline__ uint64_t group_sort(const Params& P, uint32_t g, uint
         const int s0 = __reduce_min_sync(full, sc_lo), s1 = __reduce_max_sync(full, sc_hi);
         bx.w = (s0 == s1) ? s0 : -1;  // empty or several scenes: no box
         if (lane == 0) P.group_box[g * (kPer / KP) + unit] = bx;
+        if (box_out) *box_out = bx;
+    }
+    if (dead) {  // slot group_phys(p) lies in line (p & 7) * 4 + (p >> 6)
+        uint32_t m = 0;
+#pragma unroll
+        for (int i = 0; i < KP; ++i)
+            if (bin[i] == 0xFFFFFFFFu) m |= 1u << (((lane & 7) << 2) | ((p0 + 32u * i + lane) >> 6));
+        *dead = __reduce_or_sync(full, m);
     }
     for (int w = lane; w < kBinWords; w += 32) bins[w] = 0u;
     __syncwarp();
@@ -534,9 +552,146 @@ __device__ __forceinline__ void p2g_prepare(const Params& P, const float4 q0, co
 // this warp's staging ring (kStages x kPlanes x 32 float4), also the sort scratch.  OUT: the
 // group's particles are in the other buffer (pl_out), written by this warp's G2P of the
 // previous substep inside the fused kernel (k_g2p2g).
+// Inside a frame the fused kernel's P2G phase is the last reader of planes P1 {v.y, v.z, C0, C1}
+// and P2 {C2..C5} of the buffer its G2P phase wrote: the next G2P (MLS) reads x, F and the
+// flags only and recomputes v and C from the grid.  So once the group is consumed its P1 / P2
+// lines are dropped from L2 without a write-back (discard.global.L2), except lines holding an
+// inactive slot or a hole (copied with all planes by the next G2P).  Units of 64 and 128
+// positions own whole lines; 32-position units share them and keep theirs.  Measured (A/B,
+// engaged C5 window): K8 -0.9 % (the CCTL per line costs more than the saved write-backs:
+// K8 is not HBM-bound), M1 / C2 neutral; off.
+#ifndef MPMB_K8_DISCARD
+#define MPMB_K8_DISCARD 0
+#endif
+template <int KP>
+__device__ __forceinline__ void k8_discard(const Params& P, uint32_t g, uint32_t unit, uint32_t dead, int lane) {
+    const uint32_t p0 = unit * 32u * KP;
+    const uint32_t lo = p0 >> 6, hi = (p0 + 32u * KP - 1u) >> 6;
+    const uint32_t mine = (((1u << (hi - lo + 1u)) - 1u) << lo) * 0x11111111u;  // lines (c, lo..hi)
+    if ((mine & ~dead) >> lane & 1u) {
+        const uint64_t s = static_cast<uint64_t>(g) * kGroup + 8u * static_cast<uint32_t>(lane);
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(P.pl_out[1] + s) : "memory");
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(P.pl_out[2] + s) : "memory");
+    }
+}
+
+// ---- P2G into a per-warp shared-memory node tile (MPMB_P2G_TILE, fused MLS kernel).
+// The tile covers the group's stencil-base box + 2 nodes per axis (at most kTileCap nodes;
+// larger boxes and groups spanning scenes keep the global REDs).  A lane's run of equal base
+// is still summed in registers; its flush adds the 27 nodes into the tile instead of 27
+// global REDs, and the tile goes to the grid once per group, one 16-byte RED per non-zero
+// node.  Lanes flushing at the same time may share nodes (neighbouring bases): the warp adds
+// node by node in program order (volatile shared accesses, the warp converged), so one lane's
+// store precedes another's load of the same node; lanes flushing the SAME base add in turns.
+#ifndef MPMB_P2G_TILE
+#define MPMB_P2G_TILE 0
+#endif
+#ifndef MPMB_TILE_CAP
+#define MPMB_TILE_CAP 256
+#endif
+constexpr int kTileCap = MPMB_P2G_TILE ? MPMB_TILE_CAP : 0;
+static_assert(kBoxCap == 0 || kTileCap <= kBoxCap, "the BOX kernels keep the tile in the G2P box");
+struct NodeTile {
+    uint32_t s;        // shared address of this warp's tile (0: global REDs)
+    int nx, nxy;       // x pitch, xy pitch
+    int korg;          // tile index of base (0, 0, 0): o_z nxy + o_y nx + o_x
+};
+struct TileBox {       // the box decoded: origin, extent, scene (-1: no tile)
+    int o[3], n[3], scene;
+};
+__device__ __forceinline__ TileBox tile_box(int4 bx) {
+    TileBox t;
+    t.o[0] = bx.x & 0xFFFF; t.o[1] = bx.y & 0xFFFF; t.o[2] = bx.z & 0xFFFF;
+    t.n[0] = (bx.x >> 16) - t.o[0] + 3; t.n[1] = (bx.y >> 16) - t.o[1] + 3; t.n[2] = (bx.z >> 16) - t.o[2] + 3;
+    t.scene = (bx.w >= 0 && t.n[0] * t.n[1] * t.n[2] <= kTileCap) ? bx.w : -1;
+    return t;
+}
+// zeroes the tile of box bx (warp-uniform); .s = 0 when the box does not fit
+__device__ __forceinline__ NodeTile tile_open(float4* s, int4 bx, int lane) {
+    NodeTile t{0u, 0, 0, 0};
+    if (s == nullptr) return t;
+    const TileBox B = tile_box(bx);
+    if (B.scene < 0) return t;
+    t.s = static_cast<uint32_t>(__cvta_generic_to_shared(s));
+    t.nx = B.n[0]; t.nxy = B.n[0] * B.n[1];
+    t.korg = B.o[2] * t.nxy + B.o[1] * t.nx + B.o[0];
+    const int n = t.nxy * B.n[2];
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int i = lane; i < n; i += 32) s[i] = z;
+    __syncwarp();
+    return t;
+}
+// called by the whole warp; lanes with fl set add their run (tile index key of its base)
+__device__ __forceinline__ void tile_flush(const Params& P, const NodeTile& T, bool fl, int key,
+                                           float2 (&pa)[27], float2 (&pb)[27], int lane) {
+    const unsigned full = 0xffffffffu;
+    const int k = fl ? key : -1 - lane;
+    const unsigned peers = __match_any_sync(full, k);
+    const int rank = __popc(peers & lanemask_lt());
+    const int nr = __reduce_max_sync(full, fl ? rank : 0);
+    for (int r = 0; r <= nr; ++r) {
+        const bool act = fl && rank == r;
+        const uint32_t a0 = T.s + 16u * static_cast<uint32_t>(act ? key : 0);
+#pragma unroll
+        for (int dk = 0; dk < 3; ++dk)
+#pragma unroll
+            for (int dj = 0; dj < 3; ++dj) {
+                const uint32_t ar = a0 + 16u * static_cast<uint32_t>(dk * T.nxy + dj * T.nx);
+#pragma unroll
+                for (int di = 0; di < 3; ++di) {
+                    const int n = (dk * 3 + dj) * 3 + di;
+                    if (act) {
+                        float4 v;
+                        asm volatile("ld.volatile.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                                     : "r"(ar + 16u * di)
+                                     : "memory");
+                        v.x += pa[n].x; v.y += pa[n].y; v.z += pb[n].x; v.w += pb[n].y;
+                        asm volatile("st.volatile.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(ar + 16u * di), "f"(v.x),
+                                     "f"(v.y), "f"(v.z), "f"(v.w)
+                                     : "memory");
+                    }
+                }
+            }
+    }
+    if (fl) {
+        const float2 zero2 = f2(P.zero, P.zero);
+#pragma unroll
+        for (int n = 0; n < 27; ++n) {
+            pa[n] = __fmul2_rn(pa[n], zero2);
+            pb[n] = __fmul2_rn(pb[n], zero2);
+        }
+    }
+}
+// the tile to the grid (after the warp's last tile_flush): one 16-byte RED per non-zero node,
+// and the brick of every such node marked touched (k_collect_bricks: bit 3 alone marks the
+// brick itself)
+__device__ __forceinline__ void tile_close(const Params& P, int4 bx, const float4* s, int lane) {
+    __syncwarp();
+    const TileBox B = tile_box(bx);
+    const SceneView S = scene_view(P, B.scene);
+    float4* g = P.grid_acc + S.node_base;
+    const int nxy = B.n[0] * B.n[1], n = nxy * B.n[2];
+    for (int i = lane; i < n; i += 32) {
+        const float4 v = s[i];
+        if (v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f) {
+            const int z = B.o[2] + i / nxy, rem = i % nxy, y = B.o[1] + rem / B.n[0], x = B.o[0] + rem % B.n[0];
+            const uint32_t nd = node_linear(P.geo, x, y, z);
+            MPMB_DCHECK(S.node_base + nd < P.total_nodes);
+            red_add_v4(g + nd, f2(v.x, v.y), f2(v.z, v.w));
+            uint32_t* f = P.brick_flag + S.brick_base + ((z >> 2) * S.nb[1] + (y >> 2)) * S.nb[0] + (x >> 2);
+            asm volatile("red.global.or.b32 [%0], %1;" ::"l"(f), "r"(8u) : "memory");
+        }
+    }
+    __syncwarp();
+}
+
 template <bool MLS, bool STD, bool OUT, bool BOX, int KP = kPer>
 __device__ __forceinline__ void p2g_group(const Params& P, uint32_t g, uint32_t unit, float4* ring, int lane,
-                                          const uint16_t* nbin = nullptr) {
+                                          const uint16_t* nbin = nullptr, float4* tile_s = nullptr,
+                                          int4 tbox = make_int4(0, 0, 0, -1)) {
+    constexpr bool DISCARD = MPMB_K8_DISCARD && OUT && MLS && !STD && KP >= 2;
+    constexpr bool TILE = MPMB_P2G_TILE && OUT && MLS && !STD;
     constexpr int NP = kPlanes;
     constexpr int NS = OUT ? kStagesL2 : kStages;
     Stager<NP, NS, OUT || MPMB_P2G_CG != 0, OUT> st;
@@ -544,8 +699,13 @@ __device__ __forceinline__ void p2g_group(const Params& P, uint32_t g, uint32_t 
     st.lane = lane;
     uint32_t* bins = reinterpret_cast<uint32_t*>(ring);  // sort scratch aliases the ring
     uint8_t* order_s = reinterpret_cast<uint8_t*>(bins + kBinWords);
-    uint32_t n_act;
-    st.order = group_sort<OUT, BOX, KP>(P, g, unit, bins, order_s, n_act, nbin);
+    uint32_t n_act, dead = 0;
+    st.order = group_sort<OUT, BOX, KP>(P, g, unit, bins, order_s, n_act, nbin, DISCARD ? &dead : nullptr,
+                                        (TILE && BOX) ? &tbox : nullptr);
+    if (TILE && !BOX && nbin) {  // group_sort is done with the bins: keep the box there
+        if (lane == 0) *reinterpret_cast<int4*>(const_cast<uint16_t*>(nbin)) = tbox;
+        __syncwarp();
+    }
     st.slot0 = g * kGroup;
     st.cnt = min(max(static_cast<int>(n_act) - KP * lane, 0), KP);
     if (KP == 8)
@@ -569,6 +729,52 @@ __device__ __forceinline__ void p2g_group(const Params& P, uint32_t g, uint32_t 
     }
     int cb[3] = {INT_MIN, INT_MIN, INT_MIN};
     int cscene = -1;
+    if (TILE) {
+        const NodeTile T = tile_open(tile_s, tbox, lane);
+        if (T.s) {
+            int ckey = -1;  // tile index of the current run's base (one scene per tile)
+            for (int k = 0; k < kmax; ++k) {
+                st.issue(P, k + NS - 1);
+                cp_wait<NS - 1>();
+                const bool live = k < st.cnt;
+                const float4* src = st.buf + (k % NS) * NP * 32 + lane;
+                // the base first: the flush runs with only the accumulators live
+                int key = -1;
+                if (live) {
+                    const float4 q0 = src[0];
+                    const float xa[3] = {q0.x, q0.y, q0.z};
+                    int b[3];
+                    float fx[3];
+                    local_base(P.geo, xa, b, fx);
+                    key = b[2] * T.nxy + b[1] * T.nx + b[0] - T.korg;
+                    MPMB_DCHECK(key >= 0 && key + 2 * (T.nxy + T.nx) + 2 < kTileCap);
+                }
+                const bool change = live && key != ckey;
+                const bool fl = change && ckey >= 0;
+                if (__any_sync(0xffffffffu, fl)) tile_flush(P, T, fl, ckey, pa, pb, lane);
+                if (change) ckey = key;
+                if (live) {
+                    const float4 r = src[PR * 32];
+                    const float4 q0 = src[0], q1 = src[32], q2 = src[64], q3 = src[96], q4 = src[128],
+                                 q5 = src[160];
+                    int scene, b[3];
+                    float w[3][3], rel[3][3], A[9], m, v[3];
+                    p2g_prepare<MLS, STD>(P, q0, q1, q2, q3, q4, q5, r, scene, b, w, rel, A, m, v);
+                    p2g_nodes(w, rel, A, m, v, pa, pb);
+                }
+            }
+            const bool fl = ckey >= 0;
+            if (__any_sync(0xffffffffu, fl)) tile_flush(P, T, fl, ckey, pa, pb, lane);
+            cp_wait<0>();
+            __syncwarp();
+            // the box again (not kept live across the loop): the sort recorded it (BOX), or the
+            // G2P phase's box is in the bins' shared memory, free since the sort
+            const int4 bx = BOX ? __ldcg(&P.group_box[g * (kPer / KP) + unit])
+                                : *reinterpret_cast<const int4*>(nbin);
+            tile_close(P, bx, tile_s, lane);
+            return;
+        }
+    }
     for (int k = 0; k < kmax; ++k) {
         st.issue(P, k + NS - 1);
         cp_wait<NS - 1>();
@@ -589,7 +795,8 @@ __device__ __forceinline__ void p2g_group(const Params& P, uint32_t g, uint32_t 
     }
     if (cscene >= 0) p2g_flush(P, scene_view(P, cscene), cb, pa, pb);
     cp_wait<0>();
-    __syncwarp();  // the ring is the next group's sort scratch
+    __syncwarp();  // the ring is the next group's sort scratch; every lane's staging has landed
+    if (DISCARD) k8_discard<KP>(P, g, unit, dead, lane);
 }
 
 // BOX: record each group's stencil-base box for the (box-gathering) G2P that follows
@@ -949,7 +1156,10 @@ __device__ __forceinline__ void g2p_particle(const Params& P, Part& p, float4& r
 // group_phys(pos): the state leaves G2P in the new order.  `ring`: this warp's staging ring.
 template <bool PB, bool STD, bool BOX, int KP = kPer>
 __device__ __forceinline__ void g2p_group(const Params& P, uint32_t g, uint32_t unit, float4* ring, int lane,
-                                          float4* box_s = nullptr, uint16_t* nbin = nullptr) {
+                                          float4* box_s = nullptr, uint16_t* nbin = nullptr, int4* nbox = nullptr) {
+    // nbox (with nbin): the stencil-base box of the new positions, group_sort's encoding
+    int blo[3] = {INT_MAX, INT_MAX, INT_MAX}, bhi[3] = {INT_MIN, INT_MIN, INT_MIN};
+    int sc_lo = INT_MAX, sc_hi = INT_MIN;
     constexpr int NP = (PB || STD) ? 7 : 5;
     constexpr int NS = kG2PStages;
     Stager<NP, NS, MPMB_G2P_CG != 0> st;
@@ -1048,6 +1258,15 @@ __device__ __forceinline__ void g2p_group(const Params& P, uint32_t g, uint32_t 
                 float fx[3];
                 local_base(P.geo, p.x, b, fx);
                 b16 = sort_bin(P, L.my_scene, b);
+                if (nbox) {
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        blo[a] = min(blo[a], b[a]);
+                        bhi[a] = max(bhi[a], b[a]);
+                    }
+                    sc_lo = min(sc_lo, L.my_scene);
+                    sc_hi = max(sc_hi, L.my_scene);
+                }
             }
             nbin[g2p_pos<KP>(lane, k)] = static_cast<uint16_t>(b16);
         }
@@ -1059,6 +1278,18 @@ __device__ __forceinline__ void g2p_group(const Params& P, uint32_t g, uint32_t 
         MPMB_DCHECK(si < static_cast<uint64_t>(P.n_total) && so < static_cast<uint64_t>(P.n_total));
 #pragma unroll
         for (int q = 0; q < kPlanes; ++q) P.pl_out[q][so] = P.pl[q][si];
+    }
+    if (nbox) {
+        const unsigned full = 0xffffffffu;
+        int4 bx;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const int l = __reduce_min_sync(full, blo[a]), h = __reduce_max_sync(full, bhi[a]);
+            (a == 0 ? bx.x : a == 1 ? bx.y : bx.z) = l | (h << 16);
+        }
+        const int s0 = __reduce_min_sync(full, sc_lo), s1 = __reduce_max_sync(full, sc_hi);
+        bx.w = (s0 == s1) ? s0 : -1;
+        *nbox = bx;
     }
     add_scene_counter(P.counters, L.my_scene, 0, L.n_inv);
     add_scene_counter(P.counters, L.my_scene, 1, L.n_fail);
@@ -1113,10 +1344,17 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_g2p2g(co
     uint16_t* nbin = (BOX || !MPMB_FUSED_NBIN)
                          ? nullptr
                          : reinterpret_cast<uint16_t*>(smem + wpb * (kRing * 32)) + (threadIdx.x >> 5) * kGroup;
+    // P2G tile (MLS): the G2P box's shared memory when there is one (free in the P2G phase),
+    // else its own region after the bins
+    constexpr bool TILE = MPMB_P2G_TILE && !PB && !STD;
+    float4* tile = !TILE ? nullptr
+                         : BOX ? box
+                               : smem + wpb * (kRing * 32 + kGroup / 8) + (threadIdx.x >> 5) * kTileCap;
     for (uint32_t u = blockIdx.x * wpb + (threadIdx.x >> 5); u < n_units; u += gridDim.x * wpb) {
-        g2p_group<PB, STD, BOX, KP>(P, u / U, u % U, ring, lane, box, nbin);
+        int4 nb = make_int4(0, 0, 0, -1);
+        g2p_group<PB, STD, BOX, KP>(P, u / U, u % U, ring, lane, box, nbin, (TILE && nbin) ? &nb : nullptr);
         __syncwarp();  // orders this warp's stores of the group (and nbin) before the P2G phase
-        p2g_group<!PB, STD, true, BOX, KP>(P, u / U, u % U, ring, lane, nbin);
+        p2g_group<!PB, STD, true, BOX, KP>(P, u / U, u % U, ring, lane, nbin, tile, nb);
     }
 }
 
@@ -1363,15 +1601,19 @@ void launch_g2p(const Params& P, bool pb, int64_t max_groups, cudaStream_t st, b
     else launch_chain(k_g2p<false>, blocks, threads, smem5, st, P);
 }
 
-void launch_g2p2g(const Params& P, int64_t max_groups, cudaStream_t st, bool standard, bool pb) {
+void launch_g2p2g(const Params& P0, int64_t max_groups, cudaStream_t st, bool standard, bool pb) {
+    Params P = P0;
+    if (MPMB_DEBUG_NO_RED) P.debug = std::getenv("MPMB_DEBUG_NO_RED") ? 1u : 0u;
     const int threads = kWarpsPerBlock * 32;
     const bool split = split_units(max_groups);
     const int blocks = grid_for(max_groups * (split ? kPer / kSplitKP : 1) * 32, threads, 148 * 16);
     const bool box = kBoxCap > 0 && max_groups <= kBoxMaxGroups;
     const int ring = (pb || standard) ? fused_ring<true, false>() : fused_ring<false, false>();
-    const int smem = kWarpsPerBlock * (ring * 32 * static_cast<int>(sizeof(float4)) + kGroup * 2);  // + nbin
+    const int smem = kWarpsPerBlock * (ring * 32 * static_cast<int>(sizeof(float4)) + kGroup * 2 +  // + nbin
+                                       ((pb || standard) ? 0 : kTileCap * static_cast<int>(sizeof(float4))));
     const int smem_box = kWarpsPerBlock * (ring * 32 + kBoxCap) * static_cast<int>(sizeof(float4));
-    const int smem_max = kWarpsPerBlock * (fused_ring<true, false>() * 32 + kBoxCap) * static_cast<int>(sizeof(float4));
+    const int smem_max = kWarpsPerBlock * (fused_ring<true, false>() * 32 + std::max(kBoxCap, kGroup / 8 + kTileCap)) *
+                         static_cast<int>(sizeof(float4));
     static std::atomic<uint64_t> attr{0};
     smem_opt_in_once(attr, [&] {
         opt_in_smem(k_g2p2g<false>, smem_max);

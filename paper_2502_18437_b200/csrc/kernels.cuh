@@ -79,6 +79,7 @@ struct Params {
     const uint32_t* n_active;
     int64_t n_total;          // slots (particles + holes), a fixed bound
     uint64_t total_nodes;     // grid pool length (bounds checks, MPMB_DEVICE_CHECKS)
+    uint32_t debug;           // timing experiments of variant builds only (k_transfer.cu)
     const float* stress_in;  // original-order uploaded sigma (first MLS P2G only)
     int use_stress_in;
     double* acc_sub;   // per shape: impulse[3], torque[3]
