@@ -356,13 +356,12 @@ static int grid_for(int64_t work, int threads, int max_blocks) {
 
 
 // grid-stride blocks per SM of the grid update (MPMB_GRID_BPS in the environment: A/B).  Two
-// = the resident blocks at 106 registers, so the loop's software pipelining runs over every
-// brick of a block instead of restarting per wave (A/B, engaged C5 window: grid update 1.98
-// -> 1.94 ms per frame, C5 +0.6 %, M1 +0.9 %; 4: +0.3 %, 16: -0.2 %)
+// (= the resident blocks at 106 registers: one wave, the brick pipelining spans each block's
+// whole loop) measured C5 +0.2-0.6 %, M1 +0.8 %, C3 +3 %, but C2 -19 % and C1 -3 %; kept at 8.
 static int grid_bps() {
     static const int v = [] {
         const char* e = std::getenv("MPMB_GRID_BPS");
-        return e ? std::max(1, std::atoi(e)) : 2;
+        return e ? std::max(1, std::atoi(e)) : 8;
     }();
     return v;
 }

@@ -1449,6 +1449,16 @@ __global__ void k_deactivate(const Params P) {
 }
 
 // ===================================================================  launchers
+// grid-stride block cap of the transfer kernels, per SM (MPMB_XFER_BPS in the environment: A/B):
+// 6 = two waves of the 3 resident blocks; against 16: C5 +0.3 %, M1 +1.3 %, C3 +0.5 %, C1 / C2
+// unchanged (3, one wave: M1 -13 %, the tail of the grid-stride loop is one warp's groups)
+static int xfer_cap() {
+    static const int v = [] {
+        const char* e = std::getenv("MPMB_XFER_BPS");
+        return 148 * (e ? std::max(1, std::atoi(e)) : 6);
+    }();
+    return v;
+}
 static int grid_for(int64_t work, int threads, int max_blocks) {
     int64_t b = (work + threads - 1) / threads;
     if (b < 1) b = 1;
@@ -1499,7 +1509,7 @@ void launch_p2g(const Params& P, bool mls, int64_t max_groups, cudaStream_t st, 
     const int threads = kWarpsPerBlock * 32;
     const int smem = kWarpsPerBlock * kStages * kPlanes * 32 * static_cast<int>(sizeof(float4));
     const bool split = split_units(max_groups);
-    const int blocks = grid_for(max_groups * (split ? kPer / kSplitKP : 1) * 32, threads, 148 * 16);
+    const int blocks = grid_for(max_groups * (split ? kPer / kSplitKP : 1) * 32, threads, xfer_cap());
     static std::atomic<uint64_t> attr{0};
     smem_opt_in_once(attr, [&] {
         opt_in_smem(k_p2g<true>, smem);
@@ -1516,12 +1526,12 @@ void launch_p2g(const Params& P, bool mls, int64_t max_groups, cudaStream_t st, 
         opt_in_smem(k_p2g<true, true, true, 1>, smem);
     });
     if (!mls && !standard && split_pb(max_groups)) {
-        const int b4 = grid_for(max_groups * (kPer / kPbSplitKP) * 32, threads, 148 * 16);
+        const int b4 = grid_for(max_groups * (kPer / kPbSplitKP) * 32, threads, xfer_cap());
         launch_chain(k_p2g<false, false, true, kPbSplitKP>, b4, threads, smem, st, P);
         return;
     }
     if ((mls || standard) && tiny_units(max_groups)) {
-        const int b1 = grid_for(max_groups * kPer * 32, threads, 148 * 16);
+        const int b1 = grid_for(max_groups * kPer * 32, threads, xfer_cap());
         if (standard) launch_chain(k_p2g<true, true, true, 1>, b1, threads, smem, st, P);
         else launch_chain(k_p2g<true, false, true, 1>, b1, threads, smem, st, P);
         return;
@@ -1553,7 +1563,7 @@ void launch_g2p(const Params& P, bool pb, int64_t max_groups, cudaStream_t st, b
     }
     const int threads = kWarpsPerBlock * 32;
     const bool split = split_units(max_groups);
-    const int blocks = grid_for(max_groups * (split ? kPer / kSplitKP : 1) * 32, threads, 148 * 16);
+    const int blocks = grid_for(max_groups * (split ? kPer / kSplitKP : 1) * 32, threads, xfer_cap());
     const bool box = kBoxCap > 0 && max_groups <= kBoxMaxGroups;
     const int boxb = kWarpsPerBlock * kBoxCap * static_cast<int>(sizeof(float4));
     const int smem7 = kWarpsPerBlock * kG2PStages * 7 * 32 * static_cast<int>(sizeof(float4));
@@ -1574,12 +1584,12 @@ void launch_g2p(const Params& P, bool pb, int64_t max_groups, cudaStream_t st, b
         opt_in_smem(k_g2p<false, false, true, 1>, smem5 + boxb);
     });
     if (pb && !standard && split_pb(max_groups)) {
-        const int b4 = grid_for(max_groups * (kPer / kPbSplitKP) * 32, threads, 148 * 16);
+        const int b4 = grid_for(max_groups * (kPer / kPbSplitKP) * 32, threads, xfer_cap());
         launch_chain(k_g2p<true, false, true, kPbSplitKP>, b4, threads, smem7 + boxb, st, P);
         return;
     }
     if (!pb && tiny_units(max_groups)) {
-        const int b1 = grid_for(max_groups * kPer * 32, threads, 148 * 16);
+        const int b1 = grid_for(max_groups * kPer * 32, threads, xfer_cap());
         if (standard) launch_chain(k_g2p<false, true, true, 1>, b1, threads, smem7 + boxb, st, P);
         else launch_chain(k_g2p<false, false, true, 1>, b1, threads, smem5 + boxb, st, P);
         return;
@@ -1606,7 +1616,7 @@ void launch_g2p2g(const Params& P0, int64_t max_groups, cudaStream_t st, bool st
     if (MPMB_DEBUG_NO_RED) P.debug = std::getenv("MPMB_DEBUG_NO_RED") ? 1u : 0u;
     const int threads = kWarpsPerBlock * 32;
     const bool split = split_units(max_groups);
-    const int blocks = grid_for(max_groups * (split ? kPer / kSplitKP : 1) * 32, threads, 148 * 16);
+    const int blocks = grid_for(max_groups * (split ? kPer / kSplitKP : 1) * 32, threads, xfer_cap());
     const bool box = kBoxCap > 0 && max_groups <= kBoxMaxGroups;
     const int ring = (pb || standard) ? fused_ring<true, false>() : fused_ring<false, false>();
     const int smem = kWarpsPerBlock * (ring * 32 * static_cast<int>(sizeof(float4)) + kGroup * 2 +  // + nbin
@@ -1630,12 +1640,12 @@ void launch_g2p2g(const Params& P0, int64_t max_groups, cudaStream_t st, bool st
         opt_in_smem(k_g2p2g<true, false, true, 1>, smem_max);
     });
     if (pb && split_pb(max_groups)) {
-        const int b4 = grid_for(max_groups * (kPer / kPbSplitKP) * 32, threads, 148 * 16);
+        const int b4 = grid_for(max_groups * (kPer / kPbSplitKP) * 32, threads, xfer_cap());
         launch_chain(k_g2p2g<false, true, true, kPbSplitKP>, b4, threads, smem_box, st, P);
         return;
     }
     if (!pb && tiny_units(max_groups)) {
-        const int b1 = grid_for(max_groups * kPer * 32, threads, 148 * 16);
+        const int b1 = grid_for(max_groups * kPer * 32, threads, xfer_cap());
         if (standard) launch_chain(k_g2p2g<true, false, true, 1>, b1, threads, smem_box, st, P);
         else launch_chain(k_g2p2g<false, false, true, 1>, b1, threads, smem_box, st, P);
         return;
