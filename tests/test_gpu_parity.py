@@ -69,7 +69,10 @@ def test_mls_single_step_grid_and_particles():
         s.step_mls(0.002, (0.0, -9.81, 0.0))
     mo, _, vo = o.grid()
     mg, _, vg = g.grid()
-    assert np.abs(mo - mg).max() <= 1e-6 * mo.max()
+    # node mass: float sums of up to 64 particle terms, the oracle's serial order vs the device's
+    # atomic order: the order difference is bounded by 64 ulp-units of the sum (64 * 2^-24 ~ 3.8e-6
+    # relative); seen up to 1.02e-6
+    assert np.abs(mo - mg).max() <= 4e-6 * mo.max()
     live = mo > 1e-9
     assert np.abs(vo[live] - vg[live]).max() <= 1e-5 * np.abs(vo[live]).max() + 1e-7
     a, b = o.get_particles(), g.get_particles()
@@ -93,7 +96,7 @@ def test_standard_single_step():
             s.step_standard(0.002, (0.0, -9.81, 0.0))
     mo, _, vo = o.grid()
     mg, _, vg = g.grid()
-    assert np.abs(mo - mg).max() <= 1e-6 * mo.max()
+    assert np.abs(mo - mg).max() <= 4e-6 * mo.max()  # summation order, as above
     live = mo > 1e-9
     assert np.abs(vo[live] - vg[live]).max() <= 1e-5 * np.abs(vo[live]).max() + 1e-7
     a, b = o.get_particles(), g.get_particles()
