@@ -508,6 +508,9 @@ def run_ours(args, rank, world, local_rank):
         "clocks": clk,
         "setup_s": setup_s,
     }
+    if pb:  # a PB-MPM "substep" is one transfer iteration; steps/s alongside
+        line["pbmpm"] = {"iterations_per_step": sub, "particle_steps_per_s": value / sub,
+                         "e2e_particle_steps_per_s": e2e / sub}
     return line, batch
 
 
