@@ -968,7 +968,23 @@ void upload(Batch& b) {
 }
 
 // Scene::run_frame (scene.hpp:176-249) for every scene of the batch, enqueued.
-void run_frame(Batch& b, float dt) {
+// export: the frame's last G2P writes the FrameResult (Engine::request_export) -- the last
+// frame of an advance, the one fetch_results reads -- when the caller bound result arrays
+// (mpmb_bind_results: a result every frame); unbound fetches gather after the frame
+void run_frame(Batch& b, float dt, bool last_of_advance = true) {
+    // Where the export pays (A/B of the e2e rate, MPMB_EXPORT=1 vs 0): scene batches (C5,
+    // 512 scenes: +1-2 %) and small frames, where the gather's and totals' launches are a
+    // visible share (C1, 32k particles: +6 %); single mid-size scenes lose the scattered
+    // stores in their short G2P more than the gather costs them overlapped (M1 -1.8 %, C2
+    // -4 %).  MPMB_EXPORT in the environment: 0 never, 2 always.
+    static const int export_mode = [] {
+        const char* e = std::getenv("MPMB_EXPORT");
+        return e ? std::atoi(e) : 1;
+    }();
+    size_t n_all = 0;
+    for (const Scene* s : b.scenes) n_all += s->count();
+    const bool pays = export_mode == 2 || (export_mode == 1 && (b.scenes.size() >= 8 || n_all <= 131072));
+    const bool export_result = pays && last_of_advance && b.bound_n > 0;
     upload(b);
     Engine& e = *b.eng;
     const mpmb_scene_config& cfg = b.scenes[0]->cfg;
@@ -1049,6 +1065,7 @@ void run_frame(Batch& b, float dt) {
             if (fuse) {
                 e.g2p2g(sub, dt_sub, standard, cfg.gravity, any_free);  // + free bodies of sub
             } else {
+                if (export_result && sub + 1 == n_sub) e.request_export();
                 if (standard) e.g2p_standard(sub, dt_sub, true, true);
                 else e.g2p_mls(sub, dt_sub, true, true);
                 if (ns > 0) e.free_bodies(sub, dt_sub, cfg.gravity, any_free, true, sub + 1 < n_sub ? sub + 1 : -1);
@@ -1072,8 +1089,12 @@ void run_frame(Batch& b, float dt) {
             if (it == 0) build_pose_table();
             e.grid_update(0, dt_sub, cfg.gravity, it == 0, true, cfg.boundary);
             fused_in = can_fuse && !last;  // the final G2P commits (solvers.hpp:269-277)
-            if (fused_in) e.g2p2g_pb(dt_sub);
-            else e.g2p_pb(0, dt_sub, last, last, last);
+            if (fused_in) {
+                e.g2p2g_pb(dt_sub);
+            } else {
+                if (export_result && last) e.request_export();
+                e.g2p_pb(0, dt_sub, last, last, last);
+            }
         }
         if (ns > 0) e.free_bodies(0, dt_sub, cfg.gravity, any_free, true);
     }
@@ -1436,7 +1457,7 @@ extern "C" mpmb_status mpmb_advance_frames(mpmb_handle h, float dt, int32_t n_fr
             fail(MPMB_LIFECYCLE_ERROR, "scene belongs to a batch: advance the batch handle");
         if (b->status == Status::advancing)
             fail(MPMB_LIFECYCLE_ERROR, "scene: advance while a frame is pending");
-        for (int f = 0; f < n_frames; ++f) run_frame(*b, dt);
+        for (int f = 0; f < n_frames; ++f) run_frame(*b, dt, f + 1 == n_frames);
         b->status = Status::advancing;
         return MPMB_OK;
     });

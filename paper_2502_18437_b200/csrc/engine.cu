@@ -192,6 +192,9 @@ struct Engine::Impl {
     // the FrameResult gather (K9) runs on copy_st while the next frame's first P2G and grid
     // update read the same particle planes; anything that WRITES planes waits for it first
     bool gather_pending = false;
+    // frame-end export (request_export): requested for the next standalone G2P; valid while
+    // the staging holds the current state's result (cleared by every plane writer)
+    bool export_req = false, export_valid = false;
     void planes_barrier() {
         if (!gather_pending) return;
         check(cudaStreamWaitEvent(st, ev_gather, 0), "wait gather");
@@ -482,6 +485,7 @@ void Engine::upload_particles(int64_t n, const float* x, const float* v, const f
                               const int32_t* material, const uint8_t* active, const int32_t* scene,
                               const uint32_t* ids) {
     Impl& I = *impl_;
+    I.export_valid = false;  // the staged frame result no longer matches the state
     if (n >= 0x7FFFFFFF) throw std::invalid_argument("engine: particle count exceeds 2^31");
     check(cudaStreamSynchronize(I.st), "sync");
     I.n = n;
@@ -699,6 +703,7 @@ std::vector<DevPose> Engine::read_free_poses() {
 // --------------------------------------------------------------- hot path
 void Engine::bin() {
     Impl& I = *impl_;
+    I.export_valid = false;  // the staged frame result no longer matches the state
     if (I.n_cap == 0) return;
     auto ev = I.begin();
     Params P = I.params();
@@ -795,11 +800,40 @@ void Engine::grid_update(int sub, float dt, const float g[3], bool gravity, bool
     I.end(CAT_GRID, ev);
 }
 
+void Engine::request_export() { impl_->export_req = true; }
+
+// Staging and totals for a frame-end export (request_export) into P; false when the launch
+// does not export (no request, exact mode, no particles).
+bool Engine::prepare_export(Params& P) {
+    Impl& I = *impl_;
+    const bool want = I.export_req && !I.exact && I.n > 0;
+    I.export_req = false;
+    I.export_valid = false;
+    if (!want) return false;
+    const size_t N = static_cast<size_t>(I.n);
+    const size_t S = std::max<size_t>(I.hs.size(), 1);
+    if (I.copy_pending && (I.io_x.bytes < 12 * N || I.io_v.bytes < 12 * N || I.io_a.bytes < N))
+        wait_results();  // the staging is about to be reallocated
+    if (I.copy_pending) check(cudaStreamWaitEvent(I.st, I.ev_copy, 0), "wait copy");  // staging reuse
+    I.io_x.alloc(12 * N);
+    I.io_v.alloc(12 * N);
+    I.io_a.alloc(N);
+    I.io_tot.alloc(sizeof(double) * 5 * S);
+    check(cudaMemsetAsync(I.io_tot.p, 0, I.io_tot.bytes, I.st), "memset");
+    P.exp_x = I.io_x.as<float>();
+    P.exp_v = I.io_v.as<float>();
+    P.exp_a = I.io_a.as<uint8_t>();
+    P.exp_tot = I.io_tot.as<double>();
+    P.exp_n = I.n;
+    return true;
+}
+
 void Engine::g2p_mls(int sub, float dt, bool pushout, bool deactivate) {
     Impl& I = *impl_;
     if (I.n_cap == 0) return;
     auto ev = I.begin();
     Params P = I.params();
+    const bool exported = prepare_export(P);
     P.sub = std::min(sub, I.table_subs - 1);
     P.dt = dt;
     P.pushout = pushout ? 1 : 0;
@@ -822,6 +856,7 @@ void Engine::g2p_mls(int sub, float dt, bool pushout, bool deactivate) {
     launch_g2p(P, false, I.max_groups(), I.st, false, I.wide);
     I.counted(1);
     I.cur = 1 - I.cur;  // G2P wrote the group-sorted state into the other buffer
+    I.export_valid = exported;
     I.end(CAT_G2P, ev);
 }
 
@@ -831,6 +866,7 @@ void Engine::g2p_mls(int sub, float dt, bool pushout, bool deactivate) {
 void Engine::g2p2g(int sub, float dt, bool standard, const float g[3], bool integrate, bool collect, bool pushout,
                    bool deactivate) {
     Impl& I = *impl_;
+    I.export_valid = false;  // the staged frame result no longer matches the state
     if (I.n_cap == 0) return;
     auto ev = I.begin();
     Params P = I.params();
@@ -862,6 +898,7 @@ void Engine::g2p2g(int sub, float dt, bool standard, const float g[3], bool inte
 
 void Engine::g2p2g_pb(float dt) {
     Impl& I = *impl_;
+    I.export_valid = false;  // the staged frame result no longer matches the state
     if (I.n_cap == 0) return;
     auto ev = I.begin();
     Params P = I.params();
@@ -902,6 +939,7 @@ void Engine::g2p_standard(int sub, float dt, bool pushout, bool deactivate) {
     if (I.exact) throw std::invalid_argument("engine: exact mode covers the MLS solver");
     auto ev = I.begin();
     Params P = I.params();
+    const bool exported = prepare_export(P);
     P.sub = std::min(sub, I.table_subs - 1);
     P.dt = dt;
     P.pushout = pushout ? 1 : 0;
@@ -910,6 +948,7 @@ void Engine::g2p_standard(int sub, float dt, bool pushout, bool deactivate) {
     launch_g2p(P, false, I.max_groups(), I.st, true, I.wide);
     I.counted(1);
     I.cur = 1 - I.cur;
+    I.export_valid = exported;
     I.end(CAT_G2P, ev);
 }
 
@@ -919,6 +958,8 @@ void Engine::g2p_pb(int sub, float dt, bool commit, bool pushout, bool deactivat
     if (I.exact) throw std::invalid_argument("engine: exact mode covers the MLS solver");
     auto ev = I.begin();
     Params P = I.params();
+    const bool exported = commit && prepare_export(P);
+    if (!commit) I.export_valid = false;
     P.sub = std::min(sub, I.table_subs - 1);
     P.dt = dt;
     P.commit = commit ? 1 : 0;
@@ -927,6 +968,7 @@ void Engine::g2p_pb(int sub, float dt, bool commit, bool pushout, bool deactivat
     launch_g2p(P, true, I.max_groups(), I.st, false, I.wide);
     I.counted(1);
     I.cur = 1 - I.cur;
+    I.export_valid = exported;
     I.end(CAT_G2P, ev);
 }
 
@@ -957,6 +999,7 @@ void Engine::bc_pass(int bc) {
 
 void Engine::materialize_stress() {
     Impl& I = *impl_;
+    I.export_valid = false;  // the staged frame result no longer matches the state
     if (I.n == 0 || I.use_stress_in) return;
     I.stress_in.alloc(36 * static_cast<size_t>(I.n));
     Params P = I.params();
@@ -967,6 +1010,7 @@ void Engine::materialize_stress() {
 
 void Engine::pushout(int sub) {
     Impl& I = *impl_;
+    I.export_valid = false;  // the staged frame result no longer matches the state
     if (I.n == 0 || I.n_shapes == 0) return;
     Params P = I.params();
     P.sub = std::min(sub, I.table_subs - 1);
@@ -976,6 +1020,7 @@ void Engine::pushout(int sub) {
 
 void Engine::deactivate() {
     Impl& I = *impl_;
+    I.export_valid = false;  // the staged frame result no longer matches the state
     if (I.n == 0) return;
     Params P = I.params();
     launch_deactivate(P, I.st);
@@ -1034,6 +1079,30 @@ void Engine::snapshot(float* x, float* v, uint8_t* active, std::vector<double>& 
     Impl& I = *impl_;
     const size_t N = static_cast<size_t>(std::max<int64_t>(I.n, 1));
     const size_t S = I.hs.size();
+    if (async && I.export_valid) {  // the frame's last G2P already wrote the result and the totals
+        I.export_valid = false;
+        if (!I.copy_st) {
+            check(cudaStreamCreateWithFlags(&I.copy_st, cudaStreamNonBlocking), "cudaStreamCreate");
+            check(cudaEventCreateWithFlags(&I.ev_dl, cudaEventDisableTiming), "event");
+            check(cudaEventCreateWithFlags(&I.ev_copy, cudaEventDisableTiming), "event");
+            check(cudaEventCreateWithFlags(&I.ev_gather, cudaEventDisableTiming), "event");
+        }
+        I.io_tot_h.alloc(sizeof(double) * 5 * std::max<size_t>(S, 1));
+        check(cudaMemcpyAsync(I.io_tot_h.p, I.io_tot.p, sizeof(double) * 5 * S, cudaMemcpyDeviceToHost, I.st),
+              "d2h");
+        check(cudaEventRecord(I.ev_dl, I.st), "event");
+        check(cudaStreamWaitEvent(I.copy_st, I.ev_dl, 0), "wait download");
+        if (x) check(cudaMemcpyAsync(x, I.io_x.p, 12 * I.n, cudaMemcpyDeviceToHost, I.copy_st), "d2h");
+        if (v) check(cudaMemcpyAsync(v, I.io_v.p, 12 * I.n, cudaMemcpyDeviceToHost, I.copy_st), "d2h");
+        if (active) check(cudaMemcpyAsync(active, I.io_a.p, I.n, cudaMemcpyDeviceToHost, I.copy_st), "d2h");
+        check(cudaEventRecord(I.ev_copy, I.copy_st), "event");
+        I.copy_pending = true;
+        check(cudaStreamSynchronize(I.st), "snapshot");
+        const double* th = static_cast<const double*>(I.io_tot_h.p);
+        totals.assign(th, th + 5 * S);
+        return;
+    }
+    I.export_valid = false;
     if (I.copy_pending && (I.io_x.bytes < 12 * N || I.io_v.bytes < 12 * N || I.io_a.bytes < N))
         wait_results();  // the staging is about to be reallocated
     if (I.copy_pending) check(cudaStreamWaitEvent(I.st, I.ev_copy, 0), "wait copy");  // staging reuse
@@ -1358,6 +1427,7 @@ void Engine::dd_migrate_buffers(void** send_lo, void** send_hi, void** recv_lo, 
 
 void Engine::dd_migrate_pack(int64_t* n_lo, int64_t* n_hi) {
     Impl& I = *impl_;
+    I.export_valid = false;  // the staged frame result no longer matches the state
     void* d[4];
     int64_t cap;
     dd_migrate_buffers(&d[0], &d[1], &d[2], &d[3], &cap);
@@ -1379,6 +1449,7 @@ void Engine::dd_migrate_pack(int64_t* n_lo, int64_t* n_hi) {
 
 void Engine::dd_migrate_unpack(int64_t n_from_lo, int64_t n_from_hi) {
     Impl& I = *impl_;
+    I.export_valid = false;  // the staged frame result no longer matches the state
     if (n_from_lo > I.mig_cap || n_from_hi > I.mig_cap) throw std::invalid_argument("engine: migration count");
     const int64_t arrivals = n_from_lo + n_from_hi;
     if (arrivals == 0 && I.binned) {
@@ -1547,6 +1618,7 @@ void Engine::dd_migration_buffers(void** send_lo, void** send_hi, void** recv_lo
 
 void Engine::dd_migrate_pack_async(bool has_lo, bool has_hi) {
     Impl& I = *impl_;
+    I.export_valid = false;  // the staged frame result no longer matches the state
     void* d[4];
     uint32_t* cnt;
     int64_t cap;
@@ -1564,6 +1636,7 @@ void Engine::dd_migrate_pack_async(bool has_lo, bool has_hi) {
 
 void Engine::dd_migrate_unpack_async() {
     Impl& I = *impl_;
+    I.export_valid = false;  // the staged frame result no longer matches the state
     if (I.n_cap == 0) return;
     Params P = I.params();
     launch_migrate_unpack_dev(P, I.mig[2].as<float4>(), I.mig[3].as<float4>(), static_cast<uint32_t>(I.mig_cap),

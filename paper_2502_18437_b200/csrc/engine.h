@@ -139,6 +139,10 @@ class Engine {
     void snapshot(float* x, float* v, uint8_t* active, std::vector<double>& totals /*5 per scene*/,
                   bool async = false);
     void wait_results();
+    // The next standalone G2P (the frame's last) exports the frame result as it writes the
+    // state: x / v / active in original order into the snapshot staging and the per-scene
+    // totals; the next async snapshot then only copies them (no gather, no totals pass).
+    void request_export();
     // page-locked host memory (cudaMallocHost) freed with the last reference: D2H of a
     // FrameResult straight into it runs at link speed, with no staging copies
     static std::shared_ptr<void> pinned_host(size_t bytes);
@@ -227,6 +231,7 @@ class Engine {
   private:
     struct Impl;
     Impl* impl_;
+    bool prepare_export(struct Params& P);  // request_export: staging + totals into P
     std::vector<SceneGrid> scenes_;
     int64_t n_total_ = 0;
     int n_shapes_ = 0;

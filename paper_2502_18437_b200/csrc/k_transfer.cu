@@ -1017,6 +1017,103 @@ __device__ __forceinline__ int pushout_particle(const Params& P, const SceneView
     return pushed;
 }
 
+// ---- frame-end export (Params::exp_x; scene.hpp:251-266).  The frame's last G2P has every
+// particle's final x, v and flags in registers: it writes them to the result staging at the
+// particle's original index and sums the per-scene totals, so the fetch needs no inverse
+// permutation, gather or totals pass over the state.  Totals: each lane sums its particles of
+// one scene in FP64 in shared memory (6 rows x 32 lanes per warp: 5 sums + the scene), the
+// warp adds them with one FP64 atomic per value per group (per lane when lanes hold different
+// scenes) -- the sums of k_totals, in another order.
+constexpr int kExportBytesPerWarp = 6 * 32 * 8;
+__device__ __forceinline__ void export_write(const Params& P, const float x[3], const float v[3], float4 r) {
+    const uint32_t o = __float_as_uint(r.w);
+    if (o == kHoleOrig || static_cast<int64_t>(o) >= P.exp_n) return;
+    float* ox = P.exp_x + 3ull * o;
+    float* ov = P.exp_v + 3ull * o;
+    ox[0] = x[0]; ox[1] = x[1]; ox[2] = x[2];
+    ov[0] = v[0]; ov[1] = v[1]; ov[2] = v[2];
+    P.exp_a[o] = (__float_as_uint(r.z) & kActiveBit) ? 1 : 0;
+}
+__device__ __forceinline__ void tot_flush_lane(const Params& P, double* T, int lane) {
+    int* tag = reinterpret_cast<int*>(T + 5 * 32);
+    const int sc = tag[lane];
+    if (sc < 0) return;
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+        atomicAdd(&P.exp_tot[5 * sc + q], T[q * 32 + lane]);
+        T[q * 32 + lane] = 0.0;
+    }
+    tag[lane] = -1;
+}
+__device__ __forceinline__ void tot_init(double* T, int lane) {
+#pragma unroll
+    for (int q = 0; q < 5; ++q) T[q * 32 + lane] = 0.0;
+    reinterpret_cast<int*>(T + 5 * 32)[lane] = -1;
+}
+// an active particle's contribution (k_totals' expressions)
+__device__ __forceinline__ void tot_add(const Params& P, double* T, int lane, int scene, float mass, const float v[3]) {
+    int* tag = reinterpret_cast<int*>(T + 5 * 32);
+    if (tag[lane] != scene) {
+        tot_flush_lane(P, T, lane);
+        tag[lane] = scene;
+    }
+    const double m = mass;
+    const float vx = v[0], vy = v[1], vz = v[2];
+    T[lane] += m;
+    T[32 + lane] += m * vx;
+    T[64 + lane] += m * vy;
+    T[96 + lane] += m * vz;
+    T[128 + lane] += 0.5 * m * static_cast<double>(vx * vx + vy * vy + vz * vz);
+}
+// the whole warp: when every lane holding sums holds the same scene, the sums move to lane 0
+// (which adds them to the next group's, or flushes them when the scene changes); otherwise
+// each lane flushes its own
+__device__ __forceinline__ void tot_fold_warp(const Params& P, double* T, int lane) {
+    const unsigned full = 0xffffffffu;
+    int* tag = reinterpret_cast<int*>(T + 5 * 32);
+    const int sc = tag[lane];
+    const int top = __reduce_max_sync(full, sc);
+    if (top >= 0 && __all_sync(full, sc < 0 || sc == top)) {
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            double t = T[q * 32 + lane];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(full, t, o);
+            T[q * 32 + lane] = lane == 0 ? t : 0.0;
+        }
+        tag[lane] = lane == 0 ? top : -1;
+    } else if (top >= 0) {
+        tot_flush_lane(P, T, lane);
+    }
+    __syncwarp();
+}
+// kernel end (the whole block): every warp folds, then one thread adds the warps' sums, one
+// FP64 atomic per value per scene per block (same-address atomics serialise in L2: one per
+// warp cost C2's export 39 us)
+__device__ __forceinline__ void tot_flush_block(const Params& P, double* T0, double* T, int lane) {
+    tot_fold_warp(P, T, lane);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int nw = static_cast<int>(blockDim.x >> 5);
+        int cur = -1;
+        double acc[5] = {0, 0, 0, 0, 0};
+        for (int w = 0; w < nw; ++w) {
+            const double* Tw = T0 + w * (kExportBytesPerWarp / 8);
+            const int sc = reinterpret_cast<const int*>(Tw + 5 * 32)[0];
+            if (sc < 0) continue;
+            if (sc != cur) {
+                if (cur >= 0)
+                    for (int q = 0; q < 5; ++q) atomicAdd(&P.exp_tot[5 * cur + q], acc[q]);
+                cur = sc;
+                for (int q = 0; q < 5; ++q) acc[q] = 0.0;
+            }
+            for (int q = 0; q < 5; ++q) acc[q] += Tw[q * 32];
+        }
+        if (cur >= 0)
+            for (int q = 0; q < 5; ++q) atomicAdd(&P.exp_tot[5 * cur + q], acc[q]);
+    }
+}
+
 __device__ __forceinline__ void store_part_out(const Params& P, uint32_t s, const Part& p, float4 r) {
     P.pl_out[0][s] = make_float4(p.x[0], p.x[1], p.x[2], p.v[0]);
     P.pl_out[1][s] = make_float4(p.v[1], p.v[2], p.C[0], p.C[1]);
@@ -1156,7 +1253,8 @@ __device__ __forceinline__ void g2p_particle(const Params& P, Part& p, float4& r
 // group_phys(pos): the state leaves G2P in the new order.  `ring`: this warp's staging ring.
 template <bool PB, bool STD, bool BOX, int KP = kPer>
 __device__ __forceinline__ void g2p_group(const Params& P, uint32_t g, uint32_t unit, float4* ring, int lane,
-                                          float4* box_s = nullptr, uint16_t* nbin = nullptr, int4* nbox = nullptr) {
+                                          float4* box_s = nullptr, uint16_t* nbin = nullptr, int4* nbox = nullptr,
+                                          double* tot = nullptr) {
     // nbox (with nbin): the stencil-base box of the new positions, group_sort's encoding
     int blo[3] = {INT_MAX, INT_MAX, INT_MAX}, bhi[3] = {INT_MIN, INT_MIN, INT_MIN};
     int sc_lo = INT_MAX, sc_hi = INT_MIN;
@@ -1251,6 +1349,10 @@ __device__ __forceinline__ void g2p_group(const Params& P, uint32_t g, uint32_t 
         }
         g2p_particle<PB, STD, BOX>(P, p, r, L, box);
         store_part_out(P, so, p, r);
+        if (tot) {  // frame-end export (the standalone G2P only)
+            export_write(P, p.x, p.v, r);
+            if (__float_as_uint(r.z) & kActiveBit) tot_add(P, tot, lane, L.my_scene, r.x, p.v);
+        }
         if (nbin) {  // the fused P2G phase sorts by these (group_sort)
             uint32_t b16 = 0xFFFFu;
             if (__float_as_uint(r.z) & kActiveBit) {
@@ -1276,9 +1378,17 @@ __device__ __forceinline__ void g2p_group(const Params& P, uint32_t g, uint32_t 
         if (nbin) nbin[g2p_pos<KP>(lane, k)] = 0xFFFFu;
         const uint32_t si = st.slot(k), so = st.slot0 + group_phys(p0 + g2p_pos<KP>(lane, k));
         MPMB_DCHECK(si < static_cast<uint64_t>(P.n_total) && so < static_cast<uint64_t>(P.n_total));
+        float4 q[kPlanes];
 #pragma unroll
-        for (int q = 0; q < kPlanes; ++q) P.pl_out[q][so] = P.pl[q][si];
+        for (int j = 0; j < kPlanes; ++j) q[j] = P.pl[j][si];
+#pragma unroll
+        for (int j = 0; j < kPlanes; ++j) P.pl_out[j][so] = q[j];
+        if (tot) {
+            const float x[3] = {q[0].x, q[0].y, q[0].z}, v[3] = {q[0].w, q[1].x, q[1].y};
+            export_write(P, x, v, q[PR]);
+        }
     }
+    if (tot) tot_fold_warp(P, tot, lane);
     if (nbox) {
         const unsigned full = 0xffffffffu;
         int4 bx;
@@ -1310,8 +1420,17 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(cons
     const uint32_t wpb = blockDim.x >> 5;
     float4* ring = smem + (threadIdx.x >> 5) * (kG2PStages * NP * 32);
     float4* box = BOX ? smem + wpb * (kG2PStages * NP * 32) + (threadIdx.x >> 5) * kBoxCap : nullptr;
+    // frame-end export: per-warp totals rows after the rings and boxes (launch_g2p sizes them)
+    double* tot = nullptr;
+    if (P.exp_x) {
+        tot = reinterpret_cast<double*>(smem + wpb * (kG2PStages * NP * 32 + (BOX ? kBoxCap : 0))) +
+              (threadIdx.x >> 5) * (kExportBytesPerWarp / 8);
+        tot_init(tot, lane);
+        __syncwarp();
+    }
     for (uint32_t u = blockIdx.x * wpb + (threadIdx.x >> 5); u < n_units; u += gridDim.x * wpb)
-        g2p_group<PB, STD, BOX, KP>(P, u / U, u % U, ring, lane, box);
+        g2p_group<PB, STD, BOX, KP>(P, u / U, u % U, ring, lane, box, nullptr, nullptr, tot);
+    if (tot) tot_flush_block(P, tot - (threadIdx.x >> 5) * (kExportBytesPerWarp / 8), tot, lane);
 }
 
 // Fused G2P of substep s + P2G of substep s+1 (MLS / standard MPM inside a frame), one warp
@@ -1366,6 +1485,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_g2p2g(co
 template <bool PB, bool STD = false>
 __global__ void __launch_bounds__(128) k_g2p_wide(const __grid_constant__ Params P) {
     pdl_enter();
+    extern __shared__ float4 smem[];
+    const int lane = threadIdx.x & 31;
+    double* tot = nullptr;  // frame-end export (launch_g2p gives it the rows)
+    if (P.exp_x) {
+        tot = reinterpret_cast<double*>(smem) + (threadIdx.x >> 5) * (kExportBytesPerWarp / 8);
+        tot_init(tot, lane);
+        __syncwarp();
+    }
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < P.n_total; base += stride) {
         const int64_t s = base + threadIdx.x;  // the warp stays converged for the counters
@@ -1373,8 +1500,15 @@ __global__ void __launch_bounds__(128) k_g2p_wide(const __grid_constant__ Params
         if (s < P.n_total) {
             float4 r = P.pl[PR][s];
             if (__float_as_uint(r.w) == kHoleOrig || !(__float_as_uint(r.z) & kActiveBit)) {
+                float4 q[kPlanes];
 #pragma unroll
-                for (int q = 0; q < kPlanes; ++q) P.pl_out[q][s] = P.pl[q][s];
+                for (int j = 0; j < kPlanes; ++j) q[j] = P.pl[j][s];
+#pragma unroll
+                for (int j = 0; j < kPlanes; ++j) P.pl_out[j][s] = q[j];
+                if (tot) {
+                    const float x[3] = {q[0].x, q[0].y, q[0].z}, v[3] = {q[0].w, q[1].x, q[1].y};
+                    export_write(P, x, v, q[PR]);
+                }
             } else {
                 Part p;
                 const float4 q0 = P.pl[0][s], q3 = P.pl[3][s], q4 = P.pl[4][s], q5 = P.pl[5][s];
@@ -1388,6 +1522,10 @@ __global__ void __launch_bounds__(128) k_g2p_wide(const __grid_constant__ Params
                 }
                 g2p_particle<PB, STD>(P, p, r, L);
                 store_part_out(P, static_cast<uint32_t>(s), p, r);
+                if (tot) {
+                    export_write(P, p.x, p.v, r);
+                    if (__float_as_uint(r.z) & kActiveBit) tot_add(P, tot, lane, L.my_scene, r.x, p.v);
+                }
             }
         }
         add_scene_counter(P.counters, L.my_scene, 0, L.n_inv);
@@ -1395,6 +1533,7 @@ __global__ void __launch_bounds__(128) k_g2p_wide(const __grid_constant__ Params
         add_scene_counter(P.counters, L.my_scene, 2, L.n_push);
         add_scene_counter(P.counters, L.my_scene, 3, L.n_deact);
     }
+    if (tot) tot_flush_block(P, tot - (threadIdx.x >> 5) * (kExportBytesPerWarp / 8), tot, lane);
 }
 
 // ================================================  standalone push-out / deactivation
@@ -1554,11 +1693,14 @@ void launch_p2g(const Params& P, bool mls, int64_t max_groups, cudaStream_t st, 
 }
 
 void launch_g2p(const Params& P, bool pb, int64_t max_groups, cudaStream_t st, bool standard, bool wide) {
+    // frame-end export (P.exp_x): the totals rows after the rings and boxes
+    const int ex = P.exp_x ? kWarpsPerBlock * kExportBytesPerWarp : 0;
     if (wide) {
         const int b = grid_for(P.n_total, 128, 148 * 16);
-        if (standard) launch_chain(k_g2p_wide<false, true>, b, 128, 0, st, P);
-        else if (pb) launch_chain(k_g2p_wide<true>, b, 128, 0, st, P);
-        else launch_chain(k_g2p_wide<false>, b, 128, 0, st, P);
+        const int exw = P.exp_x ? 4 * kExportBytesPerWarp : 0;
+        if (standard) launch_chain(k_g2p_wide<false, true>, b, 128, exw, st, P);
+        else if (pb) launch_chain(k_g2p_wide<true>, b, 128, exw, st, P);
+        else launch_chain(k_g2p_wide<false>, b, 128, exw, st, P);
         return;
     }
     const int threads = kWarpsPerBlock * 32;
@@ -1566,22 +1708,26 @@ void launch_g2p(const Params& P, bool pb, int64_t max_groups, cudaStream_t st, b
     const int blocks = grid_for(max_groups * (split ? kPer / kSplitKP : 1) * 32, threads, xfer_cap());
     const bool box = kBoxCap > 0 && max_groups <= kBoxMaxGroups;
     const int boxb = kWarpsPerBlock * kBoxCap * static_cast<int>(sizeof(float4));
-    const int smem7 = kWarpsPerBlock * kG2PStages * 7 * 32 * static_cast<int>(sizeof(float4));
-    const int smem5 = kWarpsPerBlock * kG2PStages * 5 * 32 * static_cast<int>(sizeof(float4));
+    const int smem7 = kWarpsPerBlock * kG2PStages * 7 * 32 * static_cast<int>(sizeof(float4)) + ex;
+    const int smem5 = kWarpsPerBlock * kG2PStages * 5 * 32 * static_cast<int>(sizeof(float4)) + ex;
     static std::atomic<uint64_t> attr{0};
-    smem_opt_in_once(attr, [&] {
-        opt_in_smem(k_g2p<true>, smem7);
-        opt_in_smem(k_g2p<false, true>, smem7);
-        opt_in_smem(k_g2p<false>, smem5);
-        opt_in_smem(k_g2p<true, false, true>, smem7 + boxb);
-        opt_in_smem(k_g2p<false, true, true>, smem7 + boxb);
-        opt_in_smem(k_g2p<false, false, true>, smem5 + boxb);
-        opt_in_smem(k_g2p<true, false, true, kSplitKP>, smem7 + boxb);
-        opt_in_smem(k_g2p<false, true, true, kSplitKP>, smem7 + boxb);
-        opt_in_smem(k_g2p<false, false, true, kSplitKP>, smem5 + boxb);
-        opt_in_smem(k_g2p<true, false, true, kPbSplitKP>, smem7 + boxb);
-        opt_in_smem(k_g2p<false, true, true, 1>, smem7 + boxb);
-        opt_in_smem(k_g2p<false, false, true, 1>, smem5 + boxb);
+    smem_opt_in_once(attr, [&] {  // sized with the export rows: the larger of the two launches
+        const int x7 = kWarpsPerBlock * kG2PStages * 7 * 32 * static_cast<int>(sizeof(float4)) +
+                       kWarpsPerBlock * kExportBytesPerWarp;
+        const int x5 = kWarpsPerBlock * kG2PStages * 5 * 32 * static_cast<int>(sizeof(float4)) +
+                       kWarpsPerBlock * kExportBytesPerWarp;
+        opt_in_smem(k_g2p<true>, x7);
+        opt_in_smem(k_g2p<false, true>, x7);
+        opt_in_smem(k_g2p<false>, x5);
+        opt_in_smem(k_g2p<true, false, true>, x7 + boxb);
+        opt_in_smem(k_g2p<false, true, true>, x7 + boxb);
+        opt_in_smem(k_g2p<false, false, true>, x5 + boxb);
+        opt_in_smem(k_g2p<true, false, true, kSplitKP>, x7 + boxb);
+        opt_in_smem(k_g2p<false, true, true, kSplitKP>, x7 + boxb);
+        opt_in_smem(k_g2p<false, false, true, kSplitKP>, x5 + boxb);
+        opt_in_smem(k_g2p<true, false, true, kPbSplitKP>, x7 + boxb);
+        opt_in_smem(k_g2p<false, true, true, 1>, x7 + boxb);
+        opt_in_smem(k_g2p<false, false, true, 1>, x5 + boxb);
     });
     if (pb && !standard && split_pb(max_groups)) {
         const int b4 = grid_for(max_groups * (kPer / kPbSplitKP) * 32, threads, xfer_cap());
