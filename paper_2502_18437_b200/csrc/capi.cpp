@@ -1129,15 +1129,16 @@ void fetch(Batch& b) {
     float* x = bound ? b.bound_x : static_cast<float*>(b.frame.get());
     float* v = bound ? b.bound_v : x + 3 * total;
     uint8_t* a = bound ? b.bound_a : reinterpret_cast<uint8_t*>(v + 3 * total);
-    // counters and contact first: a device->host copy issued after the arrays' would queue
-    // behind them on the copy engine
-    std::vector<SceneCounters> cnt = e.read_counters();
-    std::vector<double> imp, tq;
-    std::vector<int32_t> cc;
-    e.read_contact(1, imp, tq, cc);
+    // counters and contact first (a device->host copy issued after the arrays' would queue
+    // behind them on the copy engine), all completed by the snapshot's one stream sync
+    e.stage_small();
     std::vector<double> totals;
     // the arrays' D2H overlaps the next frame; mpmb_result_copy waits for it
     e.snapshot(x, v, a, totals, true);
+    std::vector<SceneCounters> cnt;
+    std::vector<double> imp, tq;
+    std::vector<int32_t> cc;
+    e.small_results(cnt, imp, tq, cc);
     if (b.exact) {
         e.wait_results();  // make_result (scene.hpp:256-266): FP64 sums in particle order, on the host
         for (size_t si = 0; si < b.scenes.size(); ++si) {

@@ -206,7 +206,7 @@ struct Engine::Impl {
     bool use_stress_in = false;
     uint32_t epoch = 0;
     DevBuf io_x, io_v, io_a, io_tot, io_inv;
-    PinnedBuf io_tot_h;
+    PinnedBuf io_tot_h, small_h;
     PinnedBuf pin_io;
     // profiling
     bool profiling = false;
@@ -1052,6 +1052,40 @@ std::vector<SceneCounters> Engine::read_counters() {
                           cudaMemcpyDeviceToHost, I.st), "d2h");
     check(cudaStreamSynchronize(I.st), "sync");
     return out;
+}
+
+void Engine::stage_small() {
+    Impl& I = *impl_;
+    const size_t S = I.hs.size(), ns = static_cast<size_t>(std::max(I.n_shapes, 0));
+    const size_t cb = sizeof(SceneCounters) * std::max<size_t>(S, 1);
+    I.small_h.alloc(cb + sizeof(double) * 6 * ns + sizeof(int) * ns);
+    char* h = static_cast<char*>(I.small_h.p);
+    check(cudaMemcpyAsync(h, I.counters.p, sizeof(SceneCounters) * S, cudaMemcpyDeviceToHost, I.st), "d2h");
+    if (ns > 0) {
+        check(cudaMemcpyAsync(h + cb, I.acc_frame.p, sizeof(double) * 6 * ns, cudaMemcpyDeviceToHost, I.st), "d2h");
+        check(cudaMemcpyAsync(h + cb + sizeof(double) * 6 * ns, I.cnt_frame.p, sizeof(int) * ns,
+                              cudaMemcpyDeviceToHost, I.st), "d2h");
+    }
+}
+
+void Engine::small_results(std::vector<SceneCounters>& cnt, std::vector<double>& imp, std::vector<double>& tq,
+                           std::vector<int32_t>& cc) {
+    Impl& I = *impl_;
+    const size_t S = I.hs.size(), ns = static_cast<size_t>(std::max(I.n_shapes, 0));
+    const size_t cb = sizeof(SceneCounters) * std::max<size_t>(S, 1);
+    const char* h = static_cast<const char*>(I.small_h.p);
+    cnt.assign(reinterpret_cast<const SceneCounters*>(h), reinterpret_cast<const SceneCounters*>(h) + S);
+    imp.assign(3 * ns, 0.0);
+    tq.assign(3 * ns, 0.0);
+    cc.assign(ns, 0);
+    if (ns == 0) return;
+    const double* b = reinterpret_cast<const double*>(h + cb);
+    std::memcpy(cc.data(), h + cb + sizeof(double) * 6 * ns, sizeof(int) * ns);
+    for (size_t i = 0; i < ns; ++i)
+        for (int a = 0; a < 3; ++a) {
+            imp[3 * i + a] = b[6 * i + a];
+            tq[3 * i + a] = b[6 * i + 3 + a];
+        }
 }
 
 void Engine::read_contact(int which, std::vector<double>& imp, std::vector<double>& tq,

@@ -127,6 +127,12 @@ class Engine {
     void reset_counters();
     void reset_contact(bool frame, bool sub);
     std::vector<SceneCounters> read_counters();
+    // fetch's small results in one round trip: stage_small() enqueues the counters and the
+    // frame's contact sums into pinned memory; after the next stream sync (snapshot) read them
+    // with small_results()
+    void stage_small();
+    void small_results(std::vector<SceneCounters>& counters, std::vector<double>& impulse,
+                       std::vector<double>& torque, std::vector<int32_t>& count);
     // contact accumulators (per shape, double): which = 0 substep, 1 frame
     void read_contact(int which, std::vector<double>& impulse, std::vector<double>& torque,
                       std::vector<int32_t>& count);
