@@ -1030,6 +1030,7 @@ void Engine::deactivate() {
 // ---------------------------------------------------------------- results
 void Engine::reset_counters() {
     Impl& I = *impl_;
+    I.export_req = false;  // a new frame: an export request left by a frame without particles lapses
     check(cudaMemsetAsync(I.counters.p, 0, I.counters.bytes, I.st), "memset");
 }
 
