@@ -141,10 +141,14 @@ template <>
 struct PlaneSet<5> {  // P0 {x, vx}, P3 {C6..8, F0}, P4, P5 {F}, PR
     __device__ static constexpr int plane(int q) { return q == 0 ? 0 : (q == 4 ? PR : q + 2); }
 };
+template <>
+struct PlaneSet<4> {  // (5 planes) P0 {x, vx}, P1 {vy, vz, A0, A1}, P2 {A2..5}, P3 {A6..8, F0}, PR
+    __device__ static constexpr int plane(int q) { return q == 4 ? PR : q; }
+};
 
 // Per-lane producer of the staging ring: issues the planes of the lane's k-th sorted
 // particle (lanes past their count commit an empty group, keeping the wait counts uniform).
-template <int NP, int NS = kStages, bool CG = false, bool OUT = false>
+template <int NP, int NS = kStages, bool CG = false, bool OUT = false, int PSET = NP>
 struct Stager {
     float4* buf;        // this warp's ring: [NS][NP][32]
     uint32_t slot0;     // first slot of the group
@@ -161,7 +165,7 @@ struct Stager {
             float4* dst = buf + (k % NS) * NP * 32 + lane;
 #pragma unroll
             for (int q = 0; q < NP; ++q)
-                cp_async16<CG>(dst + q * 32, (OUT ? P.pl_out : P.pl)[PlaneSet<NP>::plane(q)] + s);
+                cp_async16<CG>(dst + q * 32, (OUT ? P.pl_out : P.pl)[PlaneSet<PSET>::plane(q)] + s);
         }
         cp_commit();
     }
@@ -487,10 +491,31 @@ __device__ __forceinline__ uint64_t group_sort(const Params& P, uint32_t g, uint
     return mine;
 }
 
+// MLS affine momentum term A = m C - dt V (4/dx^2) sigma(F), V = det(F) V0 (solvers.hpp:154-156)
+__device__ __forceinline__ void mls_affine(const Params& P, const float Cm[9], const float F[9], float m, float vol0,
+                                           uint32_t flags, float m_inv, float A[9]) {
+    float sig[9];
+    const float4 mat = material(P, flags & kMatMask);
+    const float J = neo_hookean_f32(F, mat.y, mat.z, sig);
+    const float sc = -P.dt * (J * vol0) * m_inv;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) A[i] = fmaf(Cm[i], m, sig[i] * sc);
+}
+
+// Inside a frame the fused kernel's G2P phase evaluates A for the P2G phase that follows
+// (MPMB_K8_PREA): it has the new C and F in registers, writes A in C's planes (P1..P3) and the
+// P2G phase stages 5 planes instead of 7 and skips the stress.  The next G2P recomputes C
+// from the grid and never reads the old one; particles that leave the active set keep C, and
+// the frame's last G2P (unfused) stores C.  A/B on the engaged C5 window: K8 -2.8 %, C5
+// +2.2 %, M1 +1.5 %, C2 +1 %; the GPU parity suite unchanged.
+#ifndef MPMB_K8_PREA
+#define MPMB_K8_PREA 1
+#endif
+
 // One particle's P2G inputs (solvers.hpp:151-169 / 88-104 / 218-235) from its 7 planes:
 // scene, stencil base b, weights w, rel = node - x (STD: the weight derivatives), the
 // affine / impulse matrix A, mass m and velocity v.
-template <bool MLS, bool STD>
+template <bool MLS, bool STD, bool PREA = false>
 __device__ __forceinline__ void p2g_prepare(const Params& P, const float4 q0, const float4 q1, const float4 q2,
                                             const float4 q3, const float4 q4, const float4 q5, const float4 r,
                                             int& scene, int b[3], float w[3][3], float rel[3][3], float A[9],
@@ -505,7 +530,10 @@ __device__ __forceinline__ void p2g_prepare(const Params& P, const float4 q0, co
     local_base(P.geo, x, b, fx);
     m = r.x;
     // affine = m C - dt V (4/dx^2) sigma  (solvers.hpp:154-156; PB: m C, :222)
-    if (MLS) {
+    if (PREA) {  // evaluated by the fused kernel's G2P phase (mls_affine)
+#pragma unroll
+        for (int i = 0; i < 9; ++i) A[i] = Cm[i];
+    } else if (MLS) {
         const float F[9] = {q3.w, q4.x, q4.y, q4.z, q4.w, q5.x, q5.y, q5.z, q5.w};
         float sig[9];
         float J;  // det F (solvers.hpp:154)
@@ -692,9 +720,12 @@ __device__ __forceinline__ void p2g_group(const Params& P, uint32_t g, uint32_t 
                                           int4 tbox = make_int4(0, 0, 0, -1)) {
     constexpr bool DISCARD = MPMB_K8_DISCARD && OUT && MLS && !STD && KP >= 2;
     constexpr bool TILE = MPMB_P2G_TILE && OUT && MLS && !STD;
-    constexpr int NP = kPlanes;
+    // the fused kernel's G2P phase left A in C's planes (mls_affine): 5 planes staged
+    constexpr bool PREA = MPMB_K8_PREA && OUT && MLS && !STD;
+    constexpr int NP = PREA ? 5 : kPlanes;
+    constexpr int RI = PREA ? 4 : PR;  // ring index of the PR plane
     constexpr int NS = OUT ? kStagesL2 : kStages;
-    Stager<NP, NS, OUT || MPMB_P2G_CG != 0, OUT> st;
+    Stager<NP, NS, OUT || MPMB_P2G_CG != 0, OUT, PREA ? 4 : NP> st;
     st.buf = ring;
     st.lane = lane;
     uint32_t* bins = reinterpret_cast<uint32_t*>(ring);  // sort scratch aliases the ring
@@ -754,12 +785,13 @@ __device__ __forceinline__ void p2g_group(const Params& P, uint32_t g, uint32_t 
                 if (__any_sync(0xffffffffu, fl)) tile_flush(P, T, fl, ckey, pa, pb, lane);
                 if (change) ckey = key;
                 if (live) {
-                    const float4 r = src[PR * 32];
-                    const float4 q0 = src[0], q1 = src[32], q2 = src[64], q3 = src[96], q4 = src[128],
-                                 q5 = src[160];
+                    const float4 r = src[RI * 32];
+                    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+                    const float4 q0 = src[0], q1 = src[32], q2 = src[64], q3 = src[96],
+                                 q4 = PREA ? z4 : src[128], q5 = PREA ? z4 : src[160];
                     int scene, b[3];
                     float w[3][3], rel[3][3], A[9], m, v[3];
-                    p2g_prepare<MLS, STD>(P, q0, q1, q2, q3, q4, q5, r, scene, b, w, rel, A, m, v);
+                    p2g_prepare<MLS, STD, PREA>(P, q0, q1, q2, q3, q4, q5, r, scene, b, w, rel, A, m, v);
                     p2g_nodes(w, rel, A, m, v, pa, pb);
                 }
             }
@@ -780,11 +812,13 @@ __device__ __forceinline__ void p2g_group(const Params& P, uint32_t g, uint32_t 
         cp_wait<NS - 1>();
         if (k >= st.cnt) continue;
         const float4* src = st.buf + (k % NS) * NP * 32 + lane;
-        const float4 r = src[PR * 32];
-        const float4 q0 = src[0], q1 = src[32], q2 = src[64], q3 = src[96], q4 = src[128], q5 = src[160];
+        const float4 r = src[RI * 32];
+        const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 q0 = src[0], q1 = src[32], q2 = src[64], q3 = src[96], q4 = PREA ? z4 : src[128],
+                     q5 = PREA ? z4 : src[160];
         int scene, b[3];
         float w[3][3], rel[3][3], A[9], m, v[3];  // STD: rel holds the weight derivatives
-        p2g_prepare<MLS, STD>(P, q0, q1, q2, q3, q4, q5, r, scene, b, w, rel, A, m, v);
+        p2g_prepare<MLS, STD, PREA>(P, q0, q1, q2, q3, q4, q5, r, scene, b, w, rel, A, m, v);
         if (b[0] != cb[0] || b[1] != cb[1] || b[2] != cb[2] || scene != cscene) {
             if (cscene >= 0) p2g_flush(P, scene_view(P, cscene), cb, pa, pb);
             cb[0] = b[0]; cb[1] = b[1]; cb[2] = b[2];
@@ -1251,7 +1285,7 @@ __device__ __forceinline__ void g2p_particle(const Params& P, Part& p, float4& r
 // positions g2p_pos(L, k): the warp's 32 lanes gather around a few neighbouring stencils at
 // every iteration.  Every position is written to the other buffer at slot
 // group_phys(pos): the state leaves G2P in the new order.  `ring`: this warp's staging ring.
-template <bool PB, bool STD, bool BOX, int KP = kPer>
+template <bool PB, bool STD, bool BOX, int KP = kPer, bool PREA = false>
 __device__ __forceinline__ void g2p_group(const Params& P, uint32_t g, uint32_t unit, float4* ring, int lane,
                                           float4* box_s = nullptr, uint16_t* nbin = nullptr, int4* nbox = nullptr,
                                           double* tot = nullptr) {
@@ -1348,6 +1382,12 @@ __device__ __forceinline__ void g2p_group(const Params& P, uint32_t g, uint32_t 
             }
         }
         g2p_particle<PB, STD, BOX>(P, p, r, L, box);
+        if (PREA && (__float_as_uint(r.z) & kActiveBit)) {  // A for the fused P2G phase, in C's place
+            float A[9];
+            mls_affine(P, p.C, p.F, r.x, r.y, __float_as_uint(r.z), scene_view(P, L.my_scene).m_inv, A);
+#pragma unroll
+            for (int i = 0; i < 9; ++i) p.C[i] = A[i];
+        }
         store_part_out(P, so, p, r);
         if (tot) {  // frame-end export (the standalone G2P only)
             export_write(P, p.x, p.v, r);
@@ -1471,7 +1511,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_P2G_MINB) k_g2p2g(co
                                : smem + wpb * (kRing * 32 + kGroup / 8) + (threadIdx.x >> 5) * kTileCap;
     for (uint32_t u = blockIdx.x * wpb + (threadIdx.x >> 5); u < n_units; u += gridDim.x * wpb) {
         int4 nb = make_int4(0, 0, 0, -1);
-        g2p_group<PB, STD, BOX, KP>(P, u / U, u % U, ring, lane, box, nbin, (TILE && nbin) ? &nb : nullptr);
+        g2p_group<PB, STD, BOX, KP, MPMB_K8_PREA && !PB && !STD>(P, u / U, u % U, ring, lane, box, nbin,
+                                                                 (TILE && nbin) ? &nb : nullptr);
         __syncwarp();  // orders this warp's stores of the group (and nbin) before the P2G phase
         p2g_group<!PB, STD, true, BOX, KP>(P, u / U, u % U, ring, lane, nbin, tile, nb);
     }
