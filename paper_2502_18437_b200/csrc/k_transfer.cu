@@ -44,11 +44,17 @@ constexpr int kStages = MPMB_P2G_STAGES;     // P2G staging ring depth (from HBM
 // K8's P2G phase stages from L2 (the lines its G2P phase just wrote): a shallower ring hides
 // that latency and leaves more of the SM's shared memory to L1 (A/B at C5: K8 -0.7%)
 constexpr int kStagesL2 = MPMB_P2G_STAGES_L2;
+// K8's MLS G2P phase evaluates the P2G's affine term (mls_affine below); its P2G phase then
+// stages 5 planes instead of 7
+#ifndef MPMB_K8_PREA
+#define MPMB_K8_PREA 1
+#endif
 // K8's per-warp ring (float4 x 32 units): the G2P phase's and the P2G phase's, aliased
 template <bool PB, bool STD>
 __host__ __device__ constexpr int fused_ring() {
-    return kStagesL2 * 7 > MPMB_G2P_STAGES * ((PB || STD) ? 7 : 5) ? kStagesL2 * 7
-                                                                   : MPMB_G2P_STAGES * ((PB || STD) ? 7 : 5);
+    return kStagesL2 * ((PB || STD || !MPMB_K8_PREA) ? 7 : 5) > MPMB_G2P_STAGES * ((PB || STD) ? 7 : 5)
+               ? kStagesL2 * ((PB || STD || !MPMB_K8_PREA) ? 7 : 5)
+               : MPMB_G2P_STAGES * ((PB || STD) ? 7 : 5);
 }
 constexpr int kG2PStages = MPMB_G2P_STAGES;  // G2P: one more, so particle k+1 has landed while k computes
 #ifndef MPMB_WPB
@@ -507,10 +513,7 @@ __device__ __forceinline__ void mls_affine(const Params& P, const float Cm[9], c
 // P2G phase stages 5 planes instead of 7 and skips the stress.  The next G2P recomputes C
 // from the grid and never reads the old one; particles that leave the active set keep C, and
 // the frame's last G2P (unfused) stores C.  A/B on the engaged C5 window: K8 -2.8 %, C5
-// +2.2 %, M1 +1.5 %, C2 +1 %; the GPU parity suite unchanged.
-#ifndef MPMB_K8_PREA
-#define MPMB_K8_PREA 1
-#endif
+// +2.2 %, M1 +1.5 %, C2 +1 %; the GPU parity suite unchanged.  (MPMB_K8_PREA: top of file.)
 
 // One particle's P2G inputs (solvers.hpp:151-169 / 88-104 / 218-235) from its 7 planes:
 // scene, stencil base b, weights w, rel = node - x (STD: the weight derivatives), the

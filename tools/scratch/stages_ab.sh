@@ -1,0 +1,4 @@
+for r in 1 2; do
+  bash tools/ab_engaged.sh c5 512 10
+  bash tools/ab_engaged.sh m1 1 20
+done
