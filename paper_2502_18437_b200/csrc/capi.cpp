@@ -798,6 +798,9 @@ struct Batch {
     }
     size_t frame_bytes = 0;
     bool device_valid = false;   // device holds the newest particle state
+    // advance_frames: the previous frame's last kernel was the fused G2P + this frame's first
+    // P2G (run_frame, cross-frame fusion); valid only inside one advance_frames call
+    bool carry_fused = false;
     bool particles_dirty = true; // host changed: re-upload
     bool shapes_dirty = true;
     Status status = Status::idle;
@@ -971,7 +974,21 @@ void upload(Batch& b) {
 // export: the frame's last G2P writes the FrameResult (Engine::request_export) -- the last
 // frame of an advance, the one fetch_results reads -- when the caller bound result arrays
 // (mpmb_bind_results: a result every frame); unbound fetches gather after the frame
-void run_frame(Batch& b, float dt, bool last_of_advance = true) {
+// cross-frame fusion (MPMB_CROSS_FRAME=0 in the environment: off, for A/B)
+static bool cross_frame_fusion() {
+    static const bool on = [] {
+        const char* e = std::getenv("MPMB_CROSS_FRAME");
+        return !e || std::atoi(e) != 0;
+    }();
+    return on;
+}
+
+// into_next: another frame of the same advance_frames call follows, so when no binning falls
+// between them the last G2P runs fused with that frame's first P2G (K8 across the frame
+// boundary; nothing between them reads or writes particles: free bodies, pose targets and the
+// next frame's pose table, counters and contact resets touch neither the planes nor the P2G
+// accumulator, and the next frame's set_pose_table invalidates the shape cull)
+void run_frame(Batch& b, float dt, bool last_of_advance = true, bool into_next = false) {
     // Where the export pays (A/B of the e2e rate, MPMB_EXPORT=1 vs 0): scene batches (C5,
     // 512 scenes: +1-2 %) and small frames, where the gather's and totals' launches are a
     // visible share (C1, 32k particles: +6 %); single mid-size scenes lose the scattered
@@ -1051,9 +1068,11 @@ void run_frame(Batch& b, float dt, bool last_of_advance = true) {
         // unless a binning falls between them
         const bool standard = cfg.solver == MPMB_SOLVER_STANDARD;  // scene.hpp:200-207
         const bool can_fuse = e.fuse_ok();
-        bool fused_in = false;  // P2G of this substep already ran inside the previous kernel
+        bool fused_in = b.carry_fused;  // P2G of this substep already ran inside the previous kernel
+        b.carry_fused = false;
         for (int sub = 0; sub < n_sub; ++sub) {
             if (b.since_sort >= resort) {
+                if (fused_in) throw std::logic_error("run_frame: binning after a carried P2G");
                 e.bin();
                 b.since_sort = 0;
             }
@@ -1061,7 +1080,8 @@ void run_frame(Batch& b, float dt, bool last_of_advance = true) {
             if (!fused_in) e.p2g(true, dt_sub, true, standard);
             if (sub == 0) build_pose_table();
             e.grid_update(sub, dt_sub, cfg.gravity, true, true, cfg.boundary);
-            const bool fuse = can_fuse && sub + 1 < n_sub && b.since_sort < resort;
+            const bool fuse = can_fuse && b.since_sort < resort &&
+                              (sub + 1 < n_sub || (into_next && cross_frame_fusion()));
             if (fuse) {
                 e.g2p2g(sub, dt_sub, standard, cfg.gravity, any_free);  // + free bodies of sub
             } else {
@@ -1072,6 +1092,7 @@ void run_frame(Batch& b, float dt, bool last_of_advance = true) {
             }
             fused_in = fuse;
         }
+        b.carry_fused = fused_in;  // the last substep fused into the next frame's first P2G
     } else {
         // PB-MPM: one step per frame; positions move only at the commit, so the per-iteration
         // group sort absorbs the drift and binning follows the same interval as MLS (every 4
@@ -1442,6 +1463,7 @@ extern "C" mpmb_status mpmb_advance(mpmb_handle h, float dt) {
         if (b->status == Status::advancing)
             fail(MPMB_LIFECYCLE_ERROR, "scene: advance while a frame is pending");
         b->status = Status::advancing;
+        b->carry_fused = false;
         run_frame(*b, dt);
         return MPMB_OK;
     });
@@ -1458,7 +1480,9 @@ extern "C" mpmb_status mpmb_advance_frames(mpmb_handle h, float dt, int32_t n_fr
             fail(MPMB_LIFECYCLE_ERROR, "scene belongs to a batch: advance the batch handle");
         if (b->status == Status::advancing)
             fail(MPMB_LIFECYCLE_ERROR, "scene: advance while a frame is pending");
-        for (int f = 0; f < n_frames; ++f) run_frame(*b, dt, f + 1 == n_frames);
+        b->carry_fused = false;
+        for (int f = 0; f < n_frames; ++f) run_frame(*b, dt, f + 1 == n_frames, f + 1 < n_frames);
+        b->carry_fused = false;
         b->status = Status::advancing;
         return MPMB_OK;
     });
