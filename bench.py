@@ -462,10 +462,10 @@ def run_ours(args, rank, world, local_rank):
     # dominant kernel class and its roofline (per-launch averages over the timed region)
     # with substep fusion (mpmb_set_fusion) the frame runs P2G and G2P alone once each and
     # k_g2p2g sub-1 times
-    fused = prof["ms_fused"] > 0.0
-    n_sep = args.steps if fused else sub * args.steps
-    launches_per_class = {"p2g": n_sep, "g2p": n_sep, "grid": sub * args.steps, "sort": args.steps,
-                          "fused": (sub - 1) * args.steps if fused else 0}
+    # operations per class in the profiled replay, counted by the library (substep fusion and
+    # cross-frame fusion change how many standalone P2G / G2P launches a frame has)
+    launches_per_class = {"p2g": prof["n_p2g"], "g2p": prof["n_g2p"], "grid": prof["n_grid"],
+                          "sort": prof["n_sort"], "fused": prof["n_fused"]}
     cls_ms = {"p2g": prof["ms_p2g"], "g2p": prof["ms_g2p"], "grid": prof["ms_grid"], "sort": prof["ms_sort"],
               "fused": prof["ms_fused"]}
     dom = max(cls_ms, key=lambda k: cls_ms[k])

@@ -169,6 +169,8 @@ typedef struct {
     int64_t launches;            /* kernels launched by the library while profiling */
     int64_t particle_substeps;   /* active particles x substeps (PB: x iterations) */
     double ms_fused;             /* k_g2p2g: G2P of substep s fused with P2G of s+1 (+ collect) */
+    /* timed operations per class (one binning, P2G, grid update, G2P or fused launch each) */
+    int64_t n_sort, n_p2g, n_grid, n_g2p, n_fused;
 } mpmb_profile;
 
 /* ------------------------------------------------------------------ library */

@@ -83,7 +83,8 @@ class DDStats(C.Structure):
 class Profile(C.Structure):
     _fields_ = [("ms_sort", C.c_double), ("ms_p2g", C.c_double), ("ms_grid", C.c_double),
                 ("ms_g2p", C.c_double), ("ms_other", C.c_double), ("launches", C.c_int64),
-                ("particle_substeps", C.c_int64), ("ms_fused", C.c_double)]
+                ("particle_substeps", C.c_int64), ("ms_fused", C.c_double), ("n_sort", C.c_int64),
+                ("n_p2g", C.c_int64), ("n_grid", C.c_int64), ("n_g2p", C.c_int64), ("n_fused", C.c_int64)]
 
 
 GridHook = C.CFUNCTYPE(None, C.c_void_p, C.c_int32, C.POINTER(C.c_float),

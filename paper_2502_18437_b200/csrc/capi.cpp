@@ -1775,6 +1775,11 @@ extern "C" mpmb_status mpmb_get_profile(mpmb_handle h, mpmb_profile* out) {
             out->ms_other = t.ms_other;
             out->launches = t.launches;
             out->ms_fused = t.ms_fused;
+            out->n_sort = t.n_sort;
+            out->n_p2g = t.n_p2g;
+            out->n_grid = t.n_grid;
+            out->n_g2p = t.n_g2p;
+            out->n_fused = t.n_fused;
         }
         return MPMB_OK;
     });

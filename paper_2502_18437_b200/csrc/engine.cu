@@ -248,6 +248,13 @@ struct Engine::Impl {
                           : e.first == CAT_FUSED ? &times.ms_fused
                                                : &times.ms_other;
             *dst += ms;
+            int64_t* cnt = e.first == CAT_SORT ? &times.n_sort
+                           : e.first == CAT_P2G ? &times.n_p2g
+                           : e.first == CAT_GRID ? &times.n_grid
+                           : e.first == CAT_G2P ? &times.n_g2p
+                           : e.first == CAT_FUSED ? &times.n_fused
+                                                : nullptr;
+            if (cnt) ++*cnt;
             event_pool.push_back(e.second.first);
             event_pool.push_back(e.second.second);
         }

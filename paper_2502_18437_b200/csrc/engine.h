@@ -48,6 +48,7 @@ struct KernelTimes {
     double ms_sort = 0, ms_p2g = 0, ms_grid = 0, ms_g2p = 0, ms_other = 0;
     double ms_fused = 0;  // k_g2p2g (G2P of substep s + P2G of s+1) + its brick collect
     int64_t launches = 0;
+    int64_t n_sort = 0, n_p2g = 0, n_grid = 0, n_g2p = 0, n_fused = 0;  // timed operations
 };
 
 class Engine {
