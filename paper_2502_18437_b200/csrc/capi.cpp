@@ -989,18 +989,12 @@ static bool cross_frame_fusion() {
 // next frame's pose table, counters and contact resets touch neither the planes nor the P2G
 // accumulator, and the next frame's set_pose_table invalidates the shape cull)
 void run_frame(Batch& b, float dt, bool last_of_advance = true, bool into_next = false) {
-    // Where the export pays (A/B of the e2e rate, MPMB_EXPORT=1 vs 0): scene batches (C5,
-    // 512 scenes: +1-2 %) and small frames, where the gather's and totals' launches are a
-    // visible share (C1, 32k particles: +6 %); single mid-size scenes lose the scattered
-    // stores in their short G2P more than the gather costs them overlapped (M1 -1.8 %, C2
-    // -4 %).  MPMB_EXPORT in the environment: 0 never, 2 always.
-    static const int export_mode = [] {
+    // A/B of the e2e rate against the gather at fetch (MPMB_EXPORT=0 in the environment):
+    // C5 +1.9 %, M1 +1.8 %, C2 +4.3 %, C1 +6 %, C3 +2 %
+    static const bool pays = [] {
         const char* e = std::getenv("MPMB_EXPORT");
-        return e ? std::atoi(e) : 1;
+        return !e || std::atoi(e) != 0;
     }();
-    size_t n_all = 0;
-    for (const Scene* s : b.scenes) n_all += s->count();
-    const bool pays = export_mode == 2 || (export_mode == 1 && (b.scenes.size() >= 8 || n_all <= 131072));
     const bool export_result = pays && last_of_advance && b.bound_n > 0;
     upload(b);
     Engine& e = *b.eng;

@@ -205,7 +205,7 @@ struct Engine::Impl {
     DevBuf stress_in;
     bool use_stress_in = false;
     uint32_t epoch = 0;
-    DevBuf io_x, io_v, io_a, io_tot, io_inv;
+    DevBuf io_x, io_v, io_a, io_tot, io_inv, io_pad;
     PinnedBuf io_tot_h, small_h;
     PinnedBuf pin_io;
     // profiling
@@ -819,17 +819,13 @@ bool Engine::prepare_export(Params& P) {
     if (!want) return false;
     const size_t N = static_cast<size_t>(I.n);
     const size_t S = std::max<size_t>(I.hs.size(), 1);
-    if (I.copy_pending && (I.io_x.bytes < 12 * N || I.io_v.bytes < 12 * N || I.io_a.bytes < N))
-        wait_results();  // the staging is about to be reallocated
-    if (I.copy_pending) check(cudaStreamWaitEvent(I.st, I.ev_copy, 0), "wait copy");  // staging reuse
-    I.io_x.alloc(12 * N);
-    I.io_v.alloc(12 * N);
-    I.io_a.alloc(N);
+    if (I.copy_pending && I.io_pad.bytes < 32 * N) wait_results();  // about to be reallocated
+    // the previous frame's unpack (copy stream) still reads the padded staging
+    if (I.copy_pending) check(cudaStreamWaitEvent(I.st, I.ev_copy, 0), "wait copy");
+    I.io_pad.alloc(32 * N);
     I.io_tot.alloc(sizeof(double) * 5 * S);
     check(cudaMemsetAsync(I.io_tot.p, 0, I.io_tot.bytes, I.st), "memset");
-    P.exp_x = I.io_x.as<float>();
-    P.exp_v = I.io_v.as<float>();
-    P.exp_a = I.io_a.as<uint8_t>();
+    P.exp_pad = I.io_pad.as<float4>();
     P.exp_tot = I.io_tot.as<double>();
     P.exp_n = I.n;
     return true;
@@ -1134,6 +1130,15 @@ void Engine::snapshot(float* x, float* v, uint8_t* active, std::vector<double>& 
               "d2h");
         check(cudaEventRecord(I.ev_dl, I.st), "event");
         check(cudaStreamWaitEvent(I.copy_st, I.ev_dl, 0), "wait download");
+        // unpad on the copy stream (overlaps the next frame), then the packed arrays' D2H
+        if (I.copy_pending && (I.io_x.bytes < 12 * N || I.io_v.bytes < 12 * N || I.io_a.bytes < N))
+            wait_results();
+        I.io_x.alloc(12 * N);
+        I.io_v.alloc(12 * N);
+        I.io_a.alloc(N);
+        launch_export_pack(I.io_pad.as<float4>(), I.n, x ? I.io_x.as<float>() : nullptr,
+                           v ? I.io_v.as<float>() : nullptr, active ? I.io_a.as<uint8_t>() : nullptr, I.copy_st);
+        I.counted(1);
         if (x) check(cudaMemcpyAsync(x, I.io_x.p, 12 * I.n, cudaMemcpyDeviceToHost, I.copy_st), "d2h");
         if (v) check(cudaMemcpyAsync(v, I.io_v.p, 12 * I.n, cudaMemcpyDeviceToHost, I.copy_st), "d2h");
         if (active) check(cudaMemcpyAsync(active, I.io_a.p, I.n, cudaMemcpyDeviceToHost, I.copy_st), "d2h");

@@ -278,6 +278,21 @@ __global__ void k_grid_upload(const Params P, DevScene S, int64_t n_nodes, const
     }
 }
 
+// frame-end export staging (2 float4 per original index) -> the packed x / v / active arrays
+__global__ void k_export_pack(const float4* pad, int64_t n, float* x, float* v, uint8_t* a) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t o = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; o < n; o += stride) {
+        const float4 p = pad[2 * o], q = pad[2 * o + 1];
+        if (x) { x[3 * o] = p.x; x[3 * o + 1] = p.y; x[3 * o + 2] = p.z; }
+        if (v) { v[3 * o] = p.w; v[3 * o + 1] = q.x; v[3 * o + 2] = q.y; }
+        if (a) a[o] = q.z != 0.f ? 1 : 0;
+    }
+}
+void launch_export_pack(const float4* pad, int64_t n, float* x, float* v, uint8_t* a, cudaStream_t st) {
+    k_export_pack<<<blocks_for(n, 256, 148 * 16), 256, 0, st>>>(pad, n, x, v, a);
+    MPMB_LAUNCHED("k_export_pack");
+}
+
 void launch_upload(const Params& P, const IoArrays& in, int64_t n, cudaStream_t st) {
     k_upload<<<blocks_for(n, 256, 148 * 16), 256, 0, st>>>(P, in, n);
     MPMB_LAUNCHED("k_upload");

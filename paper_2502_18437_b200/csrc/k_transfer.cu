@@ -1054,7 +1054,7 @@ __device__ __forceinline__ int pushout_particle(const Params& P, const SceneView
     return pushed;
 }
 
-// ---- frame-end export (Params::exp_x; scene.hpp:251-266).  The frame's last G2P has every
+// ---- frame-end export (Params::exp_pad; scene.hpp:251-266).  The frame's last G2P has every
 // particle's final x, v and flags in registers: it writes them to the result staging at the
 // particle's original index and sums the per-scene totals, so the fetch needs no inverse
 // permutation, gather or totals pass over the state.  Totals: each lane sums its particles of
@@ -1062,14 +1062,14 @@ __device__ __forceinline__ int pushout_particle(const Params& P, const SceneView
 // warp adds them with one FP64 atomic per value per group (per lane when lanes hold different
 // scenes) -- the sums of k_totals, in another order.
 constexpr int kExportBytesPerWarp = 6 * 32 * 8;
+// two 16-byte stores into one 32-byte sector per particle (k_export_pack unpads them on the copy
+// stream): 7 scattered scalar stores cost the short G2P of a mid-size scene more
 __device__ __forceinline__ void export_write(const Params& P, const float x[3], const float v[3], float4 r) {
     const uint32_t o = __float_as_uint(r.w);
     if (o == kHoleOrig || static_cast<int64_t>(o) >= P.exp_n) return;
-    float* ox = P.exp_x + 3ull * o;
-    float* ov = P.exp_v + 3ull * o;
-    ox[0] = x[0]; ox[1] = x[1]; ox[2] = x[2];
-    ov[0] = v[0]; ov[1] = v[1]; ov[2] = v[2];
-    P.exp_a[o] = (__float_as_uint(r.z) & kActiveBit) ? 1 : 0;
+    float4* d = P.exp_pad + 2ull * o;
+    d[0] = make_float4(x[0], x[1], x[2], v[0]);
+    d[1] = make_float4(v[1], v[2], (__float_as_uint(r.z) & kActiveBit) ? 1.f : 0.f, 0.f);
 }
 __device__ __forceinline__ void tot_flush_lane(const Params& P, double* T, int lane) {
     int* tag = reinterpret_cast<int*>(T + 5 * 32);
@@ -1465,7 +1465,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MPMB_G2P_MINB) k_g2p(cons
     float4* box = BOX ? smem + wpb * (kG2PStages * NP * 32) + (threadIdx.x >> 5) * kBoxCap : nullptr;
     // frame-end export: per-warp totals rows after the rings and boxes (launch_g2p sizes them)
     double* tot = nullptr;
-    if (P.exp_x) {
+    if (P.exp_pad) {
         tot = reinterpret_cast<double*>(smem + wpb * (kG2PStages * NP * 32 + (BOX ? kBoxCap : 0))) +
               (threadIdx.x >> 5) * (kExportBytesPerWarp / 8);
         tot_init(tot, lane);
@@ -1532,7 +1532,7 @@ __global__ void __launch_bounds__(128) k_g2p_wide(const __grid_constant__ Params
     extern __shared__ float4 smem[];
     const int lane = threadIdx.x & 31;
     double* tot = nullptr;  // frame-end export (launch_g2p gives it the rows)
-    if (P.exp_x) {
+    if (P.exp_pad) {
         tot = reinterpret_cast<double*>(smem) + (threadIdx.x >> 5) * (kExportBytesPerWarp / 8);
         tot_init(tot, lane);
         __syncwarp();
@@ -1737,11 +1737,11 @@ void launch_p2g(const Params& P, bool mls, int64_t max_groups, cudaStream_t st, 
 }
 
 void launch_g2p(const Params& P, bool pb, int64_t max_groups, cudaStream_t st, bool standard, bool wide) {
-    // frame-end export (P.exp_x): the totals rows after the rings and boxes
-    const int ex = P.exp_x ? kWarpsPerBlock * kExportBytesPerWarp : 0;
+    // frame-end export (P.exp_pad): the totals rows after the rings and boxes
+    const int ex = P.exp_pad ? kWarpsPerBlock * kExportBytesPerWarp : 0;
     if (wide) {
         const int b = grid_for(P.n_total, 128, 148 * 16);
-        const int exw = P.exp_x ? 4 * kExportBytesPerWarp : 0;
+        const int exw = P.exp_pad ? 4 * kExportBytesPerWarp : 0;
         if (standard) launch_chain(k_g2p_wide<false, true>, b, 128, exw, st, P);
         else if (pb) launch_chain(k_g2p_wide<true>, b, 128, exw, st, P);
         else launch_chain(k_g2p_wide<false>, b, 128, exw, st, P);

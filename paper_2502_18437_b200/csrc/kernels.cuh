@@ -80,11 +80,10 @@ struct Params {
     int64_t n_total;          // slots (particles + holes), a fixed bound
     uint64_t total_nodes;     // grid pool length (bounds checks, MPMB_DEVICE_CHECKS)
     uint32_t debug;           // timing experiments of variant builds only (k_transfer.cu)
-    // frame-end export (Engine::request_export): the frame's last G2P writes x, v, active in
-    // original order (indices < exp_n) and adds the per-scene FP64 totals; nullptr: off
-    float* exp_x;
-    float* exp_v;
-    uint8_t* exp_a;
+    // frame-end export (Engine::request_export): the frame's last G2P writes {x, v.x}, {v.y, v.z,
+    // active, 0} at 2 o, 2 o + 1 (original index o < exp_n) and adds the per-scene FP64
+    // totals; nullptr: off
+    float4* exp_pad;
     double* exp_tot;
     int64_t exp_n;
     const float* stress_in;  // original-order uploaded sigma (first MLS P2G only)

@@ -104,6 +104,7 @@ void launch_upload(const Params& P, const IoArrays& in, int64_t n, cudaStream_t 
 void launch_download(const Params& P, const IoArrays& out, cudaStream_t st);
 void launch_totals(const Params& P, double* totals /*5 per scene*/, cudaStream_t st);
 // x / v / active (original order) + the totals through the inverse permutation (inv: n words)
+void launch_export_pack(const float4* pad, int64_t n, float* x, float* v, uint8_t* a, cudaStream_t st);
 void launch_frame_result_orig(const Params& P, uint32_t* inv, int64_t n, const IoArrays& out, double* totals,
                               cudaStream_t st);
 void launch_stress(const Params& P, float* stress_orig, cudaStream_t st);

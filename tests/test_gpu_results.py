@@ -8,10 +8,9 @@ and totals passes after the frame.
       momentum / kinetic energy 1e-4 of the scene's |p| / KE (the twins differ only by the
       float atomic order of 20 substeps)
 
-Paths (the export runs for scene batches of >= 8 scenes and frames of <= 131,072 particles;
-C2, one 262k-particle scene, keeps the gather and is checked the same way): thread-per-slot
-G2P (8 cutting replicas, 518k; C1; PB-MPM cube and suture with free capsules), grouped G2P
-with node boxes (12 replicas, 778k) and without (30 replicas, 1.94M)."""
+Paths: thread-per-slot G2P (8 cutting replicas, 518k; C1; C2; PB-MPM cube and suture with
+free capsules), grouped G2P with node boxes (12 replicas, 778k) and without (30 replicas,
+1.94M)."""
 import numpy as np
 import pytest
 
